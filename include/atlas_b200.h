@@ -1,0 +1,168 @@
+/*
+ * atlas_b200.h — C-ABI of the B200 broadcast layer engine (libatlas_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or C++ types cross this line.
+ * Each entry point replaces one reference interface of the `oocgnn`
+ * package (paths relative to /root/reference/pkg/src):
+ *
+ *   atlas_graph_create      TopologySource + in-degrees as one layer sees
+ *                           them (oocgnn/chunks.py:51-78,
+ *                           oocgnn/storage.py:205-250); builds the
+ *                           destination-major (CSC) view on the device
+ *   atlas_layer_create      init_layer (oocgnn/orchestrator.py:93-145):
+ *                           pending counters, state table, hot-slot budget,
+ *                           eviction policy, sub_batch / evict_batch
+ *   atlas_chunk_submit      process_chunk (oocgnn/orchestrator.py:216-299)
+ *                           for one caller-supplied source chunk
+ *   atlas_chunk_graduated   the sink hand-off of process_chunk
+ *                           (oocgnn/orchestrator.py:148-150): ids + rows of
+ *                           every vertex that graduated in the last chunk
+ *   atlas_layer_run_resident  one whole layer over a resident input with the
+ *                           reference chunk plan (oocgnn/runtime.py:114-220
+ *                           minus the disk stages): scatter-aggregate +
+ *                           pending counters + min-pending control plane
+ *   atlas_transform         MatmulBackend.apply + activation
+ *                           (oocgnn/compute.py:25-97)
+ *   atlas_layer_finish      finalize_layer (oocgnn/orchestrator.py:302-323)
+ *
+ * Status codes map 1:1 onto the reference's exception classes
+ * (oocgnn/errors.py:8-78); the Python shim raises them.
+ * Threading: one handle per GPU, single owner.
+ */
+#ifndef ATLAS_B200_H
+#define ATLAS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ATLAS_ABI_VERSION 1
+
+enum {
+  ATLAS_OK = 0,
+  ATLAS_ECONFIG = -1,      /* ConfigError */
+  ATLAS_ECONSISTENCY = -2, /* ConsistencyError */
+  ATLAS_ESTATE = -3,       /* StateTransitionError */
+  ATLAS_EBUDGET = -4,      /* BudgetError */
+  ATLAS_EINCOMPLETE = -5,  /* IncompleteLayerError */
+  ATLAS_ECOVERAGE = -6,    /* CoverageError */
+  ATLAS_EFORMAT = -7,      /* FormatError */
+  ATLAS_EDEVICE = -8,      /* CUDA/NCCL failure (DeviceError) */
+  ATLAS_EINVARIANT = -9    /* InvariantError */
+};
+
+enum { ATLAS_GCN = 0, ATLAS_SAGE = 1, ATLAS_GIN = 2 };          /* ModelKind */
+enum { ATLAS_F32 = 0, ATLAS_F16 = 1, ATLAS_BF16 = 2 };         /* row dtype */
+enum { ATLAS_MINPEND = 0, ATLAS_LRU = 1, ATLAS_RND = 2 };      /* policy */
+enum { ATLAS_BACKEND_STABLE = 0, ATLAS_BACKEND_TCGEN05 = 1 };  /* transform */
+enum { ATLAS_LOG_VICTIMS = 0, ATLAS_LOG_RELOADS = 1, ATLAS_LOG_GRADUATED = 2 };
+
+typedef struct atlas_graph atlas_graph;
+typedef struct atlas_layer atlas_layer;
+
+typedef struct {
+  int64_t num_vertices;  /* V of the whole graph */
+  int64_t dst_lo;        /* destination range owned by this handle: */
+  int64_t dst_hi;        /*   partition_ranges(V, G)[rank] */
+  int32_t model;         /* ATLAS_GCN / ATLAS_SAGE / ATLAS_GIN */
+  float gin_epsilon;
+  int64_t embed_dim;     /* width of streamed rows */
+  int64_t agg_dim;       /* aggregation record width (2*embed for SAGE) */
+  int64_t slot_count;    /* hot slots of this GPU (MemoryBudget.slot_count) */
+  int64_t evict_batch;   /* 0 -> max(1, slot_count / 100) */
+  int32_t policy;        /* ATLAS_MINPEND / ATLAS_LRU / ATLAS_RND */
+  int32_t record_log;    /* keep victim / reload / graduation logs */
+  uint64_t rnd_state[4]; /* numpy PCG64 (state_hi, state_lo, inc_hi, inc_lo) */
+  int32_t device;
+  int32_t force_exact;   /* 1: never take the parallel eviction-free path */
+} atlas_layer_desc;
+
+typedef struct {
+  int64_t messages;
+  int64_t evictions;
+  int64_t reloads;
+  int64_t unique_reloads;
+  int64_t admissions;
+  int64_t graduations;
+  int64_t hot_peak;
+  int64_t hot_slot_count;
+  int64_t chunks;          /* chunks seen */
+  int64_t span_count;      /* vertices with a first step */
+  int64_t span_sum;        /* exact sum of (last - first) over them */
+  int64_t span_q_lo;       /* order statistics at floor / floor+1 of */
+  int64_t span_q_hi;       /*   (span_count - 1) * 0.99 (np.percentile) */
+  int64_t incomplete;      /* vertices not COMPLETED */
+  int64_t first_incomplete[16];
+  int64_t cold_bytes_read;
+  int64_t cold_bytes_written;
+  int32_t fast_path;       /* 1: control plane proved eviction-free */
+  int32_t pad_;
+} atlas_layer_metrics;
+
+const char* atlas_last_error(void);
+int atlas_abi_version(void);
+
+/* ---- topology ------------------------------------------------------- */
+int atlas_graph_create(int32_t device, int64_t num_vertices,
+                       int64_t num_edges, const int64_t* offsets_host,
+                       const uint32_t* neighbors_host,
+                       const uint32_t* in_degrees_host, int64_t dst_lo,
+                       int64_t dst_hi, void* stream, atlas_graph** out);
+void atlas_graph_destroy(atlas_graph* g);
+/* device pointers of the CSC view (csc_ptr int64[nloc+1], csc_src u32) */
+int atlas_graph_csc(const atlas_graph* g, const int64_t** csc_ptr,
+                    const uint32_t** csc_src, int64_t* num_local_edges);
+
+/* ---- one layer ------------------------------------------------------ */
+int atlas_layer_create(const atlas_layer_desc* desc,
+                       const uint32_t* in_degrees_host, void* stream,
+                       atlas_layer** out);
+void atlas_layer_destroy(atlas_layer* layer);
+
+/* process_chunk: rows (n x embed_dim, dtype) and the chunk CSR slice are
+ * HOST pointers (pinned or pageable); the library stages them to HBM. */
+int atlas_chunk_submit(atlas_layer* layer, int64_t start, int64_t end,
+                       const void* rows_host, int32_t dtype,
+                       const int64_t* local_offsets_host,
+                       const int64_t* neighbors_host, int64_t num_edges,
+                       void* stream);
+/* graduations of the last submitted chunk, in reference order.
+ * ids/rows/batch_len may be NULL to query counts only. */
+int atlas_chunk_graduated(atlas_layer* layer, int64_t* ids, float* rows,
+                          int64_t cap, int64_t* count, int64_t* batch_len,
+                          int64_t batch_cap, int64_t* num_batches);
+
+/* whole layer over a resident input x (device pointer, V rows of
+ * embed_dim, leading dimension ldx) with the reference chunk plan of
+ * chunk_rows rows per chunk. Aggregation records land in the layer's
+ * device accumulator (atlas_layer_accumulator). */
+int atlas_layer_run_resident(atlas_layer* layer, const atlas_graph* graph,
+                             const void* x_dev, int32_t dtype, int64_t ldx,
+                             int64_t chunk_rows, void* stream);
+int atlas_layer_accumulator(atlas_layer* layer, float** acc_dev,
+                            int64_t* ld);
+
+/* y = act(x . W^T + b); x (rows x k, f32, ldx), W (n x k, f32), b (n). */
+int atlas_transform(int32_t backend, const float* x_dev, int64_t rows,
+                    int64_t k, int64_t ldx, const float* w_dev,
+                    const float* b_dev, int64_t n, int32_t relu, void* y_dev,
+                    int32_t y_dtype, int64_t ldy, void* stream);
+
+int atlas_layer_finish(atlas_layer* layer, atlas_layer_metrics* out);
+/* per-chunk reload and touched counters (for mean_reload_pct) */
+int atlas_layer_chunk_stats(atlas_layer* layer, int64_t* reloads,
+                            int64_t* touched, int64_t cap, int64_t* count);
+/* flattened log [len, v0, v1, ..., len, ...]; victims within an event are
+ * ordered like PendingBucketHeap.pop_min (key, then arrival) */
+int atlas_layer_log(atlas_layer* layer, int32_t which, int64_t* out,
+                    int64_t cap, int64_t* count);
+
+/* number of kernels this library launched since load (evidence counter) */
+int64_t atlas_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATLAS_B200_H */

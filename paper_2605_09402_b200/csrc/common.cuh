@@ -1,0 +1,106 @@
+// Shared helpers for the sm_100a engine library (libatlas_b200.so).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/atlas_b200.h"
+
+namespace atlas {
+
+// Thread-local last error string returned by atlas_last_error().
+void set_error(const std::string& msg);
+
+struct Status {
+  int code = ATLAS_OK;
+  std::string msg;
+};
+
+// Thrown inside the library, converted to a status code at the C-ABI edge.
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) {
+  throw Error{code, msg};
+}
+
+#define ATLAS_CUDA(expr)                                                    \
+  do {                                                                      \
+    cudaError_t e_ = (expr);                                                \
+    if (e_ != cudaSuccess)                                                  \
+      ::atlas::fail(ATLAS_EDEVICE, std::string(#expr) + ": " +             \
+                                       cudaGetErrorString(e_) + " at " +    \
+                                       __FILE__ + ":" +                     \
+                                       std::to_string(__LINE__));          \
+  } while (0)
+
+#define ATLAS_LAUNCH_CHECK() ATLAS_CUDA(cudaGetLastError())
+
+constexpr int kWarp = 32;
+constexpr int kNumSMs = 148;
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Device buffer owned by a handle (RAII, no torch types).
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t count = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    count = 0;
+  }
+  void alloc(size_t n) {
+    if (n == count && ptr) return;
+    release();
+    if (n == 0) return;
+    ATLAS_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+    count = n;
+  }
+  // grow-only reallocation (contents not preserved)
+  void reserve(size_t n) {
+    if (n > count) alloc(n);
+  }
+  size_t bytes() const { return count * sizeof(T); }
+};
+
+template <typename T>
+struct PinnedBuf {
+  T* ptr = nullptr;
+  size_t count = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (ptr) cudaFreeHost(ptr);
+  }
+  void reserve(size_t n) {
+    if (n <= count) return;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    ATLAS_CUDA(cudaMallocHost(&ptr, n * sizeof(T)));
+    count = n;
+  }
+};
+
+// --- device helpers --------------------------------------------------------
+
+__device__ __forceinline__ float to_f32(float x) { return x; }
+__device__ __forceinline__ float to_f32(__half x) { return __half2float(x); }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 x) {
+  return __bfloat162float(x);
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+}  // namespace atlas

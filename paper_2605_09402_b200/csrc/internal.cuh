@@ -1,0 +1,170 @@
+// Handle layouts and launcher declarations shared by the .cu files.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+struct atlas_graph {
+  int device = 0;
+  int64_t V = 0;        // whole-graph vertices
+  int64_t E = 0;        // whole-graph edges
+  int64_t lo = 0, hi = 0;
+  int64_t nloc = 0;     // hi - lo
+  int64_t eloc = 0;     // edges with dst in [lo, hi)
+  atlas::DevBuf<int64_t> offsets;   // CSR offsets of the whole graph (V+1)
+  atlas::DevBuf<int64_t> csc_ptr;   // nloc + 1
+  atlas::DevBuf<uint32_t> csc_src;  // eloc, source id (global), ascending per dst
+  atlas::DevBuf<uint32_t> csc_eid;  // eloc, CSR edge index of the entry
+  atlas::DevBuf<uint32_t> indeg;    // nloc
+};
+
+namespace atlas {
+
+// Exact single-CTA control engine state (control.cu). Plain device arrays.
+struct EngineState {
+  // per local vertex
+  uint32_t* pending;
+  uint8_t* state;
+  uint32_t* seq;
+  int32_t* slot_of;
+  uint8_t* unique_reloaded;
+  // hot set
+  int32_t* hot_list;   // slot -> local vertex or -1
+  int32_t* free_stack; // LIFO of free slots
+  // scratch (size >= slot_count + 1024)
+  int32_t* scratch_a;
+  int32_t* scratch_b;
+  // RND policy
+  int32_t* rnd_members;
+  int32_t* rnd_pos;
+  // logs (record_log): victims as (vertex, key) pairs, others as vertices
+  int64_t* log_victims;  // pairs
+  int64_t* log_reloads;
+  int64_t* log_grad;
+  int64_t log_cap;
+  // current-chunk graduation list (operator path)
+  int32_t* chunk_grad;
+  int64_t* chunk_grad_batches;
+  // scalars live in EngineScalars (device memory)
+};
+
+struct EngineScalars {
+  int64_t free_top;
+  int64_t hot_pop;
+  uint64_t seq_ctr;
+  int64_t messages, evictions, reloads, admissions, graduations, hot_peak;
+  int64_t log_victims_n, log_reloads_n, log_grad_n;
+  int64_t chunk_grad_n, chunk_grad_batches_n;
+  int64_t chunk_index;  // chunks processed so far
+  uint64_t rng_state_hi, rng_state_lo, rng_inc_hi, rng_inc_lo;
+  int32_t rng_has32;
+  uint32_t rng_u32;
+  int64_t rnd_n;
+  int32_t err;          // ATLAS_* code
+  int64_t err_info[4];
+};
+
+struct EngineConfig {
+  int64_t lo, hi, nloc;
+  int64_t slot_count, evict_batch, sub_batch;
+  int32_t model, policy, record_log;
+};
+
+}  // namespace atlas
+
+struct atlas_layer {
+  atlas_layer_desc desc{};
+  int64_t nloc = 0;
+  int64_t sub_batch = 1, evict_batch = 1;
+  cudaStream_t stream = nullptr;  // default launch stream for internal work
+  atlas::DevBuf<uint32_t> indeg;  // local in-degrees
+  // data plane
+  atlas::DevBuf<float> acc;       // nloc x agg_dim
+  atlas::DevBuf<uint8_t> touched; // first-touch flags (chunk path)
+  // control plane
+  atlas::DevBuf<uint32_t> pending;
+  atlas::DevBuf<uint8_t> state;
+  atlas::DevBuf<uint32_t> seq;
+  atlas::DevBuf<int32_t> slot_of;
+  atlas::DevBuf<uint8_t> unique_reloaded;
+  atlas::DevBuf<int32_t> hot_list, free_stack, scratch_a, scratch_b;
+  atlas::DevBuf<int32_t> rnd_members, rnd_pos;
+  atlas::DevBuf<int64_t> log_victims, log_reloads, log_grad;
+  atlas::DevBuf<int32_t> chunk_grad;
+  atlas::DevBuf<int64_t> chunk_grad_batches;
+  atlas::DevBuf<atlas::EngineScalars> scalars;
+  atlas::DevBuf<int64_t> first_pos, last_pos;  // spans (per local vertex)
+  std::vector<int64_t> chunk_reloads, chunk_touched;
+  bool engine_initialized = false;
+  bool fast_path = false;
+  bool spans_host_done = false;
+  int64_t chunks_seen = 0;
+  int64_t stream_step = 0;  // global stream position counter (operator path)
+  // staging for the operator path
+  atlas::DevBuf<uint8_t> tile;          // chunk rows on device
+  atlas::DevBuf<int64_t> ch_offsets;    // n+1
+  atlas::DevBuf<int64_t> ch_nbrs;       // m
+  atlas::DevBuf<uint8_t> sort_tmp;
+  atlas::DevBuf<uint32_t> keys_a, keys_b, vals_a, vals_b;
+  atlas::DevBuf<uint64_t> runs;
+  atlas::DevBuf<int64_t> run_beg;
+  atlas::DevBuf<uint32_t> run_dst, ent_src;
+  atlas::DevBuf<int64_t> misc64;
+  atlas::DevBuf<float> grad_rows;
+  atlas::PinnedBuf<int64_t> pin64;
+  atlas::PinnedBuf<atlas::EngineScalars> pin_scalars;
+  // fast-path metrics
+  int64_t span_count = 0, span_sum = 0, span_q_lo = 0, span_q_hi = 0;
+  int64_t fp_hot_peak = 0;
+};
+
+namespace atlas {
+
+// graph.cu
+void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs_dev,
+               const uint32_t* indeg_host, cudaStream_t s);
+
+// aggregate.cu
+void launch_agg_resident(const atlas_graph* g, const void* x, int dtype,
+                         int64_t ldx, int model, float gin_epsilon, int d,
+                         float* acc, int64_t ldacc, cudaStream_t s);
+void launch_agg_runs(const void* tile, int dtype, int64_t ldx,
+                     int64_t tile_lo, const uint32_t* run_dst,
+                     const int64_t* run_beg, int64_t nruns,
+                     const uint32_t* ent_src, const uint32_t* indeg,
+                     int model, float gin_epsilon, int d, float* acc,
+                     int64_t ldacc, uint8_t* touched, cudaStream_t s);
+void launch_sage_self(const void* tile, int dtype, int64_t ldx,
+                      int64_t row0, int64_t nrows, int d, float* acc_rows,
+                      int64_t ldacc, cudaStream_t s);
+void launch_gather_rows(const float* acc, int64_t ldacc, const int32_t* ids,
+                        int64_t n, int64_t width, float* out, cudaStream_t s);
+
+// transform.cu
+void launch_transform_stable(const float* x, int64_t rows, int64_t k,
+                             int64_t ldx, const float* w, const float* b,
+                             int64_t n, int relu, void* y, int y_dtype,
+                             int64_t ldy, cudaStream_t s);
+bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
+                         const float* w, const float* b, int64_t n, int relu,
+                         void* y, int y_dtype, int64_t ldy, cudaStream_t s);
+
+// control.cu
+void engine_init(atlas_layer* L, cudaStream_t s);
+void engine_run_chunks(atlas_layer* L, const uint64_t* runs,
+                       const int64_t* run_off, const int64_t* chunk_bounds,
+                       int64_t nchunks, const int64_t* host_run_off,
+                       cudaStream_t s);
+void resident_control(atlas_layer* L, const atlas_graph* g,
+                      int64_t chunk_rows, cudaStream_t s);
+void chunk_spans(atlas_layer* L, int64_t start, int64_t end,
+                 const int64_t* offsets_dev, const int64_t* nbrs_dev,
+                 int64_t m, cudaStream_t s);
+void finish_spans(atlas_layer* L, cudaStream_t s);
+void check_engine_error(atlas_layer* L, cudaStream_t s);
+
+// launch accounting
+void count_launch(int n = 1);
+
+}  // namespace atlas

@@ -1,0 +1,237 @@
+"""Regenerate tests/golden/*.json|npz by running the UNMODIFIED reference.
+
+Run here (the container holding /root/reference):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports ``oocgnn`` read-only from /root/reference/pkg/src, runs
+``run_inference`` and the ``init_layer/process_chunk/finalize_layer``
+operator triple on the cases below, and records:
+
+* per-layer engine outputs (full arrays for small cases, sha256 otherwise);
+* per-layer metrics (every CSV column except wall time, plus hot_peak);
+* the integer event log: victims of every eviction, every reload batch and
+  every graduation batch, captured by wrapping the reference's policy,
+  ``MemoryManager._reload_batch`` and ``orchestrator._graduate``;
+* the reference's float64 ``oracle_inference`` output.
+
+The GPU box has no /root/reference, so these files are what the GPU
+parity tests compare against.
+"""
+
+import hashlib
+import json
+import sys
+import tempfile
+from pathlib import Path
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+import oocgnn.memstore as mem  # noqa: E402
+import oocgnn.orchestrator as orch  # noqa: E402
+import oocgnn.runtime as rt  # noqa: E402
+from oocgnn.iostats import IOCounters  # noqa: E402
+from oocgnn.chunks import Chunk, plan_chunks  # noqa: E402
+from oocgnn.oracle import oracle_inference  # noqa: E402
+from oocgnn.storage import (  # noqa: E402
+    ModelKind, edges_to_csr, generate_synthetic, load_layer_matrix,
+    random_weights, read_csr, write_csr, write_matrix_as_layer)
+
+OUT = Path(__file__).resolve().parent
+
+
+def digest_array(a) -> str:
+    a = np.ascontiguousarray(a)
+    h = hashlib.sha256()
+    h.update(str(a.dtype).encode() + str(a.shape).encode())
+    h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def flatten_events(events) -> np.ndarray:
+    """[[a,b],[c]] -> int64 [2,a,b,1,c]."""
+    out = []
+    for ev in events:
+        out.append(len(ev))
+        out.extend(int(x) for x in ev)
+    return np.asarray(out, dtype=np.int64)
+
+
+class Recorder:
+    """Wraps the reference's hooks; one log per layer."""
+
+    def __init__(self):
+        self.layers = []
+
+    def new_layer(self):
+        self.layers.append({"victims": [], "reloads": [], "graduated": []})
+
+    @property
+    def cur(self):
+        return self.layers[-1]
+
+
+REC = Recorder()
+_make_policy = mem.make_policy
+_reload = mem.MemoryManager._reload_batch
+_graduate = orch._graduate
+_run_layer = rt.run_layer
+
+
+def traced_make_policy(name, max_pending, seed):
+    pol = _make_policy(name, max_pending, seed)
+    choose = pol.choose_victims
+
+    def wrapped(k):
+        got = choose(k)
+        REC.cur["victims"].append(list(got))
+        return got
+    pol.choose_victims = wrapped
+    return pol
+
+
+def traced_reload(self, vertices):
+    REC.cur["reloads"].append(np.asarray(vertices).tolist())
+    return _reload(self, vertices)
+
+
+def traced_graduate(ctx, vertices, sink):
+    REC.cur["graduated"].append(np.asarray(vertices).tolist())
+    return _graduate(ctx, vertices, sink)
+
+
+def traced_run_layer(*a, **k):
+    REC.new_layer()
+    return _run_layer(*a, **k)
+
+
+mem.make_policy = traced_make_policy
+orch.make_policy = traced_make_policy
+mem.MemoryManager._reload_batch = traced_reload
+orch._graduate = traced_graduate
+rt.run_layer = traced_run_layer
+
+
+METRIC_FIELDS = ["messages", "evictions", "reloads", "unique_reloads",
+                 "mean_span", "p99_span", "mean_reload_pct", "hot_peak",
+                 "hot_slot_count"]
+
+
+def fig2_dataset(root):
+    edges = [(0, 1), (0, 3), (2, 3), (4, 1), (4, 3)]
+    g = edges_to_csr(np.array([e[0] for e in edges]),
+                     np.array([e[1] for e in edges]), 6)
+    feats = np.random.default_rng(3).uniform(-1, 1, (6, 8)).astype(np.float32)
+    d = root / "fig2"
+    write_csr(g, d)
+    write_matrix_as_layer(d / "features", feats)
+    return d
+
+
+DATASETS = {
+    # name: (kind, V, degree, dim, seed, dtype)
+    "small": ("uniform", 2000, 6, 8, 3, "f32"),
+    "uniform": ("uniform", 10_000, 10, 32, 7, "f32"),
+    "pa": ("pa", 100_000, 10, 64, 12, "f32"),
+    "cfg1": ("uniform", 100_000, 10, 128, 7, "f32"),
+    "half": ("uniform", 4000, 8, 16, 11, "f16"),
+}
+
+SMALL_CFG = dict(hot_budget=1 << 20, chunk_budget=64 << 10,
+                 graduation_budget=256 << 10, spill_buffer=256 << 10,
+                 partitions=3, queue_capacity=4)
+
+# (case id, dataset, model, dims, weight seed, eps, gain, config, full)
+CASES = []
+for kind in ModelKind:
+    eps = 0.1 if kind == ModelKind.GIN else 0.0
+    gain = 0.15 if kind == ModelKind.GIN else 1.0
+    CASES.append((f"fig2_{kind.cli_name}", "fig2", kind, [8, 4, 2], 5, eps,
+                  gain, {}, True))
+    CASES.append((f"small_{kind.cli_name}", "small", kind, [8, 4, 2], 5, eps,
+                  1.0, dict(SMALL_CFG), True))
+    CASES.append((f"small_{kind.cli_name}_tight", "small", kind, [8, 4, 2],
+                  5, eps, 1.0, dict(SMALL_CFG, chunk_budget=4096,
+                                    hot_slots=32), True))
+    CASES.append((f"uniform_{kind.cli_name}", "uniform", kind, [32, 16, 8],
+                  5, eps, gain, {}, False))
+    CASES.append((f"uniform_{kind.cli_name}_slots500", "uniform", kind,
+                  [32, 16, 8], 5, eps, gain,
+                  dict(hot_slots=500, chunk_budget=4096 * 32 * 4), False))
+    CASES.append((f"half_{kind.cli_name}_slots300", "half", kind,
+                  [16, 8, 4], 5, eps, gain,
+                  dict(hot_slots=300, chunk_budget=16 << 10), False))
+for pol in ("minpend", "lru", "rnd"):
+    CASES.append((f"pa_gcn_{pol}_5pct", "pa", ModelKind.GCN, [64, 32, 16], 5,
+                  0.0, 1.0, dict(hot_slots=5000, eviction=pol, seed=1), False))
+CASES.append(("pa_sage_10pct", "pa", ModelKind.SAGE, [64, 32, 16], 5, 0.0,
+              1.0, dict(hot_slots=10_000), False))
+CASES.append(("cfg1_sage", "cfg1", ModelKind.SAGE, [128, 128, 128], 5, 0.0,
+              1.0, dict(chunk_budget=64 << 20, hot_slots=100_000), False))
+CASES.append(("cfg1_sage_10pct", "cfg1", ModelKind.SAGE, [128, 128, 128], 5,
+              0.0, 1.0, dict(chunk_budget=1 << 20, hot_slots=10_000), False))
+
+
+def main(only=None):
+    work = Path(tempfile.mkdtemp(prefix="golden_"))
+    ds_dirs = {"fig2": fig2_dataset(work)}
+    manifest = {}
+    for case, ds, kind, dims, wseed, eps, gain, cfg, full in CASES:
+        if only and case not in only:
+            continue
+        if ds not in ds_dirs:
+            gk, v, deg, dim, seed, dt = DATASETS[ds]
+            ds_dirs[ds] = work / ds
+            generate_synthetic(gk, v, deg, dim, seed, ds_dirs[ds], dtype=dt)
+        weights = random_weights(kind, dims, wseed, gin_epsilon=eps,
+                                 gain=gain)
+        REC.layers.clear()
+        out = work / f"run_{case}"
+        report = rt.run_inference(ds_dirs[ds], weights,
+                                  rt.PipelineConfig(**cfg), out)
+        graph = read_csr(ds_dirs[ds])
+        feats = load_layer_matrix(ds_dirs[ds] / "features")
+        ref64 = oracle_inference(graph, feats, weights, memory_cap=16 << 30)
+        entry = {"dataset": ds, "model": int(kind), "dims": dims,
+                 "weight_seed": wseed, "gin_epsilon": eps, "gain": gain,
+                 "config": cfg, "layers": []}
+        arrays = {}
+        for l, m in enumerate(report.layers):
+            y = load_layer_matrix(out / f"layer_{l}")
+            log = REC.layers[l]
+            lay = {f: getattr(m, f) for f in METRIC_FIELDS}
+            lay["output_sha"] = digest_array(y)
+            for key in ("victims", "reloads", "graduated"):
+                flat = flatten_events(log[key])
+                lay[f"{key}_sha"] = digest_array(flat)
+                lay[f"{key}_events"] = len(log[key])
+                if full:
+                    arrays[f"L{l}_{key}"] = flat
+            if full:
+                arrays[f"L{l}_out"] = y
+            entry["layers"].append(lay)
+        entry["oracle64_sha"] = digest_array(ref64)
+        arrays["oracle64"] = ref64 if full else ref64[:64]
+        entry["oracle64_absmax"] = float(np.abs(ref64).max())
+        manifest[case] = entry
+        np.savez_compressed(OUT / f"{case}.npz", **arrays)
+        print(case, [(l["messages"], l["evictions"], l["reloads"])
+                     for l in entry["layers"]], flush=True)
+    # operator-triple chunk plans (oocgnn/chunks.py:36-48)
+    plans = {f"{v}_{d}_{t}_{b}": plan_chunks(v, d, t, b) for v, d, t, b in
+             [(10, 4, "f32", 64), (10, 4, "f16", 64), (7, 3, "f32", 1),
+              (0, 8, "f32", 64), (2_400_000, 100, "f32", 8 << 20),
+              (2_400_000, 128, "f32", 8 << 20)]}
+    manifest["_plans"] = {k: [len(p), p[:3], p[-1:]] for k, p in plans.items()}
+    manifest["_datasets"] = DATASETS
+    path = OUT / "golden.json"
+    old = json.loads(path.read_text()) if (only and path.exists()) else {}
+    old.update(manifest)
+    path.write_text(json.dumps(old, indent=1, sort_keys=True))
+
+
+if __name__ == "__main__":
+    main(set(sys.argv[1:]) or None)
