@@ -40,6 +40,12 @@ extern "C" {
 
 #define ATLAS_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define ATLAS_API __attribute__((visibility("default")))
+#else
+#define ATLAS_API
+#endif
+
 enum {
   ATLAS_OK = 0,
   ATLAS_ECONFIG = -1,      /* ConfigError */
@@ -101,36 +107,36 @@ typedef struct {
   int32_t pad_;
 } atlas_layer_metrics;
 
-const char* atlas_last_error(void);
-int atlas_abi_version(void);
+ATLAS_API const char* atlas_last_error(void);
+ATLAS_API int atlas_abi_version(void);
 
 /* ---- topology ------------------------------------------------------- */
-int atlas_graph_create(int32_t device, int64_t num_vertices,
+ATLAS_API int atlas_graph_create(int32_t device, int64_t num_vertices,
                        int64_t num_edges, const int64_t* offsets_host,
                        const uint32_t* neighbors_host,
                        const uint32_t* in_degrees_host, int64_t dst_lo,
                        int64_t dst_hi, void* stream, atlas_graph** out);
-void atlas_graph_destroy(atlas_graph* g);
+ATLAS_API void atlas_graph_destroy(atlas_graph* g);
 /* device pointers of the CSC view (csc_ptr int64[nloc+1], csc_src u32) */
-int atlas_graph_csc(const atlas_graph* g, const int64_t** csc_ptr,
+ATLAS_API int atlas_graph_csc(const atlas_graph* g, const int64_t** csc_ptr,
                     const uint32_t** csc_src, int64_t* num_local_edges);
 
 /* ---- one layer ------------------------------------------------------ */
-int atlas_layer_create(const atlas_layer_desc* desc,
+ATLAS_API int atlas_layer_create(const atlas_layer_desc* desc,
                        const uint32_t* in_degrees_host, void* stream,
                        atlas_layer** out);
-void atlas_layer_destroy(atlas_layer* layer);
+ATLAS_API void atlas_layer_destroy(atlas_layer* layer);
 
 /* process_chunk: rows (n x embed_dim, dtype) and the chunk CSR slice are
  * HOST pointers (pinned or pageable); the library stages them to HBM. */
-int atlas_chunk_submit(atlas_layer* layer, int64_t start, int64_t end,
+ATLAS_API int atlas_chunk_submit(atlas_layer* layer, int64_t start, int64_t end,
                        const void* rows_host, int32_t dtype,
                        const int64_t* local_offsets_host,
                        const int64_t* neighbors_host, int64_t num_edges,
                        void* stream);
 /* graduations of the last submitted chunk, in reference order.
  * ids/rows/batch_len may be NULL to query counts only. */
-int atlas_chunk_graduated(atlas_layer* layer, int64_t* ids, float* rows,
+ATLAS_API int atlas_chunk_graduated(atlas_layer* layer, int64_t* ids, float* rows,
                           int64_t cap, int64_t* count, int64_t* batch_len,
                           int64_t batch_cap, int64_t* num_batches);
 
@@ -138,29 +144,39 @@ int atlas_chunk_graduated(atlas_layer* layer, int64_t* ids, float* rows,
  * embed_dim, leading dimension ldx) with the reference chunk plan of
  * chunk_rows rows per chunk. Aggregation records land in the layer's
  * device accumulator (atlas_layer_accumulator). */
-int atlas_layer_run_resident(atlas_layer* layer, const atlas_graph* graph,
+ATLAS_API int atlas_layer_run_resident(atlas_layer* layer, const atlas_graph* graph,
                              const void* x_dev, int32_t dtype, int64_t ldx,
                              int64_t chunk_rows, void* stream);
-int atlas_layer_accumulator(atlas_layer* layer, float** acc_dev,
+ATLAS_API int atlas_layer_accumulator(atlas_layer* layer, float** acc_dev,
                             int64_t* ld);
 
 /* y = act(x . W^T + b); x (rows x k, f32, ldx), W (n x k, f32), b (n). */
-int atlas_transform(int32_t backend, const float* x_dev, int64_t rows,
+ATLAS_API int atlas_transform(int32_t backend, const float* x_dev, int64_t rows,
                     int64_t k, int64_t ldx, const float* w_dev,
                     const float* b_dev, int64_t n, int32_t relu, void* y_dev,
                     int32_t y_dtype, int64_t ldy, void* stream);
 
-int atlas_layer_finish(atlas_layer* layer, atlas_layer_metrics* out);
+ATLAS_API int atlas_layer_finish(atlas_layer* layer, atlas_layer_metrics* out);
 /* per-chunk reload and touched counters (for mean_reload_pct) */
-int atlas_layer_chunk_stats(atlas_layer* layer, int64_t* reloads,
+ATLAS_API int atlas_layer_chunk_stats(atlas_layer* layer, int64_t* reloads,
                             int64_t* touched, int64_t cap, int64_t* count);
 /* flattened log [len, v0, v1, ..., len, ...]; victims within an event are
  * ordered like PendingBucketHeap.pop_min (key, then arrival) */
-int atlas_layer_log(atlas_layer* layer, int32_t which, int64_t* out,
+ATLAS_API int atlas_layer_log(atlas_layer* layer, int32_t which, int64_t* out,
                     int64_t cap, int64_t* count);
 
+/* copies of the per-vertex control state of the layer's range
+ * (pending u32, lifecycle u8 0..3, first/last step int64); NULL skips */
+ATLAS_API int atlas_layer_state(atlas_layer* layer, uint32_t* pending, uint8_t* state,
+                      int64_t* first_step, int64_t* last_step);
+
+/* device time (CUDA events on the launching stream) of the last
+ * atlas_layer_run_resident: [0] scatter-aggregate kernel, [1] control
+ * plane (walk + optional exact replay), in milliseconds */
+ATLAS_API int atlas_layer_timing(atlas_layer* layer, float* ms, int32_t n);
+
 /* number of kernels this library launched since load (evidence counter) */
-int64_t atlas_kernel_launches(void);
+ATLAS_API int64_t atlas_kernel_launches(void);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,390 @@
+// Broadcast scatter-aggregate (kernel plan K3/K4 of SURVEY.md §2.1).
+//
+// Reference semantics (oocgnn/orchestrator.py:262-268, :186-191): every
+// addend is m = h_u / max(1, d_in(v)) for the mean models (GCN, SAGE) or
+// m = h_u for GIN (its own self term is (1 + eps) * h_v), rounded to f32,
+// and np.add.at applies the addends of one destination in stream
+// (source-major) order onto a zeroed f32 record. Here each warp owns one
+// destination and a 32*VEC column slice of its record; lanes walk the
+// destination's sources in ascending order and apply exactly the same
+// rounded f32 divide and add per column (__fdiv_rn / __fadd_rn, no FMA
+// contraction), so records are bit-identical to the reference for ANY
+// chunking. Parallelism is over destinations and columns; memory-level
+// parallelism comes from issuing UNROLL independent 16-byte row loads per
+// lane before the dependent adds.
+//
+// Two front ends share the inner loop:
+//  * resident: the whole layer input is in HBM; destinations are walked
+//    through the CSC view (graph.cu) in one pass and each record is
+//    written once (no read-modify-write). GIN's self term is inserted
+//    before the first source >= v, which is its stream position.
+//  * runs: one caller-supplied chunk tile; destination runs come from the
+//    per-chunk stable sort (chunk.cu); a record is read back only if an
+//    earlier chunk already touched it.
+#include "internal.cuh"
+
+namespace atlas {
+namespace {
+
+constexpr int kUnroll = 8;
+constexpr uint32_t kSelfBit = 0x80000000u;
+
+// 16-byte (or narrower) raw row fragment of VEC elements.
+template <typename T, int VEC>
+struct Frag {
+  static constexpr int kBytes = VEC * sizeof(T);
+  using Raw = typename std::conditional<
+      kBytes == 16, uint4,
+      typename std::conditional<
+          kBytes == 8, uint2,
+          typename std::conditional<kBytes == 4, uint32_t,
+                                    uint16_t>::type>::type>::type;
+  Raw raw;
+  __device__ __forceinline__ void load(const T* p) {
+    raw = __ldg(reinterpret_cast<const Raw*>(p));
+  }
+  __device__ __forceinline__ float get(int e) const {
+    const T* t = reinterpret_cast<const T*>(&raw);
+    return to_f32(t[e]);
+  }
+};
+
+template <int VEC>
+__device__ __forceinline__ void store_f32(float* p, const float (&a)[VEC]) {
+  if constexpr (VEC % 4 == 0) {
+#pragma unroll
+    for (int e = 0; e < VEC; e += 4)
+      *reinterpret_cast<float4*>(p + e) =
+          make_float4(a[e], a[e + 1], a[e + 2], a[e + 3]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; e++) p[e] = a[e];
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void load_f32(const float* p, float (&a)[VEC]) {
+  if constexpr (VEC % 4 == 0) {
+#pragma unroll
+    for (int e = 0; e < VEC; e += 4) {
+      float4 t = *reinterpret_cast<const float4*>(p + e);
+      a[e] = t.x;
+      a[e + 1] = t.y;
+      a[e + 2] = t.z;
+      a[e + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; e++) a[e] = p[e];
+  }
+}
+
+// a += (self ? m * self_scale : (MEAN ? m / denom : m)), per element.
+template <typename T, int VEC, bool MEAN>
+__device__ __forceinline__ void add_msg(float (&a)[VEC],
+                                        const Frag<T, VEC>& f, bool self,
+                                        float denom, float self_scale) {
+#pragma unroll
+  for (int e = 0; e < VEC; e++) {
+    float m = f.get(e);
+    if (self)
+      m = __fmul_rn(m, self_scale);
+    else if (MEAN)
+      m = __fdiv_rn(m, denom);
+    a[e] = __fadd_rn(a[e], m);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// resident front end: warp per destination, CSC walk
+
+template <typename T, int VEC, int MODEL>
+__global__ void __launch_bounds__(256)
+    agg_resident(const T* __restrict__ x, int64_t ldx,
+                 const int64_t* __restrict__ csc_ptr,
+                 const uint32_t* __restrict__ csc_src,
+                 const uint32_t* __restrict__ indeg, int64_t lo,
+                 int64_t nloc, int d, float* __restrict__ acc,
+                 int64_t ldacc, float self_scale) {
+  constexpr bool kMean = MODEL != ATLAS_GIN;
+  const int lane = threadIdx.x & 31;
+  const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (v >= nloc) return;
+  const int64_t beg = csc_ptr[v], end = csc_ptr[v + 1];
+  const uint32_t vg = (uint32_t)(v + lo);
+  const float denom = kMean ? (float)max(1u, indeg[v]) : 1.0f;
+  float* out = acc + v * ldacc;
+  for (int c0 = 0; c0 < d; c0 += 32 * VEC) {
+    const int col = c0 + lane * VEC;
+    const bool active = col < d;
+    float a[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; e++) a[e] = 0.0f;
+    bool self_pending = MODEL == ATLAS_GIN;
+    for (int64_t base = beg; base < end; base += 32) {
+      const int cnt = (int)((end - base) < 32 ? (end - base) : 32);
+      const uint32_t mine = lane < cnt ? csc_src[base + lane] : 0u;
+      for (int i = 0; i < cnt; i += kUnroll) {
+        Frag<T, VEC> f[kUnroll];
+        uint32_t s[kUnroll];
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++) {
+          s[j] = __shfl_sync(0xffffffffu, mine, (i + j) & 31);
+          if (active && i + j < cnt) f[j].load(x + (int64_t)s[j] * ldx + col);
+        }
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++) {
+          if (i + j < cnt) {
+            if (MODEL == ATLAS_GIN && self_pending && s[j] >= vg) {
+              self_pending = false;
+              if (active) {
+                Frag<T, VEC> me;
+                me.load(x + (int64_t)vg * ldx + col);
+                add_msg<T, VEC, false>(a, me, true, 1.0f, self_scale);
+              }
+            }
+            if (active) add_msg<T, VEC, kMean>(a, f[j], false, denom, 1.0f);
+          }
+        }
+      }
+    }
+    if (MODEL == ATLAS_GIN && self_pending && active) {
+      Frag<T, VEC> me;
+      me.load(x + (int64_t)vg * ldx + col);
+      add_msg<T, VEC, false>(a, me, true, 1.0f, self_scale);
+    }
+    if (active) {
+      store_f32<VEC>(out + col, a);
+      if (MODEL == ATLAS_SAGE) {  // self half: f32 copy of h_v
+        Frag<T, VEC> me;
+        me.load(x + (int64_t)vg * ldx + col);
+        float h[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; e++) h[e] = me.get(e);
+        store_f32<VEC>(out + d + col, h);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// runs front end: warp per (chunk, destination) run
+
+template <typename T, int VEC, int MODEL>
+__global__ void __launch_bounds__(256)
+    agg_runs(const T* __restrict__ tile, int64_t ldx,
+             const uint32_t* __restrict__ run_dst,
+             const int64_t* __restrict__ run_beg, int64_t nruns,
+             const uint32_t* __restrict__ ent_src,
+             const uint32_t* __restrict__ indeg, int d,
+             float* __restrict__ acc, int64_t ldacc,
+             uint8_t* __restrict__ touched, float self_scale) {
+  constexpr bool kMean = MODEL != ATLAS_GIN;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (r >= nruns) return;
+  const uint32_t v = run_dst[r];
+  const int64_t beg = run_beg[r], end = run_beg[r + 1];
+  const float denom = kMean ? (float)max(1u, indeg[v]) : 1.0f;
+  const bool resume = touched[v] != 0;
+  float* out = acc + (int64_t)v * ldacc;
+  for (int c0 = 0; c0 < d; c0 += 32 * VEC) {
+    const int col = c0 + lane * VEC;
+    const bool active = col < d;
+    float a[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; e++) a[e] = 0.0f;
+    if (resume && active) load_f32<VEC>(out + col, a);
+    for (int64_t base = beg; base < end; base += 32) {
+      const int cnt = (int)((end - base) < 32 ? (end - base) : 32);
+      const uint32_t mine = lane < cnt ? ent_src[base + lane] : 0u;
+      for (int i = 0; i < cnt; i += kUnroll) {
+        Frag<T, VEC> f[kUnroll];
+        uint32_t s[kUnroll];
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++) {
+          s[j] = __shfl_sync(0xffffffffu, mine, (i + j) & 31);
+          if (active && i + j < cnt)
+            f[j].load(tile + (int64_t)(s[j] & ~kSelfBit) * ldx + col);
+        }
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++)
+          if (active && i + j < cnt)
+            add_msg<T, VEC, kMean>(a, f[j], (s[j] & kSelfBit) != 0, denom,
+                                   self_scale);
+      }
+    }
+    if (active) store_f32<VEC>(out + col, a);
+  }
+  if (lane == 0) touched[v] = 1;
+}
+
+template <typename T>
+__global__ void sage_self_rows(const T* __restrict__ tile, int64_t ldx,
+                               int64_t nrows, int d, float* __restrict__ out,
+                               int64_t ldacc) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.y + threadIdx.y;
+  if (i >= nrows) return;
+  for (int c = threadIdx.x; c < d; c += blockDim.x)
+    out[i * ldacc + c] = to_f32(tile[i * ldx + c]);
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ acc,
+                                   int64_t ldacc,
+                                   const int32_t* __restrict__ ids, int64_t n,
+                                   int64_t width, float* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.y + threadIdx.y;
+  if (i >= n) return;
+  const float* src = acc + (int64_t)ids[i] * ldacc;
+  for (int64_t c = threadIdx.x; c < width; c += blockDim.x)
+    out[i * width + c] = src[c];
+}
+
+template <typename T>
+int pick_vec(int d, int64_t ldx) {
+  if (sizeof(T) == 4) return (d % 4 == 0 && ldx % 4 == 0) ? 4 : 1;
+  if (d % 8 == 0 && ldx % 8 == 0) return 8;
+  if (d % 2 == 0 && ldx % 2 == 0) return 2;
+  return 1;
+}
+
+template <typename T, int VEC>
+void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
+                    float eps1, int d, float* acc, int64_t ldacc,
+                    cudaStream_t s) {
+  const int64_t blocks = ceil_div(g->nloc, 8);
+  if (blocks == 0) return;
+  auto go = [&](auto kern) {
+    kern<<<(unsigned)blocks, 256, 0, s>>>(x, ldx, g->csc_ptr.ptr,
+                                          g->csc_src.ptr, g->indeg.ptr, g->lo,
+                                          g->nloc, d, acc, ldacc, eps1);
+  };
+  if (model == ATLAS_GCN) go(agg_resident<T, VEC, ATLAS_GCN>);
+  else if (model == ATLAS_SAGE) go(agg_resident<T, VEC, ATLAS_SAGE>);
+  else go(agg_resident<T, VEC, ATLAS_GIN>);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+}
+
+template <typename T>
+void resident_typed(const atlas_graph* g, const void* x, int64_t ldx,
+                    int model, float eps1, int d, float* acc, int64_t ldacc,
+                    cudaStream_t s) {
+  const T* xt = static_cast<const T*>(x);
+  int vec = pick_vec<T>(d, ldx);
+  if (vec > 1 && ldacc % 4 != 0) vec = 1;
+  if (sizeof(T) == 4) {
+    if (vec == 4) resident_model<T, 4>(g, xt, ldx, model, eps1, d, acc, ldacc, s);
+    else resident_model<T, 1>(g, xt, ldx, model, eps1, d, acc, ldacc, s);
+  } else {
+    if (vec == 8) resident_model<T, 8>(g, xt, ldx, model, eps1, d, acc, ldacc, s);
+    else if (vec == 2) resident_model<T, 2>(g, xt, ldx, model, eps1, d, acc, ldacc, s);
+    else resident_model<T, 1>(g, xt, ldx, model, eps1, d, acc, ldacc, s);
+  }
+}
+
+template <typename T, int VEC>
+void runs_model(const T* tile, int64_t ldx, const uint32_t* run_dst,
+                const int64_t* run_beg, int64_t nruns, const uint32_t* ent,
+                const uint32_t* indeg, int model, float eps1, int d,
+                float* acc, int64_t ldacc, uint8_t* touched, cudaStream_t s) {
+  const int64_t blocks = ceil_div(nruns, 8);
+  if (blocks == 0) return;
+  auto go = [&](auto kern) {
+    kern<<<(unsigned)blocks, 256, 0, s>>>(tile, ldx, run_dst, run_beg, nruns,
+                                          ent, indeg, d, acc, ldacc, touched,
+                                          eps1);
+  };
+  if (model == ATLAS_GCN) go(agg_runs<T, VEC, ATLAS_GCN>);
+  else if (model == ATLAS_SAGE) go(agg_runs<T, VEC, ATLAS_SAGE>);
+  else go(agg_runs<T, VEC, ATLAS_GIN>);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+}
+
+template <typename T>
+void runs_typed(const void* tile, int64_t ldx, const uint32_t* run_dst,
+                const int64_t* run_beg, int64_t nruns, const uint32_t* ent,
+                const uint32_t* indeg, int model, float eps1, int d,
+                float* acc, int64_t ldacc, uint8_t* touched, cudaStream_t s) {
+  const T* t = static_cast<const T*>(tile);
+  int vec = pick_vec<T>(d, ldx);
+  if (vec > 1 && ldacc % 4 != 0) vec = 1;
+  if (sizeof(T) == 4) {
+    if (vec == 4) runs_model<T, 4>(t, ldx, run_dst, run_beg, nruns, ent, indeg, model, eps1, d, acc, ldacc, touched, s);
+    else runs_model<T, 1>(t, ldx, run_dst, run_beg, nruns, ent, indeg, model, eps1, d, acc, ldacc, touched, s);
+  } else {
+    if (vec == 8) runs_model<T, 8>(t, ldx, run_dst, run_beg, nruns, ent, indeg, model, eps1, d, acc, ldacc, touched, s);
+    else if (vec == 2) runs_model<T, 2>(t, ldx, run_dst, run_beg, nruns, ent, indeg, model, eps1, d, acc, ldacc, touched, s);
+    else runs_model<T, 1>(t, ldx, run_dst, run_beg, nruns, ent, indeg, model, eps1, d, acc, ldacc, touched, s);
+  }
+}
+
+}  // namespace
+
+// numpy: np.float32(1.0) + np.float32(eps), rounded to f32
+static float self_scale_of(float eps) { return 1.0f + eps; }
+
+void launch_agg_resident(const atlas_graph* g, const void* x, int dtype,
+                         int64_t ldx, int model, float gin_epsilon, int d,
+                         float* acc, int64_t ldacc, cudaStream_t s) {
+  const float e1 = self_scale_of(gin_epsilon);
+  if (dtype == ATLAS_F32)
+    resident_typed<float>(g, x, ldx, model, e1, d, acc, ldacc, s);
+  else if (dtype == ATLAS_F16)
+    resident_typed<__half>(g, x, ldx, model, e1, d, acc, ldacc, s);
+  else
+    resident_typed<__nv_bfloat16>(g, x, ldx, model, e1, d, acc, ldacc, s);
+}
+
+void launch_agg_runs(const void* tile, int dtype, int64_t ldx,
+                     int64_t /*tile_lo*/, const uint32_t* run_dst,
+                     const int64_t* run_beg, int64_t nruns,
+                     const uint32_t* ent_src, const uint32_t* indeg,
+                     int model, float gin_epsilon, int d, float* acc,
+                     int64_t ldacc, uint8_t* touched, cudaStream_t s) {
+  const float e1 = self_scale_of(gin_epsilon);
+  if (dtype == ATLAS_F32)
+    runs_typed<float>(tile, ldx, run_dst, run_beg, nruns, ent_src, indeg,
+                      model, e1, d, acc, ldacc, touched, s);
+  else if (dtype == ATLAS_F16)
+    runs_typed<__half>(tile, ldx, run_dst, run_beg, nruns, ent_src, indeg,
+                       model, e1, d, acc, ldacc, touched, s);
+  else
+    runs_typed<__nv_bfloat16>(tile, ldx, run_dst, run_beg, nruns, ent_src,
+                              indeg, model, e1, d, acc, ldacc, touched, s);
+}
+
+void launch_sage_self(const void* tile, int dtype, int64_t ldx, int64_t row0,
+                      int64_t nrows, int d, float* acc_rows, int64_t ldacc,
+                      cudaStream_t s) {
+  if (nrows <= 0) return;
+  dim3 block(32, 8);
+  unsigned grid = (unsigned)ceil_div(nrows, 8);
+  if (dtype == ATLAS_F32)
+    sage_self_rows<float><<<grid, block, 0, s>>>(
+        static_cast<const float*>(tile) + row0 * ldx, ldx, nrows, d, acc_rows,
+        ldacc);
+  else if (dtype == ATLAS_F16)
+    sage_self_rows<__half><<<grid, block, 0, s>>>(
+        static_cast<const __half*>(tile) + row0 * ldx, ldx, nrows, d,
+        acc_rows, ldacc);
+  else
+    sage_self_rows<__nv_bfloat16><<<grid, block, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(tile) + row0 * ldx, ldx, nrows, d,
+        acc_rows, ldacc);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+}
+
+void launch_gather_rows(const float* acc, int64_t ldacc, const int32_t* ids,
+                        int64_t n, int64_t width, float* out, cudaStream_t s) {
+  if (n <= 0) return;
+  dim3 block(32, 8);
+  gather_rows_kernel<<<(unsigned)ceil_div(n, 8), block, 0, s>>>(
+      acc, ldacc, ids, n, width, out);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+}
+
+}  // namespace atlas

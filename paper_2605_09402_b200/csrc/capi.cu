@@ -1,0 +1,412 @@
+// C-ABI edge of libatlas_b200.so (include/atlas_b200.h).
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace atlas {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches += n; }
+
+EngineScalars read_scalars(atlas_layer* L, cudaStream_t s);
+void submit_chunk(atlas_layer* L, int64_t start, int64_t end,
+                  const void* rows_host, int dtype, const int64_t* off_host,
+                  const int64_t* nbrs_host, int64_t m, cudaStream_t s);
+
+template <typename F>
+static int guarded(F f) {
+  try {
+    f();
+    return ATLAS_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(std::string("internal: ") + e.what());
+    return ATLAS_EINVARIANT;
+  }
+}
+
+static void use_device(int dev) { ATLAS_CUDA(cudaSetDevice(dev)); }
+
+}  // namespace atlas
+
+using namespace atlas;
+
+extern "C" {
+
+const char* atlas_last_error(void) { return g_last_error.c_str(); }
+int atlas_abi_version(void) { return ATLAS_ABI_VERSION; }
+int64_t atlas_kernel_launches(void) { return g_launches.load(); }
+
+int atlas_graph_create(int32_t device, int64_t V, int64_t E,
+                       const int64_t* offsets_host,
+                       const uint32_t* neighbors_host,
+                       const uint32_t* in_degrees_host, int64_t lo,
+                       int64_t hi, void* stream, atlas_graph** out) {
+  return guarded([&] {
+    if (!out || V < 0 || E < 0 || lo < 0 || hi < lo || hi > V)
+      fail(ATLAS_ECONFIG, "bad graph arguments");
+    if (V >= (int64_t)0x7FFFFFFF || E >= (int64_t)0xFFFFFFFF)
+      fail(ATLAS_ECONFIG, "graph exceeds 32-bit vertex/edge ids per rank");
+    use_device(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto g = new atlas_graph();
+    try {
+      g->device = device;
+      g->V = V;
+      g->E = E;
+      g->lo = lo;
+      g->hi = hi;
+      g->nloc = hi - lo;
+      g->offsets.alloc(V + 1);
+      ATLAS_CUDA(cudaMemcpyAsync(g->offsets.ptr, offsets_host,
+                                 (V + 1) * sizeof(int64_t),
+                                 cudaMemcpyHostToDevice, s));
+      DevBuf<uint32_t> nbrs;
+      nbrs.alloc(E > 0 ? E : 1);
+      if (E > 0)
+        ATLAS_CUDA(cudaMemcpyAsync(nbrs.ptr, neighbors_host,
+                                   E * sizeof(uint32_t),
+                                   cudaMemcpyHostToDevice, s));
+      build_csc(g, nbrs, in_degrees_host, s);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+void atlas_graph_destroy(atlas_graph* g) { delete g; }
+
+int atlas_graph_csc(const atlas_graph* g, const int64_t** csc_ptr,
+                    const uint32_t** csc_src, int64_t* n) {
+  return guarded([&] {
+    if (!g) fail(ATLAS_ECONFIG, "null graph");
+    if (csc_ptr) *csc_ptr = g->csc_ptr.ptr;
+    if (csc_src) *csc_src = g->csc_src.ptr;
+    if (n) *n = g->eloc;
+  });
+}
+
+int atlas_layer_create(const atlas_layer_desc* desc,
+                       const uint32_t* in_degrees_host, void* stream,
+                       atlas_layer** out) {
+  return guarded([&] {
+    if (!desc || !out) fail(ATLAS_ECONFIG, "null argument");
+    const atlas_layer_desc& D = *desc;
+    if (D.slot_count < 1) fail(ATLAS_ECONFIG, "hot_slots must be >= 1");
+    if (D.dst_lo < 0 || D.dst_hi < D.dst_lo || D.dst_hi > D.num_vertices)
+      fail(ATLAS_ECONFIG, "bad destination range");
+    if (D.model < ATLAS_GCN || D.model > ATLAS_GIN)
+      fail(ATLAS_ECONFIG, "unknown model kind");
+    if (D.policy < ATLAS_MINPEND || D.policy > ATLAS_RND)
+      fail(ATLAS_ECONFIG, "unknown eviction policy");
+    const int64_t want = D.model == ATLAS_SAGE ? 2 * D.embed_dim : D.embed_dim;
+    if (D.embed_dim < 1 || D.agg_dim != want)
+      fail(ATLAS_ECONFIG, "agg_dim must be embed_dim (2x for SAGE)");
+    use_device(D.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto L = new atlas_layer();
+    try {
+      L->desc = D;
+      L->nloc = D.dst_hi - D.dst_lo;
+      L->sub_batch = std::max<int64_t>(1, D.slot_count / 2);
+      L->evict_batch =
+          D.evict_batch > 0 ? D.evict_batch
+                            : std::max<int64_t>(1, D.slot_count / 100);
+      const int64_t nn = std::max<int64_t>(L->nloc, 1);
+      L->indeg.alloc(nn);
+      if (L->nloc > 0)
+        ATLAS_CUDA(cudaMemcpyAsync(L->indeg.ptr, in_degrees_host + D.dst_lo,
+                                   L->nloc * sizeof(uint32_t),
+                                   cudaMemcpyHostToDevice, s));
+      L->acc.alloc(nn * D.agg_dim);
+      L->touched.alloc(nn);
+      ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
+      engine_init(L, s);
+    } catch (...) {
+      delete L;
+      throw;
+    }
+    *out = L;
+  });
+}
+
+void atlas_layer_destroy(atlas_layer* L) { delete L; }
+
+int atlas_chunk_submit(atlas_layer* L, int64_t start, int64_t end,
+                       const void* rows_host, int32_t dtype,
+                       const int64_t* off, const int64_t* nbrs, int64_t m,
+                       void* stream) {
+  return guarded([&] {
+    if (!L) fail(ATLAS_ECONFIG, "null layer");
+    use_device(L->desc.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (L->chunks_seen == 0) {
+      // records start at zero; later chunks resume via touched flags
+      ATLAS_CUDA(cudaMemsetAsync(L->acc.ptr, 0, L->acc.bytes(), s));
+    }
+    submit_chunk(L, start, end, rows_host, dtype, off, nbrs, m, s);
+  });
+}
+
+int atlas_chunk_graduated(atlas_layer* L, int64_t* ids, float* rows,
+                          int64_t cap, int64_t* count, int64_t* batch_len,
+                          int64_t batch_cap, int64_t* num_batches) {
+  return guarded([&] {
+    if (!L) fail(ATLAS_ECONFIG, "null layer");
+    use_device(L->desc.device);
+    cudaStream_t s = nullptr;
+    EngineScalars sc = read_scalars(L, s);
+    const int64_t n = sc.chunk_grad_n, nb = sc.chunk_grad_batches_n;
+    if (count) *count = n;
+    if (num_batches) *num_batches = nb;
+    if (!ids && !rows && !batch_len) return;
+    if (cap < n || (batch_len && batch_cap < nb))
+      fail(ATLAS_ECONFIG, "graduation buffers too small");
+    std::vector<int32_t> loc(n);
+    if (n > 0)
+      ATLAS_CUDA(cudaMemcpy(loc.data(), L->chunk_grad.ptr, n * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost));
+    if (ids)
+      for (int64_t i = 0; i < n; i++) ids[i] = loc[i] + L->desc.dst_lo;
+    if (batch_len && nb > 0)
+      ATLAS_CUDA(cudaMemcpy(batch_len, L->chunk_grad_batches.ptr,
+                            nb * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (rows && n > 0) {
+      const int64_t w = L->desc.agg_dim;
+      L->grad_rows.reserve(n * w);
+      launch_gather_rows(L->acc.ptr, w, L->chunk_grad.ptr, n, w,
+                         L->grad_rows.ptr, s);
+      ATLAS_CUDA(cudaMemcpy(rows, L->grad_rows.ptr, n * w * sizeof(float),
+                            cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
+                             const void* x, int32_t dtype, int64_t ldx,
+                             int64_t chunk_rows, void* stream) {
+  return guarded([&] {
+    if (!L || !g) fail(ATLAS_ECONFIG, "null argument");
+    const atlas_layer_desc& D = L->desc;
+    if (g->V != D.num_vertices || g->lo != D.dst_lo || g->hi != D.dst_hi)
+      fail(ATLAS_ECONFIG, "graph and layer disagree on the vertex range");
+    if (chunk_rows < 1) fail(ATLAS_ECONFIG, "chunk_rows must be >= 1");
+    if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
+    use_device(D.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaEvent_t ev[3];
+    for (auto& e : ev) ATLAS_CUDA(cudaEventCreate(&e));
+    ATLAS_CUDA(cudaEventRecord(ev[0], s));
+    if (L->nloc > 0)
+      launch_agg_resident(g, x, dtype, ldx, D.model, D.gin_epsilon,
+                          (int)D.embed_dim, L->acc.ptr, D.agg_dim, s);
+    ATLAS_CUDA(cudaEventRecord(ev[1], s));
+    resident_control(L, g, chunk_rows, s);
+    ATLAS_CUDA(cudaEventRecord(ev[2], s));
+    ATLAS_CUDA(cudaEventSynchronize(ev[2]));
+    ATLAS_CUDA(cudaEventElapsedTime(&L->timing_ms[0], ev[0], ev[1]));
+    ATLAS_CUDA(cudaEventElapsedTime(&L->timing_ms[1], ev[1], ev[2]));
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
+int atlas_layer_timing(atlas_layer* L, float* ms, int32_t n) {
+  return guarded([&] {
+    if (!L || !ms) fail(ATLAS_ECONFIG, "null argument");
+    for (int i = 0; i < n && i < 2; i++) ms[i] = L->timing_ms[i];
+  });
+}
+
+int atlas_layer_accumulator(atlas_layer* L, float** acc, int64_t* ld) {
+  return guarded([&] {
+    if (!L) fail(ATLAS_ECONFIG, "null layer");
+    if (acc) *acc = L->acc.ptr;
+    if (ld) *ld = L->desc.agg_dim;
+  });
+}
+
+int atlas_transform(int32_t backend, const float* x, int64_t rows, int64_t k,
+                    int64_t ldx, const float* w, const float* b, int64_t n,
+                    int32_t relu, void* y, int32_t y_dtype, int64_t ldy,
+                    void* stream) {
+  return guarded([&] {
+    if (rows < 0 || k < 1 || n < 1 || ldx < k || ldy < n)
+      fail(ATLAS_ECONFIG, "bad transform shape");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (backend == ATLAS_BACKEND_STABLE) {
+      launch_transform_stable(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
+                              s);
+    } else if (backend == ATLAS_BACKEND_TCGEN05) {
+      if (!launch_transform_tc(x, rows, k, ldx, w, b, n, relu, y, y_dtype,
+                               ldy, s))
+        fail(ATLAS_ECONFIG, "tcgen05 backend does not support this shape");
+    } else {
+      fail(ATLAS_ECONFIG, "unknown transform backend");
+    }
+  });
+}
+
+int atlas_layer_finish(atlas_layer* L, atlas_layer_metrics* m) {
+  return guarded([&] {
+    if (!L || !m) fail(ATLAS_ECONFIG, "null argument");
+    use_device(L->desc.device);
+    cudaStream_t s = nullptr;
+    ATLAS_CUDA(cudaDeviceSynchronize());
+    std::memset(m, 0, sizeof(*m));
+    finish_spans(L, s);
+    m->span_count = L->span_count;
+    m->span_sum = L->span_sum;
+    m->span_q_lo = L->span_q_lo;
+    m->span_q_hi = L->span_q_hi;
+    m->hot_slot_count = L->desc.slot_count;
+    m->chunks = L->chunks_seen;
+    const int64_t w = L->desc.agg_dim * 4;
+    if (L->fast_path) {
+      m->fast_path = 1;
+      m->messages = L->fp_messages;
+      m->admissions = L->nloc;
+      m->graduations = L->nloc;
+      m->hot_peak = L->fp_hot_peak;
+      return;
+    }
+    EngineScalars sc = read_scalars(L, s);
+    m->messages = sc.messages;
+    m->evictions = sc.evictions;
+    m->reloads = sc.reloads;
+    m->admissions = sc.admissions;
+    m->graduations = sc.graduations;
+    m->hot_peak = sc.hot_peak;
+    m->cold_bytes_written = sc.evictions * w;
+    m->cold_bytes_read = sc.reloads * w;
+    // unique reloads and incomplete vertices
+    const int64_t n = L->nloc;
+    std::vector<uint8_t> ur(n), st(n);
+    if (n > 0) {
+      ATLAS_CUDA(cudaMemcpy(ur.data(), L->unique_reloaded.ptr, n,
+                            cudaMemcpyDeviceToHost));
+      ATLAS_CUDA(cudaMemcpy(st.data(), L->state.ptr, n,
+                            cudaMemcpyDeviceToHost));
+    }
+    int64_t uniq = 0, inc = 0;
+    for (int64_t i = 0; i < n; i++) {
+      uniq += ur[i] != 0;
+      if (st[i] != 3) {
+        if (inc < 16) m->first_incomplete[inc] = i + L->desc.dst_lo;
+        inc++;
+      }
+    }
+    m->unique_reloads = uniq;
+    m->incomplete = inc;
+  });
+}
+
+int atlas_layer_state(atlas_layer* L, uint32_t* pending, uint8_t* state,
+                      int64_t* first_step, int64_t* last_step) {
+  return guarded([&] {
+    if (!L) fail(ATLAS_ECONFIG, "null layer");
+    use_device(L->desc.device);
+    ATLAS_CUDA(cudaDeviceSynchronize());
+    const int64_t n = L->nloc;
+    if (n == 0) return;
+    if (L->fast_path && (pending || state)) {
+      // the eviction-free replay never materialises per-vertex state:
+      // every vertex ran to COMPLETED with zero pending
+      if (pending) std::memset(pending, 0, n * sizeof(uint32_t));
+      if (state) std::memset(state, 3, n);
+    } else {
+      if (pending)
+        ATLAS_CUDA(cudaMemcpy(pending, L->pending.ptr, n * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost));
+      if (state)
+        ATLAS_CUDA(cudaMemcpy(state, L->state.ptr, n, cudaMemcpyDeviceToHost));
+    }
+    if (first_step)
+      ATLAS_CUDA(cudaMemcpy(first_step, L->first_pos.ptr, n * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost));
+    if (last_step)
+      ATLAS_CUDA(cudaMemcpy(last_step, L->last_pos.ptr, n * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost));
+  });
+}
+
+int atlas_layer_chunk_stats(atlas_layer* L, int64_t* reloads, int64_t* touched,
+                            int64_t cap, int64_t* count) {
+  return guarded([&] {
+    if (!L) fail(ATLAS_ECONFIG, "null layer");
+    const int64_t n = (int64_t)L->chunk_reloads.size();
+    if (count) *count = n;
+    if (!reloads && !touched) return;
+    if (cap < n) fail(ATLAS_ECONFIG, "chunk stats buffer too small");
+    for (int64_t i = 0; i < n; i++) {
+      if (reloads) reloads[i] = L->chunk_reloads[i];
+      if (touched) touched[i] = L->chunk_touched[i];
+    }
+  });
+}
+
+int atlas_layer_log(atlas_layer* L, int32_t which, int64_t* out, int64_t cap,
+                    int64_t* count) {
+  return guarded([&] {
+    if (!L) fail(ATLAS_ECONFIG, "null layer");
+    if (!L->desc.record_log) fail(ATLAS_ECONFIG, "layer was not logging");
+    EngineScalars sc = read_scalars(L, nullptr);
+    DevBuf<int64_t>* buf;
+    int64_t used;
+    if (which == ATLAS_LOG_VICTIMS) {
+      buf = &L->log_victims;
+      used = sc.log_victims_n;
+    } else if (which == ATLAS_LOG_RELOADS) {
+      buf = &L->log_reloads;
+      used = sc.log_reloads_n;
+    } else {
+      buf = &L->log_grad;
+      used = sc.log_grad_n;
+    }
+    if (used > (int64_t)buf->count) fail(ATLAS_EINVARIANT, "log overflowed");
+    std::vector<int64_t> raw(used);
+    if (used > 0)
+      ATLAS_CUDA(cudaMemcpy(raw.data(), buf->ptr, used * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost));
+    std::vector<int64_t> flat;
+    flat.reserve(used);
+    const int64_t lo = L->desc.dst_lo;
+    if (which == ATLAS_LOG_VICTIMS) {
+      // [-k, (v, key) x k] -> [k, v...] ordered like pop_min (key order);
+      // RandomPolicy victims keep their draw order
+      size_t i = 0;
+      while (i < raw.size()) {
+        const int64_t k = -raw[i++];
+        std::vector<std::pair<uint64_t, int64_t>> ev;
+        for (int64_t j = 0; j < k; j++, i += 2)
+          ev.push_back({(uint64_t)raw[i + 1], raw[i]});
+        if (L->desc.policy != ATLAS_RND) std::sort(ev.begin(), ev.end());
+        flat.push_back(k);
+        for (auto& e : ev) flat.push_back(e.second + lo);
+      }
+    } else {
+      size_t i = 0;
+      while (i < raw.size()) {
+        const int64_t k = raw[i++];
+        flat.push_back(k);
+        for (int64_t j = 0; j < k; j++) flat.push_back(raw[i++] + lo);
+      }
+    }
+    if (count) *count = (int64_t)flat.size();
+    if (out) {
+      if (cap < (int64_t)flat.size()) fail(ATLAS_ECONFIG, "log buffer small");
+      std::copy(flat.begin(), flat.end(), out);
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,361 @@
+// Whole-layer control plane over the resident CSC view.
+//
+// Stream positions (the reference's ctx.step, oocgnn/orchestrator.py:
+// 224-277) are closed-form in CSR coordinates for a chunk plan of R rows
+// (chunk c = [s_c, e_c), s_c = cR, e_c = min(s_c + R, V)):
+//   GCN : edge j (source u)  -> j
+//   SAGE: self term of v     -> off[s_c(v)] + v ;  edge j -> j + e_c(u)
+//   GIN : self term of v     -> off[v] + v      ;  edge j -> j + u + 1
+// so first/last steps (spans), per-chunk destination runs (P_c) and the
+// (chunk, pass) at which each destination is first admitted and finally
+// graduated all come from ONE parallel walk of every destination's
+// ascending source list. If no pass is split into sub-batches and the
+// eviction-free hot-population trajectory never exceeds the slot budget,
+// the reference machine provably never evicts; its integer results are
+// then exactly these closed forms (the "fast path"). Otherwise the
+// per-chunk destination runs are materialised in first-appearance order
+// (flag at the run's first stream position + ordered compaction) and the
+// exact engine (engine.cu) replays the machine.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace atlas {
+
+EngineScalars read_scalars(atlas_layer* L, cudaStream_t s);
+int64_t phys_slots_of(const atlas_layer* L);
+
+namespace {
+
+constexpr uint64_t kNoRun = ~0ull;
+
+struct Plan {
+  int64_t R, V, nchunks;
+  __device__ __forceinline__ int64_t chunk(int64_t u) const { return u / R; }
+  __device__ __forceinline__ int64_t start(int64_t c) const { return c * R; }
+  __device__ __forceinline__ int64_t end(int64_t c) const {
+    return min((c + 1) * R, V);
+  }
+};
+
+// position of an edge (CSR index j, source u) in the reference stream
+__device__ __forceinline__ int64_t edge_pos(int model, const Plan& p,
+                                            int64_t j, int64_t u) {
+  if (model == ATLAS_GCN) return j;
+  if (model == ATLAS_SAGE) return j + p.end(p.chunk(u));
+  return j + u + 1;
+}
+
+__device__ __forceinline__ int64_t self_pos(int model, const Plan& p,
+                                            const int64_t* off, int64_t v) {
+  if (model == ATLAS_SAGE) return off[p.start(p.chunk(v))] + v;
+  return off[v] + v;  // GIN
+}
+
+// warp-aggregated atomic add of 1 to counter[key]
+__device__ __forceinline__ void agg_inc(unsigned long long* counter,
+                                        int64_t key, bool pred) {
+  const unsigned act = __ballot_sync(0xffffffffu, pred);
+  if (!pred) return;
+  const unsigned peers = __match_any_sync(act, (unsigned long long)key);
+  const int leader = __ffs(peers) - 1;
+  if ((int)(threadIdx.x & 31) == leader)
+    atomicAdd(counter + key, (unsigned long long)__popc(peers));
+}
+
+// One warp per local destination: spans, admission / graduation
+// (chunk, pass), per-chunk run counts and (optionally) run records.
+__global__ void __launch_bounds__(256)
+    walk_destinations(int model, Plan p, const int64_t* __restrict__ off,
+                      const int64_t* __restrict__ csc_ptr,
+                      const uint32_t* __restrict__ csc_src,
+                      const uint32_t* __restrict__ csc_eid, int64_t lo,
+                      int64_t nloc, int64_t* __restrict__ first_pos,
+                      int64_t* __restrict__ last_pos,
+                      unsigned long long* __restrict__ admit_hist,
+                      unsigned long long* __restrict__ grad_hist,
+                      unsigned long long* __restrict__ runs_per_chunk,
+                      uint64_t* __restrict__ run_at_pos) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const bool valid = w < nloc;
+  const int64_t v = valid ? w : 0;
+  const int64_t vg = v + lo;
+  int64_t beg = 0, end = 0;
+  if (valid) {
+    beg = csc_ptr[v];
+    end = csc_ptr[v + 1];
+  }
+  const bool has_self = model != ATLAS_GCN;
+  const int64_t cv = p.chunk(vg);
+  // ---- spans and admit/grad (chunk, pass) --------------------------------
+  if (valid && lane == 0) {
+    int64_t first = -1, last = -1;
+    int64_t a_key, g_key;  // chunk * 3 + pass
+    if (end > beg) {
+      const int64_t u0 = csc_src[beg], u1 = csc_src[end - 1];
+      first = edge_pos(model, p, csc_eid[beg], u0);
+      last = edge_pos(model, p, csc_eid[end - 1], u1);
+      a_key = p.chunk(u0) * 3 + 2;
+      g_key = p.chunk(u1) * 3 + 2;
+    }
+    if (has_self) {
+      const int64_t sp = self_pos(model, p, off, vg);
+      const int64_t sk = cv * 3 + (model == ATLAS_SAGE ? 1 : 2);
+      if (end > beg) {
+        first = min(first, sp);
+        last = max(last, sp);
+        a_key = min(a_key, sk);
+        g_key = max(g_key, sk);
+      } else {
+        first = last = sp;
+        a_key = g_key = sk;
+      }
+    } else if (end == beg) {
+      a_key = g_key = cv * 3 + 0;  // GCN zero in-degree pre-pass
+    }
+    first_pos[v] = first;
+    last_pos[v] = last;
+    atomicAdd(admit_hist + a_key, 1ull);
+    atomicAdd(grad_hist + g_key, 1ull);
+  }
+  // ---- runs: maximal same-chunk stretches of the ascending source list ---
+  bool self_merged = false;  // GIN self term joins the run of chunk cv
+  for (int64_t base = beg; base < end; base += 32) {
+    const int64_t i = base + lane;
+    const bool in = i < end;
+    int64_t u = 0, c = -1;
+    if (in) {
+      u = csc_src[i];
+      c = p.chunk(u);
+    }
+    int64_t prev_c = __shfl_up_sync(0xffffffffu, c, 1);
+    const int64_t carry = (base > beg) ? p.chunk((int64_t)csc_src[base - 1]) : -2;
+    if (lane == 0) prev_c = carry;
+    const bool starts = in && c != prev_c;
+    if (model == ATLAS_GIN && __any_sync(0xffffffffu, in && c == cv))
+      self_merged = true;
+    agg_inc(runs_per_chunk, c, starts);
+    if (run_at_pos && starts) {
+      // run [i, j): count its entries; GIN adds the self term
+      int64_t j = i + 1;
+      while (j < end && p.chunk((int64_t)csc_src[j]) == c) j++;
+      uint64_t cnt = (uint64_t)(j - i);
+      int64_t pos = edge_pos(model, p, csc_eid[i], u);
+      if (model == ATLAS_GIN && c == cv) {
+        cnt += 1;
+        pos = min(pos, self_pos(model, p, off, vg));
+      }
+      run_at_pos[pos] = (cnt << 32) | (uint64_t)(uint32_t)v;
+    }
+  }
+  if (valid && model == ATLAS_GIN && !self_merged && lane == 0) {
+    atomicAdd(runs_per_chunk + cv, 1ull);
+    if (run_at_pos)
+      run_at_pos[self_pos(model, p, off, vg)] =
+          (1ull << 32) | (uint64_t)(uint32_t)v;
+  }
+}
+
+__global__ void fill_u64(uint64_t* p, int64_t n, uint64_t val) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = val;
+}
+
+__global__ void span_values(const int64_t* first, const int64_t* last,
+                            int64_t n, int64_t* spans,
+                            unsigned long long* sum_count) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t my_sum = 0, my_cnt = 0;
+  for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool got = first[i] >= 0;
+    spans[i] = got ? last[i] - first[i] : INT64_MAX;
+    if (got) {
+      my_sum += last[i] - first[i];
+      my_cnt++;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    my_sum += __shfl_xor_sync(0xffffffffu, my_sum, o);
+    my_cnt += __shfl_xor_sync(0xffffffffu, my_cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(sum_count, (unsigned long long)my_sum);
+    atomicAdd(sum_count + 1, (unsigned long long)my_cnt);
+  }
+}
+
+struct NotNoRun {
+  __device__ bool operator()(const uint64_t& x) const { return x != kNoRun; }
+};
+
+unsigned grid_of(int64_t n, int block = 256) {
+  int64_t g = ceil_div(n, block);
+  if (g > 148 * 16) g = 148 * 16;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+// spans -> exact integer sum, count and the two order statistics that
+// np.percentile(spans, 99) interpolates between.
+void finish_spans(atlas_layer* L, cudaStream_t s) {
+  const int64_t n = L->nloc;
+  L->span_count = L->span_sum = L->span_q_lo = L->span_q_hi = 0;
+  if (n == 0) return;
+  DevBuf<int64_t> spans, sorted;
+  DevBuf<unsigned long long> sc;
+  spans.alloc(n);
+  sorted.alloc(n);
+  sc.alloc(2);
+  ATLAS_CUDA(cudaMemsetAsync(sc.ptr, 0, 2 * sizeof(unsigned long long), s));
+  span_values<<<grid_of(n), 256, 0, s>>>(L->first_pos.ptr, L->last_pos.ptr, n,
+                                         spans.ptr, sc.ptr);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  unsigned long long h[2];
+  ATLAS_CUDA(cudaMemcpyAsync(h, sc.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+  ATLAS_CUDA(cudaStreamSynchronize(s));
+  L->span_sum = (int64_t)h[0];
+  L->span_count = (int64_t)h[1];
+  if (L->span_count == 0) return;
+  size_t tmp_bytes = 0;
+  ATLAS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, spans.ptr,
+                                            sorted.ptr, n, 0, 64, s));
+  DevBuf<uint8_t> tmp;
+  tmp.alloc(tmp_bytes);
+  ATLAS_CUDA(cub::DeviceRadixSort::SortKeys(tmp.ptr, tmp_bytes, spans.ptr,
+                                            sorted.ptr, n, 0, 64, s));
+  count_launch();
+  // numpy 'linear': virtual index (n - 1) * 0.99
+  const double vi = (double)(L->span_count - 1) * 0.99;
+  int64_t lo_i = (int64_t)std::floor(vi);
+  int64_t hi_i = std::min<int64_t>(lo_i + 1, L->span_count - 1);
+  ATLAS_CUDA(cudaMemcpyAsync(&L->span_q_lo, sorted.ptr + lo_i, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, s));
+  ATLAS_CUDA(cudaMemcpyAsync(&L->span_q_hi, sorted.ptr + hi_i, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, s));
+  ATLAS_CUDA(cudaStreamSynchronize(s));
+}
+
+void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
+                      cudaStream_t s) {
+  const int64_t V = g->V;
+  const int model = L->desc.model;
+  Plan p{R, V, ceil_div(V, R)};
+  const int64_t nchunks = p.nchunks;
+  DevBuf<unsigned long long> hist;  // admit[3C], grad[3C], runs[C]
+  hist.alloc(7 * std::max<int64_t>(nchunks, 1));
+  ATLAS_CUDA(cudaMemsetAsync(hist.ptr, 0, hist.bytes(), s));
+  unsigned long long* admit_h = hist.ptr;
+  unsigned long long* grad_h = hist.ptr + 3 * nchunks;
+  unsigned long long* runs_h = hist.ptr + 6 * nchunks;
+  const unsigned blocks = (unsigned)ceil_div(std::max<int64_t>(L->nloc, 1), 8);
+  walk_destinations<<<blocks, 256, 0, s>>>(
+      model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
+      g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
+      admit_h, grad_h, runs_h, nullptr);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  std::vector<unsigned long long> h(7 * nchunks);
+  ATLAS_CUDA(cudaMemcpyAsync(h.data(), hist.ptr, h.size() * sizeof(h[0]),
+                             cudaMemcpyDeviceToHost, s));
+  ATLAS_CUDA(cudaStreamSynchronize(s));
+
+  // eviction-free trajectory at (chunk, pass) granularity
+  bool single = true;
+  int64_t hot = 0, peak = 0;
+  std::vector<int64_t> touched(nchunks, 0);
+  for (int64_t c = 0; c < nchunks; c++) {
+    const int64_t cs = c * R, ce = std::min(cs + R, V);
+    const int64_t self_n = std::max<int64_t>(
+        0, std::min(ce, g->hi) - std::max(cs, g->lo));
+    const int64_t sizes[3] = {(int64_t)h[3 * c + 0],
+                              model == ATLAS_SAGE ? self_n : 0,
+                              (int64_t)h[6 * nchunks + c]};
+    for (int ph = 0; ph < 3; ph++) {
+      if (sizes[ph] > L->sub_batch) single = false;
+      const int64_t a = (int64_t)h[3 * c + ph];
+      if (a > 0) {
+        hot += a;
+        peak = std::max(peak, hot);
+      }
+      hot -= (int64_t)h[3 * nchunks + 3 * c + ph];
+    }
+    touched[c] = sizes[1] + sizes[2];
+  }
+  const bool fast = single && peak <= L->desc.slot_count &&
+                    !L->desc.record_log && !L->desc.force_exact;
+  L->chunks_seen += nchunks;
+  if (fast) {
+    L->fast_path = true;
+    L->fp_hot_peak = peak;
+    L->fp_messages = g->eloc + (model == ATLAS_GCN ? 0 : L->nloc);
+    for (int64_t c = 0; c < nchunks; c++) {
+      L->chunk_reloads.push_back(0);
+      L->chunk_touched.push_back(touched[c]);
+    }
+    return;
+  }
+  // exact replay: materialise runs in first-appearance order
+  L->fast_path = false;
+  const int64_t npos = g->E + (model == ATLAS_GCN ? 0 : V) + 1;
+  DevBuf<uint64_t> at_pos, runs;
+  DevBuf<int64_t> nsel;
+  at_pos.alloc(npos);
+  nsel.alloc(1);
+  fill_u64<<<grid_of(npos), 256, 0, s>>>(at_pos.ptr, npos, kNoRun);
+  count_launch();
+  ATLAS_CUDA(cudaMemsetAsync(hist.ptr, 0, hist.bytes(), s));
+  walk_destinations<<<blocks, 256, 0, s>>>(
+      model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
+      g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
+      admit_h, grad_h, runs_h, at_pos.ptr);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  int64_t total_runs = 0;
+  std::vector<int64_t> run_off(nchunks + 1, 0);
+  for (int64_t c = 0; c < nchunks; c++) {
+    run_off[c + 1] = run_off[c] + (int64_t)h[6 * nchunks + c];
+  }
+  total_runs = run_off[nchunks];
+  runs.alloc(std::max<int64_t>(total_runs, 1));
+  size_t tmp_bytes = 0;
+  NotNoRun pred;
+  ATLAS_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, at_pos.ptr, runs.ptr,
+                                   nsel.ptr, npos, pred, s));
+  DevBuf<uint8_t> tmp;
+  tmp.alloc(tmp_bytes);
+  ATLAS_CUDA(cub::DeviceSelect::If(tmp.ptr, tmp_bytes, at_pos.ptr, runs.ptr,
+                                   nsel.ptr, npos, pred, s));
+  count_launch();
+  int64_t got = 0;
+  ATLAS_CUDA(cudaMemcpyAsync(&got, nsel.ptr, sizeof(got),
+                             cudaMemcpyDeviceToHost, s));
+  ATLAS_CUDA(cudaStreamSynchronize(s));
+  if (got != total_runs)
+    fail(ATLAS_EINVARIANT, "run materialisation mismatch " +
+                               std::to_string(got) + " vs " +
+                               std::to_string(total_runs));
+  DevBuf<int64_t> d_off, d_bounds;
+  d_off.alloc(nchunks + 1);
+  d_bounds.alloc(2 * nchunks);
+  std::vector<int64_t> bounds(2 * nchunks);
+  for (int64_t c = 0; c < nchunks; c++) {
+    bounds[2 * c] = c * R;
+    bounds[2 * c + 1] = std::min((c + 1) * R, V);
+  }
+  ATLAS_CUDA(cudaMemcpyAsync(d_off.ptr, run_off.data(),
+                             (nchunks + 1) * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, s));
+  ATLAS_CUDA(cudaMemcpyAsync(d_bounds.ptr, bounds.data(),
+                             2 * nchunks * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, s));
+  engine_run_chunks(L, runs.ptr, d_off.ptr, d_bounds.ptr, nchunks,
+                    run_off.data(), s);
+}
+
+}  // namespace atlas

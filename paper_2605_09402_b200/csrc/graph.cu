@@ -8,6 +8,7 @@
 // whose per-destination sources ascend. This file builds that view once
 // per graph and rank: a stable radix sort of (dst, csr_edge_index) pairs.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "internal.cuh"
 
@@ -96,12 +97,10 @@ void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs,
   DevBuf<uint32_t> sel;
   int64_t nsel = E;
   if (!full && E > 0) {
-    DevBuf<uint32_t> iota;
-    iota.alloc(E);
     DevBuf<int64_t> nsel_dev;
     nsel_dev.alloc(1);
     sel.alloc(E);
-    cub::CountingInputIterator<uint32_t> it(0);
+    thrust::counting_iterator<uint32_t> it(0);
     size_t tmp_bytes = 0;
     InRange pred{nbrs.ptr, (uint32_t)g->lo, (uint32_t)g->hi};
     ATLAS_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, it, sel.ptr,

@@ -117,6 +117,8 @@ struct atlas_layer {
   // fast-path metrics
   int64_t span_count = 0, span_sum = 0, span_q_lo = 0, span_q_hi = 0;
   int64_t fp_hot_peak = 0;
+  int64_t fp_messages = 0;
+  float timing_ms[2] = {0.f, 0.f};
 };
 
 namespace atlas {

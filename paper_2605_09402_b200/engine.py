@@ -1,0 +1,292 @@
+"""Device-side objects behind the reference API: topology and layer state.
+
+``DeviceGraph`` holds one destination range's CSR + CSC in HBM
+(atlas_graph_create). ``DeviceLayer`` is the GPU LayerContext
+(atlas_layer_create): pending counters, lifecycle states, the hot-slot
+budget and its eviction policy, the f32 aggregation records, and the
+integer logs. Both are thin owners of C-ABI handles; all compute happens in
+libatlas_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConfigError
+
+DTYPE_CODES = {np.dtype(np.float32): N.F32, np.dtype(np.float16): N.F16}
+
+
+def torch_dtype_code(t) -> int:
+    import torch
+
+    return {torch.float32: N.F32, torch.float16: N.F16,
+            torch.bfloat16: N.BF16}[t.dtype]
+
+
+def rnd_state_of(seed: int):
+    """numpy default_rng(seed)'s PCG64 state as (hi, lo, inc_hi, inc_lo)."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    m = (1 << 64) - 1
+    return (st["state"] >> 64, st["state"] & m, st["inc"] >> 64,
+            st["inc"] & m)
+
+
+class DeviceGraph:
+    """CSR + destination-major view of [lo, hi) resident on one GPU."""
+
+    def __init__(self, offsets, neighbors, in_degrees, dst_range=None,
+                 device: int = 0, stream=None):
+        lib = N.lib()
+        self.offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        nbrs = np.ascontiguousarray(neighbors, dtype=np.uint32)
+        self.in_degrees = np.ascontiguousarray(in_degrees, dtype=np.uint32)
+        self.num_vertices = len(self.offsets) - 1
+        self.num_edges = len(nbrs)
+        lo, hi = dst_range if dst_range else (0, self.num_vertices)
+        self.lo, self.hi = int(lo), int(hi)
+        self.device = device
+        h = ctypes.c_void_p()
+        N.check(lib.atlas_graph_create(
+            device, self.num_vertices, self.num_edges, N.ptr(self.offsets),
+            N.ptr(nbrs), N.ptr(self.in_degrees), self.lo, self.hi,
+            N.stream_handle(stream), ctypes.byref(h)))
+        self.handle = h
+        n = ctypes.c_int64()
+        N.check(lib.atlas_graph_csc(h, None, None, ctypes.byref(n)))
+        self.local_edges = n.value
+
+    @classmethod
+    def from_csr(cls, graph, **kw):
+        return cls(graph.offsets, graph.neighbors, graph.in_degrees, **kw)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            N.load_library().atlas_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class RawMetrics:
+    messages: int
+    evictions: int
+    reloads: int
+    unique_reloads: int
+    admissions: int
+    graduations: int
+    hot_peak: int
+    hot_slot_count: int
+    chunks: int
+    span_count: int
+    span_sum: int
+    span_q_lo: int
+    span_q_hi: int
+    cold_bytes_read: int
+    cold_bytes_written: int
+    fast_path: bool
+
+
+class DeviceLayer:
+    """One layer's engine state on the GPU (the LayerContext of
+    oocgnn/orchestrator.py:68-145)."""
+
+    def __init__(self, in_degrees, model: int, embed_dim: int, agg_dim: int,
+                 slot_count: int, *, gin_epsilon: float = 0.0,
+                 eviction: str = "minpend", seed: int = 0, evict_batch=None,
+                 dst_range=None, record_log: bool = False,
+                 force_exact: bool = False, device: int = 0, stream=None):
+        lib = N.lib()
+        if eviction not in N.POLICY_CODES:
+            raise ConfigError(f"unknown eviction policy {eviction!r}")
+        self.in_degrees = np.ascontiguousarray(in_degrees, dtype=np.uint32)
+        v = len(self.in_degrees)
+        lo, hi = dst_range if dst_range else (0, v)
+        self.lo, self.hi = int(lo), int(hi)
+        self.num_vertices = v
+        self.model, self.embed_dim, self.agg_dim = model, embed_dim, agg_dim
+        self.slot_count = int(slot_count)
+        self.eviction = eviction
+        self.record_log = record_log
+        self.device = device
+        d = N.LayerDesc()
+        d.num_vertices = v
+        d.dst_lo, d.dst_hi = self.lo, self.hi
+        d.model = int(model)
+        d.gin_epsilon = float(gin_epsilon)
+        d.embed_dim, d.agg_dim = embed_dim, agg_dim
+        d.slot_count = self.slot_count
+        d.evict_batch = int(evict_batch or 0)
+        d.policy = N.POLICY_CODES[eviction]
+        d.record_log = int(record_log)
+        if eviction == "rnd":
+            for i, x in enumerate(rnd_state_of(seed)):
+                d.rnd_state[i] = x
+        d.device = device
+        d.force_exact = int(force_exact)
+        h = ctypes.c_void_p()
+        N.check(lib.atlas_layer_create(ctypes.byref(d),
+                                       N.ptr(self.in_degrees),
+                                       N.stream_handle(stream),
+                                       ctypes.byref(h)))
+        self.handle = h
+        self.h2d_bytes = 0
+
+    # -- operator path ------------------------------------------------------
+    def submit_chunk(self, start, end, rows, local_offsets, neighbors,
+                     stream=None):
+        rows = np.ascontiguousarray(rows)
+        if rows.dtype not in DTYPE_CODES:
+            rows = rows.astype(np.float32)
+        off = np.ascontiguousarray(local_offsets, dtype=np.int64)
+        nb = np.ascontiguousarray(neighbors, dtype=np.int64)
+        n = end - start
+        if rows.shape != (n, self.embed_dim):
+            raise ConfigError(
+                f"chunk rows {rows.shape} != ({n}, {self.embed_dim})")
+        if off.shape != (n + 1,) or (n and (off[0] != 0 or off[-1] != len(nb))):
+            raise ConfigError("chunk offsets do not bracket its neighbors")
+        N.check(N.load_library().atlas_chunk_submit(
+            self.handle, start, end, N.ptr(rows), DTYPE_CODES[rows.dtype],
+            N.ptr(off), N.ptr(nb), len(nb), N.stream_handle(stream)))
+        self.h2d_bytes += rows.nbytes + off.nbytes + nb.nbytes
+
+    def graduated(self, with_rows=True):
+        """(ids int64, rows f32 (n, agg_dim) or None, batch lengths)."""
+        lib = N.load_library()
+        cnt, nb = ctypes.c_int64(), ctypes.c_int64()
+        N.check(lib.atlas_chunk_graduated(self.handle, None, None, 0,
+                                          ctypes.byref(cnt), None, 0,
+                                          ctypes.byref(nb)))
+        ids = np.empty(cnt.value, dtype=np.int64)
+        rows = (np.empty((cnt.value, self.agg_dim), dtype=np.float32)
+                if with_rows else None)
+        lens = np.empty(nb.value, dtype=np.int64)
+        N.check(lib.atlas_chunk_graduated(
+            self.handle, N.ptr(ids), N.ptr(rows), cnt.value,
+            ctypes.byref(cnt), N.ptr(lens), nb.value, ctypes.byref(nb)))
+        return ids, rows, lens
+
+    # -- whole-layer path ---------------------------------------------------
+    def run_resident(self, graph: DeviceGraph, x, chunk_rows: int,
+                     stream=None):
+        """x: torch CUDA tensor (V, embed_dim) f32/f16/bf16."""
+        if x.shape[1] != self.embed_dim or x.shape[0] != self.num_vertices:
+            raise ConfigError(f"input {tuple(x.shape)} does not match layer "
+                              f"({self.num_vertices}, {self.embed_dim})")
+        N.check(N.load_library().atlas_layer_run_resident(
+            self.handle, graph.handle, x.data_ptr(), torch_dtype_code(x),
+            x.stride(0), int(chunk_rows), N.stream_handle(stream)))
+
+    def accumulator_ptr(self):
+        p, ld = ctypes.c_void_p(), ctypes.c_int64()
+        N.check(N.load_library().atlas_layer_accumulator(
+            self.handle, ctypes.byref(p), ctypes.byref(ld)))
+        return p.value, ld.value
+
+    def accumulator(self):
+        """Host copy of the f32 aggregation records of [lo, hi)."""
+        import torch
+
+        p, ld = self.accumulator_ptr()
+        n = self.hi - self.lo
+        out = torch.empty((n, ld), dtype=torch.float32, device="cuda")
+        if n:
+            cudart = torch.cuda.cudart()
+            cudart.cudaMemcpy(out.data_ptr(), p, n * ld * 4, 4)
+        return out
+
+    # -- results ------------------------------------------------------------
+    def finish(self) -> RawMetrics:
+        m = N.LayerMetricsC()
+        N.check(N.load_library().atlas_layer_finish(self.handle,
+                                                    ctypes.byref(m)))
+        if m.incomplete:
+            N.raise_incomplete(m)
+        return RawMetrics(
+            m.messages, m.evictions, m.reloads, m.unique_reloads,
+            m.admissions, m.graduations, m.hot_peak, m.hot_slot_count,
+            m.chunks, m.span_count, m.span_sum, m.span_q_lo, m.span_q_hi,
+            m.cold_bytes_read, m.cold_bytes_written, bool(m.fast_path))
+
+    def timing(self):
+        """(aggregate_ms, control_ms) of the last run_resident, measured
+        with CUDA events on the launching stream."""
+        ms = (ctypes.c_float * 2)()
+        N.check(N.load_library().atlas_layer_timing(self.handle, ms, 2))
+        return float(ms[0]), float(ms[1])
+
+    def chunk_stats(self):
+        lib = N.load_library()
+        n = ctypes.c_int64()
+        N.check(lib.atlas_layer_chunk_stats(self.handle, None, None, 0,
+                                            ctypes.byref(n)))
+        rel = np.empty(n.value, dtype=np.int64)
+        tou = np.empty(n.value, dtype=np.int64)
+        N.check(lib.atlas_layer_chunk_stats(self.handle, N.ptr(rel),
+                                            N.ptr(tou), n.value,
+                                            ctypes.byref(n)))
+        return rel, tou
+
+    def log(self, which: int) -> np.ndarray:
+        lib = N.load_library()
+        n = ctypes.c_int64()
+        N.check(lib.atlas_layer_log(self.handle, which, None, 0,
+                                    ctypes.byref(n)))
+        out = np.empty(n.value, dtype=np.int64)
+        N.check(lib.atlas_layer_log(self.handle, which, N.ptr(out), n.value,
+                                    ctypes.byref(n)))
+        return out
+
+    def state_arrays(self):
+        n = self.hi - self.lo
+        pend = np.empty(n, dtype=np.uint32)
+        st = np.empty(n, dtype=np.uint8)
+        first = np.empty(n, dtype=np.int64)
+        last = np.empty(n, dtype=np.int64)
+        N.check(N.load_library().atlas_layer_state(
+            self.handle, N.ptr(pend), N.ptr(st), N.ptr(first), N.ptr(last)))
+        return pend, st, first, last
+
+    def close(self):
+        if getattr(self, "handle", None):
+            N.load_library().atlas_layer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def transform_device(x_ptr: int, rows: int, k: int, ldx: int, w, b,
+                     relu: bool, y, backend_code: int, stream=None):
+    """y = act(x . W^T + b) on the GPU; w, b, y torch CUDA tensors."""
+    N.check(N.load_library().atlas_transform(
+        backend_code, x_ptr, rows, k, ldx, w.data_ptr(), b.data_ptr(),
+        w.shape[0], int(relu), y.data_ptr(), torch_dtype_code(y),
+        y.stride(0), N.stream_handle(stream)))
+
+
+def percentile99(count: int, q_lo: int, q_hi: int) -> float:
+    """np.percentile(spans, 99) from its two order statistics
+    (numpy 'linear' method: virtual index (n-1)*0.99, _lerp)."""
+    if count == 0:
+        return 0.0
+    vi = (count - 1) * (99 / 100)
+    t = vi - np.floor(vi)
+    a, b = float(q_lo), float(q_hi)
+    diff = b - a
+    if t >= 0.5:
+        return float(b - diff * (1 - t))
+    return float(a + diff * t)

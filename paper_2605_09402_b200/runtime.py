@@ -1,0 +1,399 @@
+"""Public layer-wise inference API on the B200 engine.
+
+Same entry points as oocgnn/runtime.py:60-329 — ``PipelineConfig``,
+``run_layer``, ``run_inference``, ``write_metrics_csv``,
+``final_layer_dir``, ``compare_outputs``, ``clone_config`` — reading and
+writing the reference's dataset / layer-directory / weights formats.
+
+What changes underneath: the reference's four Python
+threads (reader -> orchestrator -> compute -> writer) become
+  host loader -> one H2D copy of the layer input into HBM
+  -> ``atlas_layer_run_resident`` (bit-exact scatter-aggregate over the
+     destination-major view + the pending/eviction control plane on the
+     reference chunk plan)
+  -> ``atlas_transform`` (stable SIMT or tcgen05 backend)
+  -> next layer's embeddings stay in HBM; the layer directory is written
+     from one D2H copy.
+``Engine`` is the device-resident core used by ``run_inference`` and by
+bench.py; it also runs one destination range per GPU rank, exchanging the
+layer outputs with an NCCL all-gather between layers.
+"""
+
+from __future__ import annotations
+
+import csv
+import shutil
+import time
+from dataclasses import dataclass, field, replace
+from pathlib import Path
+
+import numpy as np
+
+from .chunks import chunk_rows as plan_rows
+from .chunks import load_layer_input
+from .compute import device_code, get_backend
+from .engine import DeviceGraph, DeviceLayer, transform_device
+from .errors import ConfigError
+from .iostats import IOCounters
+from .orchestrator import CSV_FIELDS, LayerMetrics, metrics_from_device
+from .orchestrator import slot_budget
+from .storage import (
+    INDEGREE_FILE,
+    TOPOLOGY_FILE,
+    ModelKind,
+    ModelWeights,
+    load_layer_matrix,
+    partition_ranges,
+    read_in_degrees,
+    read_layer_meta,
+    read_topology_arrays,
+    read_weights,
+    write_matrix_as_layer,
+)
+
+
+@dataclass
+class PipelineConfig:
+    """oocgnn/runtime.py:60-85 plus the device knobs (last block)."""
+
+    hot_budget: int = 64 << 20
+    chunk_budget: int = 8 << 20
+    graduation_budget: int = 16 << 20
+    spill_buffer: int = 8 << 20
+    partitions: int = 8
+    queue_capacity: int = 20
+    eviction: str = "minpend"
+    seed: int = 0
+    direct_io: bool = True
+    discard_intermediate: bool = False
+    hot_slots: int | None = None
+    evict_batch: int | None = None
+    max_open_files: int = 128
+    backend: object = field(default=None, repr=False)
+    # device knobs
+    device: int = 0
+    embed_dtype: str = "f32"       # next-layer embedding store: f32|f16|bf16
+    record_log: bool = False        # keep victim/reload/graduation logs
+    force_exact: bool = False       # always replay the exact control engine
+
+    def validate(self) -> None:
+        if self.partitions < 1:
+            raise ConfigError("partitions must be >= 1")
+        if self.queue_capacity < 1:
+            raise ConfigError("queue capacity must be >= 1")
+        if self.chunk_budget < 1:
+            raise ConfigError("chunk budget must be positive")
+        if self.embed_dtype not in ("f32", "f16", "bf16"):
+            raise ConfigError(f"unknown embed dtype {self.embed_dtype!r}")
+
+
+@dataclass
+class RunReport:
+    layers: list
+    out_dir: Path
+    wall_seconds: float
+
+    def total(self, field_name: str):
+        return sum(getattr(m, field_name) for m in self.layers)
+
+
+def write_metrics_csv(path, layers) -> None:
+    with open(path, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(CSV_FIELDS)
+        for m in layers:
+            w.writerow([m.layer, m.messages, m.evictions, m.reloads,
+                        m.unique_reloads, f"{m.mean_span:.3f}",
+                        f"{m.p99_span:.3f}", f"{m.mean_reload_pct:.3f}",
+                        m.bytes_read, m.bytes_written,
+                        f"{m.wall_seconds:.3f}"])
+
+
+def _torch_dtype(name):
+    import torch
+
+    return {"f32": torch.float32, "f16": torch.float16,
+            "bf16": torch.bfloat16}[name]
+
+
+def _plan_dtype(x) -> str:
+    import torch
+
+    return "f32" if x.dtype == torch.float32 else "f16"
+
+
+class Engine:
+    """Device-resident layer-wise inference over one destination range.
+
+    graph: storage.GraphCSR; weights: ModelWeights. With ``dist`` (a
+    torch.distributed group of G ranks) rank g owns
+    partition_ranges(V, G)[g] and the layer outputs are all-gathered
+    (NCCL) so every rank holds the next layer's full input."""
+
+    def __init__(self, graph, weights: ModelWeights, config: PipelineConfig,
+                 *, rank: int = 0, world: int = 1, dist_group=None):
+        import torch
+
+        config.validate()
+        self.config = config
+        self.weights = weights
+        self.kind = weights.kind
+        self.rank, self.world, self.group = rank, world, dist_group
+        self.num_vertices = graph.num_vertices
+        self.in_degrees = np.asarray(graph.in_degrees, dtype=np.uint32)
+        self.ranges = partition_ranges(graph.num_vertices, world)
+        self.lo, self.hi = self.ranges[rank]
+        self.device = config.device
+        torch.cuda.set_device(self.device)
+        self.graph = DeviceGraph(graph.offsets, graph.neighbors,
+                                 graph.in_degrees, (self.lo, self.hi),
+                                 device=self.device)
+        self.backend = get_backend(config.backend)
+        self.W = [torch.as_tensor(np.ascontiguousarray(lw.weight)).cuda()
+                  for lw in weights.layers]
+        self.b = [torch.as_tensor(np.ascontiguousarray(lw.bias)).cuda()
+                  for lw in weights.layers]
+        self.last_layers = []
+
+    def close(self):
+        self.graph.close()
+
+    def layer(self, l: int, x, *, chunk_budget=None):
+        """One layer: x (V, d) CUDA tensor -> (y (V or range, out), metrics,
+        device layer handle)."""
+        import torch
+
+        cfg = self.config
+        w = self.weights
+        last = l == len(w.layers) - 1
+        t0 = time.perf_counter()
+        d = w.embedding_dim(l)
+        if x.shape[1] != d:
+            raise ConfigError(
+                f"layer {l} expects {d}-wide rows, input holds {x.shape[1]}")
+        rows = plan_rows(self.num_vertices, d, _plan_dtype(x),
+                         chunk_budget or cfg.chunk_budget)
+        budget = slot_budget(w, l, cfg.hot_budget, cfg.hot_slots)
+        layer = DeviceLayer(
+            self.in_degrees, int(self.kind), d, w.agg_dim(l),
+            budget.slot_count, gin_epsilon=w.gin_epsilon,
+            eviction=cfg.eviction, seed=cfg.seed,
+            evict_batch=cfg.evict_batch, dst_range=(self.lo, self.hi),
+            record_log=cfg.record_log, force_exact=cfg.force_exact,
+            device=self.device)
+        layer.run_resident(self.graph, x, rows)
+        nloc = self.hi - self.lo
+        out_dim = w.layers[l].out_dim
+        y = torch.empty((nloc, out_dim), dtype=_torch_dtype(cfg.embed_dtype),
+                        device="cuda")
+        acc_ptr, ld = layer.accumulator_ptr()
+        code = device_code(self.backend)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        if nloc:
+            if code is not None:
+                transform_device(acc_ptr, nloc, w.agg_dim(l), ld, self.W[l],
+                                 self.b[l], not last, y, code)
+            else:  # host plug-in backend (reference MatmulBackend protocol)
+                from .compute import transform
+                agg = layer.accumulator().cpu().numpy()
+                y.copy_(torch.as_tensor(transform(
+                    agg, w.layers[l], apply_activation=not last,
+                    backend=self.backend)))
+        ev1.record()
+        m = metrics_from_device(layer, l)
+        m.agg_ms, m.control_ms = layer.timing()
+        m.transform_ms = ev0.elapsed_time(ev1)
+        m.gpu_seconds = time.perf_counter() - t0
+        return y, m, layer
+
+    def gather(self, y_local):
+        """All ranks' ranges -> full (V, out) next-layer input (NCCL)."""
+        if self.world == 1:
+            return y_local
+        import torch
+        import torch.distributed as dist
+
+        w = max(h - l for l, h in self.ranges)
+        pad = torch.zeros((w, y_local.shape[1]), dtype=y_local.dtype,
+                          device=y_local.device)
+        pad[:y_local.shape[0]] = y_local
+        full = torch.empty((w * self.world, y_local.shape[1]),
+                           dtype=y_local.dtype, device=y_local.device)
+        dist.all_gather_into_tensor(full, pad, group=self.group)
+        parts = [full[g * w:g * w + (h - l)]
+                 for g, (l, h) in enumerate(self.ranges)]
+        return torch.cat(parts, dim=0)
+
+    def infer(self, x, keep_layers: bool = False):
+        """All layers; returns (final local output, [LayerMetrics])."""
+        metrics, outs = [], []
+        h = x
+        for l in range(len(self.weights.layers)):
+            y, m, layer = self.layer(l, h)
+            layer.close()
+            metrics.append(m)
+            if keep_layers:
+                outs.append(y)
+            if l != len(self.weights.layers) - 1:
+                h = self.gather(y)
+        self.last_layers = outs
+        return y, metrics
+
+
+def _load_graph(topology_path, in_degrees):
+    from .storage import GraphCSR
+
+    hdr, offsets, nbrs = read_topology_arrays(topology_path,
+                                              nbr_dtype=np.uint32)
+    indeg = np.asarray(in_degrees, dtype=np.int64)
+    topo_bytes = offsets.nbytes + nbrs.nbytes
+    return GraphCSR(hdr.num_vertices, hdr.num_edges, offsets, nbrs,
+                    indeg), topo_bytes
+
+
+def _write_output(layer_dir, y, config, num_vertices) -> int:
+    host = y.float().cpu().numpy() if config.embed_dtype == "bf16" \
+        else y.cpu().numpy()
+    dtype = "f16" if config.embed_dtype == "f16" else "f32"
+    if layer_dir.exists():
+        shutil.rmtree(layer_dir)
+    return write_matrix_as_layer(layer_dir, host, partitions=config.partitions,
+                                 dtype=dtype)
+
+
+def _upload(rows):
+    import torch
+
+    t = torch.from_numpy(rows)
+    if t.dtype == torch.float64:
+        t = t.float()
+    return t.pin_memory().cuda(non_blocking=True)
+
+
+def run_layer(topology_path, in_degrees: np.ndarray, input_dir, output_dir,
+              weights: ModelWeights, layer_index: int,
+              config: PipelineConfig, scratch_dir=None) -> LayerMetrics:
+    """One layer (oocgnn/runtime.py:114-220) through the device engine."""
+    t0 = time.perf_counter()
+    config.validate()
+    meta = read_layer_meta(input_dir)
+    expect = weights.embedding_dim(layer_index)
+    if meta.dim != expect:
+        raise ConfigError(f"layer {layer_index} expects {expect}-wide rows, "
+                          f"input holds {meta.dim}")
+    graph, topo_bytes = _load_graph(topology_path, in_degrees)
+    _, rows, feat_bytes, delivery = load_layer_input(input_dir)
+    eng = Engine(graph, weights, config)
+    try:
+        y, m, layer = eng.layer(layer_index, _upload(rows))
+        layer.close()
+    finally:
+        eng.close()
+    written = _write_output(Path(output_dir), y, config, graph.num_vertices)
+    m.feature_bytes_read = feat_bytes
+    m.bytes_read += feat_bytes + topo_bytes
+    m.bytes_written += written
+    m.delivery_counts = delivery
+    m.wall_seconds = time.perf_counter() - t0
+    return m
+
+
+def run_inference(graph_dir, weights, config: PipelineConfig, out_dir,
+                  metrics_path=None) -> RunReport:
+    """Every layer; embeddings stay in HBM between layers and each
+    layer_l/ directory is written like the reference's
+    (oocgnn/runtime.py:223-264)."""
+    t0 = time.perf_counter()
+    config.validate()
+    graph_dir, out_dir = Path(graph_dir), Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    if not isinstance(weights, ModelWeights):
+        weights = read_weights(weights)
+    hdr_path = graph_dir / TOPOLOGY_FILE
+    hdr, offsets, nbrs = read_topology_arrays(hdr_path, nbr_dtype=np.uint32)
+    in_degrees = read_in_degrees(graph_dir / INDEGREE_FILE, hdr.num_vertices)
+    features_dir = graph_dir / "features"
+    weights.validate(read_layer_meta(features_dir).dim)
+    from .storage import GraphCSR
+
+    graph = GraphCSR(hdr.num_vertices, hdr.num_edges, offsets, nbrs,
+                     in_degrees)
+    topo_bytes = offsets.nbytes + nbrs.nbytes
+    _, rows, feat_bytes, delivery = load_layer_input(features_dir)
+    eng = Engine(graph, weights, config)
+    layers = []
+    prev_dir = None
+    try:
+        h = _upload(rows)
+        for l in range(len(weights.layers)):
+            tl = time.perf_counter()
+            y, m, layer = eng.layer(l, h)
+            layer.close()
+            layer_out = out_dir / f"layer_{l}"
+            m.bytes_written += _write_output(layer_out, y, config,
+                                             hdr.num_vertices)
+            if l == 0:
+                m.feature_bytes_read = feat_bytes
+                m.bytes_read += feat_bytes + topo_bytes
+                m.delivery_counts = delivery
+            else:
+                nb = y.element_size() * h.numel()
+                m.feature_bytes_read = nb
+                m.delivery_counts = np.ones(hdr.num_vertices, np.uint16)
+            m.wall_seconds = time.perf_counter() - tl
+            layers.append(m)
+            if config.discard_intermediate and l > 0 and prev_dir:
+                shutil.rmtree(prev_dir, ignore_errors=True)
+            prev_dir = layer_out
+            h = y
+    finally:
+        eng.close()
+    report = RunReport(layers, out_dir, time.perf_counter() - t0)
+    write_metrics_csv(metrics_path or out_dir / "metrics.csv", layers)
+    return report
+
+
+def final_layer_dir(out_dir) -> Path:
+    cands = sorted((p for p in Path(out_dir).glob("layer_*") if p.is_dir()),
+                   key=lambda p: int(p.name.split("_")[1]))
+    if not cands:
+        raise ConfigError(f"{out_dir}: no layer outputs found")
+    return cands[-1]
+
+
+@dataclass
+class CompareReport:
+    max_abs_err: float
+    mean_abs_err: float
+    argmax_mismatches: int
+    rows: int
+    tolerance: float
+
+    @property
+    def ok(self) -> bool:
+        return (self.max_abs_err <= self.tolerance
+                and self.argmax_mismatches == 0)
+
+
+def compare_outputs(dir_a, dir_b, tolerance: float) -> CompareReport:
+    a = load_layer_matrix(final_layer_dir(dir_a))
+    b = load_layer_matrix(final_layer_dir(dir_b))
+    if a.shape != b.shape:
+        raise ConfigError(f"shape mismatch: {a.shape} vs {b.shape}")
+    diff = np.abs(a.astype(np.float64) - b.astype(np.float64))
+    return CompareReport(
+        float(diff.max(initial=0.0)),
+        float(diff.mean()) if diff.size else 0.0,
+        int(np.count_nonzero(a.argmax(axis=1) != b.argmax(axis=1))),
+        a.shape[0], tolerance)
+
+
+def clone_config(config: PipelineConfig, **overrides) -> PipelineConfig:
+    return replace(config, **overrides)
+
+
+__all__ = ["PipelineConfig", "RunReport", "Engine", "run_layer",
+           "run_inference", "write_metrics_csv", "final_layer_dir",
+           "compare_outputs", "clone_config", "ModelKind"]
