@@ -1,12 +1,461 @@
-// tcgen05 transform backend: placeholder until the tensor-core kernel lands.
+// Dense layer transform on the 5th-gen tensor cores (kernel plan K9).
+//
+// y = act(x . W^T + b), x (M x K) f32 row-major, W (N x K) f32.
+// The reference computes this in f32 (oocgnn/compute.py:39-47); tcgen05
+// has no f32 kind, so we use the 3xTF32 split: a = a_hi + a_lo with a_hi
+// = a truncated to tf32 and a_lo = a - a_hi (exact in f32), and
+//   D = a_hi.w_hi + a_hi.w_lo + a_lo.w_hi       (f32 accumulate in TMEM)
+// which keeps ~f32 accuracy (dropped a_lo.w_lo and the tf32 rounding of
+// the lo parts are ~2^-22 relative). The tensor-core work is 3x a plain
+// GEMM, which is free here: at N <= 256 the transform is HBM-bound.
+//
+// Structure (persistent, one CTA per SM, warp-specialised):
+//   warp 0      TMA producer: x tile (128 x 32 f32, SWIZZLE_128B) and the
+//               w_hi / w_lo tiles (BN x 32) per k-block, mbarrier tx count
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5   splitter: x tile -> x_hi (in place) + x_lo (generic proxy
+//               writes, then fence.proxy.async before the MMA reads)
+//   warps 6-9   epilogue: tcgen05.ld 32x32b -> +bias -> ReLU -> global
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile t
+// overlap the MMAs of tile t+1.
+#include <cuda.h>
+
+#include <mutex>
+
 #include "internal.cuh"
 
 namespace atlas {
+namespace {
 
-bool launch_transform_tc(const float*, int64_t, int64_t, int64_t,
-                         const float*, const float*, int64_t, int, void*, int,
-                         int64_t, cudaStream_t) {
-  return false;
+constexpr int BM = 128, BK = 32;  // BK f32 = 128 B = one swizzle atom row
+constexpr int kThreads = 320;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map,
+                                            uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx"
+      "::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0),
+      "r"(c1)
+      : "memory");
+}
+
+// K-major, SWIZZLE_128B UMMA shared-memory descriptor (sm100 version 1):
+// start >> 4, LBO = 1 (unused when swizzled), SBO = 1024 B (8 rows x 128 B)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // leading byte offset (16 B units)
+  d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset
+  d |= (uint64_t)1 << 46;            // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc,
+                                         uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(
+          tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 "
+      "[%0];" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, "
+      "%7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]),
+        "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),
+        "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float relu_np(float v) {
+  return (v >= 0.0f || v != v) ? v : 0.0f;
+}
+
+template <typename OutT>
+__device__ __forceinline__ OutT cvt_out(float v);
+template <>
+__device__ __forceinline__ float cvt_out<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __half cvt_out<__half>(float v) {
+  return __float2half_rn(v);
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+struct TcParams {
+  int64_t M;
+  int K, N, BN, stages, kblocks, relu;
+  int64_t ldy;
+  const float* bias;
+  void* y;
+  uint32_t tmem_cols;
+};
+
+template <typename OutT>
+__global__ void __launch_bounds__(kThreads, 1)
+    transform_tc_kernel(const __grid_constant__ CUtensorMap map_x,
+                        const __grid_constant__ CUtensorMap map_whi,
+                        const __grid_constant__ CUtensorMap map_wlo,
+                        TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B aligned carve-up: per stage [x | x_lo | w_hi | w_lo]
+  uint8_t* base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t x_bytes = BM * BK * 4;
+  const uint32_t w_bytes = p.BN * BK * 4;
+  const uint32_t stage_bytes = 2 * x_bytes + 2 * w_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + p.stages * stage_bytes);
+  uint64_t* split = full + p.stages;
+  uint64_t* empty = split + p.stages;
+  uint64_t* tfull = empty + p.stages;  // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (p.M + BM - 1) / BM;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; a++) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = threadIdx.x; j < p.BN; j += kThreads)
+    sbias[j] = j < p.N ? p.bias[j] : 0.0f;
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::
+            "r"(smem_u32(tmem_slot)),
+        "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kb = 0; kb < p.kblocks; kb++) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = base + s * stage_bytes;
+          mbar_expect_tx(&full[s], x_bytes + 2 * w_bytes);
+          tma_load_2d(st, &map_x, &full[s], kb * BK, (int)(t * BM));
+          tma_load_2d(st + 2 * x_bytes, &map_whi, &full[s], kb * BK, 0);
+          tma_load_2d(st + 2 * x_bytes + w_bytes, &map_wlo, &full[s], kb * BK,
+                      0);
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = (1u << 4)                       // D = f32
+                           | (2u << 7) | (2u << 10)        // A, B = tf32
+                           | ((uint32_t)(p.BN >> 3) << 17)  // N
+                           | ((uint32_t)(BM >> 4) << 24);   // M
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t aph[2] = {0, 0};
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], aph[acc] ^ 1);
+      aph[acc] ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dt = tmem_base + (uint32_t)(acc * p.BN);
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        mbar_wait(&split[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          uint8_t* st = base + s * stage_bytes;
+          const uint32_t a_hi = smem_u32(st), a_lo = smem_u32(st + x_bytes);
+          const uint32_t b_hi = smem_u32(st + 2 * x_bytes);
+          const uint32_t b_lo = b_hi + w_bytes;
+#pragma unroll
+          for (int k = 0; k < BK / 8; k++) {  // UMMA_K = 8 tf32 = 32 B
+            const uint32_t off = k * 32;
+            const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
+            mma_tf32(dt, sw128_desc(a_lo + off), sw128_desc(b_hi + off),
+                     idesc, first);
+            mma_tf32(dt, sw128_desc(a_hi + off), sw128_desc(b_lo + off),
+                     idesc, 1u);
+            mma_tf32(dt, sw128_desc(a_hi + off), sw128_desc(b_hi + off),
+                     idesc, 1u);
+          }
+          mma_commit(&empty[s]);
+          if (kb == p.kblocks - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      acc ^= 1;
+    }
+  } else if (warp < 6) {
+    // ---------------- splitter: x -> x_hi (in place) + x_lo -------------
+    const int tid = threadIdx.x - 64;  // 0..127
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        mbar_wait(&full[s], ph);
+        float4* xs = reinterpret_cast<float4*>(base + s * stage_bytes);
+        float4* xl = reinterpret_cast<float4*>(base + s * stage_bytes +
+                                               x_bytes);
+#pragma unroll
+        for (int i = 0; i < (BM * BK / 4) / 128; i++) {
+          const int e = tid + i * 128;
+          float4 v = xs[e];
+          float4 h, l;
+          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          l.x = v.x - h.x;
+          l.y = v.y - h.y;
+          l.z = v.z - h.z;
+          l.w = v.w - h.w;
+          xs[e] = h;
+          xl[e] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&split[s]);
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+    const int row_in_tile = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t aph[2] = {0, 0};
+    OutT* y = static_cast<OutT*>(p.y);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&tfull[acc], aph[acc]);
+      aph[acc] ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t row = t * BM + row_in_tile;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                             (uint32_t)(acc * p.BN);
+      for (int c0 = 0; c0 < p.BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
+        if (row < p.M) {
+          OutT* out = y + row * p.ldy;
+#pragma unroll
+          for (int j = 0; j < 16; j++) {
+            const int c = c0 + j;
+            if (c < p.N) {
+              float r = __fadd_rn(v[j], sbias[c]);
+              if (p.relu) r = relu_np(r);
+              out[c] = cvt_out<OutT>(r);
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile(
+        "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(
+            tmem_base),
+        "r"(p.tmem_cols));
+  }
+}
+
+__global__ void split_weights(const float* __restrict__ w, int64_t n,
+                              float* __restrict__ hi, float* __restrict__ lo) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = w[i];
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
+                              void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p,
+                                cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 2-D f32 map: inner dim `cols` (K), outer `rows`, row pitch `ld` elements,
+// box = 32 x box_rows, 128-B swizzle, zero fill out of bounds
+bool make_map(CUtensorMap* m, const float* ptr, int64_t rows, int64_t cols,
+              int64_t ld, int box_rows) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr),
+             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = kNumSMs;
+  }
+  return n;
+}
+
+}  // namespace
+
+bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
+                         const float* w, const float* b, int64_t n, int relu,
+                         void* y, int y_dtype, int64_t ldy, cudaStream_t s) {
+  if (rows <= 0) return true;
+  if (n < 1 || n > 256 || k < 1 || ldx % 4 != 0 || k % 4 != 0 ||
+      (reinterpret_cast<uintptr_t>(x) & 15) != 0)
+    return false;
+  const int BN = (int)((n + 15) / 16 * 16);
+  const int kblocks = (int)((k + BK - 1) / BK);
+  // split W once per call (tiny) into tf32 hi / lo halves
+  DevBuf<float> whl;
+  whl.alloc(2 * n * k);
+  split_weights<<<(unsigned)ceil_div(n * k, 256), 256, 0, s>>>(
+      w, n * k, whl.ptr, whl.ptr + n * k);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  CUtensorMap mx, mwh, mwl;
+  if (!make_map(&mx, x, rows, k, ldx, BM) ||
+      !make_map(&mwh, whl.ptr, n, k, k, BN) ||
+      !make_map(&mwl, whl.ptr + n * k, n, k, k, BN))
+    return false;
+  const int stage_bytes = 2 * BM * BK * 4 + 2 * BN * BK * 4;
+  const int budget = 220 * 1024 - 1024 - 2048;
+  int stages = budget / stage_bytes;
+  if (stages > 4) stages = 4;
+  if (stages < 2) return false;
+  const int smem = 1024 + stages * stage_bytes + 8 * (3 * stages + 4) + 16 +
+                   4 * 256;
+  TcParams p{};
+  p.M = rows;
+  p.K = (int)k;
+  p.N = (int)n;
+  p.BN = BN;
+  p.stages = stages;
+  p.kblocks = kblocks;
+  p.relu = relu;
+  p.ldy = ldy;
+  p.bias = b;
+  p.y = y;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * BN)) cols <<= 1;
+  p.tmem_cols = cols;
+  const int64_t ntiles = (rows + BM - 1) / BM;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, num_sms());
+  auto launch = [&](auto kern) {
+    ATLAS_CUDA(cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kThreads, smem, s>>>(mx, mwh, mwl, p);
+  };
+  if (y_dtype == ATLAS_F32) launch(transform_tc_kernel<float>);
+  else if (y_dtype == ATLAS_F16) launch(transform_tc_kernel<__half>);
+  else launch(transform_tc_kernel<__nv_bfloat16>);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  // whl is freed at scope exit; cudaFree synchronises with the kernel
+  return true;
 }
 
 }  // namespace atlas

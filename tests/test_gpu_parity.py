@@ -173,3 +173,27 @@ def test_stable_transform_bit_exact_vs_reference_backend():
         got = MatmulBackend().apply(x, w, b)
         want = OE.stable_transform(x, w, b, relu=False)
         np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("m,k,n,relu", [(1000, 100, 128, True),
+                                        (4099, 128, 47, False),
+                                        (300, 256, 128, True),
+                                        (129, 8, 2, True), (64, 2048, 19, False),
+                                        (5000, 128, 256, True)])
+def test_tcgen05_transform_3xtf32_accuracy(m, k, n, relu):
+    """tcgen05 backend: |y - y_f64| <= 2e-6 * (|x| |w| row-col scale)."""
+    from paper_2605_09402_b200.compute import Tcgen05Backend
+    from paper_2605_09402_b200.storage import LayerWeights
+    from paper_2605_09402_b200.compute import transform
+    rng = np.random.default_rng(m + k + n)
+    x = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    w = (rng.uniform(-1, 1, (n, k)) / np.sqrt(k)).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, n).astype(np.float32)
+    got = transform(x, LayerWeights(k, n, w, b), apply_activation=relu,
+                    backend=Tcgen05Backend())
+    ref = x.astype(np.float64) @ w.astype(np.float64).T + b
+    if relu:
+        ref = np.maximum(ref, 0.0)
+    scale = np.abs(x).astype(np.float64) @ np.abs(w).astype(np.float64).T
+    err = np.abs(got - ref)
+    assert np.all(err <= 4e-6 * (scale + 1e-3)), float((err / (scale + 1e-3)).max())
