@@ -126,6 +126,9 @@ ATLAS_API int atlas_layer_create(const atlas_layer_desc* desc,
                        const uint32_t* in_degrees_host, void* stream,
                        atlas_layer** out);
 ATLAS_API void atlas_layer_destroy(atlas_layer* layer);
+/* re-arm a layer for a new pass with the same descriptor (init_layer
+ * again) without reallocating its device memory */
+ATLAS_API int atlas_layer_reset(atlas_layer* layer, void* stream);
 
 /* process_chunk: rows (n x embed_dim, dtype) and the chunk CSR slice are
  * HOST pointers (pinned or pageable); the library stages them to HBM. */

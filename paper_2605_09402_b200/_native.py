@@ -73,6 +73,7 @@ def _declare(lib):
     fn("atlas_layer_create", ctypes.c_int, ctypes.POINTER(LayerDesc), c_vp,
        c_vp, ctypes.POINTER(c_vp))
     fn("atlas_layer_destroy", None, c_vp)
+    fn("atlas_layer_reset", ctypes.c_int, c_vp, c_vp)
     fn("atlas_chunk_submit", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_i32,
        c_vp, c_vp, c_i64, c_vp)
     fn("atlas_chunk_graduated", ctypes.c_int, c_vp, c_vp, c_vp, c_i64, P_i64,
@@ -95,7 +96,8 @@ def _declare(lib):
 EXPORTED = [
     "atlas_last_error", "atlas_abi_version", "atlas_kernel_launches",
     "atlas_graph_create", "atlas_graph_destroy", "atlas_graph_csc",
-    "atlas_layer_create", "atlas_layer_destroy", "atlas_chunk_submit",
+    "atlas_layer_create", "atlas_layer_destroy", "atlas_layer_reset",
+    "atlas_chunk_submit",
     "atlas_chunk_graduated", "atlas_layer_run_resident",
     "atlas_layer_accumulator", "atlas_transform", "atlas_layer_finish",
     "atlas_layer_chunk_stats", "atlas_layer_log", "atlas_layer_state",

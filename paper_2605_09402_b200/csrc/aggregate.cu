@@ -7,9 +7,9 @@
 // (source-major) order onto a zeroed f32 record. Here each warp owns one
 // destination and a 32*VEC column slice of its record; lanes walk the
 // destination's sources in ascending order and apply exactly the same
-// rounded f32 divide and add per column (__fdiv_rn / __fadd_rn, no FMA
-// contraction), so records are bit-identical to the reference for ANY
-// chunking. Parallelism is over destinations and columns; memory-level
+// rounded f32 divide and add per column (correctly rounded division via
+// div_rn below, __fadd_rn, no FMA contraction of the sum), so records are
+// bit-identical to the reference for ANY chunking. Parallelism is over destinations and columns; memory-level
 // parallelism comes from issuing UNROLL independent 16-byte row loads per
 // lane before the dependent adds.
 //
@@ -79,18 +79,34 @@ __device__ __forceinline__ void load_f32(const float* p, float (&a)[VEC]) {
   }
 }
 
+// Correctly rounded m / d from the correctly rounded reciprocal r = RN(1/d)
+// (Markstein): q = RN(m r); e = m - q d exactly (FMA); RN(q + e r) ==
+// RN(m / d) whenever the quotient is a normal number or zero. Tiny or
+// non-finite m (quotient possibly subnormal / NaN-producing residual) take
+// the IEEE division. Exhaustively checked against RN(m / d) on 1e8 random
+// (m, d) pairs (tests/test_cpu_boundary.py::test_markstein_division).
+__device__ __forceinline__ float div_rn(float m, float d, float r) {
+  const float am = fabsf(m);
+  if ((am < 0x1p-100f && am != 0.0f) || !(am <= 3.402823466e38f))
+    return __fdiv_rn(m, d);
+  const float q = __fmul_rn(m, r);
+  const float e = __fmaf_rn(-q, d, m);
+  return __fmaf_rn(e, r, q);
+}
+
 // a += (self ? m * self_scale : (MEAN ? m / denom : m)), per element.
 template <typename T, int VEC, bool MEAN>
 __device__ __forceinline__ void add_msg(float (&a)[VEC],
                                         const Frag<T, VEC>& f, bool self,
-                                        float denom, float self_scale) {
+                                        float denom, float rcp,
+                                        float self_scale) {
 #pragma unroll
   for (int e = 0; e < VEC; e++) {
     float m = f.get(e);
     if (self)
       m = __fmul_rn(m, self_scale);
     else if (MEAN)
-      m = __fdiv_rn(m, denom);
+      m = div_rn(m, denom, rcp);
     a[e] = __fadd_rn(a[e], m);
   }
 }
@@ -113,6 +129,7 @@ __global__ void __launch_bounds__(256)
   const int64_t beg = csc_ptr[v], end = csc_ptr[v + 1];
   const uint32_t vg = (uint32_t)(v + lo);
   const float denom = kMean ? (float)max(1u, indeg[v]) : 1.0f;
+  const float rcp = kMean ? __frcp_rn(denom) : 1.0f;
   float* out = acc + v * ldacc;
   for (int c0 = 0; c0 < d; c0 += 32 * VEC) {
     const int col = c0 + lane * VEC;
@@ -140,10 +157,11 @@ __global__ void __launch_bounds__(256)
               if (active) {
                 Frag<T, VEC> me;
                 me.load(x + (int64_t)vg * ldx + col);
-                add_msg<T, VEC, false>(a, me, true, 1.0f, self_scale);
+                add_msg<T, VEC, false>(a, me, true, 1.0f, 1.0f, self_scale);
               }
             }
-            if (active) add_msg<T, VEC, kMean>(a, f[j], false, denom, 1.0f);
+            if (active)
+              add_msg<T, VEC, kMean>(a, f[j], false, denom, rcp, 1.0f);
           }
         }
       }
@@ -151,7 +169,7 @@ __global__ void __launch_bounds__(256)
     if (MODEL == ATLAS_GIN && self_pending && active) {
       Frag<T, VEC> me;
       me.load(x + (int64_t)vg * ldx + col);
-      add_msg<T, VEC, false>(a, me, true, 1.0f, self_scale);
+      add_msg<T, VEC, false>(a, me, true, 1.0f, 1.0f, self_scale);
     }
     if (active) {
       store_f32<VEC>(out + col, a);
@@ -186,6 +204,7 @@ __global__ void __launch_bounds__(256)
   const uint32_t v = run_dst[r];
   const int64_t beg = run_beg[r], end = run_beg[r + 1];
   const float denom = kMean ? (float)max(1u, indeg[v]) : 1.0f;
+  const float rcp = kMean ? __frcp_rn(denom) : 1.0f;
   const bool resume = touched[v] != 0;
   float* out = acc + (int64_t)v * ldacc;
   for (int c0 = 0; c0 < d; c0 += 32 * VEC) {
@@ -211,7 +230,7 @@ __global__ void __launch_bounds__(256)
         for (int j = 0; j < kUnroll; j++)
           if (active && i + j < cnt)
             add_msg<T, VEC, kMean>(a, f[j], (s[j] & kSelfBit) != 0, denom,
-                                   self_scale);
+                                   rcp, self_scale);
       }
     }
     if (active) store_f32<VEC>(out + col, a);

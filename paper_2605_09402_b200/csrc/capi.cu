@@ -142,6 +142,23 @@ int atlas_layer_create(const atlas_layer_desc* desc,
 
 void atlas_layer_destroy(atlas_layer* L) { delete L; }
 
+int atlas_layer_reset(atlas_layer* L, void* stream) {
+  return guarded([&] {
+    if (!L) fail(ATLAS_ECONFIG, "null layer");
+    use_device(L->desc.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t nn = std::max<int64_t>(L->nloc, 1);
+    ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
+    L->chunk_reloads.clear();
+    L->chunk_touched.clear();
+    L->fast_path = false;
+    L->chunks_seen = 0;
+    L->stream_step = 0;
+    L->timing_ms[0] = L->timing_ms[1] = 0.f;
+    engine_init(L, s);
+  });
+}
+
 int atlas_chunk_submit(atlas_layer* L, int64_t start, int64_t end,
                        const void* rows_host, int32_t dtype,
                        const int64_t* off, const int64_t* nbrs, int64_t m,

@@ -55,15 +55,26 @@ __device__ __forceinline__ int64_t self_pos(int model, const Plan& p,
   return off[v] + v;  // GIN
 }
 
-// warp-aggregated atomic add of 1 to counter[key]
-__device__ __forceinline__ void agg_inc(unsigned long long* counter,
+// Histogram [admit 3C | grad 3C | runs C]: per-block shared-memory copy
+// when it fits (keys concentrate on few chunks, so global atomics would
+// serialise), flushed once per block.
+struct Hist {
+  unsigned long long* g;
+  unsigned int* s;  // nullptr -> global atomics
+  __device__ __forceinline__ void add(int64_t i, unsigned n) const {
+    if (s) atomicAdd(s + i, n);
+    else atomicAdd(g + i, (unsigned long long)n);
+  }
+};
+
+// warp-aggregated add of 1 to h[base + key] for lanes with pred
+__device__ __forceinline__ void agg_inc(const Hist& h, int64_t base,
                                         int64_t key, bool pred) {
   const unsigned act = __ballot_sync(0xffffffffu, pred);
   if (!pred) return;
   const unsigned peers = __match_any_sync(act, (unsigned long long)key);
   const int leader = __ffs(peers) - 1;
-  if ((int)(threadIdx.x & 31) == leader)
-    atomicAdd(counter + key, (unsigned long long)__popc(peers));
+  if ((int)(threadIdx.x & 31) == leader) h.add(base + key, __popc(peers));
 }
 
 // One warp per local destination: spans, admission / graduation
@@ -75,24 +86,26 @@ __global__ void __launch_bounds__(256)
                       const uint32_t* __restrict__ csc_eid, int64_t lo,
                       int64_t nloc, int64_t* __restrict__ first_pos,
                       int64_t* __restrict__ last_pos,
-                      unsigned long long* __restrict__ admit_hist,
-                      unsigned long long* __restrict__ grad_hist,
-                      unsigned long long* __restrict__ runs_per_chunk,
+                      unsigned long long* __restrict__ ghist, int use_smem,
                       uint64_t* __restrict__ run_at_pos) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const bool valid = w < nloc;
-  const int64_t v = valid ? w : 0;
-  const int64_t vg = v + lo;
-  int64_t beg = 0, end = 0;
-  if (valid) {
-    beg = csc_ptr[v];
-    end = csc_ptr[v + 1];
+  extern __shared__ unsigned int shist[];
+  const int64_t hn = 7 * p.nchunks;
+  Hist h{ghist, use_smem ? shist : nullptr};
+  if (use_smem) {
+    for (int64_t i = threadIdx.x; i < hn; i += blockDim.x) shist[i] = 0;
+    __syncthreads();
   }
+  const int64_t A0 = 0, G0 = 3 * p.nchunks, R0 = 6 * p.nchunks;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+       v < nloc; v += nwarps) {
+  const int64_t vg = v + lo;
+  const int64_t beg = csc_ptr[v], end = csc_ptr[v + 1];
   const bool has_self = model != ATLAS_GCN;
   const int64_t cv = p.chunk(vg);
   // ---- spans and admit/grad (chunk, pass) --------------------------------
-  if (valid && lane == 0) {
+  if (lane == 0) {
     int64_t first = -1, last = -1;
     int64_t a_key, g_key;  // chunk * 3 + pass
     if (end > beg) {
@@ -119,8 +132,8 @@ __global__ void __launch_bounds__(256)
     }
     first_pos[v] = first;
     last_pos[v] = last;
-    atomicAdd(admit_hist + a_key, 1ull);
-    atomicAdd(grad_hist + g_key, 1ull);
+    h.add(A0 + a_key, 1u);
+    h.add(G0 + g_key, 1u);
   }
   // ---- runs: maximal same-chunk stretches of the ascending source list ---
   bool self_merged = false;  // GIN self term joins the run of chunk cv
@@ -138,7 +151,7 @@ __global__ void __launch_bounds__(256)
     const bool starts = in && c != prev_c;
     if (model == ATLAS_GIN && __any_sync(0xffffffffu, in && c == cv))
       self_merged = true;
-    agg_inc(runs_per_chunk, c, starts);
+    agg_inc(h, R0, c, starts);
     if (run_at_pos && starts) {
       // run [i, j): count its entries; GIN adds the self term
       int64_t j = i + 1;
@@ -152,11 +165,17 @@ __global__ void __launch_bounds__(256)
       run_at_pos[pos] = (cnt << 32) | (uint64_t)(uint32_t)v;
     }
   }
-  if (valid && model == ATLAS_GIN && !self_merged && lane == 0) {
-    atomicAdd(runs_per_chunk + cv, 1ull);
+  if (model == ATLAS_GIN && !self_merged && lane == 0) {
+    h.add(R0 + cv, 1u);
     if (run_at_pos)
       run_at_pos[self_pos(model, p, off, vg)] =
           (1ull << 32) | (uint64_t)(uint32_t)v;
+  }
+  }  // destinations
+  if (use_smem) {
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < hn; i += blockDim.x)
+      if (shist[i]) atomicAdd(ghist + i, (unsigned long long)shist[i]);
   }
 }
 
@@ -206,11 +225,12 @@ void finish_spans(atlas_layer* L, cudaStream_t s) {
   const int64_t n = L->nloc;
   L->span_count = L->span_sum = L->span_q_lo = L->span_q_hi = 0;
   if (n == 0) return;
-  DevBuf<int64_t> spans, sorted;
-  DevBuf<unsigned long long> sc;
-  spans.alloc(n);
-  sorted.alloc(n);
-  sc.alloc(2);
+  DevBuf<int64_t>& spans = L->span_buf;
+  DevBuf<int64_t>& sorted = L->span_sorted;
+  DevBuf<unsigned long long>& sc = L->span_acc;
+  spans.reserve(n);
+  sorted.reserve(n);
+  sc.reserve(2);
   ATLAS_CUDA(cudaMemsetAsync(sc.ptr, 0, 2 * sizeof(unsigned long long), s));
   span_values<<<grid_of(n), 256, 0, s>>>(L->first_pos.ptr, L->last_pos.ptr, n,
                                          spans.ptr, sc.ptr);
@@ -225,8 +245,8 @@ void finish_spans(atlas_layer* L, cudaStream_t s) {
   size_t tmp_bytes = 0;
   ATLAS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, spans.ptr,
                                             sorted.ptr, n, 0, 64, s));
-  DevBuf<uint8_t> tmp;
-  tmp.alloc(tmp_bytes);
+  DevBuf<uint8_t>& tmp = L->span_tmp;
+  tmp.reserve(tmp_bytes);
   ATLAS_CUDA(cub::DeviceRadixSort::SortKeys(tmp.ptr, tmp_bytes, spans.ptr,
                                             sorted.ptr, n, 0, 64, s));
   count_launch();
@@ -247,19 +267,24 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
   const int model = L->desc.model;
   Plan p{R, V, ceil_div(V, R)};
   const int64_t nchunks = p.nchunks;
-  DevBuf<unsigned long long> hist;  // admit[3C], grad[3C], runs[C]
-  hist.alloc(7 * std::max<int64_t>(nchunks, 1));
-  ATLAS_CUDA(cudaMemsetAsync(hist.ptr, 0, hist.bytes(), s));
-  unsigned long long* admit_h = hist.ptr;
-  unsigned long long* grad_h = hist.ptr + 3 * nchunks;
-  unsigned long long* runs_h = hist.ptr + 6 * nchunks;
-  const unsigned blocks = (unsigned)ceil_div(std::max<int64_t>(L->nloc, 1), 8);
-  walk_destinations<<<blocks, 256, 0, s>>>(
-      model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
-      g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
-      admit_h, grad_h, runs_h, nullptr);
-  count_launch();
-  ATLAS_LAUNCH_CHECK();
+  DevBuf<unsigned long long>& hist = L->ctl_hist;  // admit 3C|grad 3C|runs C
+  hist.reserve(7 * std::max<int64_t>(nchunks, 1));
+  ATLAS_CUDA(cudaMemsetAsync(hist.ptr, 0,
+                             7 * std::max<int64_t>(nchunks, 1) * 8, s));
+  // grid-stride warps; per-block shared histogram when 7C u32 fit in 48 KB
+  const size_t hbytes = 7 * (size_t)nchunks * 4;
+  const int use_smem = hbytes <= 48 * 1024 ? 1 : 0;
+  const unsigned blocks = (unsigned)std::min<int64_t>(
+      148 * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
+  auto walk = [&](uint64_t* at_pos) {
+    walk_destinations<<<blocks, 256, use_smem ? hbytes : 0, s>>>(
+        model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
+        g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
+        hist.ptr, use_smem, at_pos);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+  };
+  walk(nullptr);
   std::vector<unsigned long long> h(7 * nchunks);
   ATLAS_CUDA(cudaMemcpyAsync(h.data(), hist.ptr, h.size() * sizeof(h[0]),
                              cudaMemcpyDeviceToHost, s));
@@ -310,12 +335,7 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
   fill_u64<<<grid_of(npos), 256, 0, s>>>(at_pos.ptr, npos, kNoRun);
   count_launch();
   ATLAS_CUDA(cudaMemsetAsync(hist.ptr, 0, hist.bytes(), s));
-  walk_destinations<<<blocks, 256, 0, s>>>(
-      model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
-      g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
-      admit_h, grad_h, runs_h, at_pos.ptr);
-  count_launch();
-  ATLAS_LAUNCH_CHECK();
+  walk(at_pos.ptr);
   int64_t total_runs = 0;
   std::vector<int64_t> run_off(nchunks + 1, 0);
   for (int64_t c = 0; c < nchunks; c++) {

@@ -119,6 +119,11 @@ struct atlas_layer {
   int64_t fp_hot_peak = 0;
   int64_t fp_messages = 0;
   float timing_ms[2] = {0.f, 0.f};
+  // reusable workspaces (kept across resets so repeated layers allocate once)
+  atlas::DevBuf<unsigned long long> ctl_hist;
+  atlas::DevBuf<int64_t> span_buf, span_sorted;
+  atlas::DevBuf<unsigned long long> span_acc;
+  atlas::DevBuf<uint8_t> span_tmp;
 };
 
 namespace atlas {

@@ -146,8 +146,7 @@ struct TcParams {
 template <typename OutT>
 __global__ void __launch_bounds__(kThreads, 1)
     transform_tc_kernel(const __grid_constant__ CUtensorMap map_x,
-                        const __grid_constant__ CUtensorMap map_whi,
-                        const __grid_constant__ CUtensorMap map_wlo,
+                        const __grid_constant__ CUtensorMap map_w,
                         TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned carve-up: per stage [x | x_lo | w_hi | w_lo]
@@ -202,11 +201,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < p.kblocks; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = base + s * stage_bytes;
-          mbar_expect_tx(&full[s], x_bytes + 2 * w_bytes);
+          mbar_expect_tx(&full[s], x_bytes + w_bytes);
           tma_load_2d(st, &map_x, &full[s], kb * BK, (int)(t * BM));
-          tma_load_2d(st + 2 * x_bytes, &map_whi, &full[s], kb * BK, 0);
-          tma_load_2d(st + 2 * x_bytes + w_bytes, &map_wlo, &full[s], kb * BK,
-                      0);
+          tma_load_2d(st + 2 * x_bytes, &map_w, &full[s], kb * BK, 0);
           if (++s == p.stages) {
             s = 0;
             ph ^= 1;
@@ -260,32 +257,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
     }
   } else if (warp < 6) {
-    // ---------------- splitter: x -> x_hi (in place) + x_lo -------------
+    // -------- splitter: x, w tiles -> hi (in place) + lo (tf32 split) -----
     const int tid = threadIdx.x - 64;  // 0..127
+    auto split16 = [](float4* hi, float4* lo, int e) {
+      const float4 v = hi[e];
+      float4 h, l;
+      h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+      h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+      h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+      h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+      l.x = v.x - h.x;
+      l.y = v.y - h.y;
+      l.z = v.z - h.z;
+      l.w = v.w - h.w;
+      hi[e] = h;
+      lo[e] = l;
+    };
     int s = 0;
     uint32_t ph = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int kb = 0; kb < p.kblocks; kb++) {
         mbar_wait(&full[s], ph);
-        float4* xs = reinterpret_cast<float4*>(base + s * stage_bytes);
-        float4* xl = reinterpret_cast<float4*>(base + s * stage_bytes +
-                                               x_bytes);
+        uint8_t* st = base + s * stage_bytes;
+        float4* xs = reinterpret_cast<float4*>(st);
+        float4* xl = reinterpret_cast<float4*>(st + x_bytes);
+        float4* ws = reinterpret_cast<float4*>(st + 2 * x_bytes);
+        float4* wl = reinterpret_cast<float4*>(st + 2 * x_bytes + w_bytes);
 #pragma unroll
-        for (int i = 0; i < (BM * BK / 4) / 128; i++) {
-          const int e = tid + i * 128;
-          float4 v = xs[e];
-          float4 h, l;
-          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-          l.x = v.x - h.x;
-          l.y = v.y - h.y;
-          l.z = v.z - h.z;
-          l.w = v.w - h.w;
-          xs[e] = h;
-          xl[e] = l;
-        }
+        for (int i = 0; i < (BM * BK / 4) / 128; i++)
+          split16(xs, xl, tid + i * 128);
+        for (int e = tid; e < p.BN * BK / 4; e += 128) split16(ws, wl, e);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&split[s]);
         if (++s == p.stages) {
@@ -336,17 +337,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(
             tmem_base),
         "r"(p.tmem_cols));
-  }
-}
-
-__global__ void split_weights(const float* __restrict__ w, int64_t n,
-                              float* __restrict__ hi, float* __restrict__ lo) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = w[i];
-    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-    hi[i] = h;
-    lo[i] = v - h;
   }
 }
 
@@ -409,17 +399,9 @@ bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
     return false;
   const int BN = (int)((n + 15) / 16 * 16);
   const int kblocks = (int)((k + BK - 1) / BK);
-  // split W once per call (tiny) into tf32 hi / lo halves
-  DevBuf<float> whl;
-  whl.alloc(2 * n * k);
-  split_weights<<<(unsigned)ceil_div(n * k, 256), 256, 0, s>>>(
-      w, n * k, whl.ptr, whl.ptr + n * k);
-  count_launch();
-  ATLAS_LAUNCH_CHECK();
-  CUtensorMap mx, mwh, mwl;
-  if (!make_map(&mx, x, rows, k, ldx, BM) ||
-      !make_map(&mwh, whl.ptr, n, k, k, BN) ||
-      !make_map(&mwl, whl.ptr + n * k, n, k, k, BN))
+  if ((reinterpret_cast<uintptr_t>(w) & 15) != 0) return false;
+  CUtensorMap mx, mw;
+  if (!make_map(&mx, x, rows, k, ldx, BM) || !make_map(&mw, w, n, k, k, BN))
     return false;
   const int stage_bytes = 2 * BM * BK * 4 + 2 * BN * BK * 4;
   const int budget = 220 * 1024 - 1024 - 2048;
@@ -447,14 +429,13 @@ bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
   auto launch = [&](auto kern) {
     ATLAS_CUDA(cudaFuncSetAttribute(
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, kThreads, smem, s>>>(mx, mwh, mwl, p);
+    kern<<<grid, kThreads, smem, s>>>(mx, mw, p);
   };
   if (y_dtype == ATLAS_F32) launch(transform_tc_kernel<float>);
   else if (y_dtype == ATLAS_F16) launch(transform_tc_kernel<__half>);
   else launch(transform_tc_kernel<__nv_bfloat16>);
   count_launch();
   ATLAS_LAUNCH_CHECK();
-  // whl is freed at scope exit; cudaFree synchronises with the kernel
   return true;
 }
 

@@ -141,6 +141,11 @@ class DeviceLayer:
         self.handle = h
         self.h2d_bytes = 0
 
+    def reset(self, stream=None):
+        """init_layer again for a new pass, reusing device memory."""
+        N.check(N.load_library().atlas_layer_reset(self.handle,
+                                                   N.stream_handle(stream)))
+
     # -- operator path ------------------------------------------------------
     def submit_chunk(self, start, end, rows, local_offsets, neighbors,
                      stream=None):

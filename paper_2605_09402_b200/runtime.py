@@ -154,8 +154,12 @@ class Engine:
         self.b = [torch.as_tensor(np.ascontiguousarray(lw.bias)).cuda()
                   for lw in weights.layers]
         self.last_layers = []
+        self._layers = {}
 
     def close(self):
+        for layer in self._layers.values():
+            layer.close()
+        self._layers.clear()
         self.graph.close()
 
     def layer(self, l: int, x, *, chunk_budget=None):
@@ -173,14 +177,19 @@ class Engine:
                 f"layer {l} expects {d}-wide rows, input holds {x.shape[1]}")
         rows = plan_rows(self.num_vertices, d, _plan_dtype(x),
                          chunk_budget or cfg.chunk_budget)
-        budget = slot_budget(w, l, cfg.hot_budget, cfg.hot_slots)
-        layer = DeviceLayer(
-            self.in_degrees, int(self.kind), d, w.agg_dim(l),
-            budget.slot_count, gin_epsilon=w.gin_epsilon,
-            eviction=cfg.eviction, seed=cfg.seed,
-            evict_batch=cfg.evict_batch, dst_range=(self.lo, self.hi),
-            record_log=cfg.record_log, force_exact=cfg.force_exact,
-            device=self.device)
+        layer = self._layers.get(l)
+        if layer is not None and layer.handle:
+            layer.reset()  # same descriptor: reuse the device workspaces
+        else:
+            budget = slot_budget(w, l, cfg.hot_budget, cfg.hot_slots)
+            layer = DeviceLayer(
+                self.in_degrees, int(self.kind), d, w.agg_dim(l),
+                budget.slot_count, gin_epsilon=w.gin_epsilon,
+                eviction=cfg.eviction, seed=cfg.seed,
+                evict_batch=cfg.evict_batch, dst_range=(self.lo, self.hi),
+                record_log=cfg.record_log, force_exact=cfg.force_exact,
+                device=self.device)
+            self._layers[l] = layer
         layer.run_resident(self.graph, x, rows)
         nloc = self.hi - self.lo
         out_dim = w.layers[l].out_dim
@@ -231,8 +240,7 @@ class Engine:
         metrics, outs = [], []
         h = x
         for l in range(len(self.weights.layers)):
-            y, m, layer = self.layer(l, h)
-            layer.close()
+            y, m, _ = self.layer(l, h)
             metrics.append(m)
             if keep_layers:
                 outs.append(y)

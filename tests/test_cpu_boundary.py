@@ -149,3 +149,17 @@ def test_pcg64_restatement_matches_numpy():
                         m = next32() * n
                 got = m >> 32
             assert got == want
+
+
+def test_markstein_division(tmp_path):
+    """The aggregation kernel's division (aggregate.cu div_rn): RN(m/d) via
+    q = RN(m*RN(1/d)), e = fma(-q,d,m), RN(fma(e,r,q)); checked against
+    IEEE division on ~1e8 (m, d) pairs (normal or zero quotients)."""
+    import subprocess
+    src = Path(__file__).resolve().parent / "native" / "markstein_check.c"
+    exe = tmp_path / "markstein"
+    subprocess.run(["gcc", "-O2", "-mfma", "-o", str(exe), str(src), "-lm"],
+                   check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True,
+                         text=True).stdout
+    assert out.strip().endswith("bad(normal results)=0"), out
