@@ -85,17 +85,22 @@ __device__ __forceinline__ void load_f32(const float* p, float (&a)[VEC]) {
 // non-finite m (quotient possibly subnormal / NaN-producing residual) take
 // the IEEE division. Exhaustively checked against RN(m / d) on 1e8 random
 // (m, d) pairs (tests/test_cpu_boundary.py::test_markstein_division).
+// GUARD=false is only used after scan_extremes() proved the layer input
+// holds no such value (one read of the input per layer).
+template <bool GUARD>
 __device__ __forceinline__ float div_rn(float m, float d, float r) {
-  const float am = fabsf(m);
-  if ((am < 0x1p-100f && am != 0.0f) || !(am <= 3.402823466e38f))
-    return __fdiv_rn(m, d);
+  if (GUARD) {
+    const float am = fabsf(m);
+    if ((am < 0x1p-100f && am != 0.0f) || !(am <= 3.402823466e38f))
+      return __fdiv_rn(m, d);
+  }
   const float q = __fmul_rn(m, r);
   const float e = __fmaf_rn(-q, d, m);
   return __fmaf_rn(e, r, q);
 }
 
 // a += (self ? m * self_scale : (MEAN ? m / denom : m)), per element.
-template <typename T, int VEC, bool MEAN>
+template <typename T, int VEC, bool MEAN, bool GUARD = true>
 __device__ __forceinline__ void add_msg(float (&a)[VEC],
                                         const Frag<T, VEC>& f, bool self,
                                         float denom, float rcp,
@@ -106,26 +111,41 @@ __device__ __forceinline__ void add_msg(float (&a)[VEC],
     if (self)
       m = __fmul_rn(m, self_scale);
     else if (MEAN)
-      m = div_rn(m, denom, rcp);
+      m = div_rn<GUARD>(m, denom, rcp);
     a[e] = __fadd_rn(a[e], m);
   }
+}
+
+// flag[0] |= 1 if any element of x (rows x d) is non-finite or a nonzero
+// with |x| < 2^-100 (the inputs for which div_rn needs the IEEE path)
+template <typename T>
+__global__ void scan_extremes(const T* __restrict__ x, int64_t rows, int d,
+                              int64_t ldx, int* __restrict__ flag) {
+  int bad = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+       r < rows; r += nwarps) {
+    const T* row = x + r * ldx;
+    for (int c = lane; c < d; c += 32) {
+      const float v = fabsf(to_f32(row[c]));
+      bad |= (v < 0x1p-100f && v != 0.0f) || !(v <= 3.402823466e38f);
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
 // ---------------------------------------------------------------------------
 // resident front end: warp per destination, CSC walk
 
-template <typename T, int VEC, int MODEL>
-__global__ void __launch_bounds__(256)
-    agg_resident(const T* __restrict__ x, int64_t ldx,
-                 const int64_t* __restrict__ csc_ptr,
-                 const uint32_t* __restrict__ csc_src,
-                 const uint32_t* __restrict__ indeg, int64_t lo,
-                 int64_t nloc, int d, float* __restrict__ acc,
-                 int64_t ldacc, float self_scale) {
+template <typename T, int VEC, int MODEL, bool GUARD>
+__device__ __forceinline__ void resident_body(
+    const T* __restrict__ x, int64_t ldx, const int64_t* __restrict__ csc_ptr,
+    const uint32_t* __restrict__ csc_src, const uint32_t* __restrict__ indeg,
+    int64_t lo, int64_t v, int d, float* __restrict__ acc, int64_t ldacc,
+    float self_scale) {
   constexpr bool kMean = MODEL != ATLAS_GIN;
   const int lane = threadIdx.x & 31;
-  const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (v >= nloc) return;
   const int64_t beg = csc_ptr[v], end = csc_ptr[v + 1];
   const uint32_t vg = (uint32_t)(v + lo);
   const float denom = kMean ? (float)max(1u, indeg[v]) : 1.0f;
@@ -161,7 +181,7 @@ __global__ void __launch_bounds__(256)
               }
             }
             if (active)
-              add_msg<T, VEC, kMean>(a, f[j], false, denom, rcp, 1.0f);
+              add_msg<T, VEC, kMean, GUARD>(a, f[j], false, denom, rcp, 1.0f);
           }
         }
       }
@@ -183,6 +203,26 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
+}
+
+// 6 blocks of 8 warps per SM (<= 40 registers): more rows in flight per SM
+template <typename T, int VEC, int MODEL>
+__global__ void __launch_bounds__(256, 6)
+    agg_resident(const T* __restrict__ x, int64_t ldx,
+                 const int64_t* __restrict__ csc_ptr,
+                 const uint32_t* __restrict__ csc_src,
+                 const uint32_t* __restrict__ indeg, int64_t lo,
+                 int64_t nloc, int d, float* __restrict__ acc,
+                 int64_t ldacc, float self_scale,
+                 const int* __restrict__ guard_flag) {
+  const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (v >= nloc) return;
+  if (*guard_flag)
+    resident_body<T, VEC, MODEL, true>(x, ldx, csc_ptr, csc_src, indeg, lo, v,
+                                       d, acc, ldacc, self_scale);
+  else
+    resident_body<T, VEC, MODEL, false>(x, ldx, csc_ptr, csc_src, indeg, lo,
+                                        v, d, acc, ldacc, self_scale);
 }
 
 // ---------------------------------------------------------------------------
@@ -273,10 +313,16 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
                     cudaStream_t s) {
   const int64_t blocks = ceil_div(g->nloc, 8);
   if (blocks == 0) return;
+  // one pass over the input decides whether the division guard is needed
+  g->scan_flag.reserve(1);
+  ATLAS_CUDA(cudaMemsetAsync(g->scan_flag.ptr, 0, sizeof(int), s));
+  scan_extremes<T><<<148 * 8, 256, 0, s>>>(x, g->V, d, ldx, g->scan_flag.ptr);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
   auto go = [&](auto kern) {
-    kern<<<(unsigned)blocks, 256, 0, s>>>(x, ldx, g->csc_ptr.ptr,
-                                          g->csc_src.ptr, g->indeg.ptr, g->lo,
-                                          g->nloc, d, acc, ldacc, eps1);
+    kern<<<(unsigned)blocks, 256, 0, s>>>(
+        x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo, g->nloc,
+        d, acc, ldacc, eps1, g->scan_flag.ptr);
   };
   if (model == ATLAS_GCN) go(agg_resident<T, VEC, ATLAS_GCN>);
   else if (model == ATLAS_SAGE) go(agg_resident<T, VEC, ATLAS_SAGE>);

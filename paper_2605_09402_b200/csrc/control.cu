@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256)
                       int64_t nloc, int64_t* __restrict__ first_pos,
                       int64_t* __restrict__ last_pos,
                       unsigned long long* __restrict__ ghist, int use_smem,
-                      uint64_t* __restrict__ run_at_pos) {
+                      uint64_t* __restrict__ run_at_pos, int count_runs) {
   extern __shared__ unsigned int shist[];
   const int64_t hn = 7 * p.nchunks;
   Hist h{ghist, use_smem ? shist : nullptr};
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256)
   }
   // ---- runs: maximal same-chunk stretches of the ascending source list ---
   bool self_merged = false;  // GIN self term joins the run of chunk cv
-  for (int64_t base = beg; base < end; base += 32) {
+  for (int64_t base = beg; count_runs && base < end; base += 32) {
     const int64_t i = base + lane;
     const bool in = i < end;
     int64_t u = 0, c = -1;
@@ -276,15 +276,21 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
   const int use_smem = hbytes <= 48 * 1024 ? 1 : 0;
   const unsigned blocks = (unsigned)std::min<int64_t>(
       148 * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
-  auto walk = [&](uint64_t* at_pos) {
+  auto walk = [&](uint64_t* at_pos, int count_runs) {
     walk_destinations<<<blocks, 256, use_smem ? hbytes : 0, s>>>(
         model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
         g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
-        hist.ptr, use_smem, at_pos);
+        hist.ptr, use_smem, at_pos, count_runs);
     count_launch();
     ATLAS_LAUNCH_CHECK();
   };
-  walk(nullptr);
+  // A pass never holds more than nloc destinations, so when sub_batch >=
+  // nloc every pass is one sub-batch and the per-chunk run counts (an E-wide
+  // walk) are not needed to prove it; they only feed reload-% denominators,
+  // whose numerators are zero on the eviction-free path.
+  const bool need_runs = L->sub_batch < L->nloc || L->desc.record_log ||
+                         L->desc.force_exact;
+  walk(nullptr, need_runs ? 1 : 0);
   std::vector<unsigned long long> h(7 * nchunks);
   ATLAS_CUDA(cudaMemcpyAsync(h.data(), hist.ptr, h.size() * sizeof(h[0]),
                              cudaMemcpyDeviceToHost, s));
@@ -335,7 +341,10 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
   fill_u64<<<grid_of(npos), 256, 0, s>>>(at_pos.ptr, npos, kNoRun);
   count_launch();
   ATLAS_CUDA(cudaMemsetAsync(hist.ptr, 0, hist.bytes(), s));
-  walk(at_pos.ptr);
+  walk(at_pos.ptr, 1);
+  ATLAS_CUDA(cudaMemcpyAsync(h.data(), hist.ptr, h.size() * sizeof(h[0]),
+                             cudaMemcpyDeviceToHost, s));
+  ATLAS_CUDA(cudaStreamSynchronize(s));
   int64_t total_runs = 0;
   std::vector<int64_t> run_off(nchunks + 1, 0);
   for (int64_t c = 0; c < nchunks; c++) {

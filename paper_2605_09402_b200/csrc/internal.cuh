@@ -17,6 +17,7 @@ struct atlas_graph {
   atlas::DevBuf<uint32_t> csc_src;  // eloc, source id (global), ascending per dst
   atlas::DevBuf<uint32_t> csc_eid;  // eloc, CSR edge index of the entry
   atlas::DevBuf<uint32_t> indeg;    // nloc
+  mutable atlas::DevBuf<int> scan_flag;  // input needs the guarded division
 };
 
 namespace atlas {

@@ -297,33 +297,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------- epilogue ----------------
+    // each thread owns one accumulator row (TMEM lane); 32x16 blocks go
+    // through a per-warp smem transpose so global stores are 64-B runs
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
-    const int row_in_tile = quarter * 32 + lane;
+    float* stage = sbias + 256 + (warp - 6) * 32 * 17;
     int acc = 0;
     uint32_t aph[2] = {0, 0};
     OutT* y = static_cast<OutT*>(p.y);
+    const int half = lane >> 4, col16 = lane & 15;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       mbar_wait(&tfull[acc], aph[acc]);
       aph[acc] ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int64_t row = t * BM + row_in_tile;
+      const int64_t row0 = t * BM + quarter * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
                              (uint32_t)(acc * p.BN);
       for (int c0 = 0; c0 < p.BN; c0 += 16) {
         float v[16];
         tmem_ld16(taddr + c0, v);
-        if (row < p.M) {
-          OutT* out = y + row * p.ldy;
 #pragma unroll
-          for (int j = 0; j < 16; j++) {
-            const int c = c0 + j;
-            if (c < p.N) {
-              float r = __fadd_rn(v[j], sbias[c]);
-              if (p.relu) r = relu_np(r);
-              out[c] = cvt_out<OutT>(r);
-            }
+        for (int j = 0; j < 16; j++) stage[lane * 17 + j] = v[j];
+        __syncwarp();
+        const int c = c0 + col16;
+        const float bias = sbias[c];
+#pragma unroll 4
+        for (int rr = 0; rr < 32; rr += 2) {
+          const int r = rr + half;
+          const int64_t row = row0 + r;
+          if (row < p.M && c < p.N) {
+            float o = __fadd_rn(stage[r * 17 + col16], bias);
+            if (p.relu) o = relu_np(o);
+            y[row * p.ldy + c] = cvt_out<OutT>(o);
           }
         }
+        __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[acc]);
@@ -404,12 +411,12 @@ bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
   if (!make_map(&mx, x, rows, k, ldx, BM) || !make_map(&mw, w, n, k, k, BN))
     return false;
   const int stage_bytes = 2 * BM * BK * 4 + 2 * BN * BK * 4;
-  const int budget = 220 * 1024 - 1024 - 2048;
+  const int budget = 220 * 1024 - 1024 - 2048 - 4 * 32 * 17 * 4;
   int stages = budget / stage_bytes;
   if (stages > 4) stages = 4;
   if (stages < 2) return false;
   const int smem = 1024 + stages * stage_bytes + 8 * (3 * stages + 4) + 16 +
-                   4 * 256;
+                   4 * 256 + 4 * 32 * 17 * 4;
   TcParams p{};
   p.M = rows;
   p.K = (int)k;

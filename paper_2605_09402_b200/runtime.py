@@ -221,19 +221,7 @@ class Engine:
         """All ranks' ranges -> full (V, out) next-layer input (NCCL)."""
         if self.world == 1:
             return y_local
-        import torch
-        import torch.distributed as dist
-
-        w = max(h - l for l, h in self.ranges)
-        pad = torch.zeros((w, y_local.shape[1]), dtype=y_local.dtype,
-                          device=y_local.device)
-        pad[:y_local.shape[0]] = y_local
-        full = torch.empty((w * self.world, y_local.shape[1]),
-                           dtype=y_local.dtype, device=y_local.device)
-        dist.all_gather_into_tensor(full, pad, group=self.group)
-        parts = [full[g * w:g * w + (h - l)]
-                 for g, (l, h) in enumerate(self.ranges)]
-        return torch.cat(parts, dim=0)
+        return gather_ranges(y_local, self.ranges, self.group)
 
     def infer(self, x, keep_layers: bool = False):
         """All layers; returns (final local output, [LayerMetrics])."""
@@ -248,6 +236,30 @@ class Engine:
                 h = self.gather(y)
         self.last_layers = outs
         return y, metrics
+
+
+def gather_ranges(y_local, ranges, group=None):
+    """Reassemble the next layer's full input from every rank's
+    destination range (partition_ranges order). One all-gather of
+    equal-size padded blocks: NCCL over NVLink on GPUs, gloo on CPU."""
+    import torch
+    import torch.distributed as dist
+
+    world = len(ranges)
+    w = max(h - l for l, h in ranges)
+    pad = torch.zeros((w, y_local.shape[1]), dtype=y_local.dtype,
+                      device=y_local.device)
+    pad[:y_local.shape[0]] = y_local
+    if dist.get_backend(group) == "nccl":
+        full = torch.empty((w * world, y_local.shape[1]), dtype=y_local.dtype,
+                           device=y_local.device)
+        dist.all_gather_into_tensor(full, pad, group=group)
+        blocks = [full[g * w:(g + 1) * w] for g in range(world)]
+    else:
+        blocks = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(blocks, pad, group=group)
+    return torch.cat([blocks[g][:h - l] for g, (l, h) in enumerate(ranges)],
+                     dim=0)
 
 
 def _load_graph(topology_path, in_degrees):
