@@ -116,6 +116,15 @@ ATLAS_API int atlas_graph_create(int32_t device, int64_t num_vertices,
                        const uint32_t* neighbors_host,
                        const uint32_t* in_degrees_host, int64_t dst_lo,
                        int64_t dst_hi, void* stream, atlas_graph** out);
+/* re-upload a (new) CSR for the same destination range into the existing
+ * device buffers and rebuild the CSC view; no allocation when the graph
+ * has the same or a smaller size */
+ATLAS_API int atlas_graph_update(atlas_graph* g, int64_t num_vertices,
+                                 int64_t num_edges,
+                                 const int64_t* offsets_host,
+                                 const uint32_t* neighbors_host,
+                                 const uint32_t* in_degrees_host,
+                                 void* stream);
 ATLAS_API void atlas_graph_destroy(atlas_graph* g);
 /* device pointers of the CSC view (csc_ptr int64[nloc+1], csc_src u32) */
 ATLAS_API int atlas_graph_csc(const atlas_graph* g, const int64_t** csc_ptr,
@@ -150,6 +159,15 @@ ATLAS_API int atlas_chunk_graduated(atlas_layer* layer, int64_t* ids, float* row
 ATLAS_API int atlas_layer_run_resident(atlas_layer* layer, const atlas_graph* graph,
                              const void* x_dev, int32_t dtype, int64_t ldx,
                              int64_t chunk_rows, void* stream);
+/* same layer pass, but the input stays in (pinned) HOST memory: it is
+ * streamed to HBM in tiles of tile_rows rows, double-buffered on a side
+ * copy stream, and every tile is aggregated as soon as it lands (SURVEY.md
+ * kernel K1 + K3). Records are bit-identical to the resident pass. */
+ATLAS_API int atlas_layer_run_streamed(atlas_layer* layer,
+                                       const atlas_graph* graph,
+                                       const void* x_host, int32_t dtype,
+                                       int64_t ldx, int64_t tile_rows,
+                                       int64_t chunk_rows, void* stream);
 ATLAS_API int atlas_layer_accumulator(atlas_layer* layer, float** acc_dev,
                             int64_t* ld);
 

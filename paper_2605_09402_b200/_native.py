@@ -68,6 +68,8 @@ def _declare(lib):
     fn("atlas_graph_create", ctypes.c_int, c_i32, c_i64, c_i64, c_vp, c_vp,
        c_vp, c_i64, c_i64, c_vp, ctypes.POINTER(c_vp))
     fn("atlas_graph_destroy", None, c_vp)
+    fn("atlas_graph_update", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp,
+       c_vp, c_vp)
     fn("atlas_graph_csc", ctypes.c_int, c_vp, ctypes.POINTER(c_vp),
        ctypes.POINTER(c_vp), P_i64)
     fn("atlas_layer_create", ctypes.c_int, ctypes.POINTER(LayerDesc), c_vp,
@@ -80,6 +82,8 @@ def _declare(lib):
        c_vp, c_i64, P_i64)
     fn("atlas_layer_run_resident", ctypes.c_int, c_vp, c_vp, c_vp, c_i32,
        c_i64, c_i64, c_vp)
+    fn("atlas_layer_run_streamed", ctypes.c_int, c_vp, c_vp, c_vp, c_i32,
+       c_i64, c_i64, c_i64, c_vp)
     fn("atlas_layer_accumulator", ctypes.c_int, c_vp, ctypes.POINTER(c_vp),
        P_i64)
     fn("atlas_transform", ctypes.c_int, c_i32, c_vp, c_i64, c_i64, c_i64,
@@ -96,9 +100,11 @@ def _declare(lib):
 EXPORTED = [
     "atlas_last_error", "atlas_abi_version", "atlas_kernel_launches",
     "atlas_graph_create", "atlas_graph_destroy", "atlas_graph_csc",
+    "atlas_graph_update",
     "atlas_layer_create", "atlas_layer_destroy", "atlas_layer_reset",
     "atlas_chunk_submit",
     "atlas_chunk_graduated", "atlas_layer_run_resident",
+    "atlas_layer_run_streamed",
     "atlas_layer_accumulator", "atlas_transform", "atlas_layer_finish",
     "atlas_layer_chunk_stats", "atlas_layer_log", "atlas_layer_state",
     "atlas_layer_timing",

@@ -226,6 +226,104 @@ __global__ void __launch_bounds__(256, 6)
 }
 
 // ---------------------------------------------------------------------------
+// streamed front end: the layer input arrives in row tiles [tile_lo,
+// tile_hi) (host -> HBM, double-buffered); every destination consumes the
+// part of its ascending source list that falls in the tile, resuming at
+// cursor[v]. Per-column addition order is unchanged, so the records are
+// the same bits as the resident pass.
+
+template <typename T, int VEC, int MODEL>
+__global__ void __launch_bounds__(256, 6)
+    agg_tile(const T* __restrict__ tile, int64_t ldx, int64_t tile_lo,
+             int64_t tile_hi, const int64_t* __restrict__ csc_ptr,
+             const uint32_t* __restrict__ csc_src,
+             const uint32_t* __restrict__ indeg, int64_t lo, int64_t nloc,
+             int d, float* __restrict__ acc, int64_t ldacc,
+             int64_t* __restrict__ cursor, uint8_t* __restrict__ touched,
+             float self_scale) {
+  constexpr bool kMean = MODEL != ATLAS_GIN;
+  const int lane = threadIdx.x & 31;
+  const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (v >= nloc) return;
+  const int64_t vg = v + lo;
+  const bool own = vg >= tile_lo && vg < tile_hi;  // v's own row is here
+  const int64_t beg = cursor[v], end = csc_ptr[v + 1];
+  const bool has_src = beg < end && (int64_t)csc_src[beg] < tile_hi;
+  const bool self_here = own && MODEL != ATLAS_GCN;
+  const bool zero_row = own && MODEL == ATLAS_GCN && indeg[v] == 0;
+  if (!has_src && !self_here && !zero_row) return;
+  const float denom = kMean ? (float)max(1u, indeg[v]) : 1.0f;
+  const float rcp = kMean ? __frcp_rn(denom) : 1.0f;
+  const bool resume = touched[v] != 0;
+  float* out = acc + v * ldacc;
+  int64_t consumed = 0;
+  for (int c0 = 0; c0 < d; c0 += 32 * VEC) {
+    const int col = c0 + lane * VEC;
+    const bool active = col < d;
+    float a[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; e++) a[e] = 0.0f;
+    if (resume && active) load_f32<VEC>(out + col, a);
+    bool self_pending = MODEL == ATLAS_GIN && own;
+    int64_t base = beg;
+    while (base < end) {
+      const int64_t i = base + lane;
+      const uint32_t mine = i < end ? csc_src[i] : 0xFFFFFFFFu;
+      const unsigned ok = __ballot_sync(0xffffffffu,
+                                        i < end && (int64_t)mine < tile_hi);
+      const int cnt = __popc(ok);  // sources ascend: a prefix is in the tile
+      for (int k = 0; k < cnt; k += kUnroll) {
+        Frag<T, VEC> f[kUnroll];
+        uint32_t s[kUnroll];
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++) {
+          s[j] = __shfl_sync(0xffffffffu, mine, (k + j) & 31);
+          if (active && k + j < cnt)
+            f[j].load(tile + ((int64_t)s[j] - tile_lo) * ldx + col);
+        }
+#pragma unroll
+        for (int j = 0; j < kUnroll; j++) {
+          if (k + j < cnt) {
+            if (MODEL == ATLAS_GIN && self_pending && (int64_t)s[j] >= vg) {
+              self_pending = false;
+              if (active) {
+                Frag<T, VEC> me;
+                me.load(tile + (vg - tile_lo) * ldx + col);
+                add_msg<T, VEC, false>(a, me, true, 1.0f, 1.0f, self_scale);
+              }
+            }
+            if (active) add_msg<T, VEC, kMean>(a, f[j], false, denom, rcp, 1.0f);
+          }
+        }
+      }
+      base += cnt;
+      if (cnt < 32) break;
+    }
+    if (MODEL == ATLAS_GIN && self_pending && active) {
+      Frag<T, VEC> me;
+      me.load(tile + (vg - tile_lo) * ldx + col);
+      add_msg<T, VEC, false>(a, me, true, 1.0f, 1.0f, self_scale);
+    }
+    if (active) {
+      store_f32<VEC>(out + col, a);
+      if (MODEL == ATLAS_SAGE && own) {
+        Frag<T, VEC> me;
+        me.load(tile + (vg - tile_lo) * ldx + col);
+        float h[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; e++) h[e] = me.get(e);
+        store_f32<VEC>(out + d + col, h);
+      }
+    }
+    consumed = base - beg;
+  }
+  if (lane == 0) {
+    cursor[v] = beg + consumed;
+    touched[v] = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // runs front end: warp per (chunk, destination) run
 
 template <typename T, int VEC, int MODEL>
@@ -385,7 +483,61 @@ void runs_typed(const void* tile, int64_t ldx, const uint32_t* run_dst,
   }
 }
 
+struct TileArgs {
+  int64_t ldx, tile_lo, tile_hi;
+  const atlas_graph* g;
+  int model, d;
+  float eps1;
+  float* acc;
+  int64_t ldacc;
+  int64_t* cursor;
+  uint8_t* touched;
+};
+
+template <typename T, int VEC>
+void tile_model(const T* x, const TileArgs& a, cudaStream_t s) {
+  const int64_t blocks = ceil_div(a.g->nloc, 8);
+  if (blocks == 0) return;
+  auto go = [&](auto kern) {
+    kern<<<(unsigned)blocks, 256, 0, s>>>(
+        x, a.ldx, a.tile_lo, a.tile_hi, a.g->csc_ptr.ptr, a.g->csc_src.ptr,
+        a.g->indeg.ptr, a.g->lo, a.g->nloc, a.d, a.acc, a.ldacc, a.cursor,
+        a.touched, a.eps1);
+  };
+  if (a.model == ATLAS_GCN) go(agg_tile<T, VEC, ATLAS_GCN>);
+  else if (a.model == ATLAS_SAGE) go(agg_tile<T, VEC, ATLAS_SAGE>);
+  else go(agg_tile<T, VEC, ATLAS_GIN>);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+}
+
+template <typename T>
+void tile_typed(const void* x, const TileArgs& a, cudaStream_t s) {
+  const T* t = static_cast<const T*>(x);
+  int vec = pick_vec<T>(a.d, a.ldx);
+  if (vec > 1 && a.ldacc % 4 != 0) vec = 1;
+  if (sizeof(T) == 4) {
+    if (vec == 4) tile_model<T, 4>(t, a, s);
+    else tile_model<T, 1>(t, a, s);
+  } else {
+    if (vec == 8) tile_model<T, 8>(t, a, s);
+    else if (vec == 2) tile_model<T, 2>(t, a, s);
+    else tile_model<T, 1>(t, a, s);
+  }
+}
+
 }  // namespace
+
+void launch_agg_tile(const void* tile, int dtype, int64_t ldx, int64_t tile_lo,
+                     int64_t tile_hi, const atlas_graph* g, int model,
+                     float gin_epsilon, int d, float* acc, int64_t ldacc,
+                     int64_t* cursor, uint8_t* touched, cudaStream_t s) {
+  TileArgs a{ldx, tile_lo, tile_hi, g, model, d, 1.0f + gin_epsilon, acc,
+             ldacc, cursor, touched};
+  if (dtype == ATLAS_F32) tile_typed<float>(tile, a, s);
+  else if (dtype == ATLAS_F16) tile_typed<__half>(tile, a, s);
+  else tile_typed<__nv_bfloat16>(tile, a, s);
+}
 
 // numpy: np.float32(1.0) + np.float32(eps), rounded to f32
 static float self_scale_of(float eps) { return 1.0f + eps; }

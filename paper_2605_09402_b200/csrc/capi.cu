@@ -35,6 +35,25 @@ static int guarded(F f) {
 
 static void use_device(int dev) { ATLAS_CUDA(cudaSetDevice(dev)); }
 
+// upload a CSR (host) into the graph's buffers and rebuild its CSC view
+static void load_graph(atlas_graph* g, int64_t V, int64_t E,
+                       const int64_t* offsets_host,
+                       const uint32_t* neighbors_host,
+                       const uint32_t* in_degrees_host, cudaStream_t s) {
+  g->V = V;
+  g->E = E;
+  g->offsets.reserve(V + 1);
+  ATLAS_CUDA(cudaMemcpyAsync(g->offsets.ptr, offsets_host,
+                             (V + 1) * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, s));
+  g->ws_nbrs.reserve(E > 0 ? E : 1);
+  if (E > 0)
+    ATLAS_CUDA(cudaMemcpyAsync(g->ws_nbrs.ptr, neighbors_host,
+                               E * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                               s));
+  build_csc(g, g->ws_nbrs, in_degrees_host, s);
+}
+
 }  // namespace atlas
 
 using namespace atlas;
@@ -60,27 +79,30 @@ int atlas_graph_create(int32_t device, int64_t V, int64_t E,
     auto g = new atlas_graph();
     try {
       g->device = device;
-      g->V = V;
-      g->E = E;
       g->lo = lo;
       g->hi = hi;
       g->nloc = hi - lo;
-      g->offsets.alloc(V + 1);
-      ATLAS_CUDA(cudaMemcpyAsync(g->offsets.ptr, offsets_host,
-                                 (V + 1) * sizeof(int64_t),
-                                 cudaMemcpyHostToDevice, s));
-      DevBuf<uint32_t> nbrs;
-      nbrs.alloc(E > 0 ? E : 1);
-      if (E > 0)
-        ATLAS_CUDA(cudaMemcpyAsync(nbrs.ptr, neighbors_host,
-                                   E * sizeof(uint32_t),
-                                   cudaMemcpyHostToDevice, s));
-      build_csc(g, nbrs, in_degrees_host, s);
+      load_graph(g, V, E, offsets_host, neighbors_host, in_degrees_host, s);
     } catch (...) {
       delete g;
       throw;
     }
     *out = g;
+  });
+}
+
+int atlas_graph_update(atlas_graph* g, int64_t V, int64_t E,
+                       const int64_t* offsets_host,
+                       const uint32_t* neighbors_host,
+                       const uint32_t* in_degrees_host, void* stream) {
+  return guarded([&] {
+    if (!g || V < 0 || E < 0 || g->hi > V)
+      fail(ATLAS_ECONFIG, "bad graph arguments");
+    if (V >= (int64_t)0x7FFFFFFF || E >= (int64_t)0xFFFFFFFF)
+      fail(ATLAS_ECONFIG, "graph exceeds 32-bit vertex/edge ids per rank");
+    use_device(g->device);
+    load_graph(g, V, E, offsets_host, neighbors_host, in_degrees_host,
+               static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -227,6 +249,73 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
     if (L->nloc > 0)
       launch_agg_resident(g, x, dtype, ldx, D.model, D.gin_epsilon,
                           (int)D.embed_dim, L->acc.ptr, D.agg_dim, s);
+    ATLAS_CUDA(cudaEventRecord(ev[1], s));
+    resident_control(L, g, chunk_rows, s);
+    ATLAS_CUDA(cudaEventRecord(ev[2], s));
+    ATLAS_CUDA(cudaEventSynchronize(ev[2]));
+    ATLAS_CUDA(cudaEventElapsedTime(&L->timing_ms[0], ev[0], ev[1]));
+    ATLAS_CUDA(cudaEventElapsedTime(&L->timing_ms[1], ev[1], ev[2]));
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
+int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
+                             const void* x_host, int32_t dtype, int64_t ldx,
+                             int64_t tile_rows, int64_t chunk_rows,
+                             void* stream) {
+  return guarded([&] {
+    if (!L || !g || !x_host) fail(ATLAS_ECONFIG, "null argument");
+    const atlas_layer_desc& D = L->desc;
+    if (g->V != D.num_vertices || g->lo != D.dst_lo || g->hi != D.dst_hi)
+      fail(ATLAS_ECONFIG, "graph and layer disagree on the vertex range");
+    if (chunk_rows < 1 || tile_rows < 1 || ldx < D.embed_dim)
+      fail(ATLAS_ECONFIG, "bad tile / chunk rows");
+    if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
+    use_device(D.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t item = dtype == ATLAS_F32 ? 4 : 2;
+    const int64_t V = D.num_vertices;
+    tile_rows = std::min<int64_t>(tile_rows, std::max<int64_t>(V, 1));
+    for (auto& b : L->stream_tile) b.reserve(tile_rows * ldx * item);
+    if (!L->copy_stream) {
+      ATLAS_CUDA(cudaStreamCreateWithFlags(&L->copy_stream,
+                                           cudaStreamNonBlocking));
+      for (int i = 0; i < 2; i++) {
+        ATLAS_CUDA(cudaEventCreateWithFlags(&L->ev_ready[i],
+                                            cudaEventDisableTiming));
+        ATLAS_CUDA(cudaEventCreateWithFlags(&L->ev_free[i],
+                                            cudaEventDisableTiming));
+      }
+    }
+    const int64_t nn = std::max<int64_t>(L->nloc, 1);
+    L->cursor.reserve(nn);
+    if (L->nloc > 0)
+      ATLAS_CUDA(cudaMemcpyAsync(L->cursor.ptr, g->csc_ptr.ptr,
+                                 L->nloc * sizeof(int64_t),
+                                 cudaMemcpyDeviceToDevice, s));
+    ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
+    cudaEvent_t ev[3];
+    for (auto& e : ev) ATLAS_CUDA(cudaEventCreate(&e));
+    ATLAS_CUDA(cudaEventRecord(ev[0], s));
+    // the copy stream may only start once s has the cursor/touched resets
+    ATLAS_CUDA(cudaStreamWaitEvent(L->copy_stream, ev[0], 0));
+    const int64_t ntiles = ceil_div(V, tile_rows);
+    for (int64_t t = 0; t < ntiles; t++) {
+      const int b = (int)(t & 1);
+      const int64_t r0 = t * tile_rows, r1 = std::min(V, r0 + tile_rows);
+      if (t >= 2) ATLAS_CUDA(cudaStreamWaitEvent(L->copy_stream, L->ev_free[b], 0));
+      ATLAS_CUDA(cudaMemcpy2DAsync(
+          L->stream_tile[b].ptr, ldx * item,
+          static_cast<const uint8_t*>(x_host) + r0 * ldx * item, ldx * item,
+          ldx * item, r1 - r0, cudaMemcpyHostToDevice, L->copy_stream));
+      ATLAS_CUDA(cudaEventRecord(L->ev_ready[b], L->copy_stream));
+      ATLAS_CUDA(cudaStreamWaitEvent(s, L->ev_ready[b], 0));
+      if (L->nloc > 0)
+        launch_agg_tile(L->stream_tile[b].ptr, dtype, ldx, r0, r1, g, D.model,
+                        D.gin_epsilon, (int)D.embed_dim, L->acc.ptr,
+                        D.agg_dim, L->cursor.ptr, L->touched.ptr, s);
+      ATLAS_CUDA(cudaEventRecord(L->ev_free[b], s));
+    }
     ATLAS_CUDA(cudaEventRecord(ev[1], s));
     resident_control(L, g, chunk_rows, s);
     ATLAS_CUDA(cudaEventRecord(ev[2], s));

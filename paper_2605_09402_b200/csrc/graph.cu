@@ -83,8 +83,15 @@ int bits_for(int64_t n) {
 void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs,
                const uint32_t* indeg_host, cudaStream_t s) {
   const int64_t V = g->V, E = g->E;
-  DevBuf<uint32_t> src_of_edge, keys, vals, keys_out;
-  src_of_edge.alloc(E > 0 ? E : 1);
+  const int64_t e1 = E > 0 ? E : 1;
+  // workspaces live in the graph handle: a refresh of the same shape
+  // (atlas_graph_update) allocates nothing
+  DevBuf<uint32_t>& src_of_edge = g->ws_src;
+  DevBuf<uint32_t>& keys = g->ws_keys;
+  DevBuf<uint32_t>& vals = g->ws_vals;
+  DevBuf<uint32_t>& keys_out = g->ws_keys_out;
+  DevBuf<uint8_t>& tmp = g->ws_tmp;
+  src_of_edge.reserve(e1);
   if (E > 0) {
     expand_sources<<<grid_for(V * 32, 256), 256, 0, s>>>(g->offsets.ptr, V,
                                                         src_of_edge.ptr);
@@ -94,35 +101,34 @@ void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs,
 
   // select in-range edges (order preserved) when this rank owns a sub-range
   const bool full = (g->lo == 0 && g->hi == V);
-  DevBuf<uint32_t> sel;
   int64_t nsel = E;
   if (!full && E > 0) {
-    DevBuf<int64_t> nsel_dev;
-    nsel_dev.alloc(1);
-    sel.alloc(E);
+    g->ws_sel.reserve(e1);
+    g->ws_nsel.reserve(1);
     thrust::counting_iterator<uint32_t> it(0);
     size_t tmp_bytes = 0;
     InRange pred{nbrs.ptr, (uint32_t)g->lo, (uint32_t)g->hi};
-    ATLAS_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, it, sel.ptr,
-                                     nsel_dev.ptr, E, pred, s));
-    DevBuf<uint8_t> tmp;
-    tmp.alloc(tmp_bytes);
-    ATLAS_CUDA(cub::DeviceSelect::If(tmp.ptr, tmp_bytes, it, sel.ptr,
-                                     nsel_dev.ptr, E, pred, s));
+    ATLAS_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, it, g->ws_sel.ptr,
+                                     g->ws_nsel.ptr, E, pred, s));
+    tmp.reserve(tmp_bytes);
+    ATLAS_CUDA(cub::DeviceSelect::If(tmp.ptr, tmp_bytes, it, g->ws_sel.ptr,
+                                     g->ws_nsel.ptr, E, pred, s));
     count_launch();
-    ATLAS_CUDA(cudaMemcpyAsync(&nsel, nsel_dev.ptr, sizeof(int64_t),
+    ATLAS_CUDA(cudaMemcpyAsync(&nsel, g->ws_nsel.ptr, sizeof(int64_t),
                                cudaMemcpyDeviceToHost, s));
     ATLAS_CUDA(cudaStreamSynchronize(s));
   }
   g->eloc = nsel;
   const int64_t n = nsel;
-  keys.alloc(n > 0 ? n : 1);
-  vals.alloc(n > 0 ? n : 1);
-  keys_out.alloc(n > 0 ? n : 1);
-  g->csc_eid.alloc(n > 0 ? n : 1);
+  const int64_t n1 = n > 0 ? n : 1;
+  keys.reserve(n1);
+  vals.reserve(n1);
+  keys_out.reserve(n1);
+  g->csc_eid.reserve(n1);
   if (n > 0) {
     make_pairs<<<grid_for(n, 256), 256, 0, s>>>(
-        nbrs.ptr, E, g->lo, full ? nullptr : sel.ptr, n, keys.ptr, vals.ptr);
+        nbrs.ptr, E, g->lo, full ? nullptr : g->ws_sel.ptr, n, keys.ptr,
+        vals.ptr);
     count_launch();
     ATLAS_LAUNCH_CHECK();
     size_t tmp_bytes = 0;
@@ -130,15 +136,13 @@ void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs,
     ATLAS_CUDA(cub::DeviceRadixSort::SortPairs(
         nullptr, tmp_bytes, keys.ptr, keys_out.ptr, vals.ptr,
         g->csc_eid.ptr, n, 0, end_bit, s));
-    DevBuf<uint8_t> tmp;
-    tmp.alloc(tmp_bytes);
+    tmp.reserve(tmp_bytes);
     ATLAS_CUDA(cub::DeviceRadixSort::SortPairs(
         tmp.ptr, tmp_bytes, keys.ptr, keys_out.ptr, vals.ptr,
         g->csc_eid.ptr, n, 0, end_bit, s));
     count_launch();
   }
-  // csc_src replaces the neighbor scratch
-  g->csc_src.alloc(n > 0 ? n : 1);
+  g->csc_src.reserve(n1);
   if (n > 0) {
     gather_u32<<<grid_for(n, 256), 256, 0, s>>>(src_of_edge.ptr,
                                                 g->csc_eid.ptr, n,
@@ -147,8 +151,8 @@ void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs,
     ATLAS_LAUNCH_CHECK();
   }
   // csc_ptr = exclusive scan of local in-degrees
-  g->indeg.alloc(g->nloc > 0 ? g->nloc : 1);
-  g->csc_ptr.alloc(g->nloc + 1);
+  g->indeg.reserve(g->nloc > 0 ? g->nloc : 1);
+  g->csc_ptr.reserve(g->nloc + 1);
   ATLAS_CUDA(cudaMemsetAsync(g->csc_ptr.ptr, 0, sizeof(int64_t), s));
   if (g->nloc > 0) {
     ATLAS_CUDA(cudaMemcpyAsync(g->indeg.ptr, indeg_host + g->lo,
@@ -157,16 +161,15 @@ void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs,
     size_t tmp_bytes = 0;
     ATLAS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, g->indeg.ptr,
                                              g->csc_ptr.ptr + 1, g->nloc, s));
-    DevBuf<uint8_t> tmp;
-    tmp.alloc(tmp_bytes);
+    tmp.reserve(tmp_bytes);
     ATLAS_CUDA(cub::DeviceScan::InclusiveSum(tmp.ptr, tmp_bytes, g->indeg.ptr,
                                              g->csc_ptr.ptr + 1, g->nloc, s));
     count_launch();
   }
-  ATLAS_CUDA(cudaStreamSynchronize(s));
   int64_t total = 0;
-  ATLAS_CUDA(cudaMemcpy(&total, g->csc_ptr.ptr + g->nloc, sizeof(int64_t),
-                        cudaMemcpyDeviceToHost));
+  ATLAS_CUDA(cudaMemcpyAsync(&total, g->csc_ptr.ptr + g->nloc,
+                             sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ATLAS_CUDA(cudaStreamSynchronize(s));
   if (total != n)
     fail(ATLAS_EINVARIANT, "in-degrees disagree with adjacency (" +
                                std::to_string(total) + " vs " +

@@ -18,6 +18,11 @@ struct atlas_graph {
   atlas::DevBuf<uint32_t> csc_eid;  // eloc, CSR edge index of the entry
   atlas::DevBuf<uint32_t> indeg;    // nloc
   mutable atlas::DevBuf<int> scan_flag;  // input needs the guarded division
+  // CSC build workspaces (kept for atlas_graph_update)
+  atlas::DevBuf<uint32_t> ws_nbrs, ws_src, ws_keys, ws_vals, ws_keys_out,
+      ws_sel;
+  atlas::DevBuf<int64_t> ws_nsel;
+  atlas::DevBuf<uint8_t> ws_tmp;
 };
 
 namespace atlas {
@@ -125,6 +130,19 @@ struct atlas_layer {
   atlas::DevBuf<int64_t> span_buf, span_sorted;
   atlas::DevBuf<unsigned long long> span_acc;
   atlas::DevBuf<uint8_t> span_tmp;
+  // chunk streamer (host -> HBM double buffer)
+  atlas::DevBuf<uint8_t> stream_tile[2];
+  atlas::DevBuf<int64_t> cursor;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_ready[2] = {nullptr, nullptr};
+  cudaEvent_t ev_free[2] = {nullptr, nullptr};
+  ~atlas_layer() {
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (int i = 0; i < 2; i++) {
+      if (ev_ready[i]) cudaEventDestroy(ev_ready[i]);
+      if (ev_free[i]) cudaEventDestroy(ev_free[i]);
+    }
+  }
 };
 
 namespace atlas {
@@ -143,6 +161,10 @@ void launch_agg_runs(const void* tile, int dtype, int64_t ldx,
                      const uint32_t* ent_src, const uint32_t* indeg,
                      int model, float gin_epsilon, int d, float* acc,
                      int64_t ldacc, uint8_t* touched, cudaStream_t s);
+void launch_agg_tile(const void* tile, int dtype, int64_t ldx, int64_t tile_lo,
+                     int64_t tile_hi, const atlas_graph* g, int model,
+                     float gin_epsilon, int d, float* acc, int64_t ldacc,
+                     int64_t* cursor, uint8_t* touched, cudaStream_t s);
 void launch_sage_self(const void* tile, int dtype, int64_t ldx,
                       int64_t row0, int64_t nrows, int d, float* acc_rows,
                       int64_t ldacc, cudaStream_t s);

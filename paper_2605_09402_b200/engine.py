@@ -64,6 +64,27 @@ class DeviceGraph:
     def from_csr(cls, graph, **kw):
         return cls(graph.offsets, graph.neighbors, graph.in_degrees, **kw)
 
+    def update(self, offsets, neighbors, in_degrees, stream=None):
+        """Re-upload a CSR for the same destination range (host arrays:
+        numpy, or pinned torch tensors for full-speed copies) and rebuild
+        the CSC view in the existing device buffers."""
+        def host(a, dtype):
+            if isinstance(a, np.ndarray):
+                return np.ascontiguousarray(a, dtype=dtype)
+            return a
+        off = host(offsets, np.int64)
+        nb = host(neighbors, np.uint32)
+        deg = host(in_degrees, np.uint32)
+        v, e = len(off) - 1, len(nb)
+        N.check(N.load_library().atlas_graph_update(
+            self.handle, v, e, N.ptr(off), N.ptr(nb), N.ptr(deg),
+            N.stream_handle(stream)))
+        self.num_vertices, self.num_edges = v, e
+        n = ctypes.c_int64()
+        N.check(N.load_library().atlas_graph_csc(self.handle, None, None,
+                                                 ctypes.byref(n)))
+        self.local_edges = n.value
+
     def close(self):
         if getattr(self, "handle", None):
             N.load_library().atlas_graph_destroy(self.handle)
@@ -191,6 +212,21 @@ class DeviceLayer:
         N.check(N.load_library().atlas_layer_run_resident(
             self.handle, graph.handle, x.data_ptr(), torch_dtype_code(x),
             x.stride(0), int(chunk_rows), N.stream_handle(stream)))
+
+    def run_streamed(self, graph: DeviceGraph, x_host, chunk_rows: int,
+                     tile_bytes: int = 128 << 20, stream=None):
+        """x_host: pinned CPU torch tensor (V, embed_dim); streamed to HBM
+        in double-buffered tiles while earlier tiles aggregate."""
+        if x_host.shape[1] != self.embed_dim or \
+                x_host.shape[0] != self.num_vertices:
+            raise ConfigError(f"input {tuple(x_host.shape)} does not match "
+                              f"layer ({self.num_vertices}, {self.embed_dim})")
+        row_bytes = x_host.stride(0) * x_host.element_size()
+        tile_rows = max(1, tile_bytes // max(1, row_bytes))
+        N.check(N.load_library().atlas_layer_run_streamed(
+            self.handle, graph.handle, x_host.data_ptr(),
+            torch_dtype_code(x_host), x_host.stride(0), int(tile_rows),
+            int(chunk_rows), N.stream_handle(stream)))
 
     def accumulator_ptr(self):
         p, ld = ctypes.c_void_p(), ctypes.c_int64()

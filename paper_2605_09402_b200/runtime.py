@@ -75,6 +75,7 @@ class PipelineConfig:
     embed_dtype: str = "f32"       # next-layer embedding store: f32|f16|bf16
     record_log: bool = False        # keep victim/reload/graduation logs
     force_exact: bool = False       # always replay the exact control engine
+    stream_tile_bytes: int = 128 << 20  # host->HBM tile of a streamed input
 
     def validate(self) -> None:
         if self.partitions < 1:
@@ -190,7 +191,11 @@ class Engine:
                 record_log=cfg.record_log, force_exact=cfg.force_exact,
                 device=self.device)
             self._layers[l] = layer
-        layer.run_resident(self.graph, x, rows)
+        if x.is_cuda:
+            layer.run_resident(self.graph, x, rows)
+        else:  # host (pinned) input: stream it in tiles (K1 streamer)
+            layer.run_streamed(self.graph, x, rows,
+                               tile_bytes=self.config.stream_tile_bytes)
         nloc = self.hi - self.lo
         out_dim = w.layers[l].out_dim
         y = torch.empty((nloc, out_dim), dtype=_torch_dtype(cfg.embed_dtype),
