@@ -226,6 +226,149 @@ __global__ void __launch_bounds__(256, 6)
 }
 
 // ---------------------------------------------------------------------------
+// resident front end, ring variant (rows of <= 32*VEC elements): each warp
+// grabs batches of consecutive destinations, whose in-edges are one
+// contiguous CSC range, and streams that range through a per-warp
+// shared-memory ring with cp.async (LDGSTS, 16 B per lane per edge).
+// Every lane reads back only the slots it filled itself, so no warp
+// synchronisation is needed, and kRing row loads stay in flight across
+// destination boundaries without holding registers.
+
+constexpr int kRing = 16;
+constexpr int kGrab = 32;  // destinations per work grab
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <typename T, int VEC, int MODEL, bool GUARD>
+__device__ __forceinline__ void ring_body(
+    const T* __restrict__ x, int64_t ldx, const int64_t* __restrict__ csc_ptr,
+    const uint32_t* __restrict__ csc_src, const uint32_t* __restrict__ indeg,
+    int64_t lo, int64_t nloc, int d, float* __restrict__ acc, int64_t ldacc,
+    float self_scale, unsigned long long* __restrict__ work,
+    uint4* __restrict__ ring) {
+  using F = Frag<T, VEC>;
+  static_assert(sizeof(F) == 16, "ring slots are 16 B");
+  constexpr bool kMean = MODEL != ATLAS_GIN;
+  const int lane = threadIdx.x & 31;
+  const int col = lane * VEC;
+  const bool active = col < d;
+  while (true) {
+    unsigned long long v0 = 0;
+    if (lane == 0) v0 = atomicAdd(work, (unsigned long long)kGrab);
+    v0 = __shfl_sync(0xffffffffu, v0, 0);
+    if ((int64_t)v0 >= nloc) break;
+    const int64_t v1 = min((int64_t)v0 + kGrab, nloc);
+    const int64_t e0 = csc_ptr[v0], e1 = csc_ptr[v1];
+    // issue side: edges [pe, e1) not yet requested; src ids 32 at a time
+    int64_t pe = e0, ibase = e0;
+    uint32_t isrc = (e0 + lane < e1) ? csc_src[e0 + lane] : 0u;
+    auto issue = [&]() {
+      if (pe < e1) {
+        if (pe - ibase == 32) {
+          ibase = pe;
+          isrc = (pe + lane < e1) ? csc_src[pe + lane] : 0u;
+        }
+        const uint32_t s = __shfl_sync(0xffffffffu, isrc, (int)(pe - ibase));
+        if (active)
+          cp_async16(&ring[(pe % kRing) * 32 + lane],
+                     x + (int64_t)s * ldx + col);
+        pe++;
+      }
+      cp_async_commit();  // empty groups keep the wait count uniform
+    };
+#pragma unroll 1
+    for (int k = 0; k < kRing; k++) issue();
+    // consume side (GIN needs the source id to place its self term)
+    int64_t ce = e0, cbase = e0;
+    uint32_t csrc = isrc;
+    for (int64_t v = (int64_t)v0; v < v1; v++) {
+      const int64_t dend = csc_ptr[v + 1];
+      const uint32_t vg = (uint32_t)(v + lo);
+      const float denom = kMean ? (float)max(1u, indeg[v]) : 1.0f;
+      const float rcp = kMean ? __frcp_rn(denom) : 1.0f;
+      float a[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; e++) a[e] = 0.0f;
+      bool self_pending = MODEL == ATLAS_GIN;
+      for (; ce < dend; ce++) {
+        if (MODEL == ATLAS_GIN) {
+          if (ce - cbase == 32) {
+            cbase = ce;
+            csrc = (ce + lane < e1) ? csc_src[ce + lane] : 0u;
+          }
+          const uint32_t s = __shfl_sync(0xffffffffu, csrc, (int)(ce - cbase));
+          if (self_pending && s >= vg) {
+            self_pending = false;
+            if (active) {
+              F me;
+              me.load(x + (int64_t)vg * ldx + col);
+              add_msg<T, VEC, false>(a, me, true, 1.0f, 1.0f, self_scale);
+            }
+          }
+        }
+        cp_async_wait<kRing - 1>();  // this lane's copy of edge ce landed
+        if (active) {
+          F f;
+          f.raw = *reinterpret_cast<const typename F::Raw*>(
+              &ring[(ce % kRing) * 32 + lane]);
+          add_msg<T, VEC, kMean, GUARD>(a, f, false, denom, rcp, 1.0f);
+        }
+        issue();  // refill the slot just consumed
+      }
+      if (MODEL == ATLAS_GIN && self_pending && active) {
+        F me;
+        me.load(x + (int64_t)vg * ldx + col);
+        add_msg<T, VEC, false>(a, me, true, 1.0f, 1.0f, self_scale);
+      }
+      if (active) {
+        float* out = acc + v * ldacc;
+        store_f32<VEC>(out + col, a);
+        if (MODEL == ATLAS_SAGE) {
+          F me;
+          me.load(x + (int64_t)vg * ldx + col);
+          float h[VEC];
+#pragma unroll
+          for (int e = 0; e < VEC; e++) h[e] = me.get(e);
+          store_f32<VEC>(out + d + col, h);
+        }
+      }
+    }
+    cp_async_wait<0>();
+  }
+}
+
+template <typename T, int VEC, int MODEL>
+__global__ void __launch_bounds__(256, 3)
+    agg_ring(const T* __restrict__ x, int64_t ldx,
+             const int64_t* __restrict__ csc_ptr,
+             const uint32_t* __restrict__ csc_src,
+             const uint32_t* __restrict__ indeg, int64_t lo, int64_t nloc,
+             int d, float* __restrict__ acc, int64_t ldacc, float self_scale,
+             const int* __restrict__ guard_flag,
+             unsigned long long* __restrict__ work) {
+  extern __shared__ uint4 ring_smem[];
+  uint4* ring = ring_smem + (threadIdx.x >> 5) * (kRing * 32);
+  if (*guard_flag)
+    ring_body<T, VEC, MODEL, true>(x, ldx, csc_ptr, csc_src, indeg, lo, nloc,
+                                   d, acc, ldacc, self_scale, work, ring);
+  else
+    ring_body<T, VEC, MODEL, false>(x, ldx, csc_ptr, csc_src, indeg, lo, nloc,
+                                    d, acc, ldacc, self_scale, work, ring);
+}
+
+// ---------------------------------------------------------------------------
 // streamed front end: the layer input arrives in row tiles [tile_lo,
 // tile_hi) (host -> HBM, double-buffered); every destination consumes the
 // part of its ascending source list that falls in the tile, resuming at
@@ -417,6 +560,25 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
   scan_extremes<T><<<148 * 8, 256, 0, s>>>(x, g->V, d, ldx, g->scan_flag.ptr);
   count_launch();
   ATLAS_LAUNCH_CHECK();
+  if constexpr (VEC * sizeof(T) == 16) if (d <= 32 * VEC) {
+    // ring kernel: persistent warps, dynamic destination batches
+    g->work.reserve(1);
+    ATLAS_CUDA(cudaMemsetAsync(g->work.ptr, 0, sizeof(unsigned long long), s));
+    const int smem = 8 * kRing * 32 * 16;
+    auto ring = [&](auto kern) {
+      ATLAS_CUDA(cudaFuncSetAttribute(
+          kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<148 * 3, 256, smem, s>>>(
+          x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
+          g->nloc, d, acc, ldacc, eps1, g->scan_flag.ptr, g->work.ptr);
+    };
+    if (model == ATLAS_GCN) ring(agg_ring<T, VEC, ATLAS_GCN>);
+    else if (model == ATLAS_SAGE) ring(agg_ring<T, VEC, ATLAS_SAGE>);
+    else ring(agg_ring<T, VEC, ATLAS_GIN>);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+    return;
+  }
   auto go = [&](auto kern) {
     kern<<<(unsigned)blocks, 256, 0, s>>>(
         x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo, g->nloc,

@@ -18,6 +18,7 @@ struct atlas_graph {
   atlas::DevBuf<uint32_t> csc_eid;  // eloc, CSR edge index of the entry
   atlas::DevBuf<uint32_t> indeg;    // nloc
   mutable atlas::DevBuf<int> scan_flag;  // input needs the guarded division
+  mutable atlas::DevBuf<unsigned long long> work;  // ring kernel scheduler
   // CSC build workspaces (kept for atlas_graph_update)
   atlas::DevBuf<uint32_t> ws_nbrs, ws_src, ws_keys, ws_vals, ws_keys_out,
       ws_sel;
