@@ -304,10 +304,11 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
       const int b = (int)(t & 1);
       const int64_t r0 = t * tile_rows, r1 = std::min(V, r0 + tile_rows);
       if (t >= 2) ATLAS_CUDA(cudaStreamWaitEvent(L->copy_stream, L->ev_free[b], 0));
-      ATLAS_CUDA(cudaMemcpy2DAsync(
-          L->stream_tile[b].ptr, ldx * item,
-          static_cast<const uint8_t*>(x_host) + r0 * ldx * item, ldx * item,
-          ldx * item, r1 - r0, cudaMemcpyHostToDevice, L->copy_stream));
+      // whole rows (pitch included) are one contiguous block: a single DMA
+      ATLAS_CUDA(cudaMemcpyAsync(
+          L->stream_tile[b].ptr,
+          static_cast<const uint8_t*>(x_host) + r0 * ldx * item,
+          (r1 - r0) * ldx * item, cudaMemcpyHostToDevice, L->copy_stream));
       ATLAS_CUDA(cudaEventRecord(L->ev_ready[b], L->copy_stream));
       ATLAS_CUDA(cudaStreamWaitEvent(s, L->ev_ready[b], 0));
       if (L->nloc > 0)
