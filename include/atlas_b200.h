@@ -196,6 +196,17 @@ ATLAS_API int atlas_layer_state(atlas_layer* layer, uint32_t* pending, uint8_t* 
  * plane (walk + optional exact replay), in milliseconds */
 ATLAS_API int atlas_layer_timing(atlas_layer* layer, float* ms, int32_t n);
 
+/* greedy reordering (oocgnn/reorder.py:30-88): scores, the bit-exact
+ * old->new permutation and the relabelled CSR (rows ascending), all on the
+ * device; host in / host out. scores may be NULL. */
+ATLAS_API int atlas_reorder(int32_t device, int64_t num_vertices,
+                            int64_t num_edges, const int64_t* offsets,
+                            const uint32_t* neighbors,
+                            const uint32_t* in_degrees, int64_t* old_to_new,
+                            int64_t* new_offsets, uint32_t* new_neighbors,
+                            uint32_t* new_in_degrees, double* scores,
+                            void* stream);
+
 /* number of kernels this library launched since load (evidence counter) */
 ATLAS_API int64_t atlas_kernel_launches(void);
 

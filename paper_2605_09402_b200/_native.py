@@ -95,6 +95,8 @@ def _declare(lib):
     fn("atlas_layer_log", ctypes.c_int, c_vp, c_i32, c_vp, c_i64, P_i64)
     fn("atlas_layer_state", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp)
     fn("atlas_layer_timing", ctypes.c_int, c_vp, c_vp, c_i32)
+    fn("atlas_reorder", ctypes.c_int, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp,
+       c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
 
 
 EXPORTED = [
@@ -107,7 +109,7 @@ EXPORTED = [
     "atlas_layer_run_streamed",
     "atlas_layer_accumulator", "atlas_transform", "atlas_layer_finish",
     "atlas_layer_chunk_stats", "atlas_layer_log", "atlas_layer_state",
-    "atlas_layer_timing",
+    "atlas_layer_timing", "atlas_reorder",
 ]
 
 

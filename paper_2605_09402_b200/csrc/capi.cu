@@ -327,6 +327,21 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
   });
 }
 
+int atlas_reorder(int32_t device, int64_t V, int64_t E, const int64_t* off,
+                  const uint32_t* nbrs, const uint32_t* indeg,
+                  int64_t* old_to_new, int64_t* new_off, uint32_t* new_nbrs,
+                  uint32_t* new_indeg, double* scores, void* stream) {
+  return guarded([&] {
+    if (V < 0 || E < 0 || !off || !old_to_new || !new_off)
+      fail(ATLAS_ECONFIG, "bad reorder arguments");
+    if (V >= (int64_t)0x7FFFFFFF || E >= (int64_t)0x7FFFFFFF)
+      fail(ATLAS_ECONFIG, "graph exceeds 32-bit ids");
+    use_device(device);
+    reorder_graph(V, E, off, nbrs, indeg, old_to_new, new_off, new_nbrs,
+                  new_indeg, scores, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int atlas_layer_timing(atlas_layer* L, float* ms, int32_t n) {
   return guarded([&] {
     if (!L || !ms) fail(ATLAS_ECONFIG, "null argument");

@@ -195,6 +195,13 @@ void chunk_spans(atlas_layer* L, int64_t start, int64_t end,
 void finish_spans(atlas_layer* L, cudaStream_t s);
 void check_engine_error(atlas_layer* L, cudaStream_t s);
 
+// reorder.cu
+void reorder_graph(int64_t V, int64_t E, const int64_t* off_h,
+                   const uint32_t* nbrs_h, const uint32_t* indeg_h,
+                   int64_t* old_to_new_h, int64_t* new_off_h,
+                   uint32_t* new_nbrs_h, uint32_t* new_indeg_h,
+                   double* scores_h, cudaStream_t s);
+
 // launch accounting
 void count_launch(int n = 1);
 

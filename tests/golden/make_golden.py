@@ -233,5 +233,39 @@ def main(only=None):
     path.write_text(json.dumps(old, indent=1, sort_keys=True))
 
 
+def reorder_goldens():
+    """Greedy reordering (oocgnn/reorder.py): permutation, scores and the
+    relabelled CSR of three graphs."""
+    from oocgnn.reorder import build_order, relabel_graph, score_vertices
+    work = Path(tempfile.mkdtemp(prefix="golden_reorder_"))
+    out = {}
+    for name in ("fig2", "uniform", "pa"):
+        if name == "fig2":
+            d = fig2_dataset(work)
+        else:
+            gk, v, deg, dim, seed, dt = DATASETS[name]
+            d = work / name
+            generate_synthetic(gk, v, deg, dim, seed, d, dtype=dt)
+        g = read_csr(d)
+        scores = score_vertices(g)
+        o2n = build_order(g)
+        rg = relabel_graph(g, o2n)
+        out[name] = {"scores_sha": digest_array(scores),
+                     "old_to_new_sha": digest_array(o2n),
+                     "offsets_sha": digest_array(rg.offsets),
+                     "neighbors_sha": digest_array(rg.neighbors),
+                     "in_degrees_sha": digest_array(rg.in_degrees)}
+        if name == "fig2":
+            out[name]["old_to_new"] = o2n.tolist()
+            out[name]["scores"] = scores.tolist()
+    path = OUT / "golden.json"
+    man = json.loads(path.read_text())
+    man["_reorder"] = out
+    path.write_text(json.dumps(man, indent=1, sort_keys=True))
+
+
 if __name__ == "__main__":
-    main(set(sys.argv[1:]) or None)
+    if sys.argv[1:] == ["reorder"]:
+        reorder_goldens()
+    else:
+        main(set(sys.argv[1:]) or None)
