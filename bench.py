@@ -306,11 +306,12 @@ def main():
                     "d2h_bytes_per_step": host_out.numel() * 4,
                     "includes": "graph upload + CSC build, feature H2D, "
                                 "3 layers, output D2H"},
-            "gpu_launches": launches // max(1, args.steps),
+            "gpu_launches": launches,
+            "gpu_launches_per_step": launches / max(1, args.steps),
             "clocks": clk,
             "setup_s": setup_s,
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(graph, feats, weights)
         print(json.dumps(line), flush=True)
     eng.close()
