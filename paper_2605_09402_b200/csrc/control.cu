@@ -77,6 +77,71 @@ __device__ __forceinline__ void agg_inc(const Hist& h, int64_t base,
   if ((int)(threadIdx.x & 31) == leader) h.add(base + key, __popc(peers));
 }
 
+// first/last stream step of v and the (chunk * 3 + pass) keys of its
+// first admission and its graduation
+__device__ __forceinline__ void dest_summary(
+    int model, const Plan& p, const int64_t* __restrict__ off,
+    const uint32_t* __restrict__ csc_src, const uint32_t* __restrict__ csc_eid,
+    int64_t v, int64_t vg, int64_t beg, int64_t end,
+    int64_t* __restrict__ first_pos, int64_t* __restrict__ last_pos,
+    const Hist& h, int64_t A0, int64_t G0) {
+  const int64_t cv = p.chunk(vg);
+  int64_t first = -1, last = -1;
+  int64_t a_key = 0, g_key = 0;
+  if (end > beg) {
+    const int64_t u0 = csc_src[beg], u1 = csc_src[end - 1];
+    first = edge_pos(model, p, csc_eid[beg], u0);
+    last = edge_pos(model, p, csc_eid[end - 1], u1);
+    a_key = p.chunk(u0) * 3 + 2;
+    g_key = p.chunk(u1) * 3 + 2;
+  }
+  if (model != ATLAS_GCN) {
+    const int64_t sp = self_pos(model, p, off, vg);
+    const int64_t sk = cv * 3 + (model == ATLAS_SAGE ? 1 : 2);
+    if (end > beg) {
+      first = min(first, sp);
+      last = max(last, sp);
+      a_key = min(a_key, sk);
+      g_key = max(g_key, sk);
+    } else {
+      first = last = sp;
+      a_key = g_key = sk;
+    }
+  } else if (end == beg) {
+    a_key = g_key = cv * 3 + 0;  // GCN zero in-degree pre-pass
+  }
+  first_pos[v] = first;
+  last_pos[v] = last;
+  h.add(A0 + a_key, 1u);
+  h.add(G0 + g_key, 1u);
+}
+
+// thread per destination when no run counting is needed
+__global__ void __launch_bounds__(256)
+    walk_light(int model, Plan p, const int64_t* __restrict__ off,
+               const int64_t* __restrict__ csc_ptr,
+               const uint32_t* __restrict__ csc_src,
+               const uint32_t* __restrict__ csc_eid, int64_t lo, int64_t nloc,
+               int64_t* __restrict__ first_pos, int64_t* __restrict__ last_pos,
+               unsigned long long* __restrict__ ghist, int use_smem) {
+  extern __shared__ unsigned int shist[];
+  const int64_t hn = 7 * p.nchunks;
+  Hist h{ghist, use_smem ? shist : nullptr};
+  if (use_smem) {
+    for (int64_t i = threadIdx.x; i < hn; i += blockDim.x) shist[i] = 0;
+    __syncthreads();
+  }
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nloc;
+       v += (int64_t)gridDim.x * blockDim.x)
+    dest_summary(model, p, off, csc_src, csc_eid, v, v + lo, csc_ptr[v],
+                 csc_ptr[v + 1], first_pos, last_pos, h, 0, 3 * p.nchunks);
+  if (use_smem) {
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < hn; i += blockDim.x)
+      if (shist[i]) atomicAdd(ghist + i, (unsigned long long)shist[i]);
+  }
+}
+
 // One warp per local destination: spans, admission / graduation
 // (chunk, pass), per-chunk run counts and (optionally) run records.
 __global__ void __launch_bounds__(256)
@@ -102,39 +167,12 @@ __global__ void __launch_bounds__(256)
        v < nloc; v += nwarps) {
   const int64_t vg = v + lo;
   const int64_t beg = csc_ptr[v], end = csc_ptr[v + 1];
-  const bool has_self = model != ATLAS_GCN;
+
   const int64_t cv = p.chunk(vg);
   // ---- spans and admit/grad (chunk, pass) --------------------------------
-  if (lane == 0) {
-    int64_t first = -1, last = -1;
-    int64_t a_key, g_key;  // chunk * 3 + pass
-    if (end > beg) {
-      const int64_t u0 = csc_src[beg], u1 = csc_src[end - 1];
-      first = edge_pos(model, p, csc_eid[beg], u0);
-      last = edge_pos(model, p, csc_eid[end - 1], u1);
-      a_key = p.chunk(u0) * 3 + 2;
-      g_key = p.chunk(u1) * 3 + 2;
-    }
-    if (has_self) {
-      const int64_t sp = self_pos(model, p, off, vg);
-      const int64_t sk = cv * 3 + (model == ATLAS_SAGE ? 1 : 2);
-      if (end > beg) {
-        first = min(first, sp);
-        last = max(last, sp);
-        a_key = min(a_key, sk);
-        g_key = max(g_key, sk);
-      } else {
-        first = last = sp;
-        a_key = g_key = sk;
-      }
-    } else if (end == beg) {
-      a_key = g_key = cv * 3 + 0;  // GCN zero in-degree pre-pass
-    }
-    first_pos[v] = first;
-    last_pos[v] = last;
-    h.add(A0 + a_key, 1u);
-    h.add(G0 + g_key, 1u);
-  }
+  if (lane == 0)
+    dest_summary(model, p, off, csc_src, csc_eid, v, vg, beg, end, first_pos,
+                 last_pos, h, A0, G0);
   // ---- runs: maximal same-chunk stretches of the ascending source list ---
   bool self_merged = false;  // GIN self term joins the run of chunk cv
   for (int64_t base = beg; count_runs && base < end; base += 32) {
@@ -290,7 +328,16 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
   // whose numerators are zero on the eviction-free path.
   const bool need_runs = L->sub_batch < L->nloc || L->desc.record_log ||
                          L->desc.force_exact;
-  walk(nullptr, need_runs ? 1 : 0);
+  if (need_runs) {
+    walk(nullptr, 1);
+  } else {
+    walk_light<<<blocks, 256, use_smem ? hbytes : 0, s>>>(
+        model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
+        g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
+        hist.ptr, use_smem);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+  }
   std::vector<unsigned long long> h(7 * nchunks);
   ATLAS_CUDA(cudaMemcpyAsync(h.data(), hist.ptr, h.size() * sizeof(h[0]),
                              cudaMemcpyDeviceToHost, s));

@@ -143,25 +143,31 @@ struct TcParams {
   uint32_t tmem_cols;
 };
 
-template <typename OutT>
+template <typename OutT, bool RES_W>
 __global__ void __launch_bounds__(kThreads, 1)
     transform_tc_kernel(const __grid_constant__ CUtensorMap map_x,
                         const __grid_constant__ CUtensorMap map_w,
                         TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B aligned carve-up: per stage [x | x_lo | w_hi | w_lo]
-  uint8_t* base = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned carve-up (pointer arithmetic keeps the shared space):
+  //   RES_W : [w_hi kb0..kbN | w_lo kb0..kbN] then per stage [x | x_lo]
+  //   !RES_W: per stage [x | x_lo | w | w_lo]
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t x_bytes = BM * BK * 4;
   const uint32_t w_bytes = p.BN * BK * 4;
-  const uint32_t stage_bytes = 2 * x_bytes + 2 * w_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + p.stages * stage_bytes);
+  const uint32_t wres_bytes = RES_W ? 2u * w_bytes * p.kblocks : 0u;
+  const uint32_t stage_bytes = 2 * x_bytes + (RES_W ? 0u : 2 * w_bytes);
+  uint8_t* stages = base + wres_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + p.stages * stage_bytes);
   uint64_t* split = full + p.stages;
   uint64_t* empty = split + p.stages;
   uint64_t* tfull = empty + p.stages;  // [2]
   uint64_t* tempty = tfull + 2;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* wfull = tempty + 2;        // resident W landed
+  uint64_t* wsplit = wfull + 1;        // resident W split
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wsplit + 1);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+  float* stage_out = sbias + 256;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (p.M + BM - 1) / BM;
@@ -176,6 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
     }
+    mbar_init(wfull, 1);
+    mbar_init(wsplit, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int j = threadIdx.x; j < p.BN; j += kThreads)
@@ -191,19 +199,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  // W tiles of k-block kb: resident area, or inside stage s
+  auto w_hi_ptr = [&](int s, int kb) -> uint8_t* {
+    return RES_W ? base + kb * w_bytes
+                 : stages + s * stage_bytes + 2 * x_bytes;
+  };
+  auto w_lo_ptr = [&](int s, int kb) -> uint8_t* {
+    return RES_W ? base + (p.kblocks + kb) * w_bytes
+                 : stages + s * stage_bytes + 2 * x_bytes + w_bytes;
+  };
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
+      if (RES_W) {  // W once per CTA
+        mbar_expect_tx(wfull, w_bytes * p.kblocks);
+        for (int kb = 0; kb < p.kblocks; kb++)
+          tma_load_2d(base + kb * w_bytes, &map_w, wfull, kb * BK, 0);
+      }
       int s = 0;
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kb = 0; kb < p.kblocks; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = base + s * stage_bytes;
-          mbar_expect_tx(&full[s], x_bytes + w_bytes);
+          uint8_t* st = stages + s * stage_bytes;
+          mbar_expect_tx(&full[s], x_bytes + (RES_W ? 0u : w_bytes));
           tma_load_2d(st, &map_x, &full[s], kb * BK, (int)(t * BM));
-          tma_load_2d(st + 2 * x_bytes, &map_w, &full[s], kb * BK, 0);
+          if (!RES_W)
+            tma_load_2d(st + 2 * x_bytes, &map_w, &full[s], kb * BK, 0);
           if (++s == p.stages) {
             s = 0;
             ph ^= 1;
@@ -217,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            | (2u << 7) | (2u << 10)        // A, B = tf32
                            | ((uint32_t)(p.BN >> 3) << 17)  // N
                            | ((uint32_t)(BM >> 4) << 24);   // M
+    if (RES_W) mbar_wait(wsplit, 0);
     int s = 0;
     uint32_t ph = 0;
     int acc = 0;
@@ -230,10 +254,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&split[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
-          uint8_t* st = base + s * stage_bytes;
+          uint8_t* st = stages + s * stage_bytes;
           const uint32_t a_hi = smem_u32(st), a_lo = smem_u32(st + x_bytes);
-          const uint32_t b_hi = smem_u32(st + 2 * x_bytes);
-          const uint32_t b_lo = b_hi + w_bytes;
+          const uint32_t b_hi = smem_u32(w_hi_ptr(s, kb));
+          const uint32_t b_lo = smem_u32(w_lo_ptr(s, kb));
 #pragma unroll
           for (int k = 0; k < BK / 8; k++) {  // UMMA_K = 8 tf32 = 32 B
             const uint32_t off = k * 32;
@@ -257,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
     }
   } else if (warp < 6) {
-    // -------- splitter: x, w tiles -> hi (in place) + lo (tf32 split) -----
+    // -------- splitter: tiles -> tf32 hi (in place) + lo ----------------
     const int tid = threadIdx.x - 64;  // 0..127
     auto split16 = [](float4* hi, float4* lo, int e) {
       const float4 v = hi[e];
@@ -273,20 +297,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       hi[e] = h;
       lo[e] = l;
     };
+    if (RES_W) {
+      mbar_wait(wfull, 0);
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        float4* wh = reinterpret_cast<float4*>(w_hi_ptr(0, kb));
+        float4* wl = reinterpret_cast<float4*>(w_lo_ptr(0, kb));
+        for (int e = tid; e < p.BN * BK / 4; e += 128) split16(wh, wl, e);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(wsplit);
+    }
     int s = 0;
     uint32_t ph = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int kb = 0; kb < p.kblocks; kb++) {
         mbar_wait(&full[s], ph);
-        uint8_t* st = base + s * stage_bytes;
+        uint8_t* st = stages + s * stage_bytes;
         float4* xs = reinterpret_cast<float4*>(st);
         float4* xl = reinterpret_cast<float4*>(st + x_bytes);
-        float4* ws = reinterpret_cast<float4*>(st + 2 * x_bytes);
-        float4* wl = reinterpret_cast<float4*>(st + 2 * x_bytes + w_bytes);
 #pragma unroll
         for (int i = 0; i < (BM * BK / 4) / 128; i++)
           split16(xs, xl, tid + i * 128);
-        for (int e = tid; e < p.BN * BK / 4; e += 128) split16(ws, wl, e);
+        if (!RES_W) {
+          float4* ws = reinterpret_cast<float4*>(w_hi_ptr(s, kb));
+          float4* wl = reinterpret_cast<float4*>(w_lo_ptr(s, kb));
+          for (int e = tid; e < p.BN * BK / 4; e += 128) split16(ws, wl, e);
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&split[s]);
         if (++s == p.stages) {
@@ -300,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // each thread owns one accumulator row (TMEM lane); 32x16 blocks go
     // through a per-warp smem transpose so global stores are 64-B runs
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
-    float* stage = sbias + 256 + (warp - 6) * 32 * 17;
+    float* stage = stage_out + (warp - 6) * 32 * 17;
     int acc = 0;
     uint32_t aph[2] = {0, 0};
     OutT* y = static_cast<OutT*>(p.y);
@@ -410,13 +446,18 @@ bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
   CUtensorMap mx, mw;
   if (!make_map(&mx, x, rows, k, ldx, BM) || !make_map(&mw, w, n, k, k, BN))
     return false;
-  const int stage_bytes = 2 * BM * BK * 4 + 2 * BN * BK * 4;
+  // W (hi + lo, all k-blocks) stays resident when it leaves room for two
+  // x stages; otherwise it streams through the stages with x
   const int budget = 220 * 1024 - 1024 - 2048 - 4 * 32 * 17 * 4;
-  int stages = budget / stage_bytes;
+  const int x_stage = 2 * BM * BK * 4;
+  const int w_res = 2 * BN * BK * 4 * kblocks;
+  const bool res_w = w_res + 2 * x_stage <= budget;
+  const int stage_bytes = res_w ? x_stage : x_stage + 2 * BN * BK * 4;
+  int stages = (budget - (res_w ? w_res : 0)) / stage_bytes;
   if (stages > 4) stages = 4;
   if (stages < 2) return false;
-  const int smem = 1024 + stages * stage_bytes + 8 * (3 * stages + 4) + 16 +
-                   4 * 256 + 4 * 32 * 17 * 4;
+  const int smem = 1024 + (res_w ? w_res : 0) + stages * stage_bytes +
+                   8 * (3 * stages + 6) + 16 + 4 * 256 + 4 * 32 * 17 * 4;
   TcParams p{};
   p.M = rows;
   p.K = (int)k;
@@ -438,9 +479,15 @@ bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid, kThreads, smem, s>>>(mx, mw, p);
   };
-  if (y_dtype == ATLAS_F32) launch(transform_tc_kernel<float>);
-  else if (y_dtype == ATLAS_F16) launch(transform_tc_kernel<__half>);
-  else launch(transform_tc_kernel<__nv_bfloat16>);
+  if (res_w) {
+    if (y_dtype == ATLAS_F32) launch(transform_tc_kernel<float, true>);
+    else if (y_dtype == ATLAS_F16) launch(transform_tc_kernel<__half, true>);
+    else launch(transform_tc_kernel<__nv_bfloat16, true>);
+  } else {
+    if (y_dtype == ATLAS_F32) launch(transform_tc_kernel<float, false>);
+    else if (y_dtype == ATLAS_F16) launch(transform_tc_kernel<__half, false>);
+    else launch(transform_tc_kernel<__nv_bfloat16, false>);
+  }
   count_launch();
   ATLAS_LAUNCH_CHECK();
   return true;
