@@ -155,10 +155,13 @@ ATLAS_API int atlas_chunk_graduated(atlas_layer* layer, int64_t* ids, float* row
 /* whole layer over a resident input x (device pointer, V rows of
  * embed_dim, leading dimension ldx) with the reference chunk plan of
  * chunk_rows rows per chunk. Aggregation records land in the layer's
- * device accumulator (atlas_layer_accumulator). */
+ * device accumulator (atlas_layer_accumulator). input_flag (device int,
+ * may be NULL) is the extremes flag atlas_transform wrote for x; NULL makes
+ * the layer scan x itself. */
 ATLAS_API int atlas_layer_run_resident(atlas_layer* layer, const atlas_graph* graph,
                              const void* x_dev, int32_t dtype, int64_t ldx,
-                             int64_t chunk_rows, void* stream);
+                             int64_t chunk_rows, const int32_t* input_flag,
+                             void* stream);
 /* same layer pass, but the input stays in (pinned) HOST memory: it is
  * streamed to HBM in tiles of tile_rows rows, double-buffered on a side
  * copy stream, and every tile is aggregated as soon as it lands (SURVEY.md
@@ -171,11 +174,15 @@ ATLAS_API int atlas_layer_run_streamed(atlas_layer* layer,
 ATLAS_API int atlas_layer_accumulator(atlas_layer* layer, float** acc_dev,
                             int64_t* ld);
 
-/* y = act(x . W^T + b); x (rows x k, f32, ldx), W (n x k, f32), b (n). */
+/* y = act(x . W^T + b); x (rows x k, f32, ldx), W (n x k, f32), b (n).
+ * extremes_flag (device int, may be NULL) is set to 1 iff some output is
+ * non-finite or a nonzero below 2^-100 (then the next layer's exact
+ * division takes its IEEE path); it spares that layer a scan of y. */
 ATLAS_API int atlas_transform(int32_t backend, const float* x_dev, int64_t rows,
                     int64_t k, int64_t ldx, const float* w_dev,
                     const float* b_dev, int64_t n, int32_t relu, void* y_dev,
-                    int32_t y_dtype, int64_t ldy, void* stream);
+                    int32_t y_dtype, int64_t ldy, int32_t* extremes_flag,
+                    void* stream);
 
 ATLAS_API int atlas_layer_finish(atlas_layer* layer, atlas_layer_metrics* out);
 /* per-chunk reload and touched counters (for mean_reload_pct) */

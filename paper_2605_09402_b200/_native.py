@@ -81,13 +81,13 @@ def _declare(lib):
     fn("atlas_chunk_graduated", ctypes.c_int, c_vp, c_vp, c_vp, c_i64, P_i64,
        c_vp, c_i64, P_i64)
     fn("atlas_layer_run_resident", ctypes.c_int, c_vp, c_vp, c_vp, c_i32,
-       c_i64, c_i64, c_vp)
+       c_i64, c_i64, c_vp, c_vp)
     fn("atlas_layer_run_streamed", ctypes.c_int, c_vp, c_vp, c_vp, c_i32,
        c_i64, c_i64, c_i64, c_vp)
     fn("atlas_layer_accumulator", ctypes.c_int, c_vp, ctypes.POINTER(c_vp),
        P_i64)
     fn("atlas_transform", ctypes.c_int, c_i32, c_vp, c_i64, c_i64, c_i64,
-       c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i64, c_vp)
+       c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i64, c_vp, c_vp)
     fn("atlas_layer_finish", ctypes.c_int, c_vp,
        ctypes.POINTER(LayerMetricsC))
     fn("atlas_layer_chunk_stats", ctypes.c_int, c_vp, c_vp, c_vp, c_i64,

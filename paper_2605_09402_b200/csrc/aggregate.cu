@@ -554,12 +554,18 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
                     cudaStream_t s) {
   const int64_t blocks = ceil_div(g->nloc, 8);
   if (blocks == 0) return;
-  // one pass over the input decides whether the division guard is needed
+  // whether the division guard is needed: the producing transform's flag,
+  // or one pass over the input
   g->scan_flag.reserve(1);
-  ATLAS_CUDA(cudaMemsetAsync(g->scan_flag.ptr, 0, sizeof(int), s));
-  scan_extremes<T><<<148 * 8, 256, 0, s>>>(x, g->V, d, ldx, g->scan_flag.ptr);
-  count_launch();
-  ATLAS_LAUNCH_CHECK();
+  const int* flag = g->known_flag;
+  if (!flag) {
+    ATLAS_CUDA(cudaMemsetAsync(g->scan_flag.ptr, 0, sizeof(int), s));
+    scan_extremes<T><<<148 * 8, 256, 0, s>>>(x, g->V, d, ldx,
+                                             g->scan_flag.ptr);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+    flag = g->scan_flag.ptr;
+  }
   if constexpr (VEC * sizeof(T) == 16) if (d <= 32 * VEC) {
     // ring kernel: persistent warps, dynamic destination batches
     g->work.reserve(1);
@@ -570,7 +576,7 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
           kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       kern<<<148 * 3, 256, smem, s>>>(
           x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
-          g->nloc, d, acc, ldacc, eps1, g->scan_flag.ptr, g->work.ptr);
+          g->nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
     };
     if (model == ATLAS_GCN) ring(agg_ring<T, VEC, ATLAS_GCN>);
     else if (model == ATLAS_SAGE) ring(agg_ring<T, VEC, ATLAS_SAGE>);
@@ -582,7 +588,7 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
   auto go = [&](auto kern) {
     kern<<<(unsigned)blocks, 256, 0, s>>>(
         x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo, g->nloc,
-        d, acc, ldacc, eps1, g->scan_flag.ptr);
+        d, acc, ldacc, eps1, flag);
   };
   if (model == ATLAS_GCN) go(agg_resident<T, VEC, ATLAS_GCN>);
   else if (model == ATLAS_SAGE) go(agg_resident<T, VEC, ATLAS_SAGE>);
@@ -706,8 +712,10 @@ static float self_scale_of(float eps) { return 1.0f + eps; }
 
 void launch_agg_resident(const atlas_graph* g, const void* x, int dtype,
                          int64_t ldx, int model, float gin_epsilon, int d,
-                         float* acc, int64_t ldacc, cudaStream_t s) {
+                         float* acc, int64_t ldacc, const int32_t* input_flag,
+                         cudaStream_t s) {
   const float e1 = self_scale_of(gin_epsilon);
+  g->known_flag = input_flag;
   if (dtype == ATLAS_F32)
     resident_typed<float>(g, x, ldx, model, e1, d, acc, ldacc, s);
   else if (dtype == ATLAS_F16)

@@ -233,7 +233,8 @@ int atlas_chunk_graduated(atlas_layer* L, int64_t* ids, float* rows,
 
 int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
                              const void* x, int32_t dtype, int64_t ldx,
-                             int64_t chunk_rows, void* stream) {
+                             int64_t chunk_rows, const int32_t* input_flag,
+                             void* stream) {
   return guarded([&] {
     if (!L || !g) fail(ATLAS_ECONFIG, "null argument");
     const atlas_layer_desc& D = L->desc;
@@ -248,7 +249,8 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
     ATLAS_CUDA(cudaEventRecord(ev[0], s));
     if (L->nloc > 0)
       launch_agg_resident(g, x, dtype, ldx, D.model, D.gin_epsilon,
-                          (int)D.embed_dim, L->acc.ptr, D.agg_dim, s);
+                          (int)D.embed_dim, L->acc.ptr, D.agg_dim,
+                          input_flag, s);
     ATLAS_CUDA(cudaEventRecord(ev[1], s));
     resident_control(L, g, chunk_rows, s);
     ATLAS_CUDA(cudaEventRecord(ev[2], s));
@@ -360,17 +362,18 @@ int atlas_layer_accumulator(atlas_layer* L, float** acc, int64_t* ld) {
 int atlas_transform(int32_t backend, const float* x, int64_t rows, int64_t k,
                     int64_t ldx, const float* w, const float* b, int64_t n,
                     int32_t relu, void* y, int32_t y_dtype, int64_t ldy,
-                    void* stream) {
+                    int32_t* flag, void* stream) {
   return guarded([&] {
     if (rows < 0 || k < 1 || n < 1 || ldx < k || ldy < n)
       fail(ATLAS_ECONFIG, "bad transform shape");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (flag) ATLAS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
     if (backend == ATLAS_BACKEND_STABLE) {
       launch_transform_stable(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
-                              s);
+                              flag, s);
     } else if (backend == ATLAS_BACKEND_TCGEN05) {
       if (!launch_transform_tc(x, rows, k, ldx, w, b, n, relu, y, y_dtype,
-                               ldy, s))
+                               ldy, flag, s))
         fail(ATLAS_ECONFIG, "tcgen05 backend does not support this shape");
     } else {
       fail(ATLAS_ECONFIG, "unknown transform backend");

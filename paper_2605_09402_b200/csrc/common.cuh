@@ -103,4 +103,11 @@ __device__ __forceinline__ float to_f32(__nv_bfloat16 x) {
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// values for which the aggregation's reciprocal-based exact division must
+// fall back to IEEE division: non-finite, or nonzero with |v| < 2^-100
+__device__ __forceinline__ int is_extreme(float v) {
+  const float a = fabsf(v);
+  return ((a < 0x1p-100f && a != 0.0f) || !(a <= 3.402823466e38f)) ? 1 : 0;
+}
+
 }  // namespace atlas

@@ -217,6 +217,14 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// m_c = edges of reference chunk c (whole graph, CSR offsets)
+__global__ void chunk_edges(const int64_t* __restrict__ off, Plan p,
+                            int64_t* __restrict__ m) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; c < p.nchunks; c += (int64_t)gridDim.x * blockDim.x)
+    m[c] = off[p.end(c)] - off[p.start(c)];
+}
+
 __global__ void fill_u64(uint64_t* p, int64_t n, uint64_t val) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = val;
@@ -322,11 +330,30 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
     count_launch();
     ATLAS_LAUNCH_CHECK();
   };
-  // A pass never holds more than nloc destinations, so when sub_batch >=
-  // nloc every pass is one sub-batch and the per-chunk run counts (an E-wide
-  // walk) are not needed to prove it; they only feed reload-% denominators,
-  // whose numerators are zero on the eviction-free path.
-  const bool need_runs = L->sub_batch < L->nloc || L->desc.record_log ||
+  // An edge pass holds at most min(nloc, m_c (+ n_c for GIN)) destinations,
+  // so when that bound is <= sub_batch for every chunk each pass is one
+  // sub-batch and the per-chunk run counts (an E-wide walk) are not needed
+  // to prove it; they only feed reload-% denominators, whose numerators are
+  // zero on the eviction-free path.
+  int64_t max_pass = 0;
+  {
+    DevBuf<int64_t>& mc = L->span_buf;  // reused scratch (>= nchunks)
+    mc.reserve(std::max<int64_t>(nchunks, 1));
+    chunk_edges<<<grid_of(nchunks), 256, 0, s>>>(g->offsets.ptr, p, mc.ptr);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+    std::vector<int64_t> m(nchunks);
+    ATLAS_CUDA(cudaMemcpyAsync(m.data(), mc.ptr, nchunks * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, s));
+    ATLAS_CUDA(cudaStreamSynchronize(s));
+    for (int64_t c = 0; c < nchunks; c++) {
+      const int64_t n_c = std::min((c + 1) * R, V) - c * R;
+      max_pass = std::max(max_pass,
+                          m[c] + (model == ATLAS_GIN ? n_c : 0));
+    }
+    max_pass = std::min(max_pass, L->nloc);
+  }
+  const bool need_runs = L->sub_batch < max_pass || L->desc.record_log ||
                          L->desc.force_exact;
   if (need_runs) {
     walk(nullptr, 1);

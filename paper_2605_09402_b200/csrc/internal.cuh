@@ -19,6 +19,7 @@ struct atlas_graph {
   atlas::DevBuf<uint32_t> indeg;    // nloc
   mutable atlas::DevBuf<int> scan_flag;  // input needs the guarded division
   mutable atlas::DevBuf<unsigned long long> work;  // ring kernel scheduler
+  mutable const int32_t* known_flag = nullptr;  // producer-supplied flag
   // CSC build workspaces (kept for atlas_graph_update)
   atlas::DevBuf<uint32_t> ws_nbrs, ws_src, ws_keys, ws_vals, ws_keys_out,
       ws_sel;
@@ -155,7 +156,8 @@ void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs_dev,
 // aggregate.cu
 void launch_agg_resident(const atlas_graph* g, const void* x, int dtype,
                          int64_t ldx, int model, float gin_epsilon, int d,
-                         float* acc, int64_t ldacc, cudaStream_t s);
+                         float* acc, int64_t ldacc, const int32_t* input_flag,
+                         cudaStream_t s);
 void launch_agg_runs(const void* tile, int dtype, int64_t ldx,
                      int64_t tile_lo, const uint32_t* run_dst,
                      const int64_t* run_beg, int64_t nruns,
@@ -176,10 +178,11 @@ void launch_gather_rows(const float* acc, int64_t ldacc, const int32_t* ids,
 void launch_transform_stable(const float* x, int64_t rows, int64_t k,
                              int64_t ldx, const float* w, const float* b,
                              int64_t n, int relu, void* y, int y_dtype,
-                             int64_t ldy, cudaStream_t s);
+                             int64_t ldy, int32_t* flag, cudaStream_t s);
 bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
                          const float* w, const float* b, int64_t n, int relu,
-                         void* y, int y_dtype, int64_t ldy, cudaStream_t s);
+                         void* y, int y_dtype, int64_t ldy, int32_t* flag,
+                         cudaStream_t s);
 
 // control.cu
 void engine_init(atlas_layer* L, cudaStream_t s);

@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(256)
     transform_stable_kernel(const float* __restrict__ x, int64_t ldx,
                             int64_t M, int K, const float* __restrict__ w,
                             const float* __restrict__ b, int N, int relu,
-                            OutT* __restrict__ y, int64_t ldy) {
+                            OutT* __restrict__ y, int64_t ldy,
+                            int32_t* __restrict__ flag) {
   __shared__ __align__(16) float As[BK][BM];
   __shared__ __align__(16) float Ws[BK][BN];
   const int tid = threadIdx.x;
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
   }
+  int bad = 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     const int64_t m = m0 + ty * 4 + i;
@@ -93,9 +95,12 @@ __global__ void __launch_bounds__(256)
       if (n >= N) continue;
       float v = acc[i][j];
       if (relu) v = relu_np(v);
-      y[m * ldy + n] = cast_out<OutT>(v);
+      const OutT o = cast_out<OutT>(v);
+      y[m * ldy + n] = o;
+      bad |= is_extreme(to_f32(o));
     }
   }
+  if (__syncthreads_or(bad) && flag && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
 }  // namespace
@@ -103,20 +108,21 @@ __global__ void __launch_bounds__(256)
 void launch_transform_stable(const float* x, int64_t rows, int64_t k,
                              int64_t ldx, const float* w, const float* b,
                              int64_t n, int relu, void* y, int y_dtype,
-                             int64_t ldy, cudaStream_t s) {
+                             int64_t ldy, int32_t* flag, cudaStream_t s) {
   if (rows <= 0 || n <= 0) return;
   dim3 grid((unsigned)ceil_div(rows, BM), (unsigned)ceil_div(n, BN));
   if (y_dtype == ATLAS_F32)
     transform_stable_kernel<float><<<grid, 256, 0, s>>>(
-        x, ldx, rows, (int)k, w, b, (int)n, relu, static_cast<float*>(y), ldy);
+        x, ldx, rows, (int)k, w, b, (int)n, relu, static_cast<float*>(y), ldy,
+        flag);
   else if (y_dtype == ATLAS_F16)
     transform_stable_kernel<__half><<<grid, 256, 0, s>>>(
         x, ldx, rows, (int)k, w, b, (int)n, relu, static_cast<__half*>(y),
-        ldy);
+        ldy, flag);
   else
     transform_stable_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
         x, ldx, rows, (int)k, w, b, (int)n, relu,
-        static_cast<__nv_bfloat16*>(y), ldy);
+        static_cast<__nv_bfloat16*>(y), ldy, flag);
   count_launch();
   ATLAS_LAUNCH_CHECK();
 }

@@ -141,6 +141,7 @@ struct TcParams {
   const float* bias;
   void* y;
   uint32_t tmem_cols;
+  int32_t* flag;
 };
 
 template <typename OutT, bool RES_W>
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t aph[2] = {0, 0};
     OutT* y = static_cast<OutT*>(p.y);
     const int half = lane >> 4, col16 = lane & 15;
+    int bad = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       mbar_wait(&tfull[acc], aph[acc]);
       aph[acc] ^= 1;
@@ -363,7 +365,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (row < p.M && c < p.N) {
             float o = __fadd_rn(stage[r * 17 + col16], bias);
             if (p.relu) o = relu_np(o);
-            y[row * p.ldy + c] = cvt_out<OutT>(o);
+            const OutT q = cvt_out<OutT>(o);
+            y[row * p.ldy + c] = q;
+            bad |= is_extreme(to_f32(q));
           }
         }
         __syncwarp();
@@ -372,6 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&tempty[acc]);
       acc ^= 1;
     }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && p.flag)
+      atomicOr(p.flag, 1);
   }
   __syncthreads();
   if (warp == 1) {
@@ -435,7 +441,8 @@ int num_sms() {
 
 bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
                          const float* w, const float* b, int64_t n, int relu,
-                         void* y, int y_dtype, int64_t ldy, cudaStream_t s) {
+                         void* y, int y_dtype, int64_t ldy, int32_t* flag,
+                         cudaStream_t s) {
   if (rows <= 0) return true;
   if (n < 1 || n > 256 || k < 1 || ldx % 4 != 0 || k % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) != 0)
@@ -469,6 +476,7 @@ bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
   p.ldy = ldy;
   p.bias = b;
   p.y = y;
+  p.flag = flag;
   uint32_t cols = 32;
   while (cols < (uint32_t)(2 * BN)) cols <<= 1;
   p.tmem_cols = cols;

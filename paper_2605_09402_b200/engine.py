@@ -204,17 +204,20 @@ class DeviceLayer:
 
     # -- whole-layer path ---------------------------------------------------
     def run_resident(self, graph: DeviceGraph, x, chunk_rows: int,
-                     stream=None):
-        """x: torch CUDA tensor (V, embed_dim) f32/f16/bf16."""
+                     input_flag=None, stream=None):
+        """x: torch CUDA tensor (V, embed_dim) f32/f16/bf16. input_flag:
+        the int32 CUDA tensor the transform that produced x filled (spares
+        a scan of x), or None."""
         if x.shape[1] != self.embed_dim or x.shape[0] != self.num_vertices:
             raise ConfigError(f"input {tuple(x.shape)} does not match layer "
                               f"({self.num_vertices}, {self.embed_dim})")
         N.check(N.load_library().atlas_layer_run_resident(
             self.handle, graph.handle, x.data_ptr(), torch_dtype_code(x),
-            x.stride(0), int(chunk_rows), N.stream_handle(stream)))
+            x.stride(0), int(chunk_rows), N.ptr(input_flag),
+            N.stream_handle(stream)))
 
     def run_streamed(self, graph: DeviceGraph, x_host, chunk_rows: int,
-                     tile_bytes: int = 128 << 20, stream=None):
+                     tile_bytes: int = 256 << 20, stream=None):
         """x_host: pinned CPU torch tensor (V, embed_dim); streamed to HBM
         in double-buffered tiles while earlier tiles aggregate."""
         if x_host.shape[1] != self.embed_dim or \
@@ -311,12 +314,14 @@ class DeviceLayer:
 
 
 def transform_device(x_ptr: int, rows: int, k: int, ldx: int, w, b,
-                     relu: bool, y, backend_code: int, stream=None):
-    """y = act(x . W^T + b) on the GPU; w, b, y torch CUDA tensors."""
+                     relu: bool, y, backend_code: int, flag=None,
+                     stream=None):
+    """y = act(x . W^T + b) on the GPU; w, b, y torch CUDA tensors; flag
+    (int32 CUDA tensor or None) receives the output extremes flag."""
     N.check(N.load_library().atlas_transform(
         backend_code, x_ptr, rows, k, ldx, w.data_ptr(), b.data_ptr(),
         w.shape[0], int(relu), y.data_ptr(), torch_dtype_code(y),
-        y.stride(0), N.stream_handle(stream)))
+        y.stride(0), N.ptr(flag), N.stream_handle(stream)))
 
 
 def percentile99(count: int, q_lo: int, q_hi: int) -> float:

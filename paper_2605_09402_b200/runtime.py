@@ -75,7 +75,7 @@ class PipelineConfig:
     embed_dtype: str = "f32"       # next-layer embedding store: f32|f16|bf16
     record_log: bool = False        # keep victim/reload/graduation logs
     force_exact: bool = False       # always replay the exact control engine
-    stream_tile_bytes: int = 128 << 20  # host->HBM tile of a streamed input
+    stream_tile_bytes: int = 256 << 20  # host->HBM tile of a streamed input
 
     def validate(self) -> None:
         if self.partitions < 1:
@@ -156,6 +156,7 @@ class Engine:
                   for lw in weights.layers]
         self.last_layers = []
         self._layers = {}
+        self.out_flags = {}
 
     def close(self):
         for layer in self._layers.values():
@@ -163,9 +164,11 @@ class Engine:
         self._layers.clear()
         self.graph.close()
 
-    def layer(self, l: int, x, *, chunk_budget=None):
-        """One layer: x (V, d) CUDA tensor -> (y (V or range, out), metrics,
-        device layer handle)."""
+    def layer(self, l: int, x, *, chunk_budget=None, input_flag=None):
+        """One layer: x (V, d) CUDA tensor (or pinned host tensor, streamed)
+        -> (y (V or range, out), metrics, device layer handle).
+        ``input_flag``: extremes flag of the transform that produced x; the
+        output's flag is left in ``self.out_flags[l]``."""
         import torch
 
         cfg = self.config
@@ -192,7 +195,7 @@ class Engine:
                 device=self.device)
             self._layers[l] = layer
         if x.is_cuda:
-            layer.run_resident(self.graph, x, rows)
+            layer.run_resident(self.graph, x, rows, input_flag=input_flag)
         else:  # host (pinned) input: stream it in tiles (K1 streamer)
             layer.run_streamed(self.graph, x, rows,
                                tile_bytes=self.config.stream_tile_bytes)
@@ -207,8 +210,12 @@ class Engine:
         ev0.record()
         if nloc:
             if code is not None:
+                if l not in self.out_flags:
+                    self.out_flags[l] = torch.zeros(1, dtype=torch.int32,
+                                                    device="cuda")
                 transform_device(acc_ptr, nloc, w.agg_dim(l), ld, self.W[l],
-                                 self.b[l], not last, y, code)
+                                 self.b[l], not last, y, code,
+                                 flag=self.out_flags[l])
             else:  # host plug-in backend (reference MatmulBackend protocol)
                 from .compute import transform
                 agg = layer.accumulator().cpu().numpy()
@@ -231,14 +238,19 @@ class Engine:
     def infer(self, x, keep_layers: bool = False):
         """All layers; returns (final local output, [LayerMetrics])."""
         metrics, outs = [], []
-        h = x
+        h, flag = x, None
         for l in range(len(self.weights.layers)):
-            y, m, _ = self.layer(l, h)
+            y, m, _ = self.layer(l, h, input_flag=flag)
             metrics.append(m)
             if keep_layers:
                 outs.append(y)
             if l != len(self.weights.layers) - 1:
                 h = self.gather(y)
+                flag = self.out_flags.get(l)
+                if flag is not None and self.world > 1:
+                    import torch.distributed as dist
+                    dist.all_reduce(flag, op=dist.ReduceOp.MAX,
+                                    group=self.group)
         self.last_layers = outs
         return y, metrics
 

@@ -219,3 +219,32 @@ def test_tcgen05_transform_3xtf32_accuracy(m, k, n, relu):
     scale = np.abs(x).astype(np.float64) @ np.abs(w).astype(np.float64).T
     err = np.abs(got - ref)
     assert np.all(err <= 4e-6 * (scale + 1e-3)), float((err / (scale + 1e-3)).max())
+
+
+def test_tiny_and_huge_inputs_take_the_exact_division():
+    """Subnormal / tiny / huge inputs: the guarded IEEE division path must
+    keep records bit-identical to the reference order of f32 operations."""
+    from oracle import engine as OE
+    from paper_2605_09402_b200.storage import (ModelKind, random_weights,
+                                               synthetic_in_memory)
+    graph, feats = synthetic_in_memory("uniform", 3000, 7, 8, 21)
+    rng = np.random.default_rng(4)
+    pick = rng.random(feats.shape)
+    feats = feats.copy()
+    feats[pick < 0.05] = np.float32(1e-39)      # subnormal
+    feats[(pick > 0.05) & (pick < 0.1)] = np.float32(3e-31)  # tiny normal
+    feats[pick > 0.97] = np.float32(3e37)       # huge
+    for kind in (ModelKind.GCN, ModelKind.SAGE):
+        w = random_weights(kind, [8, 4], 5)
+        eng = Engine(graph, w, PipelineConfig(chunk_budget=4096,
+                                              hot_slots=3000))
+        y, m, _ = eng.layer(0, torch.as_tensor(feats).cuda())
+        rows = max(1, 4096 // (8 * 4))
+        want, _, _ = OE.run_layer(graph.offsets, graph.neighbors,
+                                  graph.in_degrees, feats, int(kind),
+                                  w.layers[0].weight, w.layers[0].bias,
+                                  relu=False, embed_dim=8,
+                                  agg_dim=w.agg_dim(0), chunk_rows=rows,
+                                  slot_count=3000)
+        np.testing.assert_array_equal(y.cpu().numpy(), want)
+        eng.close()
