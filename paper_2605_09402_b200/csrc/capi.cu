@@ -40,6 +40,7 @@ static void load_graph(atlas_graph* g, int64_t V, int64_t E,
                        const int64_t* offsets_host,
                        const uint32_t* neighbors_host,
                        const uint32_t* in_degrees_host, cudaStream_t s) {
+  g->maxpass_cache.clear();
   g->V = V;
   g->E = E;
   g->offsets.reserve(V + 1);
@@ -52,6 +53,37 @@ static void load_graph(atlas_graph* g, int64_t V, int64_t E,
                                E * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                s));
   build_csc(g, g->ws_nbrs, in_degrees_host, s);
+}
+
+// control stream + timing events of whole-layer passes (created once)
+static void ensure_ctl(atlas_layer* L) {
+  if (L->ctl_stream) return;
+  ATLAS_CUDA(cudaStreamCreateWithFlags(&L->ctl_stream, cudaStreamNonBlocking));
+  for (auto& e : L->tev) ATLAS_CUDA(cudaEventCreate(&e));
+}
+
+// take any deferred control verdict and the pending pass timings
+static void settle(atlas_layer* L) {
+  settle_control(L);
+  if (L->timing_pending) {
+    L->timing_pending = false;
+    ATLAS_CUDA(cudaEventSynchronize(L->tev[1]));
+    ATLAS_CUDA(cudaEventSynchronize(L->tev[3]));
+    ATLAS_CUDA(cudaEventElapsedTime(&L->timing_ms[0], L->tev[0], L->tev[1]));
+    ATLAS_CUDA(cudaEventElapsedTime(&L->timing_ms[1], L->tev[2], L->tev[3]));
+  }
+}
+
+// queue the control plane of a whole-layer pass on the control stream,
+// ordered after everything already queued on the launch stream s
+static void launch_control(atlas_layer* L, const atlas_graph* g,
+                           int64_t chunk_rows, cudaStream_t s) {
+  ensure_ctl(L);
+  ATLAS_CUDA(cudaEventRecord(L->tev[0], s));
+  ATLAS_CUDA(cudaStreamWaitEvent(L->ctl_stream, L->tev[0], 0));
+  ATLAS_CUDA(cudaEventRecord(L->tev[2], L->ctl_stream));
+  resident_control(L, g, chunk_rows, L->ctl_stream);
+  ATLAS_CUDA(cudaEventRecord(L->tev[3], L->ctl_stream));
 }
 
 }  // namespace atlas
@@ -169,6 +201,7 @@ int atlas_layer_reset(atlas_layer* L, void* stream) {
     if (!L) fail(ATLAS_ECONFIG, "null layer");
     use_device(L->desc.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    settle(L);
     const int64_t nn = std::max<int64_t>(L->nloc, 1);
     ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
     L->chunk_reloads.clear();
@@ -244,20 +277,17 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
     if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
     use_device(D.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cudaEvent_t ev[3];
-    for (auto& e : ev) ATLAS_CUDA(cudaEventCreate(&e));
-    ATLAS_CUDA(cudaEventRecord(ev[0], s));
+    settle(L);
+    // control plane first (own stream, runs beside the data plane), then
+    // the scatter-aggregate; s waits for the control plane at the end
+    launch_control(L, g, chunk_rows, s);
     if (L->nloc > 0)
       launch_agg_resident(g, x, dtype, ldx, D.model, D.gin_epsilon,
                           (int)D.embed_dim, L->acc.ptr, D.agg_dim,
                           input_flag, s);
-    ATLAS_CUDA(cudaEventRecord(ev[1], s));
-    resident_control(L, g, chunk_rows, s);
-    ATLAS_CUDA(cudaEventRecord(ev[2], s));
-    ATLAS_CUDA(cudaEventSynchronize(ev[2]));
-    ATLAS_CUDA(cudaEventElapsedTime(&L->timing_ms[0], ev[0], ev[1]));
-    ATLAS_CUDA(cudaEventElapsedTime(&L->timing_ms[1], ev[1], ev[2]));
-    for (auto& e : ev) cudaEventDestroy(e);
+    ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
+    ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
+    L->timing_pending = true;
   });
 }
 
@@ -296,11 +326,10 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
                                  L->nloc * sizeof(int64_t),
                                  cudaMemcpyDeviceToDevice, s));
     ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
-    cudaEvent_t ev[3];
-    for (auto& e : ev) ATLAS_CUDA(cudaEventCreate(&e));
-    ATLAS_CUDA(cudaEventRecord(ev[0], s));
+    settle(L);
+    launch_control(L, g, chunk_rows, s);  // records tev[0] after the resets
     // the copy stream may only start once s has the cursor/touched resets
-    ATLAS_CUDA(cudaStreamWaitEvent(L->copy_stream, ev[0], 0));
+    ATLAS_CUDA(cudaStreamWaitEvent(L->copy_stream, L->tev[0], 0));
     const int64_t ntiles = ceil_div(V, tile_rows);
     for (int64_t t = 0; t < ntiles; t++) {
       const int b = (int)(t & 1);
@@ -319,13 +348,9 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
                         D.agg_dim, L->cursor.ptr, L->touched.ptr, s);
       ATLAS_CUDA(cudaEventRecord(L->ev_free[b], s));
     }
-    ATLAS_CUDA(cudaEventRecord(ev[1], s));
-    resident_control(L, g, chunk_rows, s);
-    ATLAS_CUDA(cudaEventRecord(ev[2], s));
-    ATLAS_CUDA(cudaEventSynchronize(ev[2]));
-    ATLAS_CUDA(cudaEventElapsedTime(&L->timing_ms[0], ev[0], ev[1]));
-    ATLAS_CUDA(cudaEventElapsedTime(&L->timing_ms[1], ev[1], ev[2]));
-    for (auto& e : ev) cudaEventDestroy(e);
+    ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
+    ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
+    L->timing_pending = true;
   });
 }
 
@@ -347,6 +372,8 @@ int atlas_reorder(int32_t device, int64_t V, int64_t E, const int64_t* off,
 int atlas_layer_timing(atlas_layer* L, float* ms, int32_t n) {
   return guarded([&] {
     if (!L || !ms) fail(ATLAS_ECONFIG, "null argument");
+    use_device(L->desc.device);
+    settle(L);
     for (int i = 0; i < n && i < 2; i++) ms[i] = L->timing_ms[i];
   });
 }
@@ -386,6 +413,7 @@ int atlas_layer_finish(atlas_layer* L, atlas_layer_metrics* m) {
     if (!L || !m) fail(ATLAS_ECONFIG, "null argument");
     use_device(L->desc.device);
     cudaStream_t s = nullptr;
+    settle(L);
     ATLAS_CUDA(cudaDeviceSynchronize());
     std::memset(m, 0, sizeof(*m));
     finish_spans(L, s);
@@ -440,6 +468,7 @@ int atlas_layer_state(atlas_layer* L, uint32_t* pending, uint8_t* state,
   return guarded([&] {
     if (!L) fail(ATLAS_ECONFIG, "null layer");
     use_device(L->desc.device);
+    settle(L);
     ATLAS_CUDA(cudaDeviceSynchronize());
     const int64_t n = L->nloc;
     if (n == 0) return;
@@ -468,6 +497,8 @@ int atlas_layer_chunk_stats(atlas_layer* L, int64_t* reloads, int64_t* touched,
                             int64_t cap, int64_t* count) {
   return guarded([&] {
     if (!L) fail(ATLAS_ECONFIG, "null layer");
+    use_device(L->desc.device);
+    settle(L);
     const int64_t n = (int64_t)L->chunk_reloads.size();
     if (count) *count = n;
     if (!reloads && !touched) return;
@@ -484,6 +515,8 @@ int atlas_layer_log(atlas_layer* L, int32_t which, int64_t* out, int64_t cap,
   return guarded([&] {
     if (!L) fail(ATLAS_ECONFIG, "null layer");
     if (!L->desc.record_log) fail(ATLAS_ECONFIG, "layer was not logging");
+    use_device(L->desc.device);
+    settle(L);
     EngineScalars sc = read_scalars(L, nullptr);
     DevBuf<int64_t>* buf;
     int64_t used;

@@ -307,70 +307,40 @@ void finish_spans(atlas_layer* L, cudaStream_t s) {
   ATLAS_CUDA(cudaStreamSynchronize(s));
 }
 
-void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
-                      cudaStream_t s) {
-  const int64_t V = g->V;
-  const int model = L->desc.model;
-  Plan p{R, V, ceil_div(V, R)};
+// Largest edge pass of any chunk under plan R (GIN adds the chunk's self
+// terms): topology-only, so cached per (graph generation, R).
+static int64_t max_pass_of(atlas_layer* L, const atlas_graph* g, const Plan& p,
+                           cudaStream_t s) {
+  for (const auto& e : g->maxpass_cache)
+    if (e.first == p.R * 4 + L->desc.model) return e.second;
   const int64_t nchunks = p.nchunks;
-  DevBuf<unsigned long long>& hist = L->ctl_hist;  // admit 3C|grad 3C|runs C
-  hist.reserve(7 * std::max<int64_t>(nchunks, 1));
-  ATLAS_CUDA(cudaMemsetAsync(hist.ptr, 0,
-                             7 * std::max<int64_t>(nchunks, 1) * 8, s));
-  // grid-stride warps; per-block shared histogram when 7C u32 fit in 48 KB
-  const size_t hbytes = 7 * (size_t)nchunks * 4;
-  const int use_smem = hbytes <= 48 * 1024 ? 1 : 0;
-  const unsigned blocks = (unsigned)std::min<int64_t>(
-      148 * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
-  auto walk = [&](uint64_t* at_pos, int count_runs) {
-    walk_destinations<<<blocks, 256, use_smem ? hbytes : 0, s>>>(
-        model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
-        g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
-        hist.ptr, use_smem, at_pos, count_runs);
-    count_launch();
-    ATLAS_LAUNCH_CHECK();
-  };
-  // An edge pass holds at most min(nloc, m_c (+ n_c for GIN)) destinations,
-  // so when that bound is <= sub_batch for every chunk each pass is one
-  // sub-batch and the per-chunk run counts (an E-wide walk) are not needed
-  // to prove it; they only feed reload-% denominators, whose numerators are
-  // zero on the eviction-free path.
-  int64_t max_pass = 0;
-  {
-    DevBuf<int64_t>& mc = L->span_buf;  // reused scratch (>= nchunks)
-    mc.reserve(std::max<int64_t>(nchunks, 1));
-    chunk_edges<<<grid_of(nchunks), 256, 0, s>>>(g->offsets.ptr, p, mc.ptr);
-    count_launch();
-    ATLAS_LAUNCH_CHECK();
-    std::vector<int64_t> m(nchunks);
-    ATLAS_CUDA(cudaMemcpyAsync(m.data(), mc.ptr, nchunks * sizeof(int64_t),
-                               cudaMemcpyDeviceToHost, s));
-    ATLAS_CUDA(cudaStreamSynchronize(s));
-    for (int64_t c = 0; c < nchunks; c++) {
-      const int64_t n_c = std::min((c + 1) * R, V) - c * R;
-      max_pass = std::max(max_pass,
-                          m[c] + (model == ATLAS_GIN ? n_c : 0));
-    }
-    max_pass = std::min(max_pass, L->nloc);
-  }
-  const bool need_runs = L->sub_batch < max_pass || L->desc.record_log ||
-                         L->desc.force_exact;
-  if (need_runs) {
-    walk(nullptr, 1);
-  } else {
-    walk_light<<<blocks, 256, use_smem ? hbytes : 0, s>>>(
-        model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
-        g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
-        hist.ptr, use_smem);
-    count_launch();
-    ATLAS_LAUNCH_CHECK();
-  }
-  std::vector<unsigned long long> h(7 * nchunks);
-  ATLAS_CUDA(cudaMemcpyAsync(h.data(), hist.ptr, h.size() * sizeof(h[0]),
+  DevBuf<int64_t>& mc = L->span_buf;  // reused scratch (>= nchunks)
+  mc.reserve(std::max<int64_t>(nchunks, 1));
+  chunk_edges<<<grid_of(nchunks), 256, 0, s>>>(g->offsets.ptr, p, mc.ptr);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  std::vector<int64_t> m(nchunks);
+  ATLAS_CUDA(cudaMemcpyAsync(m.data(), mc.ptr, nchunks * sizeof(int64_t),
                              cudaMemcpyDeviceToHost, s));
   ATLAS_CUDA(cudaStreamSynchronize(s));
+  int64_t max_pass = 0;
+  for (int64_t c = 0; c < nchunks; c++) {
+    const int64_t n_c = std::min((c + 1) * p.R, p.V) - c * p.R;
+    max_pass = std::max(max_pass,
+                        m[c] + (L->desc.model == ATLAS_GIN ? n_c : 0));
+  }
+  g->maxpass_cache.emplace_back(p.R * 4 + L->desc.model, max_pass);
+  return max_pass;
+}
 
-  // eviction-free trajectory at (chunk, pass) granularity
+// Eviction-free verdict from the (chunk, pass) admission / graduation
+// histogram h (7C entries). Returns true and fills the fast-path metrics
+// when the reference provably never evicts.
+static bool fast_verdict(atlas_layer* L, const atlas_graph* g, int64_t R,
+                         const unsigned long long* h) {
+  const int64_t V = g->V;
+  const int model = L->desc.model;
+  const int64_t nchunks = ceil_div(V, R);
   bool single = true;
   int64_t hot = 0, peak = 0;
   std::vector<int64_t> touched(nchunks, 0);
@@ -394,18 +364,30 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
   }
   const bool fast = single && peak <= L->desc.slot_count &&
                     !L->desc.record_log && !L->desc.force_exact;
-  L->chunks_seen += nchunks;
-  if (fast) {
-    L->fast_path = true;
-    L->fp_hot_peak = peak;
-    L->fp_messages = g->eloc + (model == ATLAS_GCN ? 0 : L->nloc);
-    for (int64_t c = 0; c < nchunks; c++) {
-      L->chunk_reloads.push_back(0);
-      L->chunk_touched.push_back(touched[c]);
-    }
-    return;
+  if (!fast) return false;
+  L->fast_path = true;
+  L->fp_hot_peak = peak;
+  L->fp_messages = g->eloc + (model == ATLAS_GCN ? 0 : L->nloc);
+  for (int64_t c = 0; c < nchunks; c++) {
+    L->chunk_reloads.push_back(0);
+    L->chunk_touched.push_back(touched[c]);
   }
-  // exact replay: materialise runs in first-appearance order
+  return true;
+}
+
+// exact replay: materialise runs in first-appearance order and run the
+// single-CTA engine over them (synchronous)
+static void exact_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
+                         cudaStream_t s) {
+  const int64_t V = g->V;
+  const int model = L->desc.model;
+  Plan p{R, V, ceil_div(V, R)};
+  const int64_t nchunks = p.nchunks;
+  DevBuf<unsigned long long>& hist = L->ctl_hist;
+  const size_t hbytes = 7 * (size_t)nchunks * 4;
+  const int use_smem = hbytes <= 48 * 1024 ? 1 : 0;
+  const unsigned blocks = (unsigned)std::min<int64_t>(
+      148 * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
   L->fast_path = false;
   const int64_t npos = g->E + (model == ATLAS_GCN ? 0 : V) + 1;
   DevBuf<uint64_t> at_pos, runs;
@@ -415,7 +397,13 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
   fill_u64<<<grid_of(npos), 256, 0, s>>>(at_pos.ptr, npos, kNoRun);
   count_launch();
   ATLAS_CUDA(cudaMemsetAsync(hist.ptr, 0, hist.bytes(), s));
-  walk(at_pos.ptr, 1);
+  walk_destinations<<<blocks, 256, use_smem ? hbytes : 0, s>>>(
+      model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
+      g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
+      hist.ptr, use_smem, at_pos.ptr, 1);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  std::vector<unsigned long long> h(7 * nchunks);
   ATLAS_CUDA(cudaMemcpyAsync(h.data(), hist.ptr, h.size() * sizeof(h[0]),
                              cudaMemcpyDeviceToHost, s));
   ATLAS_CUDA(cudaStreamSynchronize(s));
@@ -459,6 +447,75 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
                              cudaMemcpyHostToDevice, s));
   engine_run_chunks(L, runs.ptr, d_off.ptr, d_bounds.ptr, nchunks,
                     run_off.data(), s);
+}
+
+// Control plane of a whole-layer pass on the reference chunk plan R.
+// When no chunk pass can split into sub-batches (topology-only bound,
+// cached) and no logs are requested, the parallel walk and the readback of
+// its histogram are only QUEUED on s, and the verdict is taken later by
+// settle_control(): the host never waits for the data plane here. A
+// negative verdict then runs the exact replay (which only touches control
+// state, never the records).
+void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
+                      cudaStream_t s) {
+  const int64_t V = g->V;
+  const int model = L->desc.model;
+  Plan p{R, V, ceil_div(V, R)};
+  const int64_t nchunks = p.nchunks;
+  DevBuf<unsigned long long>& hist = L->ctl_hist;  // admit 3C|grad 3C|runs C
+  hist.reserve(7 * std::max<int64_t>(nchunks, 1));
+  // An edge pass holds at most min(nloc, m_c (+ n_c for GIN)) destinations,
+  // so when that bound is <= sub_batch for every chunk each pass is one
+  // sub-batch and the per-chunk run counts (an E-wide walk) are not needed
+  // to prove it; they only feed reload-% denominators, whose numerators are
+  // zero on the eviction-free path.
+  const int64_t max_pass = std::min(max_pass_of(L, g, p, s), L->nloc);
+  const bool need_runs = L->sub_batch < max_pass || L->desc.record_log ||
+                         L->desc.force_exact;
+  ATLAS_CUDA(cudaMemsetAsync(hist.ptr, 0,
+                             7 * std::max<int64_t>(nchunks, 1) * 8, s));
+  // grid-stride warps; per-block shared histogram when 7C u32 fit in 48 KB
+  const size_t hbytes = 7 * (size_t)nchunks * 4;
+  const int use_smem = hbytes <= 48 * 1024 ? 1 : 0;
+  const unsigned blocks = (unsigned)std::min<int64_t>(
+      148 * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
+  L->chunks_seen += nchunks;
+  if (need_runs) {
+    walk_destinations<<<blocks, 256, use_smem ? hbytes : 0, s>>>(
+        model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
+        g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
+        hist.ptr, use_smem, nullptr, 1);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+    std::vector<unsigned long long> h(7 * nchunks);
+    ATLAS_CUDA(cudaMemcpyAsync(h.data(), hist.ptr, h.size() * sizeof(h[0]),
+                               cudaMemcpyDeviceToHost, s));
+    ATLAS_CUDA(cudaStreamSynchronize(s));
+    if (!fast_verdict(L, g, R, h.data())) exact_replay(L, g, R, s);
+    return;
+  }
+  walk_light<<<blocks, 256, use_smem ? hbytes : 0, s>>>(
+      model, p, g->offsets.ptr, g->csc_ptr.ptr, g->csc_src.ptr,
+      g->csc_eid.ptr, g->lo, L->nloc, L->first_pos.ptr, L->last_pos.ptr,
+      hist.ptr, use_smem);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  L->pin_hist.reserve(7 * std::max<int64_t>(nchunks, 1));
+  ATLAS_CUDA(cudaMemcpyAsync(L->pin_hist.ptr, hist.ptr,
+                             7 * nchunks * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+  L->ctl_deferred = true;
+  L->ctl_graph = g;
+  L->ctl_R = R;
+}
+
+// Take a deferred verdict (waits for the control stream only).
+void settle_control(atlas_layer* L) {
+  if (!L->ctl_deferred) return;
+  L->ctl_deferred = false;
+  ATLAS_CUDA(cudaStreamSynchronize(L->ctl_stream));
+  if (!fast_verdict(L, L->ctl_graph, L->ctl_R, L->pin_hist.ptr))
+    exact_replay(L, L->ctl_graph, L->ctl_R, L->ctl_stream);
 }
 
 }  // namespace atlas

@@ -1,6 +1,7 @@
 // Handle layouts and launcher declarations shared by the .cu files.
 #pragma once
 
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -20,6 +21,8 @@ struct atlas_graph {
   mutable atlas::DevBuf<int> scan_flag;  // input needs the guarded division
   mutable atlas::DevBuf<unsigned long long> work;  // ring kernel scheduler
   mutable const int32_t* known_flag = nullptr;  // producer-supplied flag
+  // (R * 4 + model) -> largest chunk pass; cleared by atlas_graph_update
+  mutable std::vector<std::pair<int64_t, int64_t>> maxpass_cache;
   // CSC build workspaces (kept for atlas_graph_update)
   atlas::DevBuf<uint32_t> ws_nbrs, ws_src, ws_keys, ws_vals, ws_keys_out,
       ws_sel;
@@ -127,6 +130,16 @@ struct atlas_layer {
   int64_t fp_hot_peak = 0;
   int64_t fp_messages = 0;
   float timing_ms[2] = {0.f, 0.f};
+  // whole-layer passes: the control plane runs on its own stream next to
+  // the data plane; tev = data begin/end (launch stream), control
+  // begin/end (ctl_stream). Times and a deferred verdict are read lazily.
+  cudaStream_t ctl_stream = nullptr;
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool timing_pending = false;
+  bool ctl_deferred = false;
+  const atlas_graph* ctl_graph = nullptr;
+  int64_t ctl_R = 0;
+  atlas::PinnedBuf<unsigned long long> pin_hist;
   // reusable workspaces (kept across resets so repeated layers allocate once)
   atlas::DevBuf<unsigned long long> ctl_hist;
   atlas::DevBuf<int64_t> span_buf, span_sorted;
@@ -140,6 +153,9 @@ struct atlas_layer {
   cudaEvent_t ev_free[2] = {nullptr, nullptr};
   ~atlas_layer() {
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (ctl_stream) cudaStreamDestroy(ctl_stream);
+    for (auto& e : tev)
+      if (e) cudaEventDestroy(e);
     for (int i = 0; i < 2; i++) {
       if (ev_ready[i]) cudaEventDestroy(ev_ready[i]);
       if (ev_free[i]) cudaEventDestroy(ev_free[i]);
@@ -192,6 +208,7 @@ void engine_run_chunks(atlas_layer* L, const uint64_t* runs,
                        cudaStream_t s);
 void resident_control(atlas_layer* L, const atlas_graph* g,
                       int64_t chunk_rows, cudaStream_t s);
+void settle_control(atlas_layer* L);
 void chunk_spans(atlas_layer* L, int64_t start, int64_t end,
                  const int64_t* offsets_dev, const int64_t* nbrs_dev,
                  int64_t m, cudaStream_t s);

@@ -15,7 +15,9 @@
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2-5   splitter: x tile -> x_hi (in place) + x_lo (generic proxy
 //               writes, then fence.proxy.async before the MMA reads)
-//   warps 6-9   epilogue: tcgen05.ld 32x32b -> +bias -> ReLU -> global
+//   warps 6-13  epilogue: tcgen05.ld 32x32b -> per-warp smem transpose ->
+//               +bias -> ReLU -> 16-B row-contiguous stores; warp 6+q and
+//               10+q share TMEM lane quarter q and alternate 16-col blocks
 // Two TMEM accumulators (2 x BN columns) let the epilogue of tile t
 // overlap the MMAs of tile t+1.
 #include <cuda.h>
@@ -28,7 +30,9 @@ namespace atlas {
 namespace {
 
 constexpr int BM = 128, BK = 32;  // BK f32 = 128 B = one swizzle atom row
-constexpr int kThreads = 320;
+constexpr int kEpiWarps = 8;           // two per TMEM lane quarter
+constexpr int kStageLd = 20;           // 32 x 16 staging block, padded
+constexpr int kThreads = (6 + kEpiWarps) * 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -134,6 +138,19 @@ __device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v) {
   return __float2bfloat16_rn(v);
 }
 
+__device__ __forceinline__ void store4(float* d, const float (&q)[4]) {
+  *reinterpret_cast<float4*>(d) = make_float4(q[0], q[1], q[2], q[3]);
+}
+template <typename H>
+__device__ __forceinline__ void store4(H* d, const H (&q)[4]) {
+  uint2 u;
+  u.x = (uint32_t)__half_as_ushort(*reinterpret_cast<const __half*>(&q[0])) |
+        ((uint32_t)__half_as_ushort(*reinterpret_cast<const __half*>(&q[1])) << 16);
+  u.y = (uint32_t)__half_as_ushort(*reinterpret_cast<const __half*>(&q[2])) |
+        ((uint32_t)__half_as_ushort(*reinterpret_cast<const __half*>(&q[3])) << 16);
+  *reinterpret_cast<uint2*>(d) = u;
+}
+
 struct TcParams {
   int64_t M;
   int K, N, BN, stages, kblocks, relu;
@@ -168,7 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* wsplit = wfull + 1;        // resident W split
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wsplit + 1);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
-  float* stage_out = sbias + 256;
+  float* stage_out = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(sbias + 256) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (p.M + BM - 1) / BM;
@@ -181,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; a++) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], kEpiWarps * 32);
     }
     mbar_init(wfull, 1);
     mbar_init(wsplit, 128);
@@ -334,14 +352,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------- epilogue ----------------
-    // each thread owns one accumulator row (TMEM lane); 32x16 blocks go
-    // through a per-warp smem transpose so global stores are 64-B runs
+    // thread = accumulator row (TMEM lane) for tcgen05.ld; each 32 x 16
+    // block is transposed through a per-warp smem tile so that a warp store
+    // covers 8 rows x 64 B (4 lanes x 16 B per row)
+    const int ew = warp - 6;
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
-    float* stage = stage_out + (warp - 6) * 32 * 17;
+    const int cpar = ew >> 2;      // which 16-col blocks this warp takes
+    float* stage = stage_out + ew * 32 * kStageLd;
     int acc = 0;
     uint32_t aph[2] = {0, 0};
     OutT* y = static_cast<OutT*>(p.y);
-    const int half = lane >> 4, col16 = lane & 15;
+    const int rsub = lane >> 2, c4 = (lane & 3) * 4;
+    const bool vec_ok = (p.ldy % 4) == 0 &&
+                        (reinterpret_cast<uintptr_t>(p.y) % (4 * sizeof(OutT))) == 0;
     int bad = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       mbar_wait(&tfull[acc], aph[acc]);
@@ -350,24 +373,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t row0 = t * BM + quarter * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
                              (uint32_t)(acc * p.BN);
-      for (int c0 = 0; c0 < p.BN; c0 += 16) {
+      for (int c0 = cpar * 16; c0 < p.BN; c0 += 32) {
         float v[16];
         tmem_ld16(taddr + c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; j++) stage[lane * 17 + j] = v[j];
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(&stage[lane * kStageLd + j]) =
+              make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         __syncwarp();
-        const int c = c0 + col16;
-        const float bias = sbias[c];
-#pragma unroll 4
-        for (int rr = 0; rr < 32; rr += 2) {
-          const int r = rr + half;
+        const int c = c0 + c4;
+        float bias4[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) bias4[j] = sbias[c + j];
+#pragma unroll
+        for (int rr = 0; rr < 32; rr += 8) {
+          const int r = rr + rsub;
           const int64_t row = row0 + r;
-          if (row < p.M && c < p.N) {
-            float o = __fadd_rn(stage[r * 17 + col16], bias);
-            if (p.relu) o = relu_np(o);
-            const OutT q = cvt_out<OutT>(o);
-            y[row * p.ldy + c] = q;
-            bad |= is_extreme(to_f32(q));
+          if (row < p.M) {
+            const float4 a = *reinterpret_cast<const float4*>(&stage[r * kStageLd + c4]);
+            const float av[4] = {a.x, a.y, a.z, a.w};
+            OutT q[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+              float o = __fadd_rn(av[j], bias4[j]);
+              if (p.relu) o = relu_np(o);
+              q[j] = cvt_out<OutT>(o);
+              bad |= (c + j < p.N) ? is_extreme(to_f32(q[j])) : 0;
+            }
+            OutT* dst = y + row * p.ldy + c;
+            if (vec_ok && c + 4 <= p.N) {
+              store4(dst, q);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 4; j++)
+                if (c + j < p.N) dst[j] = q[j];
+            }
           }
         }
         __syncwarp();
@@ -455,7 +495,7 @@ bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
     return false;
   // W (hi + lo, all k-blocks) stays resident when it leaves room for two
   // x stages; otherwise it streams through the stages with x
-  const int budget = 220 * 1024 - 1024 - 2048 - 4 * 32 * 17 * 4;
+  const int budget = 220 * 1024 - 1024 - 2048 - kEpiWarps * 32 * kStageLd * 4;
   const int x_stage = 2 * BM * BK * 4;
   const int w_res = 2 * BN * BK * 4 * kblocks;
   const bool res_w = w_res + 2 * x_stage <= budget;
@@ -464,7 +504,8 @@ bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
   if (stages > 4) stages = 4;
   if (stages < 2) return false;
   const int smem = 1024 + (res_w ? w_res : 0) + stages * stage_bytes +
-                   8 * (3 * stages + 6) + 16 + 4 * 256 + 4 * 32 * 17 * 4;
+                   8 * (3 * stages + 6) + 16 + 4 * 256 + 16 +
+                   kEpiWarps * 32 * kStageLd * 4;
   TcParams p{};
   p.M = rows;
   p.K = (int)k;

@@ -164,11 +164,15 @@ class Engine:
         self._layers.clear()
         self.graph.close()
 
-    def layer(self, l: int, x, *, chunk_budget=None, input_flag=None):
+    def layer(self, l: int, x, *, chunk_budget=None, input_flag=None,
+              defer_metrics: bool = False):
         """One layer: x (V, d) CUDA tensor (or pinned host tensor, streamed)
         -> (y (V or range, out), metrics, device layer handle).
         ``input_flag``: extremes flag of the transform that produced x; the
-        output's flag is left in ``self.out_flags[l]``."""
+        output's flag is left in ``self.out_flags[l]``.
+        With ``defer_metrics`` nothing waits for the device: the second
+        element is a callable that collects the metrics later (the layer's
+        control-plane verdict and timings are taken then)."""
         import torch
 
         cfg = self.config
@@ -223,11 +227,17 @@ class Engine:
                     agg, w.layers[l], apply_activation=not last,
                     backend=self.backend)))
         ev1.record()
-        m = metrics_from_device(layer, l)
-        m.agg_ms, m.control_ms = layer.timing()
-        m.transform_ms = ev0.elapsed_time(ev1)
-        m.gpu_seconds = time.perf_counter() - t0
-        return y, m, layer
+
+        def collect():
+            m = metrics_from_device(layer, l)
+            m.agg_ms, m.control_ms = layer.timing()
+            m.transform_ms = ev0.elapsed_time(ev1)
+            m.gpu_seconds = time.perf_counter() - t0
+            return m
+
+        if defer_metrics:
+            return y, collect, layer
+        return y, collect(), layer
 
     def gather(self, y_local):
         """All ranks' ranges -> full (V, out) next-layer input (NCCL)."""
@@ -237,11 +247,14 @@ class Engine:
 
     def infer(self, x, keep_layers: bool = False):
         """All layers; returns (final local output, [LayerMetrics])."""
-        metrics, outs = [], []
+        pending, outs = [], []
         h, flag = x, None
         for l in range(len(self.weights.layers)):
-            y, m, _ = self.layer(l, h, input_flag=flag)
-            metrics.append(m)
+            # every layer is queued before any metric is read back, so the
+            # host never stalls the device between layers
+            y, collect, _ = self.layer(l, h, input_flag=flag,
+                                       defer_metrics=True)
+            pending.append(collect)
             if keep_layers:
                 outs.append(y)
             if l != len(self.weights.layers) - 1:
@@ -251,6 +264,7 @@ class Engine:
                     import torch.distributed as dist
                     dist.all_reduce(flag, op=dist.ReduceOp.MAX,
                                     group=self.group)
+        metrics = [collect() for collect in pending]
         self.last_layers = outs
         return y, metrics
 

@@ -186,15 +186,26 @@ def test_completed_vertex_offered_messages_raises():
 
 def test_stable_transform_bit_exact_vs_reference_backend():
     from oracle import engine as OE
-    from paper_2605_09402_b200.compute import MatmulBackend
+    from paper_2605_09402_b200.compute import MatmulBackend, _apply_device
     rng = np.random.default_rng(0)
-    for m, k, n in [(1000, 100, 128), (37, 256, 47), (5, 8, 2), (0, 4, 3)]:
+    # covers every register-tile width (TN 8/4/3/2), K not a multiple of
+    # the 16-wide k tile, unaligned rows (scalar staging), partial row
+    # tiles, more rows than one wave of persistent CTAs, and N > 128
+    # (the untiled fallback)
+    for m, k, n in [(1000, 100, 128), (37, 256, 47), (5, 8, 2), (0, 4, 3),
+                    (40961, 100, 128), (4099, 128, 47), (1000, 99, 64),
+                    (513, 130, 33), (300, 256, 100), (10, 5, 1),
+                    (777, 64, 57), (200, 17, 130)]:
         x = rng.standard_normal((m, k)).astype(np.float32)
+        x[rng.random(x.shape) < 0.01] = -0.0
         w = rng.standard_normal((n, k)).astype(np.float32)
         b = rng.standard_normal(n).astype(np.float32)
-        got = MatmulBackend().apply(x, w, b)
-        want = OE.stable_transform(x, w, b, relu=False)
-        np.testing.assert_array_equal(got, want)
+        b[:: 7] = -0.0
+        for relu in (False, True):
+            got = _apply_device(MatmulBackend.code, x, w, b, relu=relu)
+            want = OE.stable_transform(x, w, b, relu=relu)
+            np.testing.assert_array_equal(got.view(np.uint32),
+                                          want.view(np.uint32))
 
 
 @pytest.mark.parametrize("m,k,n,relu", [(1000, 100, 128, True),
@@ -248,3 +259,41 @@ def test_tiny_and_huge_inputs_take_the_exact_division():
                                   slot_count=3000)
         np.testing.assert_array_equal(y.cpu().numpy(), want)
         eng.close()
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("feat_dtype", ["f32", "f16"])
+def test_tcgen05_pipeline_within_tolerance(kind, feat_dtype):
+    """Whole 3-layer inference with the tcgen05 (3xTF32) transform against
+    the float64 gather oracle (oracle/gather.py = oocgnn/oracle.py).
+    Stated tolerance, per layer: max |y - y64| <= 1e-4 (the reference's
+    own bar vs f64, tests/test_acceptance.py:43) and <= 2e-6 * max|y64|.
+    Integer metrics must equal the bit-exact (stable) run's."""
+    from oracle import gather as OG
+    from paper_2605_09402_b200.storage import (ModelKind, random_weights,
+                                               synthetic_in_memory)
+    graph, feats = synthetic_in_memory("uniform", 20000, 9, 64, 11)
+    if feat_dtype == "f16":
+        feats = feats.astype(np.float16)
+    w = random_weights(ModelKind(kind), [64, 96, 128, 40], 5, gin_epsilon=0.25)
+    want = OG.per_layer(graph.num_vertices, graph.offsets, graph.neighbors,
+                        graph.in_degrees, feats.astype(np.float64), kind,
+                        [(lw.weight, lw.bias) for lw in w.layers],
+                        gin_epsilon=w.gin_epsilon)
+    runs = {}
+    for backend in ("tcgen05", "stable"):
+        eng = Engine(graph, w, PipelineConfig(chunk_budget=1 << 20,
+                                              hot_slots=20000,
+                                              backend=backend))
+        _, metrics = eng.infer(torch.as_tensor(feats).cuda(),
+                               keep_layers=True)
+        runs[backend] = ([y.double().cpu().numpy() for y in eng.last_layers],
+                         metrics)
+        eng.close()
+    for l, (got, ref) in enumerate(zip(runs["tcgen05"][0], want)):
+        err = float(np.abs(got - ref).max())
+        assert err <= 1e-4, (l, err)
+        assert err <= 2e-6 * float(np.abs(ref).max()), (l, err)
+    for a, b in zip(runs["tcgen05"][1], runs["stable"][1]):
+        for f in METRICS:
+            assert getattr(a, f) == getattr(b, f), f
