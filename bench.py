@@ -39,6 +39,20 @@ WORKLOAD = ("cfg2: 3-layer GCN [100,128,128,47], synthetic uniform graph "
             "V=2,400,000 E=62,399,647 (avg degree 26, seed 7), 100-d f32 "
             "features, 8 MiB reference chunk plan (115 chunks), hot_slots=V")
 
+# extra (non-default) workloads: IGB-Medium-shaped graph of BASELINE
+# configs[2] (10M vertices, avg degree 12 -> ~120M edges, 1024-d f16
+# features). Graph and features are generated on the device (torch
+# Philox, seeded) -- the reference's numpy generator would take minutes at
+# this size; parity is pinned on the small golden cases instead.
+IGB_V, IGB_DEG, IGB_DIM = 10_000_000, 12, 1024
+EXTRA = {
+    "igb-medium-sage": ("SAGE", [1024, 128, 128, 19]),
+    "igb-medium-gcn": ("GCN", [1024, 128, 128, 19]),
+    # BASELINE configs[2] itself: 3-layer GAT, 4 heads x 32 (hidden 128)
+    "igb-medium-gat": ("GAT", [1024, 128, 128, 19]),
+}
+GAT_HEADS = 4
+
 
 def build_inputs():
     from paper_2605_09402_b200 import storage as S
@@ -48,21 +62,72 @@ def build_inputs():
     return graph, feats, weights
 
 
-def agg_bytes(graph, weights, rank_range):
+def build_igb(kind, dims, seed=SEED):
+    """Uniform random graph with the reference's semantics (multi-edges
+    removed, self loops kept, CSR rows ascending) and U[-1,1) f16
+    features, generated on cuda:0."""
+    import torch
+
+    from paper_2605_09402_b200 import storage as S
+
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    m = IGB_V * IGB_DEG
+    src = torch.randint(0, IGB_V, (m,), generator=gen, device="cuda")
+    dst = torch.randint(0, IGB_V, (m,), generator=gen, device="cuda")
+    key = torch.unique(src * IGB_V + dst)
+    del src, dst
+    s, t = key // IGB_V, key % IGB_V
+    del key
+    offsets = torch.zeros(IGB_V + 1, dtype=torch.int64, device="cuda")
+    offsets[1:] = torch.cumsum(torch.bincount(s, minlength=IGB_V), 0)
+    indeg = torch.bincount(t, minlength=IGB_V)
+    graph = S.GraphCSR(IGB_V, int(t.numel()), offsets.cpu().numpy(),
+                       t.to(torch.int32).cpu().numpy().view(np.uint32),
+                       indeg.cpu().numpy())
+    del s, t, offsets, indeg
+    feats = torch.empty((IGB_V, IGB_DIM), dtype=torch.float16, device="cuda")
+    feats.uniform_(-1.0, 1.0, generator=gen)
+    if kind == "GAT":
+        from paper_2605_09402_b200.gat import random_gat_weights
+        return graph, feats, random_gat_weights(dims, GAT_HEADS, WSEED)
+    weights = S.random_weights(S.ModelKind[kind], dims, WSEED)
+    return graph, feats, weights
+
+
+def gat_agg_bytes(graph, weights, layouts, rank_range, zsize):
+    """GAT pass B per layer: per in-edge the source's z part (H*F) and its
+    el sector (32 B), its u32 id; per destination CSC/degree (12 B), its er
+    sector, and the output row written once."""
+    lo, hi = rank_range
+    e_g, v_g = int(graph.offsets[-1]), hi - lo
+    out = []
+    for l, (lw, lay) in enumerate(zip(weights.layers, layouts)):
+        last = l == len(weights.layers) - 1
+        osz = 4 if last else zsize
+        out.append(e_g * (lw.hf * zsize + 32) + 4 * e_g + 12 * v_g + 32 * v_g
+                   + v_g * weights.out_dim(l) * osz)
+    return out
+
+
+def agg_bytes(graph, weights, rank_range, in_sizes):
     """Algorithmic HBM bytes of the resident scatter-aggregate per layer
     (DESIGN.md §4): gather every in-edge's source row once (the layer
     input does not fit in L2), read the u32 source id per edge and the
-    CSC/in-degree arrays per destination, write each f32 record once."""
+    CSC/in-degree arrays per destination, read the destination's own row
+    for the SAGE/GIN self term, write each f32 record once."""
     lo, hi = rank_range
     e_g = int(graph.offsets[-1]) if (lo, hi) == (0, graph.num_vertices) \
         else int(np.count_nonzero((graph.neighbors >= lo)
                                   & (graph.neighbors < hi)))
     v_g = hi - lo
+    self_row = weights.kind != 0
     out = []
     for l, lw in enumerate(weights.layers):
-        d = weights.embedding_dim(l)
-        out.append(e_g * d * 4 + 4 * e_g + 12 * v_g + 4 * weights.agg_dim(l)
-                   * v_g)
+        d, s = weights.embedding_dim(l), in_sizes[l]
+        out.append(e_g * d * s + 4 * e_g + 12 * v_g
+                   + (v_g * d * s if self_row else 0)
+                   + 4 * weights.agg_dim(l) * v_g)
     return out
 
 
@@ -188,7 +253,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="atlas")
     ap.add_argument("--backend", default="tcgen05")
+    ap.add_argument("--workload", default="cfg2",
+                    choices=["cfg2"] + sorted(EXTRA))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alt", action="store_true",
+                    help="skip the bit-exact (stable) backend re-run")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -206,13 +276,41 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    graph, feats, weights = build_inputs()
-    cfg = PipelineConfig(chunk_budget=CHUNK_BUDGET, hot_slots=V,
-                         backend=args.backend, device=local)
+    t_gen = time.perf_counter()
+    if args.workload == "cfg2":
+        graph, feats, weights = build_inputs()
+        x = torch.from_numpy(feats).cuda()
+        workload, dtype = WORKLOAD, "f32"
+        cfg = PipelineConfig(chunk_budget=CHUNK_BUDGET, hot_slots=V,
+                             backend=args.backend, device=local)
+    else:
+        kind, dims = EXTRA[args.workload]
+        graph, x, weights = build_igb(kind, dims)
+        feats = None
+        workload = (f"{args.workload}: 3-layer {kind} {dims}, synthetic "
+                    f"uniform graph V={IGB_V:,} E={graph.num_edges:,} (avg "
+                    f"degree {IGB_DEG}, device Philox seed {SEED}), "
+                    f"{IGB_DIM}-d f16 features, 8 MiB reference chunk plan, "
+                    f"hot_slots=V")
+        dtype = "f16 in / f32 accumulate"
+        cfg = PipelineConfig(chunk_budget=CHUNK_BUDGET, hot_slots=IGB_V,
+                             backend=args.backend, device=local)
+    gen_s = time.perf_counter() - t_gen
+    is_gat = args.workload.endswith("-gat")
+    if is_gat:
+        from paper_2605_09402_b200.gat import GATEngine
+        dims = [weights.embedding_dim(0)] + [
+            weights.out_dim(l) for l in range(len(weights.layers))]
+        cfg.backend = "tcgen05"
+        Eng = GATEngine
+    else:
+        dims = [weights.embedding_dim(0)] + [lw.out_dim
+                                             for lw in weights.layers]
+        Eng = Engine
+    nlayers = len(weights.layers)
     t_setup = time.perf_counter()
-    eng = Engine(graph, weights, cfg, rank=rank, world=world)
+    eng = Eng(graph, weights, cfg, rank=rank, world=world)
     setup_s = time.perf_counter() - t_setup
-    x = torch.from_numpy(feats).cuda()
 
     def barrier():
         torch.cuda.synchronize()
@@ -239,7 +337,8 @@ def main():
     clk = clocks.stop()
     # the bit-exact transform backend (reference f32 operation order, every
     # embedding identical to the reference's), timed the same way
-    alt = "stable" if args.backend != "stable" else None
+    alt = "stable" if (args.backend != "stable" and not args.no_alt
+                       and not is_gat) else None
     alt_ms = None
     if alt:
         from paper_2605_09402_b200.compute import get_backend
@@ -262,61 +361,77 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     edges = graph.num_edges
-    value = len(DIMS[1:]) * edges / (ms / 1e3)
+    value = nlayers * edges / (ms / 1e3)
 
     # roofline of the dominant kernel (scatter-aggregate), CUDA events
+    in_sizes = [x.element_size()] + [
+        {"f32": 4, "f16": 2, "bf16": 2}[cfg.embed_dtype]] * (nlayers - 1)
     agg_ms = [sum(m.agg_ms for m in step) for step in per_layer]
-    agg_b = sum(agg_bytes(graph, weights, (eng.lo, eng.hi)))
+    if is_gat:
+        agg_b = sum(gat_agg_bytes(graph, weights, eng.layouts,
+                                  (eng.lo, eng.hi), in_sizes[-1]))
+    else:
+        agg_b = sum(agg_bytes(graph, weights, (eng.lo, eng.hi), in_sizes))
     achieved = agg_b / (statistics.mean(agg_ms) / 1e3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
     traffic = None
-    prof = ROOT / "profiles" / "agg_traffic.json"
+    prof = ROOT / "profiles" / f"agg_traffic_{args.workload}.json"
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("bytes_per_launch")
 
-    # end to end through the public API with HOST buffers, every step:
-    # topology H2D + CSC rebuild (atlas_graph_update), features streamed
-    # H2D in double-buffered tiles overlapped with layer-1 aggregation
-    # (atlas_layer_run_streamed), 3 layers, final output D2H
-    pinned = torch.from_numpy(feats).pin_memory()
-    pin_off = torch.from_numpy(graph.offsets).pin_memory()
-    pin_nb = torch.from_numpy(
-        graph.neighbors.astype(np.uint32).view(np.int32)).pin_memory()
-    pin_deg = torch.from_numpy(
-        graph.in_degrees.astype(np.uint32).view(np.int32)).pin_memory()
-    host_out = torch.empty((eng.hi - eng.lo, DIMS[-1]),
-                           dtype=torch.float32).pin_memory()
-    e2e_ms = []
-    for i in range(args.steps + 1):
-        barrier()
-        t0 = time.perf_counter()
-        eng.graph.update(pin_off, pin_nb, pin_deg)
-        yd, _ = eng.infer(pinned)
-        host_out.copy_(yd, non_blocking=True)
-        torch.cuda.synchronize()
-        if i:
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e = statistics.median(e2e_ms)
-    assert torch.equal(host_out, y.cpu()), "e2e output differs"
-    if world > 1:
-        t = torch.tensor([e2e], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = float(t.item())
-    h2d = feats.nbytes + graph.offsets.nbytes + 4 * graph.num_edges \
-        + 4 * graph.num_vertices
+    e2e_line = None
+    if not args.no_e2e:
+        # end to end through the public API with HOST buffers, every step:
+        # topology H2D + CSC rebuild (atlas_graph_update), features
+        # streamed H2D in double-buffered tiles overlapped with layer-1
+        # aggregation (atlas_layer_run_streamed), all layers, output D2H
+        pinned = (torch.from_numpy(feats) if feats is not None
+                  else x.cpu()).pin_memory()
+        pin_off = torch.from_numpy(graph.offsets).pin_memory()
+        pin_nb = torch.from_numpy(np.ascontiguousarray(
+            graph.neighbors, dtype=np.uint32).view(np.int32)).pin_memory()
+        pin_deg = torch.from_numpy(np.ascontiguousarray(
+            graph.in_degrees, dtype=np.uint32).view(np.int32)).pin_memory()
+        host_out = torch.empty((eng.hi - eng.lo, dims[-1]),
+                               dtype=torch.float32).pin_memory()
+        e2e_ms = []
+        for i in range(args.steps + 1):
+            barrier()
+            t0 = time.perf_counter()
+            eng.graph.update(pin_off, pin_nb, pin_deg)
+            yd, _ = eng.infer(pinned)
+            host_out.copy_(yd, non_blocking=True)
+            torch.cuda.synchronize()
+            if i:
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e = statistics.median(e2e_ms)
+        assert torch.equal(host_out, y.cpu()), "e2e output differs"
+        if world > 1:
+            t = torch.tensor([e2e], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e = float(t.item())
+        h2d = pinned.numel() * pinned.element_size() + graph.offsets.nbytes \
+            + 4 * graph.num_edges + 4 * graph.num_vertices
+        e2e_line = {"value": nlayers * edges / (e2e / 1e3),
+                    "unit": "edges/s", "ms_per_step": e2e,
+                    "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": host_out.numel() * 4,
+                    "includes": "graph upload + CSC build, feature H2D, "
+                                f"{nlayers} layers, output D2H"}
     if rank == 0:
         last = per_layer[-1]
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": graph.num_vertices,
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": workload,
+                       "global_batch": graph.num_vertices,
                        "parallelism": f"dst-range x{world}",
                        "transform_backend": args.backend,
-                       "l2": "inputs larger than L2 (0.96-1.2 GB layer "
-                             "inputs vs 126 MB), no flush"},
+                       "l2": "inputs larger than L2 (layer inputs >= 0.96 "
+                             "GB vs 126 MB), no flush"},
             "step_ms": step_ms,
             "per_layer_ms": [round(m.agg_ms + m.control_ms + m.transform_ms, 3)
                              for m in last],
@@ -327,29 +442,25 @@ def main():
                            "evictions": m.evictions, "hot_peak": m.hot_peak}
                           for m in last],
             "roofline": {"bound": "hbm", "achieved": achieved,
+                         "model": "GAT" if is_gat else None,
                          "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
                          "frac": achieved / peaks.get("hbm_gbs", 6650.0),
                          "traffic": traffic,
-                         "kernel": "agg_resident (scatter-aggregate)",
+                         "kernel": "scatter-aggregate (agg_ring / agg_bulk)",
                          "algorithmic_bytes_per_step": agg_b},
-            "e2e": {"value": len(DIMS[1:]) * edges / (e2e / 1e3),
-                    "unit": "edges/s", "ms_per_step": e2e,
-                    "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": host_out.numel() * 4,
-                    "includes": "graph upload + CSC build, feature H2D, "
-                                "3 layers, output D2H"},
+            "e2e": e2e_line,
             "bit_exact_backend": None if alt is None else {
                 "backend": alt, "ms_per_step": alt_ms,
-                "value": len(DIMS[1:]) * edges / (alt_ms / 1e3),
+                "value": nlayers * edges / (alt_ms / 1e3),
                 "note": "every embedding bit-identical to the reference; "
                         "the headline backend is within the stated "
                         "tolerance (tests/test_gpu_parity.py)"},
             "gpu_launches": launches,
             "gpu_launches_per_step": launches / max(1, args.steps),
             "clocks": clk,
-            "setup_s": setup_s,
+            "setup_s": setup_s, "generate_s": gen_s,
         }
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and feats is not None:
             line["cpu_baseline"] = cpu_baseline(graph, feats, weights)
         print(json.dumps(line), flush=True)
     eng.close()

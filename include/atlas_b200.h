@@ -59,7 +59,9 @@ enum {
   ATLAS_EINVARIANT = -9    /* InvariantError */
 };
 
-enum { ATLAS_GCN = 0, ATLAS_SAGE = 1, ATLAS_GIN = 2 };          /* ModelKind */
+/* ModelKind (oocgnn/storage.py:498) + GAT, which the reference lacks
+ * (semantics in oracle/gat.py / SURVEY.md A.5) */
+enum { ATLAS_GCN = 0, ATLAS_SAGE = 1, ATLAS_GIN = 2, ATLAS_GAT = 3 };
 enum { ATLAS_F32 = 0, ATLAS_F16 = 1, ATLAS_BF16 = 2 };         /* row dtype */
 enum { ATLAS_MINPEND = 0, ATLAS_LRU = 1, ATLAS_RND = 2 };      /* policy */
 enum { ATLAS_BACKEND_STABLE = 0, ATLAS_BACKEND_TCGEN05 = 1 };  /* transform */
@@ -183,6 +185,34 @@ ATLAS_API int atlas_transform(int32_t backend, const float* x_dev, int64_t rows,
                     const float* b_dev, int64_t n, int32_t relu, void* y_dev,
                     int32_t y_dtype, int64_t ldy, int32_t* extremes_flag,
                     void* stream);
+
+/* atlas_transform with an f16/bf16 (or f32) input; 2-byte inputs need the
+ * tcgen05 backend (they are exact in tf32, so 2 MMAs per k-step). GAT's
+ * pass A (z = x . W_ext^T) uses it. */
+ATLAS_API int atlas_transform_typed(int32_t backend, const void* x_dev,
+                                    int32_t x_dtype, int64_t rows, int64_t k,
+                                    int64_t ldx, const float* w_dev,
+                                    const float* b_dev, int64_t n,
+                                    int32_t relu, void* y_dev, int32_t y_dtype,
+                                    int64_t ldy, int32_t* extremes_flag,
+                                    void* stream);
+
+/* GAT layer pass B over a resident z_ext (device, V rows of ldz elements:
+ * [z (heads*head_dim) | pad | el (heads) at el_col | er (heads) at er_col]):
+ * the control plane of a layer created with model ATLAS_GAT (GCN rules:
+ * pending = in-degree) on the reference chunk plan of chunk_rows rows, and
+ * the edge-softmax aggregation of the range with bias, head concat (+ReLU)
+ * or head mean fused, written to y (nloc x ldy). No reference counterpart
+ * (SPEC.md:8); oracle/gat.py defines the result. */
+ATLAS_API int atlas_layer_run_gat(atlas_layer* layer, const atlas_graph* graph,
+                                  const void* z_dev, int32_t z_dtype,
+                                  int64_t ldz, int32_t heads,
+                                  int32_t head_dim, int32_t el_col,
+                                  int32_t er_col, const float* bias_dev,
+                                  int32_t mean_heads, int32_t relu,
+                                  float negative_slope, void* y_dev,
+                                  int32_t y_dtype, int64_t ldy,
+                                  int64_t chunk_rows, void* stream);
 
 ATLAS_API int atlas_layer_finish(atlas_layer* layer, atlas_layer_metrics* out);
 /* per-chunk reload and touched counters (for mean_reload_pct) */

@@ -15,7 +15,7 @@ from .errors import DeviceError, IncompleteLayerError, raise_for_status
 
 LIB_PATH = Path(__file__).resolve().parent / "libatlas_b200.so"
 
-GCN, SAGE, GIN = 0, 1, 2
+GCN, SAGE, GIN, GAT = 0, 1, 2, 3
 F32, F16, BF16 = 0, 1, 2
 MINPEND, LRU, RND = 0, 1, 2
 BACKEND_STABLE, BACKEND_TCGEN05 = 0, 1
@@ -88,6 +88,12 @@ def _declare(lib):
        P_i64)
     fn("atlas_transform", ctypes.c_int, c_i32, c_vp, c_i64, c_i64, c_i64,
        c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i64, c_vp, c_vp)
+    fn("atlas_transform_typed", ctypes.c_int, c_i32, c_vp, c_i32, c_i64,
+       c_i64, c_i64, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i64, c_vp,
+       c_vp)
+    fn("atlas_layer_run_gat", ctypes.c_int, c_vp, c_vp, c_vp, c_i32, c_i64,
+       c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, ctypes.c_float, c_vp,
+       c_i32, c_i64, c_i64, c_vp)
     fn("atlas_layer_finish", ctypes.c_int, c_vp,
        ctypes.POINTER(LayerMetricsC))
     fn("atlas_layer_chunk_stats", ctypes.c_int, c_vp, c_vp, c_vp, c_i64,
@@ -109,7 +115,8 @@ EXPORTED = [
     "atlas_layer_run_streamed",
     "atlas_layer_accumulator", "atlas_transform", "atlas_layer_finish",
     "atlas_layer_chunk_stats", "atlas_layer_log", "atlas_layer_state",
-    "atlas_layer_timing", "atlas_reorder",
+    "atlas_layer_timing", "atlas_reorder", "atlas_transform_typed",
+    "atlas_layer_run_gat",
 ]
 
 

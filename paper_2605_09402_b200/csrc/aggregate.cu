@@ -369,6 +369,198 @@ __global__ void __launch_bounds__(256, 3)
 }
 
 // ---------------------------------------------------------------------------
+// resident front end, bulk-copy variant for wide rows (> 512 B, e.g. 1024-d
+// f16 = 2 KB): the same persistent warps and contiguous CSC ranges as the
+// ring kernel, but each source row moves global -> shared memory as ONE
+// cp.async.bulk (TMA engine, UBLKCP) issued by lane 0 and completed on a
+// per-slot mbarrier (expect_tx = row bytes). kSlots rows stay in flight per
+// warp without costing registers or LSU issue slots; lanes then read their
+// 16-byte chunks from shared memory (chunk j of lane l at byte
+// (32 j + l) * 16, conflict-free) and fold them in source order exactly like
+// the other front ends.
+
+__device__ __forceinline__ void mbar_init_cta(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(n));
+}
+
+__device__ __forceinline__ void bulk_row(void* smem, const void* gmem,
+                                         uint32_t bytes, uint64_t* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+      "r"(bytes)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+      "l"(gmem), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar,
+                                                 uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "BW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra BW_%=;\n}" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kBulkWarps = 4;
+constexpr int kBulkGrab = 16;
+
+template <typename T, int CH, int SLOTS, int MODEL, bool GUARD>
+__device__ __forceinline__ void bulk_body(
+    const T* __restrict__ x, int64_t ldx, const int64_t* __restrict__ csc_ptr,
+    const uint32_t* __restrict__ csc_src, const uint32_t* __restrict__ indeg,
+    int64_t lo, int64_t nloc, int d, float* __restrict__ acc, int64_t ldacc,
+    float self_scale, unsigned long long* __restrict__ work,
+    uint8_t* __restrict__ ring, uint64_t* __restrict__ bars) {
+  using F = Frag<T, 16 / sizeof(T)>;
+  static_assert((SLOTS & (SLOTS - 1)) == 0, "power-of-two ring");
+  constexpr int EPC = 16 / sizeof(T);  // elements per 16-byte chunk
+  constexpr bool kMean = MODEL != ATLAS_GIN;
+  const int lane = threadIdx.x & 31;
+  const uint32_t row_bytes = (uint32_t)(d * sizeof(T));
+  bool act[CH];
+#pragma unroll
+  for (int j = 0; j < CH; j++) act[j] = (j * 32 + lane) * EPC < d;
+  uint32_t n_issued = 0, n_used = 0;  // slot sequence numbers (per warp)
+  while (true) {
+    unsigned long long v0 = 0;
+    if (lane == 0) v0 = atomicAdd(work, (unsigned long long)kBulkGrab);
+    v0 = __shfl_sync(0xffffffffu, v0, 0);
+    if ((int64_t)v0 >= nloc) break;
+    const int64_t v1 = min((int64_t)v0 + kBulkGrab, nloc);
+    const int64_t e0 = csc_ptr[v0], e1 = csc_ptr[v1];
+    int64_t pe = e0, ibase = e0;
+    uint32_t isrc = (e0 + lane < e1) ? csc_src[e0 + lane] : 0u;
+    auto issue = [&]() {
+      if (pe < e1) {
+        if (pe - ibase == 32) {
+          ibase = pe;
+          isrc = (pe + lane < e1) ? csc_src[pe + lane] : 0u;
+        }
+        const uint32_t s = __shfl_sync(0xffffffffu, isrc, (int)(pe - ibase));
+        if (lane == 0) {
+          const int slot = (int)(n_issued & (SLOTS - 1));
+          bulk_row(ring + (size_t)slot * row_bytes, x + (int64_t)s * ldx,
+                   row_bytes, &bars[slot]);
+        }
+        n_issued++;
+        pe++;
+      }
+    };
+#pragma unroll 1
+    for (int k = 0; k < SLOTS; k++) issue();
+    int64_t ce = e0, cbase = e0;
+    uint32_t csrc = isrc;
+    if (MODEL == ATLAS_GIN) csrc = (e0 + lane < e1) ? csc_src[e0 + lane] : 0u;
+    for (int64_t v = (int64_t)v0; v < v1; v++) {
+      const int64_t dend = csc_ptr[v + 1];
+      const uint32_t vg = (uint32_t)(v + lo);
+      const float denom = kMean ? (float)max(1u, indeg[v]) : 1.0f;
+      const float rcp = kMean ? __frcp_rn(denom) : 1.0f;
+      float a[CH][EPC];
+#pragma unroll
+      for (int j = 0; j < CH; j++)
+#pragma unroll
+        for (int e = 0; e < EPC; e++) a[j][e] = 0.0f;
+      bool self_pending = MODEL == ATLAS_GIN;
+      auto self_term = [&]() {
+#pragma unroll
+        for (int j = 0; j < CH; j++)
+          if (act[j]) {
+            F me;
+            me.load(x + (int64_t)vg * ldx + (j * 32 + lane) * EPC);
+            add_msg<T, EPC, false>(a[j], me, true, 1.0f, 1.0f, self_scale);
+          }
+      };
+      for (; ce < dend; ce++) {
+        if (MODEL == ATLAS_GIN) {
+          if (ce - cbase == 32) {
+            cbase = ce;
+            csrc = (ce + lane < e1) ? csc_src[ce + lane] : 0u;
+          }
+          const uint32_t s = __shfl_sync(0xffffffffu, csrc, (int)(ce - cbase));
+          if (self_pending && s >= vg) {
+            self_pending = false;
+            self_term();
+          }
+        }
+        const int slot = (int)(n_used & (SLOTS - 1));
+        mbar_wait_parity(&bars[slot], (n_used / SLOTS) & 1u);
+        const uint4* row =
+            reinterpret_cast<const uint4*>(ring + (size_t)slot * row_bytes);
+        F f[CH];
+#pragma unroll
+        for (int j = 0; j < CH; j++)
+          if (act[j]) f[j].raw = *reinterpret_cast<const typename F::Raw*>(
+                          &row[j * 32 + lane]);
+#pragma unroll
+        for (int j = 0; j < CH; j++)
+          if (act[j])
+            add_msg<T, EPC, kMean, GUARD>(a[j], f[j], false, denom, rcp, 1.0f);
+        n_used++;
+        __syncwarp();  // every lane is done with the slot before its refill
+        issue();
+      }
+      if (MODEL == ATLAS_GIN && self_pending) self_term();
+      float* out = acc + v * ldacc;
+#pragma unroll
+      for (int j = 0; j < CH; j++)
+        if (act[j]) {
+          const int col = (j * 32 + lane) * EPC;
+          store_f32<EPC>(out + col, a[j]);
+          if (MODEL == ATLAS_SAGE) {
+            F me;
+            me.load(x + (int64_t)vg * ldx + col);
+            float h[EPC];
+#pragma unroll
+            for (int e = 0; e < EPC; e++) h[e] = me.get(e);
+            store_f32<EPC>(out + d + col, h);
+          }
+        }
+    }
+  }
+}
+
+template <typename T, int CH, int MODEL>
+__global__ void __launch_bounds__(kBulkWarps * 32, CH >= 8 ? 3 : 6)
+    agg_bulk(const T* __restrict__ x, int64_t ldx,
+             const int64_t* __restrict__ csc_ptr,
+             const uint32_t* __restrict__ csc_src,
+             const uint32_t* __restrict__ indeg, int64_t lo, int64_t nloc,
+             int d, float* __restrict__ acc, int64_t ldacc, float self_scale,
+             const int* __restrict__ guard_flag,
+             unsigned long long* __restrict__ work) {
+  constexpr int SLOTS = 16 / CH;  // <= 8 KB of rows in flight per warp
+  extern __shared__ __align__(128) uint8_t bulk_smem[];
+  const int warp = threadIdx.x >> 5;
+  const uint32_t row_bytes = (uint32_t)(d * sizeof(T));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bulk_smem) + warp * SLOTS;
+  uint8_t* ring = bulk_smem + kBulkWarps * SLOTS * 8 +
+                  (size_t)warp * SLOTS * row_bytes;
+  if ((threadIdx.x & 31) == 0) {
+    for (int k = 0; k < SLOTS; k++) mbar_init_cta(&bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  if (*guard_flag)
+    bulk_body<T, CH, SLOTS, MODEL, true>(x, ldx, csc_ptr, csc_src, indeg, lo,
+                                         nloc, d, acc, ldacc, self_scale,
+                                         work, ring, bars);
+  else
+    bulk_body<T, CH, SLOTS, MODEL, false>(x, ldx, csc_ptr, csc_src, indeg, lo,
+                                          nloc, d, acc, ldacc, self_scale,
+                                          work, ring, bars);
+}
+
+// ---------------------------------------------------------------------------
 // streamed front end: the layer input arrives in row tiles [tile_lo,
 // tile_hi) (host -> HBM, double-buffered); every destination consumes the
 // part of its ascending source list that falls in the tile, resuming at
@@ -581,6 +773,37 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
     if (model == ATLAS_GCN) ring(agg_ring<T, VEC, ATLAS_GCN>);
     else if (model == ATLAS_SAGE) ring(agg_ring<T, VEC, ATLAS_SAGE>);
     else ring(agg_ring<T, VEC, ATLAS_GIN>);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+    return;
+  }
+  const int64_t row_bytes = (int64_t)d * sizeof(T);
+  if constexpr (VEC * sizeof(T) == 16) if (row_bytes <= 8 * 512 &&
+      (ldx * (int64_t)sizeof(T)) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    // bulk-copy kernel: one TMA row copy per in-edge, mbarrier ring
+    g->work.reserve(1);
+    ATLAS_CUDA(cudaMemsetAsync(g->work.ptr, 0, sizeof(unsigned long long), s));
+    auto bulk = [&](auto kern, int slots) {
+      const int smem = kBulkWarps * slots * (8 + (int)row_bytes);
+      ATLAS_CUDA(cudaFuncSetAttribute(
+          kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      int per_sm = 0;
+      ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, kern, kBulkWarps * 32, smem));
+      kern<<<kNumSMs * std::max(1, per_sm), kBulkWarps * 32, smem, s>>>(
+          x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
+          g->nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
+    };
+    auto by_model = [&](auto ch) {
+      constexpr int CH = decltype(ch)::value;
+      if (model == ATLAS_GCN) bulk(agg_bulk<T, CH, ATLAS_GCN>, 16 / CH);
+      else if (model == ATLAS_SAGE) bulk(agg_bulk<T, CH, ATLAS_SAGE>, 16 / CH);
+      else bulk(agg_bulk<T, CH, ATLAS_GIN>, 16 / CH);
+    };
+    if (row_bytes <= 2 * 512) by_model(std::integral_constant<int, 2>());
+    else if (row_bytes <= 4 * 512) by_model(std::integral_constant<int, 4>());
+    else by_model(std::integral_constant<int, 8>());
     count_launch();
     ATLAS_LAUNCH_CHECK();
     return;

@@ -159,7 +159,7 @@ int atlas_layer_create(const atlas_layer_desc* desc,
     if (D.slot_count < 1) fail(ATLAS_ECONFIG, "hot_slots must be >= 1");
     if (D.dst_lo < 0 || D.dst_hi < D.dst_lo || D.dst_hi > D.num_vertices)
       fail(ATLAS_ECONFIG, "bad destination range");
-    if (D.model < ATLAS_GCN || D.model > ATLAS_GIN)
+    if (D.model < ATLAS_GCN || D.model > ATLAS_GAT)
       fail(ATLAS_ECONFIG, "unknown model kind");
     if (D.policy < ATLAS_MINPEND || D.policy > ATLAS_RND)
       fail(ATLAS_ECONFIG, "unknown eviction policy");
@@ -171,6 +171,11 @@ int atlas_layer_create(const atlas_layer_desc* desc,
     auto L = new atlas_layer();
     try {
       L->desc = D;
+      // GAT's control plane is GCN's (pending = in-degree, zero-degree
+      // pre-graduation); its data plane writes outputs
+      // directly, so it keeps no f32 records
+      L->gat = D.model == ATLAS_GAT;
+      if (L->gat) L->desc.model = ATLAS_GCN;
       L->nloc = D.dst_hi - D.dst_lo;
       L->sub_batch = std::max<int64_t>(1, D.slot_count / 2);
       L->evict_batch =
@@ -182,7 +187,7 @@ int atlas_layer_create(const atlas_layer_desc* desc,
         ATLAS_CUDA(cudaMemcpyAsync(L->indeg.ptr, in_degrees_host + D.dst_lo,
                                    L->nloc * sizeof(uint32_t),
                                    cudaMemcpyHostToDevice, s));
-      L->acc.alloc(nn * D.agg_dim);
+      L->acc.alloc(L->gat ? 1 : nn * D.agg_dim);
       L->touched.alloc(nn);
       ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
       engine_init(L, s);
@@ -220,6 +225,7 @@ int atlas_chunk_submit(atlas_layer* L, int64_t start, int64_t end,
                        void* stream) {
   return guarded([&] {
     if (!L) fail(ATLAS_ECONFIG, "null layer");
+    if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
     use_device(L->desc.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (L->chunks_seen == 0) {
@@ -275,6 +281,7 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
       fail(ATLAS_ECONFIG, "graph and layer disagree on the vertex range");
     if (chunk_rows < 1) fail(ATLAS_ECONFIG, "chunk_rows must be >= 1");
     if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
+    if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
     use_device(D.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     settle(L);
@@ -285,6 +292,33 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
       launch_agg_resident(g, x, dtype, ldx, D.model, D.gin_epsilon,
                           (int)D.embed_dim, L->acc.ptr, D.agg_dim,
                           input_flag, s);
+    ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
+    ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
+    L->timing_pending = true;
+  });
+}
+
+int atlas_layer_run_gat(atlas_layer* L, const atlas_graph* g, const void* z,
+                        int32_t z_dtype, int64_t ldz, int32_t heads,
+                        int32_t head_dim, int32_t el_col, int32_t er_col,
+                        const float* bias, int32_t mean_heads, int32_t relu,
+                        float negative_slope, void* y, int32_t y_dtype,
+                        int64_t ldy, int64_t chunk_rows, void* stream) {
+  return guarded([&] {
+    if (!L || !g || !z || !bias || !y) fail(ATLAS_ECONFIG, "null argument");
+    if (!L->gat) fail(ATLAS_ECONFIG, "layer was not created as GAT");
+    const atlas_layer_desc& D = L->desc;
+    if (g->V != D.num_vertices || g->lo != D.dst_lo || g->hi != D.dst_hi)
+      fail(ATLAS_ECONFIG, "graph and layer disagree on the vertex range");
+    if (chunk_rows < 1) fail(ATLAS_ECONFIG, "chunk_rows must be >= 1");
+    if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
+    use_device(D.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    settle(L);
+    launch_control(L, g, chunk_rows, s);
+    launch_gat_aggregate(g, z, z_dtype, ldz, heads, head_dim, el_col, er_col,
+                         bias, mean_heads, relu, negative_slope, y, y_dtype,
+                         ldy, s);
     ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
     ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
     L->timing_pending = true;
@@ -303,6 +337,7 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
     if (chunk_rows < 1 || tile_rows < 1 || ldx < D.embed_dim)
       fail(ATLAS_ECONFIG, "bad tile / chunk rows");
     if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
+    if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
     use_device(D.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t item = dtype == ATLAS_F32 ? 4 : 2;
@@ -399,12 +434,37 @@ int atlas_transform(int32_t backend, const float* x, int64_t rows, int64_t k,
       launch_transform_stable(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
                               flag, s);
     } else if (backend == ATLAS_BACKEND_TCGEN05) {
-      if (!launch_transform_tc(x, rows, k, ldx, w, b, n, relu, y, y_dtype,
-                               ldy, flag, s))
+      if (!launch_transform_tc(x, ATLAS_F32, rows, k, ldx, w, b, n, relu, y,
+                               y_dtype, ldy, flag, s))
         fail(ATLAS_ECONFIG, "tcgen05 backend does not support this shape");
     } else {
       fail(ATLAS_ECONFIG, "unknown transform backend");
     }
+  });
+}
+
+int atlas_transform_typed(int32_t backend, const void* x, int32_t x_dtype,
+                          int64_t rows, int64_t k, int64_t ldx,
+                          const float* w, const float* b, int64_t n,
+                          int32_t relu, void* y, int32_t y_dtype, int64_t ldy,
+                          int32_t* flag, void* stream) {
+  return guarded([&] {
+    if (x_dtype == ATLAS_F32) {
+      const int rc = atlas_transform(backend, static_cast<const float*>(x),
+                                     rows, k, ldx, w, b, n, relu, y, y_dtype,
+                                     ldy, flag, stream);
+      if (rc != ATLAS_OK) fail(rc, g_last_error);
+      return;
+    }
+    if (rows < 0 || k < 1 || n < 1 || ldx < k || ldy < n)
+      fail(ATLAS_ECONFIG, "bad transform shape");
+    if (backend != ATLAS_BACKEND_TCGEN05)
+      fail(ATLAS_ECONFIG, "f16/bf16 inputs need the tcgen05 backend");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (flag) ATLAS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+    if (!launch_transform_tc(x, x_dtype, rows, k, ldx, w, b, n, relu, y,
+                             y_dtype, ldy, flag, s))
+      fail(ATLAS_ECONFIG, "tcgen05 backend does not support this shape");
   });
 }
 

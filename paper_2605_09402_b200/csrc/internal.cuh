@@ -109,6 +109,7 @@ struct atlas_layer {
   std::vector<int64_t> chunk_reloads, chunk_touched;
   bool engine_initialized = false;
   bool fast_path = false;
+  bool gat = false;  // GAT layer: GCN control plane, fused GAT data plane
   bool spans_host_done = false;
   int64_t chunks_seen = 0;
   int64_t stream_step = 0;  // global stream position counter (operator path)
@@ -190,15 +191,22 @@ void launch_sage_self(const void* tile, int dtype, int64_t ldx,
 void launch_gather_rows(const float* acc, int64_t ldacc, const int32_t* ids,
                         int64_t n, int64_t width, float* out, cudaStream_t s);
 
+// gat.cu
+void launch_gat_aggregate(const atlas_graph* g, const void* z, int z_dtype,
+                          int64_t ldz, int heads, int head_dim, int el_col,
+                          int er_col, const float* bias, int mean_heads,
+                          int relu, float slope, void* y, int y_dtype,
+                          int64_t ldy, cudaStream_t s);
+
 // transform.cu
 void launch_transform_stable(const float* x, int64_t rows, int64_t k,
                              int64_t ldx, const float* w, const float* b,
                              int64_t n, int relu, void* y, int y_dtype,
                              int64_t ldy, int32_t* flag, cudaStream_t s);
-bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
-                         const float* w, const float* b, int64_t n, int relu,
-                         void* y, int y_dtype, int64_t ldy, int32_t* flag,
-                         cudaStream_t s);
+bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
+                         int64_t ldx, const float* w, const float* b,
+                         int64_t n, int relu, void* y, int y_dtype,
+                         int64_t ldy, int32_t* flag, cudaStream_t s);
 
 // control.cu
 void engine_init(atlas_layer* L, cudaStream_t s);

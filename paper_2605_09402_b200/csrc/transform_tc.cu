@@ -161,7 +161,7 @@ struct TcParams {
   int32_t* flag;
 };
 
-template <typename OutT, bool RES_W>
+template <typename TIn, typename OutT, bool RES_W>
 __global__ void __launch_bounds__(kThreads, 1)
     transform_tc_kernel(const __grid_constant__ CUtensorMap map_x,
                         const __grid_constant__ CUtensorMap map_w,
@@ -170,6 +170,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1024-B aligned carve-up (pointer arithmetic keeps the shared space):
   //   RES_W : [w_hi kb0..kbN | w_lo kb0..kbN] then per stage [x | x_lo]
   //   !RES_W: per stage [x | x_lo | w | w_lo]
+  // f32 input: TMA lands in x and is split in place (x -> tf32 hi, x_lo).
+  // f16/bf16 input (exact in tf32): TMA lands, unswizzled, in the x_lo
+  // area and the splitter widens it into x in the SW128 f32 layout; the
+  // MMA then needs only x.w_lo + x.w_hi.
+  constexpr bool kExact = sizeof(TIn) == 2;
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t x_bytes = BM * BK * 4;
   const uint32_t w_bytes = p.BN * BK * 4;
@@ -242,8 +247,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < p.kblocks; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = stages + s * stage_bytes;
-          mbar_expect_tx(&full[s], x_bytes + (RES_W ? 0u : w_bytes));
-          tma_load_2d(st, &map_x, &full[s], kb * BK, (int)(t * BM));
+          mbar_expect_tx(&full[s], BM * BK * (uint32_t)sizeof(TIn) +
+                                       (RES_W ? 0u : w_bytes));
+          tma_load_2d(kExact ? st + x_bytes : st, &map_x, &full[s], kb * BK,
+                      (int)(t * BM));
           if (!RES_W)
             tma_load_2d(st + 2 * x_bytes, &map_w, &full[s], kb * BK, 0);
           if (++s == p.stages) {
@@ -281,10 +288,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < BK / 8; k++) {  // UMMA_K = 8 tf32 = 32 B
             const uint32_t off = k * 32;
             const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
-            mma_tf32(dt, sw128_desc(a_lo + off), sw128_desc(b_hi + off),
-                     idesc, first);
+            if (!kExact)
+              mma_tf32(dt, sw128_desc(a_lo + off), sw128_desc(b_hi + off),
+                       idesc, first);
             mma_tf32(dt, sw128_desc(a_hi + off), sw128_desc(b_lo + off),
-                     idesc, 1u);
+                     idesc, kExact ? first : 1u);
             mma_tf32(dt, sw128_desc(a_hi + off), sw128_desc(b_hi + off),
                      idesc, 1u);
           }
@@ -334,9 +342,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* st = stages + s * stage_bytes;
         float4* xs = reinterpret_cast<float4*>(st);
         float4* xl = reinterpret_cast<float4*>(st + x_bytes);
+        if constexpr (kExact) {
+          // raw [128 rows][32] 2-byte elements -> f32 row r, 16-B chunk c
+          // at the SW128 position (c ^ (r & 7)) of the 128-B row
+          const uint2* raw = reinterpret_cast<const uint2*>(st + x_bytes);
 #pragma unroll
-        for (int i = 0; i < (BM * BK / 4) / 128; i++)
-          split16(xs, xl, tid + i * 128);
+          for (int i = 0; i < (BM * BK / 4) / 128; i++) {
+            const int g = tid + i * 128, r = g >> 3, c = g & 7;
+            const uint2 h = raw[g];
+            const TIn* e = reinterpret_cast<const TIn*>(&h);
+            xs[r * 8 + (c ^ (r & 7))] =
+                make_float4(to_f32(e[0]), to_f32(e[1]), to_f32(e[2]),
+                            to_f32(e[3]));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < (BM * BK / 4) / 128; i++)
+            split16(xs, xl, tid + i * 128);
+        }
         if (!RES_W) {
           float4* ws = reinterpret_cast<float4*>(w_hi_ptr(s, kb));
           float4* wl = reinterpret_cast<float4*>(w_lo_ptr(s, kb));
@@ -452,17 +475,25 @@ EncodeFn encode_fn() {
 
 // 2-D f32 map: inner dim `cols` (K), outer `rows`, row pitch `ld` elements,
 // box = 32 x box_rows, 128-B swizzle, zero fill out of bounds
-bool make_map(CUtensorMap* m, const float* ptr, int64_t rows, int64_t cols,
-              int64_t ld, int box_rows) {
+// 2-byte inputs use an unswizzled box (64-B rows), widened by the splitter
+bool make_map(CUtensorMap* m, const void* ptr, int dtype, int64_t rows,
+              int64_t cols, int64_t ld, int box_rows) {
   EncodeFn enc = encode_fn();
   if (!enc) return false;
+  const int es = dtype == ATLAS_F32 ? 4 : 2;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr),
-             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  const CUtensorMapDataType t = dtype == ATLAS_F32
+                                    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                : dtype == ATLAS_F16
+                                    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                    : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  return enc(m, t, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             es == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -479,19 +510,21 @@ int num_sms() {
 
 }  // namespace
 
-bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
-                         const float* w, const float* b, int64_t n, int relu,
-                         void* y, int y_dtype, int64_t ldy, int32_t* flag,
-                         cudaStream_t s) {
+bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
+                         int64_t ldx, const float* w, const float* b,
+                         int64_t n, int relu, void* y, int y_dtype,
+                         int64_t ldy, int32_t* flag, cudaStream_t s) {
   if (rows <= 0) return true;
-  if (n < 1 || n > 256 || k < 1 || ldx % 4 != 0 || k % 4 != 0 ||
+  const int xs = x_dtype == ATLAS_F32 ? 4 : 2;
+  if (n < 1 || n > 256 || k < 1 || (ldx * xs) % 16 != 0 || k % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) != 0)
     return false;
   const int BN = (int)((n + 15) / 16 * 16);
   const int kblocks = (int)((k + BK - 1) / BK);
   if ((reinterpret_cast<uintptr_t>(w) & 15) != 0) return false;
   CUtensorMap mx, mw;
-  if (!make_map(&mx, x, rows, k, ldx, BM) || !make_map(&mw, w, n, k, k, BN))
+  if (!make_map(&mx, x, x_dtype, rows, k, ldx, BM) ||
+      !make_map(&mw, w, ATLAS_F32, n, k, k, BN))
     return false;
   // W (hi + lo, all k-blocks) stays resident when it leaves room for two
   // x stages; otherwise it streams through the stages with x
@@ -528,15 +561,20 @@ bool launch_transform_tc(const float* x, int64_t rows, int64_t k, int64_t ldx,
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid, kThreads, smem, s>>>(mx, mw, p);
   };
-  if (res_w) {
-    if (y_dtype == ATLAS_F32) launch(transform_tc_kernel<float, true>);
-    else if (y_dtype == ATLAS_F16) launch(transform_tc_kernel<__half, true>);
-    else launch(transform_tc_kernel<__nv_bfloat16, true>);
-  } else {
-    if (y_dtype == ATLAS_F32) launch(transform_tc_kernel<float, false>);
-    else if (y_dtype == ATLAS_F16) launch(transform_tc_kernel<__half, false>);
-    else launch(transform_tc_kernel<__nv_bfloat16, false>);
-  }
+  auto by_out = [&](auto in_tag, auto res_tag) {
+    using TIn = decltype(in_tag);
+    constexpr bool R = decltype(res_tag)::value;
+    if (y_dtype == ATLAS_F32) launch(transform_tc_kernel<TIn, float, R>);
+    else if (y_dtype == ATLAS_F16) launch(transform_tc_kernel<TIn, __half, R>);
+    else launch(transform_tc_kernel<TIn, __nv_bfloat16, R>);
+  };
+  auto by_in = [&](auto res_tag) {
+    if (x_dtype == ATLAS_F32) by_out(float(), res_tag);
+    else if (x_dtype == ATLAS_F16) by_out(__half(), res_tag);
+    else by_out(__nv_bfloat16(), res_tag);
+  };
+  if (res_w) by_in(std::true_type());
+  else by_in(std::false_type());
   count_launch();
   ATLAS_LAUNCH_CHECK();
   return true;

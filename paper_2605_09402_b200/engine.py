@@ -216,6 +216,21 @@ class DeviceLayer:
             x.stride(0), int(chunk_rows), N.ptr(input_flag),
             N.stream_handle(stream)))
 
+    def run_gat(self, graph: DeviceGraph, z, layout, bias, y, *,
+                mean_heads: bool, relu: bool, chunk_rows: int,
+                negative_slope: float = 0.2, stream=None):
+        """GAT pass B (atlas_layer_run_gat): z (V, ldz) CUDA tensor laid
+        out as ``layout`` (gat.ZLayout) -> y (range rows) with bias, head
+        concat/ReLU or head mean fused; control plane on the chunk plan."""
+        if z.shape[0] != self.num_vertices or z.stride(1) != 1:
+            raise ConfigError(f"z {tuple(z.shape)} does not cover the graph")
+        N.check(N.load_library().atlas_layer_run_gat(
+            self.handle, graph.handle, z.data_ptr(), torch_dtype_code(z),
+            z.stride(0), layout.heads, layout.head_dim, layout.el_col,
+            layout.er_col, bias.data_ptr(), int(mean_heads), int(relu),
+            float(negative_slope), y.data_ptr(), torch_dtype_code(y),
+            y.stride(0), int(chunk_rows), N.stream_handle(stream)))
+
     def run_streamed(self, graph: DeviceGraph, x_host, chunk_rows: int,
                      tile_bytes: int = 256 << 20, stream=None):
         """x_host: pinned CPU torch tensor (V, embed_dim); streamed to HBM
@@ -322,6 +337,18 @@ def transform_device(x_ptr: int, rows: int, k: int, ldx: int, w, b,
         backend_code, x_ptr, rows, k, ldx, w.data_ptr(), b.data_ptr(),
         w.shape[0], int(relu), y.data_ptr(), torch_dtype_code(y),
         y.stride(0), N.ptr(flag), N.stream_handle(stream)))
+
+
+def transform_typed(x, w, b, relu: bool, y, backend_code: int, rows=None,
+                    flag=None, stream=None):
+    """y = act(x . W^T + b) with x a CUDA tensor of any engine dtype
+    (f16/bf16 inputs need the tcgen05 backend)."""
+    n = x.shape[0] if rows is None else rows
+    N.check(N.load_library().atlas_transform_typed(
+        backend_code, x.data_ptr(), torch_dtype_code(x), n, x.shape[1],
+        x.stride(0), w.data_ptr(), b.data_ptr(), w.shape[0], int(relu),
+        y.data_ptr(), torch_dtype_code(y), y.stride(0), N.ptr(flag),
+        N.stream_handle(stream)))
 
 
 def percentile99(count: int, q_lo: int, q_hi: int) -> float:

@@ -1,0 +1,372 @@
+"""GAT on the broadcast layer engine (BASELINE config 3, kernel plan K10).
+
+The reference has no GAT (SURVEY.md §8c "parity
+unpinned"), so this module defines the model the way SURVEY.md A.5 fixes it
+and oracle/gat.py restates it in float64 (DGL GATConv semantics, the
+reference oracle's layer conventions: ReLU between layers, heads
+concatenated in hidden layers and averaged in the last, zero in-degree ->
+bias, no added self-loops, LeakyReLU slope 0.2).
+
+GAT transforms first, so each layer is two device passes:
+
+* pass A — ``z_ext = h . W_ext^T`` on the tcgen05 tensor cores
+  (``atlas_transform_typed``; f16/bf16 inputs are exact in tf32). W_ext
+  stacks W (H*F rows), then a_l[h]^T W_h and a_r[h]^T W_h, so the GEMM
+  emits el and er as extra columns of every z row (``ZLayout``).
+* pass B — ``atlas_layer_run_gat``: the edge-softmax scatter-aggregate over
+  the rank's destination range with bias / head concat + ReLU / head mean
+  fused (csrc/gat.cu), and the layer's control plane (pending = in-degree,
+  GCN rules; the reference chunk plan sized by the z row).
+
+With G ranks, rank g computes z for its own rows only and the z rows are
+all-gathered (NCCL) before pass B: the one exchange per layer.
+
+Weights file: AWTS version 2 (the reference's v1 has no heads or attention
+vectors, oocgnn/storage.py:49-50, :556-571): header ``<4sIBIf`` (magic,
+version 2, kind 3, layers, negative slope), then per layer ``<III`` (in,
+heads, head_dim) and f32 W (H*F x in), a_l (H x F), a_r (H x F), b (H*F).
+"""
+
+from __future__ import annotations
+
+import struct
+import time
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from .chunks import chunk_rows as plan_rows
+from .errors import (BadMagicError, ConfigError, InvariantError,
+                     TruncatedFileError, VersionMismatchError)
+from .memstore import MemoryBudget
+from .orchestrator import metrics_from_device
+
+GAT_KIND = 3
+_HDR = struct.Struct("<4sIBIf")
+_HDR_LAYER = struct.Struct("<III")
+
+
+@dataclass
+class GATLayerWeights:
+    in_dim: int
+    heads: int
+    head_dim: int
+    weight: np.ndarray   # (heads*head_dim, in_dim) f32
+    attn_l: np.ndarray   # (heads, head_dim) f32
+    attn_r: np.ndarray   # (heads, head_dim) f32
+    bias: np.ndarray     # (heads*head_dim,) f32
+
+    @property
+    def hf(self) -> int:
+        return self.heads * self.head_dim
+
+
+@dataclass
+class GATWeights:
+    layers: list
+    negative_slope: float = 0.2
+    kind: int = GAT_KIND
+
+    def validate(self, feature_dim=None) -> None:
+        if not self.layers:
+            raise InvariantError("model must have at least one layer")
+        prev = feature_dim
+        for i, lw in enumerate(self.layers):
+            if lw.weight.shape != (lw.hf, lw.in_dim):
+                raise InvariantError(f"layer {i}: weight shape mismatch")
+            for name in ("attn_l", "attn_r"):
+                if getattr(lw, name).shape != (lw.heads, lw.head_dim):
+                    raise InvariantError(f"layer {i}: {name} shape mismatch")
+            if lw.bias.shape != (lw.hf,):
+                raise InvariantError(f"layer {i}: bias shape mismatch")
+            if prev is not None and lw.in_dim != prev:
+                raise InvariantError(
+                    f"layer {i}: in_dim {lw.in_dim}, expected {prev}")
+            prev = self.out_dim(i)
+
+    def embedding_dim(self, layer_index: int) -> int:
+        return self.layers[layer_index].in_dim
+
+    def out_dim(self, layer_index: int) -> int:
+        lw = self.layers[layer_index]
+        return lw.head_dim if layer_index == len(self.layers) - 1 else lw.hf
+
+    def oracle_layers(self):
+        return [(lw.weight, lw.attn_l, lw.attn_r, lw.bias, lw.heads)
+                for lw in self.layers]
+
+
+def random_gat_weights(dims, heads: int, seed: int,
+                       gain: float = 1.0) -> GATWeights:
+    """Glorot-uniform like storage.random_weights. dims = [in, hidden...,
+    out]: hidden widths are heads*head_dim (concatenated), the last layer
+    has ``heads`` heads of width dims[-1] (averaged)."""
+    if len(dims) < 2:
+        raise ConfigError("need at least [input_dim, output_dim]")
+    rng = np.random.default_rng(seed)
+    layers = []
+    for i, (w_in, w_out) in enumerate(zip(dims[:-1], dims[1:])):
+        last = i == len(dims) - 2
+        if not last and w_out % heads:
+            raise ConfigError(f"hidden width {w_out} not divisible by "
+                              f"{heads} heads")
+        f = w_out if last else w_out // heads
+        hf = heads * f
+        lim = gain * np.sqrt(6.0 / (w_in + hf))
+        w = rng.uniform(-lim, lim, (hf, w_in))
+        alim = gain * np.sqrt(6.0 / (f + 1))
+        al = rng.uniform(-alim, alim, (heads, f))
+        ar = rng.uniform(-alim, alim, (heads, f))
+        b = gain * rng.uniform(-0.1, 0.1, hf)
+        layers.append(GATLayerWeights(
+            w_in, heads, f, w.astype(np.float32), al.astype(np.float32),
+            ar.astype(np.float32), b.astype(np.float32)))
+    return GATWeights(layers)
+
+
+def write_gat_weights(path, model: GATWeights) -> None:
+    model.validate()
+    parts = [_HDR.pack(b"AWTS", 2, GAT_KIND, len(model.layers),
+                       float(model.negative_slope))]
+    for lw in model.layers:
+        parts.append(_HDR_LAYER.pack(lw.in_dim, lw.heads, lw.head_dim))
+        for a in (lw.weight, lw.attn_l, lw.attn_r, lw.bias):
+            parts.append(np.ascontiguousarray(a, "<f4").tobytes())
+    Path(path).write_bytes(b"".join(parts))
+
+
+def read_gat_weights(path) -> GATWeights:
+    path = Path(path)
+    data = path.read_bytes()
+    if len(data) < _HDR.size:
+        raise TruncatedFileError(f"{path}: header short")
+    magic, ver, kind, nlayers, slope = _HDR.unpack_from(data)
+    if magic != b"AWTS":
+        raise BadMagicError(f"{path}: expected magic b'AWTS', found {magic!r}")
+    if ver != 2 or kind != GAT_KIND:
+        raise VersionMismatchError(
+            f"{path}: not a GAT weights file (version {ver}, kind {kind})")
+    pos, layers = _HDR.size, []
+    for i in range(nlayers):
+        if pos + _HDR_LAYER.size > len(data):
+            raise TruncatedFileError(f"{path}: layer {i} header short")
+        fin, h, f = _HDR_LAYER.unpack_from(data, pos)
+        pos += _HDR_LAYER.size
+        arrs = []
+        for shape in ((h * f, fin), (h, f), (h, f), (h * f,)):
+            n = int(np.prod(shape))
+            if pos + 4 * n > len(data):
+                raise TruncatedFileError(f"{path}: layer {i} payload short")
+            arrs.append(np.frombuffer(data, "<f4", n, pos).reshape(shape)
+                        .copy())
+            pos += 4 * n
+        layers.append(GATLayerWeights(fin, h, f, *arrs))
+    model = GATWeights(layers, float(slope))
+    model.validate()
+    return model
+
+
+@dataclass(frozen=True)
+class ZLayout:
+    """Column layout of a pass-A row: [z (H*F) | pad | el (H) | er (H) |
+    pad], every part starting on a 16-byte boundary (vector loads)."""
+
+    heads: int
+    head_dim: int
+    itemsize: int
+
+    @property
+    def epc(self) -> int:
+        return 16 // self.itemsize
+
+    def _up(self, n: int) -> int:
+        return -(-n // self.epc) * self.epc
+
+    @property
+    def el_col(self) -> int:
+        return self._up(self.heads * self.head_dim)
+
+    @property
+    def er_col(self) -> int:
+        return self.el_col + self.heads
+
+    @property
+    def ldz(self) -> int:
+        return self._up(self.er_col + self.heads)
+
+
+def extended_weight(lw: GATLayerWeights, layout: ZLayout) -> np.ndarray:
+    """W_ext (ldz x in): W, zero pad, a_l[h]^T W_h, a_r[h]^T W_h, zero pad
+    (computed in float64, stored f32), so z_ext = h . W_ext^T carries el
+    and er."""
+    w = lw.weight.astype(np.float64).reshape(lw.heads, lw.head_dim, lw.in_dim)
+    ext = np.zeros((layout.ldz, lw.in_dim), dtype=np.float64)
+    ext[:lw.hf] = lw.weight
+    ext[layout.el_col:layout.el_col + lw.heads] = np.einsum(
+        "hf,hfk->hk", lw.attn_l.astype(np.float64), w)
+    ext[layout.er_col:layout.er_col + lw.heads] = np.einsum(
+        "hf,hfk->hk", lw.attn_r.astype(np.float64), w)
+    return ext.astype(np.float32)
+
+
+def _torch_dtype(name):
+    import torch
+
+    return {"f32": torch.float32, "f16": torch.float16,
+            "bf16": torch.bfloat16}[name]
+
+
+class GATEngine:
+    """Device-resident GAT inference over one destination range (the GAT
+    counterpart of runtime.Engine; same PipelineConfig knobs).
+    ``config.embed_dtype`` is the storage type of z and of the hidden
+    layers' outputs (f32 default)."""
+
+    def __init__(self, graph, weights: GATWeights, config, *, rank: int = 0,
+                 world: int = 1, dist_group=None):
+        import torch
+
+        from .compute import device_code, get_backend
+        from .engine import DeviceGraph
+        from .storage import partition_ranges
+
+        config.validate()
+        weights.validate()
+        self.config, self.weights = config, weights
+        self.rank, self.world, self.group = rank, world, dist_group
+        self.num_vertices = graph.num_vertices
+        self.in_degrees = np.asarray(graph.in_degrees, dtype=np.uint32)
+        self.ranges = partition_ranges(graph.num_vertices, world)
+        self.lo, self.hi = self.ranges[rank]
+        self.device = config.device
+        torch.cuda.set_device(self.device)
+        self.graph = DeviceGraph(graph.offsets, graph.neighbors,
+                                 graph.in_degrees, (self.lo, self.hi),
+                                 device=self.device)
+        code = device_code(get_backend(config.backend or "tcgen05"))
+        if code != 1:
+            raise ConfigError("GAT pass A runs on the tcgen05 backend")
+        self.zt = _torch_dtype(config.embed_dtype)
+        item = torch.empty(0, dtype=self.zt).element_size()
+        self.layouts, self.w_ext, self.zero_b, self.bias = [], [], [], []
+        for lw in weights.layers:
+            lay = ZLayout(lw.heads, lw.head_dim, item)
+            self.layouts.append(lay)
+            self.w_ext.append(torch.as_tensor(extended_weight(lw, lay)).cuda())
+            self.zero_b.append(torch.zeros(lay.ldz, device="cuda"))
+            self.bias.append(torch.as_tensor(lw.bias).cuda())
+        self._layers = {}
+        self.last_layers = []
+
+    def close(self):
+        for layer in self._layers.values():
+            layer.close()
+        self._layers.clear()
+        self.graph.close()
+
+    def _device_layer(self, l, lay):
+        from .engine import DeviceLayer
+        from . import _native as N
+
+        layer = self._layers.get(l)
+        if layer is not None and layer.handle:
+            layer.reset()
+            return layer
+        cfg = self.config
+        hf = lay.heads * lay.head_dim
+        # a pending record is acc (H*F) + running max and sum per head
+        rec = hf + 2 * lay.heads
+        slots = (MemoryBudget(cfg.hot_slots, rec) if cfg.hot_slots else
+                 MemoryBudget.from_bytes(cfg.hot_budget, rec)).slot_count
+        layer = DeviceLayer(self.in_degrees, N.GAT, hf, hf, slots,
+                            eviction=cfg.eviction, seed=cfg.seed,
+                            evict_batch=cfg.evict_batch,
+                            dst_range=(self.lo, self.hi),
+                            record_log=cfg.record_log,
+                            force_exact=cfg.force_exact, device=self.device)
+        self._layers[l] = layer
+        return layer
+
+    def gather(self, z_local):
+        if self.world == 1:
+            return z_local
+        from .runtime import gather_ranges
+        return gather_ranges(z_local, self.ranges, self.group)
+
+    def layer(self, l: int, h_local, defer_metrics: bool = False):
+        """h_local: this rank's rows [lo, hi) of the layer input (CUDA
+        tensor; layer 0 may pass the full feature matrix). Returns
+        (y (nloc, out), metrics or a collector, device layer)."""
+        import torch
+
+        from .engine import transform_typed
+
+        w = self.weights
+        lw, lay = w.layers[l], self.layouts[l]
+        last = l == len(w.layers) - 1
+        t0 = time.perf_counter()
+        nloc = self.hi - self.lo
+        if h_local.shape[0] == self.num_vertices and self.world > 1:
+            h_local = h_local[self.lo:self.hi]
+        if h_local.shape[1] != lw.in_dim:
+            raise ConfigError(f"layer {l} expects {lw.in_dim}-wide rows, "
+                              f"input holds {h_local.shape[1]}")
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        z_local = torch.empty((h_local.shape[0], lay.ldz), dtype=self.zt,
+                              device="cuda")
+        if h_local.shape[0]:
+            transform_typed(h_local, self.w_ext[l], self.zero_b[l], False,
+                            z_local, 1)
+        ev[1].record()
+        z = self.gather(z_local)
+        rows = plan_rows(self.num_vertices, lay.ldz,
+                         "f32" if self.zt == torch.float32 else "f16",
+                         self.config.chunk_budget)
+        layer = self._device_layer(l, lay)
+        out_dim = lw.head_dim if last else lw.hf
+        y = torch.empty((nloc, out_dim),
+                        dtype=torch.float32 if last else self.zt,
+                        device="cuda")
+        layer.run_gat(self.graph, z, lay, self.bias[l], y, mean_heads=last,
+                      relu=not last, chunk_rows=rows,
+                      negative_slope=w.negative_slope)
+
+        def collect():
+            m = metrics_from_device(layer, l)
+            m.agg_ms, m.control_ms = layer.timing()
+            m.transform_ms = ev[0].elapsed_time(ev[1])
+            m.gpu_seconds = time.perf_counter() - t0
+            return m
+
+        if defer_metrics:
+            return y, collect, layer
+        return y, collect(), layer
+
+    def infer(self, x, keep_layers: bool = False):
+        """All layers; x is the full (V, in) feature matrix on the device.
+        Returns (final local output, [LayerMetrics])."""
+        import torch
+
+        pending, outs = [], []
+        h = x
+        if not x.is_cuda:  # host (pinned) features: one H2D copy
+            lo, hi = (self.lo, self.hi) if self.world > 1 else (0, x.shape[0])
+            h = torch.empty((hi - lo, x.shape[1]), dtype=x.dtype,
+                            device="cuda")
+            h.copy_(x[lo:hi], non_blocking=True)
+        for l in range(len(self.weights.layers)):
+            y, collect, _ = self.layer(l, h, defer_metrics=True)
+            pending.append(collect)
+            if keep_layers:
+                outs.append(y)
+            h = y
+        metrics = [collect() for collect in pending]
+        self.last_layers = outs
+        return y, metrics
+
+
+__all__ = ["GATLayerWeights", "GATWeights", "random_gat_weights",
+           "write_gat_weights", "read_gat_weights", "ZLayout",
+           "extended_weight", "GATEngine"]

@@ -138,6 +138,8 @@ DATASETS = {
     "pa": ("pa", 100_000, 10, 64, 12, "f32"),
     "cfg1": ("uniform", 100_000, 10, 128, 7, "f32"),
     "half": ("uniform", 4000, 8, 16, 11, "f16"),
+    # wide rows (the IGB-shaped 1024-d f16 path: bulk-copy aggregation)
+    "wide": ("uniform", 3000, 8, 1024, 13, "f16"),
 }
 
 SMALL_CFG = dict(hot_budget=1 << 20, chunk_budget=64 << 10,
@@ -164,6 +166,9 @@ for kind in ModelKind:
     CASES.append((f"half_{kind.cli_name}_slots300", "half", kind,
                   [16, 8, 4], 5, eps, gain,
                   dict(hot_slots=300, chunk_budget=16 << 10), False))
+    CASES.append((f"wide_{kind.cli_name}", "wide", kind, [1024, 600, 16], 5,
+                  eps, gain, dict(hot_slots=400, chunk_budget=256 << 10),
+                  False))
 for pol in ("minpend", "lru", "rnd"):
     CASES.append((f"pa_gcn_{pol}_5pct", "pa", ModelKind.GCN, [64, 32, 16], 5,
                   0.0, 1.0, dict(hot_slots=5000, eviction=pol, seed=1), False))

@@ -95,7 +95,8 @@ def test_files_byte_identical_to_reference(tmp_path):
 
 FAST = ["fig2_gcn", "fig2_sage", "fig2_gin", "small_gcn_tight",
         "small_sage_tight", "small_gin_tight", "half_gcn_slots300",
-        "half_sage_slots300", "half_gin_slots300", "uniform_gcn_slots500"]
+        "half_sage_slots300", "half_gin_slots300", "uniform_gcn_slots500",
+        "wide_sage"]
 
 
 @pytest.mark.parametrize("case", FAST)
