@@ -198,7 +198,8 @@ ATLAS_API int atlas_transform_typed(int32_t backend, const void* x_dev,
                                     void* stream);
 
 /* GAT layer pass B over a resident z_ext (device, V rows of ldz elements:
- * [z (heads*head_dim) | pad | el (heads) at el_col | er (heads) at er_col]):
+ * [z: head h at columns h*head_stride .. +head_dim | el (heads) at el_col |
+ *  er (heads) at er_col]; head_stride = head_dim rounded up to 16 bytes):
  * the control plane of a layer created with model ATLAS_GAT (GCN rules:
  * pending = in-degree) on the reference chunk plan of chunk_rows rows, and
  * the edge-softmax aggregation of the range with bias, head concat (+ReLU)
@@ -207,8 +208,9 @@ ATLAS_API int atlas_transform_typed(int32_t backend, const void* x_dev,
 ATLAS_API int atlas_layer_run_gat(atlas_layer* layer, const atlas_graph* graph,
                                   const void* z_dev, int32_t z_dtype,
                                   int64_t ldz, int32_t heads,
-                                  int32_t head_dim, int32_t el_col,
-                                  int32_t er_col, const float* bias_dev,
+                                  int32_t head_dim, int32_t head_stride,
+                                  int32_t el_col, int32_t er_col,
+                                  const float* bias_dev,
                                   int32_t mean_heads, int32_t relu,
                                   float negative_slope, void* y_dev,
                                   int32_t y_dtype, int64_t ldy,

@@ -21,7 +21,7 @@
 //  * runs: one caller-supplied chunk tile; destination runs come from the
 //    per-chunk stable sort (chunk.cu); a record is read back only if an
 //    earlier chunk already touched it.
-#include "internal.cuh"
+#include "bulk.cuh"
 
 namespace atlas {
 namespace {
@@ -379,37 +379,6 @@ __global__ void __launch_bounds__(256, 3)
 // (32 j + l) * 16, conflict-free) and fold them in source order exactly like
 // the other front ends.
 
-__device__ __forceinline__ void mbar_init_cta(uint64_t* bar, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(bar)),
-               "r"(n));
-}
-
-__device__ __forceinline__ void bulk_row(void* smem, const void* gmem,
-                                         uint32_t bytes, uint64_t* bar) {
-  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
-      "r"(bytes)
-      : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1], %2, [%3];" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
-      "l"(gmem), "r"(bytes), "r"(b)
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar,
-                                                 uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "BW_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra BW_%=;\n}" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
-      "r"(parity)
-      : "memory");
-}
-
 constexpr int kBulkWarps = 4;
 constexpr int kBulkGrab = 16;
 
@@ -429,7 +398,8 @@ __device__ __forceinline__ void bulk_body(
   bool act[CH];
 #pragma unroll
   for (int j = 0; j < CH; j++) act[j] = (j * 32 + lane) * EPC < d;
-  uint32_t n_issued = 0, n_used = 0;  // slot sequence numbers (per warp)
+  RowFeeder<SLOTS, (SLOTS >= 8 ? 4 : SLOTS / 2)> feed{ring, bars, row_bytes,
+                                                   csc_src};
   while (true) {
     unsigned long long v0 = 0;
     if (lane == 0) v0 = atomicAdd(work, (unsigned long long)kBulkGrab);
@@ -437,28 +407,9 @@ __device__ __forceinline__ void bulk_body(
     if ((int64_t)v0 >= nloc) break;
     const int64_t v1 = min((int64_t)v0 + kBulkGrab, nloc);
     const int64_t e0 = csc_ptr[v0], e1 = csc_ptr[v1];
-    int64_t pe = e0, ibase = e0;
-    uint32_t isrc = (e0 + lane < e1) ? csc_src[e0 + lane] : 0u;
-    auto issue = [&]() {
-      if (pe < e1) {
-        if (pe - ibase == 32) {
-          ibase = pe;
-          isrc = (pe + lane < e1) ? csc_src[pe + lane] : 0u;
-        }
-        const uint32_t s = __shfl_sync(0xffffffffu, isrc, (int)(pe - ibase));
-        if (lane == 0) {
-          const int slot = (int)(n_issued & (SLOTS - 1));
-          bulk_row(ring + (size_t)slot * row_bytes, x + (int64_t)s * ldx,
-                   row_bytes, &bars[slot]);
-        }
-        n_issued++;
-        pe++;
-      }
-    };
-#pragma unroll 1
-    for (int k = 0; k < SLOTS; k++) issue();
+    feed.begin(e0, e1, x, ldx);
     int64_t ce = e0, cbase = e0;
-    uint32_t csrc = isrc;
+    uint32_t csrc = 0;
     if (MODEL == ATLAS_GIN) csrc = (e0 + lane < e1) ? csc_src[e0 + lane] : 0u;
     for (int64_t v = (int64_t)v0; v < v1; v++) {
       const int64_t dend = csc_ptr[v + 1];
@@ -492,10 +443,7 @@ __device__ __forceinline__ void bulk_body(
             self_term();
           }
         }
-        const int slot = (int)(n_used & (SLOTS - 1));
-        mbar_wait_parity(&bars[slot], (n_used / SLOTS) & 1u);
-        const uint4* row =
-            reinterpret_cast<const uint4*>(ring + (size_t)slot * row_bytes);
+        const uint4* row = reinterpret_cast<const uint4*>(feed.wait());
         F f[CH];
 #pragma unroll
         for (int j = 0; j < CH; j++)
@@ -505,9 +453,7 @@ __device__ __forceinline__ void bulk_body(
         for (int j = 0; j < CH; j++)
           if (act[j])
             add_msg<T, EPC, kMean, GUARD>(a[j], f[j], false, denom, rcp, 1.0f);
-        n_used++;
-        __syncwarp();  // every lane is done with the slot before its refill
-        issue();
+        feed.release(x, ldx);
       }
       if (MODEL == ATLAS_GIN && self_pending) self_term();
       float* out = acc + v * ldacc;

@@ -300,7 +300,8 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
 
 int atlas_layer_run_gat(atlas_layer* L, const atlas_graph* g, const void* z,
                         int32_t z_dtype, int64_t ldz, int32_t heads,
-                        int32_t head_dim, int32_t el_col, int32_t er_col,
+                        int32_t head_dim, int32_t head_stride,
+                        int32_t el_col, int32_t er_col,
                         const float* bias, int32_t mean_heads, int32_t relu,
                         float negative_slope, void* y, int32_t y_dtype,
                         int64_t ldy, int64_t chunk_rows, void* stream) {
@@ -316,9 +317,9 @@ int atlas_layer_run_gat(atlas_layer* L, const atlas_graph* g, const void* z,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     settle(L);
     launch_control(L, g, chunk_rows, s);
-    launch_gat_aggregate(g, z, z_dtype, ldz, heads, head_dim, el_col, er_col,
-                         bias, mean_heads, relu, negative_slope, y, y_dtype,
-                         ldy, s);
+    launch_gat_aggregate(g, z, z_dtype, ldz, heads, head_dim, head_stride,
+                         el_col, er_col, bias, mean_heads, relu,
+                         negative_slope, y, y_dtype, ldy, s);
     ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
     ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
     L->timing_pending = true;

@@ -193,10 +193,11 @@ void launch_gather_rows(const float* acc, int64_t ldacc, const int32_t* ids,
 
 // gat.cu
 void launch_gat_aggregate(const atlas_graph* g, const void* z, int z_dtype,
-                          int64_t ldz, int heads, int head_dim, int el_col,
-                          int er_col, const float* bias, int mean_heads,
-                          int relu, float slope, void* y, int y_dtype,
-                          int64_t ldy, cudaStream_t s);
+                          int64_t ldz, int heads, int head_dim,
+                          int head_stride, int el_col, int er_col,
+                          const float* bias, int mean_heads, int relu,
+                          float slope, void* y, int y_dtype, int64_t ldy,
+                          cudaStream_t s);
 
 // transform.cu
 void launch_transform_stable(const float* x, int64_t rows, int64_t k,

@@ -226,8 +226,9 @@ class DeviceLayer:
             raise ConfigError(f"z {tuple(z.shape)} does not cover the graph")
         N.check(N.load_library().atlas_layer_run_gat(
             self.handle, graph.handle, z.data_ptr(), torch_dtype_code(z),
-            z.stride(0), layout.heads, layout.head_dim, layout.el_col,
-            layout.er_col, bias.data_ptr(), int(mean_heads), int(relu),
+            z.stride(0), layout.heads, layout.head_dim, layout.head_stride,
+            layout.el_col, layout.er_col, bias.data_ptr(), int(mean_heads),
+            int(relu),
             float(negative_slope), y.data_ptr(), torch_dtype_code(y),
             y.stride(0), int(chunk_rows), N.stream_handle(stream)))
 

@@ -169,8 +169,10 @@ def read_gat_weights(path) -> GATWeights:
 
 @dataclass(frozen=True)
 class ZLayout:
-    """Column layout of a pass-A row: [z (H*F) | pad | el (H) | er (H) |
-    pad], every part starting on a 16-byte boundary (vector loads)."""
+    """Column layout of a pass-A row: [z | el (H) | er (H) | pad]. Head h
+    of z sits at columns [h*stride, h*stride + F) with stride = F rounded
+    up to a whole 16-byte chunk (zero columns between), so every 16-byte
+    chunk the aggregation loads belongs to one head."""
 
     heads: int
     head_dim: int
@@ -184,8 +186,12 @@ class ZLayout:
         return -(-n // self.epc) * self.epc
 
     @property
+    def head_stride(self) -> int:
+        return self._up(self.head_dim)
+
+    @property
     def el_col(self) -> int:
-        return self._up(self.heads * self.head_dim)
+        return self.heads * self.head_stride
 
     @property
     def er_col(self) -> int:
@@ -197,12 +203,14 @@ class ZLayout:
 
 
 def extended_weight(lw: GATLayerWeights, layout: ZLayout) -> np.ndarray:
-    """W_ext (ldz x in): W, zero pad, a_l[h]^T W_h, a_r[h]^T W_h, zero pad
-    (computed in float64, stored f32), so z_ext = h . W_ext^T carries el
-    and er."""
+    """W_ext (ldz x in): the heads of W at their strided rows, then
+    a_l[h]^T W_h and a_r[h]^T W_h, zero elsewhere (computed in float64,
+    stored f32), so z_ext = h . W_ext^T carries z, el and er."""
     w = lw.weight.astype(np.float64).reshape(lw.heads, lw.head_dim, lw.in_dim)
     ext = np.zeros((layout.ldz, lw.in_dim), dtype=np.float64)
-    ext[:lw.hf] = lw.weight
+    for h in range(lw.heads):
+        r = h * layout.head_stride
+        ext[r:r + lw.head_dim] = w[h]
     ext[layout.el_col:layout.el_col + lw.heads] = np.einsum(
         "hf,hfk->hk", lw.attn_l.astype(np.float64), w)
     ext[layout.er_col:layout.er_col + lw.heads] = np.einsum(

@@ -83,16 +83,19 @@ def test_extended_weight_emits_el_er(itemsize):
     lw = w.layers[0]
     lay = G.ZLayout(lw.heads, lw.head_dim, itemsize)
     assert lay.el_col % lay.epc == 0 and lay.ldz % lay.epc == 0
-    assert lay.el_col >= lw.hf and lay.ldz >= lay.er_col + lw.heads
+    assert lay.head_stride % lay.epc == 0 and lay.head_stride >= 19
+    assert lay.el_col == 4 * lay.head_stride
+    assert lay.ldz >= lay.er_col + lw.heads
     h = np.random.default_rng(0).uniform(-1, 1, (50, 24))
     ext = G.extended_weight(lw, lay).astype(np.float64)
     zx = h @ ext.T
     z = (h @ lw.weight.astype(np.float64).T).reshape(50, 4, 19)
     el = np.einsum("vhf,hf->vh", z, lw.attn_l.astype(np.float64))
     er = np.einsum("vhf,hf->vh", z, lw.attn_r.astype(np.float64))
-    np.testing.assert_allclose(zx[:, :lw.hf], z.reshape(50, -1), atol=1e-6)
+    zs = zx[:, :lay.el_col].reshape(50, 4, lay.head_stride)
+    np.testing.assert_allclose(zs[:, :, :19], z, atol=1e-6)
+    np.testing.assert_array_equal(zs[:, :, 19:], 0)
     np.testing.assert_allclose(zx[:, lay.el_col:lay.el_col + 4], el,
                                atol=1e-5)
     np.testing.assert_allclose(zx[:, lay.er_col:lay.er_col + 4], er,
                                atol=1e-5)
-    np.testing.assert_array_equal(zx[:, lw.hf:lay.el_col], 0)

@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_gat.py -x -q > gpurun_out/pytest_gat.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gat.log
+timeout 900 python bench.py --workload igb-medium-gat --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_igb-medium-gat.json 2> gpurun_out/bench_igb_gat.err
