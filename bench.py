@@ -110,12 +110,14 @@ def gat_agg_bytes(graph, weights, layouts, rank_range, zsize):
     return out
 
 
-def agg_bytes(graph, weights, rank_range, in_sizes):
+def agg_bytes(graph, weights, rank_range, in_sizes, eng=None, out_size=4):
     """Algorithmic HBM bytes of the resident scatter-aggregate per layer
     (DESIGN.md §4): gather every in-edge's source row once (the layer
     input does not fit in L2), read the u32 source id per edge and the
     CSC/in-degree arrays per destination, read the destination's own row
-    for the SAGE/GIN self term, write each f32 record once."""
+    for the SAGE/GIN self term, write each f32 record once. A
+    transform-first layer (eng.transform_first(l)) gathers z rows of
+    npad f32 instead and writes the layer output directly."""
     lo, hi = rank_range
     e_g = int(graph.offsets[-1]) if (lo, hi) == (0, graph.num_vertices) \
         else int(np.count_nonzero((graph.neighbors >= lo)
@@ -125,6 +127,12 @@ def agg_bytes(graph, weights, rank_range, in_sizes):
     out = []
     for l, lw in enumerate(weights.layers):
         d, s = weights.embedding_dim(l), in_sizes[l]
+        if eng is not None and eng.transform_first(l):
+            npad = -(-lw.out_dim // 4) * 4
+            out.append(e_g * npad * 4 + 4 * e_g + 12 * v_g
+                       + (v_g * npad * 4 if self_row else 0)
+                       + v_g * lw.out_dim * out_size)
+            continue
         out.append(e_g * d * s + 4 * e_g + 12 * v_g
                    + (v_g * d * s if self_row else 0)
                    + 4 * weights.agg_dim(l) * v_g)
@@ -371,7 +379,8 @@ def main():
         agg_b = sum(gat_agg_bytes(graph, weights, eng.layouts,
                                   (eng.lo, eng.hi), in_sizes[-1]))
     else:
-        agg_b = sum(agg_bytes(graph, weights, (eng.lo, eng.hi), in_sizes))
+        agg_b = sum(agg_bytes(graph, weights, (eng.lo, eng.hi), in_sizes,
+                              eng, in_sizes[-1]))
     achieved = agg_b / (statistics.mean(agg_ms) / 1e3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
@@ -446,7 +455,9 @@ def main():
                          "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
                          "frac": achieved / peaks.get("hbm_gbs", 6650.0),
                          "traffic": traffic,
-                         "kernel": "scatter-aggregate (agg_ring / agg_bulk)",
+                         "kernel": "scatter-aggregate (agg_ring / agg_bulk / "
+                                   "gat_bulk / agg_tf_narrow; per layer "
+                                   "agg_ms)",
                          "algorithmic_bytes_per_step": agg_b},
             "e2e": e2e_line,
             "bit_exact_backend": None if alt is None else {

@@ -173,6 +173,29 @@ ATLAS_API int atlas_layer_run_streamed(atlas_layer* layer,
                                        const void* x_host, int32_t dtype,
                                        int64_t ldx, int64_t tile_rows,
                                        int64_t chunk_rows, void* stream);
+/* transform-first layer pass (tcgen05 backend, out_dim < aggregated
+ * width): z = h . W_z^T was computed by atlas_transform_typed for every
+ * source (V rows, ldz); the pass runs the layer's control plane on the
+ * reference chunk plan (chunk_rows rows, as for the layer's own input) and
+ * aggregates the first d columns of z with data_model's rule (ATLAS_GCN =
+ * mean, for GCN and SAGE; ATLAS_GIN = sum + (1+eps) self, in stream
+ * order, exact division as in atlas_layer_run_resident), then writes
+ * y[v] = act(agg + self_rows[v] + b)[:n] (self_rows: SAGE's h_v . W2^T,
+ * NULL otherwise). By linearity this is the reference layer up to
+ * floating-point order; no f32 records are kept. out_flag (may be NULL)
+ * receives y's extremes flag. */
+ATLAS_API int atlas_layer_run_fused(atlas_layer* layer,
+                                    const atlas_graph* graph,
+                                    const float* z_dev, int64_t ldz,
+                                    int32_t data_model, int64_t d,
+                                    int64_t chunk_rows,
+                                    const int32_t* input_flag,
+                                    const float* bias_dev,
+                                    const float* self_rows_dev,
+                                    int64_t ld_self, int64_t n,
+                                    int32_t relu, void* y_dev,
+                                    int32_t y_dtype, int64_t ldy,
+                                    int32_t* out_flag, void* stream);
 ATLAS_API int atlas_layer_accumulator(atlas_layer* layer, float** acc_dev,
                             int64_t* ld);
 

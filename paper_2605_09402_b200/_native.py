@@ -94,6 +94,9 @@ def _declare(lib):
     fn("atlas_layer_run_gat", ctypes.c_int, c_vp, c_vp, c_vp, c_i32, c_i64,
        c_i32, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, ctypes.c_float,
        c_vp, c_i32, c_i64, c_i64, c_vp)
+    fn("atlas_layer_run_fused", ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_i32,
+       c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_i32,
+       c_i64, c_vp, c_vp)
     fn("atlas_layer_finish", ctypes.c_int, c_vp,
        ctypes.POINTER(LayerMetricsC))
     fn("atlas_layer_chunk_stats", ctypes.c_int, c_vp, c_vp, c_vp, c_i64,
@@ -116,7 +119,7 @@ EXPORTED = [
     "atlas_layer_accumulator", "atlas_transform", "atlas_layer_finish",
     "atlas_layer_chunk_stats", "atlas_layer_log", "atlas_layer_state",
     "atlas_layer_timing", "atlas_reorder", "atlas_transform_typed",
-    "atlas_layer_run_gat",
+    "atlas_layer_run_gat", "atlas_layer_run_fused",
 ]
 
 

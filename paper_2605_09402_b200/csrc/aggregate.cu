@@ -251,15 +251,45 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <typename T, int VEC, int MODEL, bool GUARD>
+// Fused epilogue of the transform-first layer (tcgen05 backend): the ring
+// aggregates z = h . W_z^T instead of h, then writes the layer output
+// y[v] = act(agg(z)[v] + self[v] + b) straight away (self = the SAGE
+// z2 = h_v . W2^T part of the same z row, or none).
+struct EpiArgs {
+  void* y;
+  int64_t ldy;
+  const float* bias;
+  const float* self_rows;  // may be null
+  int64_t ld_self;
+  int n;                   // output columns
+  int relu;
+  int32_t* flag;           // extremes flag of y for the next layer
+};
+
+template <typename OutT>
+__device__ __forceinline__ OutT cvt_from_f32(float v);
+template <>
+__device__ __forceinline__ float cvt_from_f32<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __half cvt_from_f32<__half>(float v) {
+  return __float2half_rn(v);
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt_from_f32<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+template <typename T, int VEC, int MODEL, bool GUARD, typename OutT = void>
 __device__ __forceinline__ void ring_body(
     const T* __restrict__ x, int64_t ldx, const int64_t* __restrict__ csc_ptr,
     const uint32_t* __restrict__ csc_src, const uint32_t* __restrict__ indeg,
     int64_t lo, int64_t nloc, int d, float* __restrict__ acc, int64_t ldacc,
     float self_scale, unsigned long long* __restrict__ work,
-    uint4* __restrict__ ring) {
+    uint4* __restrict__ ring, const EpiArgs& epi = EpiArgs{}) {
   using F = Frag<T, VEC>;
   static_assert(sizeof(F) == 16, "ring slots are 16 B");
+  constexpr bool kEpi = !std::is_void<OutT>::value;
+  int bad = 0;  // epilogue: extremes seen in y
   constexpr bool kMean = MODEL != ATLAS_GIN;
   const int lane = threadIdx.x & 31;
   const int col = lane * VEC;
@@ -332,7 +362,23 @@ __device__ __forceinline__ void ring_body(
         me.load(x + (int64_t)vg * ldx + col);
         add_msg<T, VEC, false>(a, me, true, 1.0f, 1.0f, self_scale);
       }
-      if (active) {
+      if constexpr (kEpi) {
+        using O = typename std::conditional<kEpi, OutT, float>::type;
+        O* yrow = static_cast<O*>(epi.y) + v * epi.ldy;
+#pragma unroll
+        for (int e = 0; e < VEC; e++) {
+          const int c = col + e;
+          if (c < epi.n) {
+            float o = a[e];
+            if (epi.self_rows) o += epi.self_rows[(int64_t)vg * epi.ld_self + c];
+            o += epi.bias[c];
+            if (epi.relu) o = (o >= 0.0f || o != o) ? o : 0.0f;
+            const O q = cvt_from_f32<O>(o);
+            bad |= is_extreme(to_f32(q));
+            yrow[c] = q;
+          }
+        }
+      } else if (active) {
         float* out = acc + v * ldacc;
         store_f32<VEC>(out + col, a);
         if (MODEL == ATLAS_SAGE) {
@@ -347,6 +393,30 @@ __device__ __forceinline__ void ring_body(
     }
     cp_async_wait<0>();
   }
+  if constexpr (kEpi)
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && epi.flag)
+      atomicOr(epi.flag, 1);
+}
+
+// transform-first layer: ring aggregation of z with the fused epilogue
+template <int MODEL, typename OutT>
+__global__ void __launch_bounds__(256, 3)
+    agg_ring_epi(const float* __restrict__ z, int64_t ldz,
+                 const int64_t* __restrict__ csc_ptr,
+                 const uint32_t* __restrict__ csc_src,
+                 const uint32_t* __restrict__ indeg, int64_t lo, int64_t nloc,
+                 int d, float self_scale, const int* __restrict__ guard_flag,
+                 unsigned long long* __restrict__ work, EpiArgs epi) {
+  extern __shared__ uint4 ring_smem[];
+  uint4* ring = ring_smem + (threadIdx.x >> 5) * (kRing * 32);
+  if (*guard_flag)
+    ring_body<float, 4, MODEL, true, OutT>(z, ldz, csc_ptr, csc_src, indeg,
+                                           lo, nloc, d, nullptr, 0,
+                                           self_scale, work, ring, epi);
+  else
+    ring_body<float, 4, MODEL, false, OutT>(z, ldz, csc_ptr, csc_src, indeg,
+                                            lo, nloc, d, nullptr, 0,
+                                            self_scale, work, ring, epi);
 }
 
 template <typename T, int VEC, int MODEL>
@@ -366,6 +436,89 @@ __global__ void __launch_bounds__(256, 3)
   else
     ring_body<T, VEC, MODEL, false>(x, ldx, csc_ptr, csc_src, indeg, lo, nloc,
                                     d, acc, ldacc, self_scale, work, ring);
+}
+
+// transform-first layer, narrow z rows (<= 64 f32): LPD lanes per
+// destination, 32/LPD destinations per warp, each lane with 8 independent
+// 16-byte row loads in flight. Tolerance path (z = h . W^T already
+// reorders the float math), so the mean is sum * RN(1/deg).
+template <int LPD, int MODEL, typename OutT>
+__global__ void __launch_bounds__(256, 4)
+    agg_tf_narrow(const float* __restrict__ z, int64_t ldz,
+                  const int64_t* __restrict__ csc_ptr,
+                  const uint32_t* __restrict__ csc_src,
+                  const uint32_t* __restrict__ indeg, int64_t lo, int64_t nloc,
+                  int d, float self_scale, EpiArgs epi) {
+  static_assert(LPD >= 8 && LPD <= 32, "8..32 lanes per destination");
+  constexpr int DPW = 32 / LPD;
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31, sub = lane / LPD, sl = lane % LPD;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t v = warp * DPW + sub;
+  const bool valid = v < nloc;
+  const int64_t beg = valid ? csc_ptr[v] : 0, end = valid ? csc_ptr[v + 1] : 0;
+  const int cnt = (int)(end - beg);
+  int maxcnt = cnt;
+#pragma unroll
+  for (int o = 16; o >= LPD; o >>= 1)
+    maxcnt = max(maxcnt, __shfl_xor_sync(0xffffffffu, maxcnt, o));
+  const int col = sl * 4;
+  const bool active = valid && col < d;
+  float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  // source ids of the next batch are fetched while this batch's rows fly
+  uint32_t next = (sl < U && sl < cnt) ? csc_src[beg + sl] : 0u;
+  for (int b = 0; b < maxcnt; b += U) {
+    const uint32_t id = next;
+    next = (sl < U && b + U + sl < cnt) ? csc_src[beg + b + U + sl] : 0u;
+    float4 f[U];
+#pragma unroll
+    for (int j = 0; j < U; j++) {
+      const uint32_t u = __shfl_sync(0xffffffffu, id, sub * LPD + j);
+      if (active && b + j < cnt)
+        f[j] = __ldg(reinterpret_cast<const float4*>(z + (int64_t)u * ldz +
+                                                     col));
+    }
+#pragma unroll
+    for (int j = 0; j < U; j++)
+      if (active && b + j < cnt) {
+        a[0] += f[j].x;
+        a[1] += f[j].y;
+        a[2] += f[j].z;
+        a[3] += f[j].w;
+      }
+  }
+  if (!valid) return;
+  const int64_t vg = v + lo;
+  if (MODEL == ATLAS_GIN) {
+    if (active) {
+      const float4 me =
+          __ldg(reinterpret_cast<const float4*>(z + vg * ldz + col));
+      a[0] += self_scale * me.x;
+      a[1] += self_scale * me.y;
+      a[2] += self_scale * me.z;
+      a[3] += self_scale * me.w;
+    }
+  } else {
+    const float r = 1.0f / (float)max(1u, indeg[v]);
+#pragma unroll
+    for (int e = 0; e < 4; e++) a[e] *= r;
+  }
+  int bad = 0;
+  OutT* yrow = static_cast<OutT*>(epi.y) + v * epi.ldy;
+#pragma unroll
+  for (int e = 0; e < 4; e++) {
+    const int c = col + e;
+    if (c < epi.n) {
+      float o = a[e];
+      if (epi.self_rows) o += epi.self_rows[vg * epi.ld_self + c];
+      o += epi.bias[c];
+      if (epi.relu) o = (o >= 0.0f || o != o) ? o : 0.0f;
+      const OutT q = cvt_from_f32<OutT>(o);
+      bad |= is_extreme(to_f32(q));
+      yrow[c] = q;
+    }
+  }
+  if (bad && epi.flag) atomicOr(epi.flag, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -891,6 +1044,77 @@ void launch_agg_resident(const atlas_graph* g, const void* x, int dtype,
     resident_typed<__half>(g, x, ldx, model, e1, d, acc, ldacc, s);
   else
     resident_typed<__nv_bfloat16>(g, x, ldx, model, e1, d, acc, ldacc, s);
+}
+
+void launch_agg_resident_epi(const atlas_graph* g, const float* z,
+                             int64_t ldz, int data_model, float gin_epsilon,
+                             int d, const int32_t* input_flag, void* y,
+                             int y_dtype, int64_t ldy, const float* bias,
+                             const float* self_rows, int64_t ld_self, int n,
+                             int relu, int32_t* out_flag, cudaStream_t s) {
+  if (g->nloc == 0) return;
+  if (d > 128 || d % 4 != 0 || ldz % 4 != 0 ||
+      (reinterpret_cast<uintptr_t>(z) & 15) != 0)
+    fail(ATLAS_ECONFIG, "transform-first aggregation needs <= 128 f32 "
+                        "columns in 16-byte rows");
+  EpiArgs epi{y, ldy, bias, self_rows, ld_self, n, relu, out_flag};
+  const float e1 = self_scale_of(gin_epsilon);
+  if (d <= 64) {  // narrow rows: several destinations per warp
+    auto narrow = [&](auto lpd_tag, auto model_tag) {
+      constexpr int LPD = decltype(lpd_tag)::value;
+      constexpr int M = decltype(model_tag)::value;
+      const int64_t warps = ceil_div(g->nloc, 32 / LPD);
+      const unsigned grid = (unsigned)ceil_div(warps, 8);
+      auto go = [&](auto kern) {
+        kern<<<grid, 256, 0, s>>>(z, ldz, g->csc_ptr.ptr, g->csc_src.ptr,
+                                  g->indeg.ptr, g->lo, g->nloc, d, e1, epi);
+      };
+      if (y_dtype == ATLAS_F32) go(agg_tf_narrow<LPD, M, float>);
+      else if (y_dtype == ATLAS_F16) go(agg_tf_narrow<LPD, M, __half>);
+      else go(agg_tf_narrow<LPD, M, __nv_bfloat16>);
+    };
+    auto by_model = [&](auto lpd_tag) {
+      if (data_model == ATLAS_GIN)
+        narrow(lpd_tag, std::integral_constant<int, ATLAS_GIN>());
+      else
+        narrow(lpd_tag, std::integral_constant<int, ATLAS_GCN>());
+    };
+    if (d <= 32) by_model(std::integral_constant<int, 8>());
+    else by_model(std::integral_constant<int, 16>());
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+    return;
+  }
+  const int* flag = input_flag;
+  if (!flag) {
+    g->scan_flag.reserve(1);
+    ATLAS_CUDA(cudaMemsetAsync(g->scan_flag.ptr, 0, sizeof(int), s));
+    scan_extremes<float><<<148 * 8, 256, 0, s>>>(z, g->V, d, ldz,
+                                                 g->scan_flag.ptr);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+    flag = g->scan_flag.ptr;
+  }
+  g->work.reserve(1);
+  ATLAS_CUDA(cudaMemsetAsync(g->work.ptr, 0, sizeof(unsigned long long), s));
+  const int smem = 8 * kRing * 32 * 16;
+  auto go = [&](auto kern) {
+    ATLAS_CUDA(cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<148 * 3, 256, smem, s>>>(z, ldz, g->csc_ptr.ptr, g->csc_src.ptr,
+                                    g->indeg.ptr, g->lo, g->nloc, d, e1, flag,
+                                    g->work.ptr, epi);
+  };
+  auto by_out = [&](auto model_tag) {
+    constexpr int M = decltype(model_tag)::value;
+    if (y_dtype == ATLAS_F32) go(agg_ring_epi<M, float>);
+    else if (y_dtype == ATLAS_F16) go(agg_ring_epi<M, __half>);
+    else go(agg_ring_epi<M, __nv_bfloat16>);
+  };
+  if (data_model == ATLAS_GIN) by_out(std::integral_constant<int, ATLAS_GIN>());
+  else by_out(std::integral_constant<int, ATLAS_GCN>());
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
 }
 
 void launch_agg_runs(const void* tile, int dtype, int64_t ldx,

@@ -86,6 +86,12 @@ static void launch_control(atlas_layer* L, const atlas_graph* g,
   ATLAS_CUDA(cudaEventRecord(L->tev[3], L->ctl_stream));
 }
 
+// the layer's f32 aggregation records (nloc x agg_dim), allocated lazily
+static void ensure_records(atlas_layer* L) {
+  const size_t want = (size_t)std::max<int64_t>(L->nloc, 1) * L->desc.agg_dim;
+  if (L->acc.count < want) L->acc.alloc(want);
+}
+
 }  // namespace atlas
 
 using namespace atlas;
@@ -187,7 +193,9 @@ int atlas_layer_create(const atlas_layer_desc* desc,
         ATLAS_CUDA(cudaMemcpyAsync(L->indeg.ptr, in_degrees_host + D.dst_lo,
                                    L->nloc * sizeof(uint32_t),
                                    cudaMemcpyHostToDevice, s));
-      L->acc.alloc(L->gat ? 1 : nn * D.agg_dim);
+      // f32 records are allocated on first use: the GAT and
+      // transform-first passes write layer outputs directly
+      L->acc.alloc(1);
       L->touched.alloc(nn);
       ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
       engine_init(L, s);
@@ -228,6 +236,7 @@ int atlas_chunk_submit(atlas_layer* L, int64_t start, int64_t end,
     if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
     use_device(L->desc.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ensure_records(L);
     if (L->chunks_seen == 0) {
       // records start at zero; later chunks resume via touched flags
       ATLAS_CUDA(cudaMemsetAsync(L->acc.ptr, 0, L->acc.bytes(), s));
@@ -282,6 +291,7 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
     if (chunk_rows < 1) fail(ATLAS_ECONFIG, "chunk_rows must be >= 1");
     if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
     if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
+    ensure_records(L);
     use_device(D.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     settle(L);
@@ -326,6 +336,41 @@ int atlas_layer_run_gat(atlas_layer* L, const atlas_graph* g, const void* z,
   });
 }
 
+int atlas_layer_run_fused(atlas_layer* L, const atlas_graph* g,
+                          const float* z, int64_t ldz, int32_t data_model,
+                          int64_t d, int64_t chunk_rows,
+                          const int32_t* input_flag, const float* bias,
+                          const float* self_rows, int64_t ld_self, int64_t n,
+                          int32_t relu, void* y, int32_t y_dtype, int64_t ldy,
+                          int32_t* out_flag, void* stream) {
+  return guarded([&] {
+    if (!L || !g || !z || !bias || !y) fail(ATLAS_ECONFIG, "null argument");
+    if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
+    const atlas_layer_desc& D = L->desc;
+    if (g->V != D.num_vertices || g->lo != D.dst_lo || g->hi != D.dst_hi)
+      fail(ATLAS_ECONFIG, "graph and layer disagree on the vertex range");
+    if (chunk_rows < 1) fail(ATLAS_ECONFIG, "chunk_rows must be >= 1");
+    if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
+    if (n < 1 || n > d || ldy < n) fail(ATLAS_ECONFIG, "bad output width");
+    if (data_model != ATLAS_GCN && data_model != ATLAS_GIN)
+      fail(ATLAS_ECONFIG, "fused data plane is a mean (GCN/SAGE) or a sum "
+                          "(GIN)");
+    if ((D.model == ATLAS_SAGE) != (self_rows != nullptr))
+      fail(ATLAS_ECONFIG, "SAGE needs its self rows (and only SAGE)");
+    use_device(D.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    settle(L);
+    launch_control(L, g, chunk_rows, s);
+    if (out_flag) ATLAS_CUDA(cudaMemsetAsync(out_flag, 0, sizeof(int32_t), s));
+    launch_agg_resident_epi(g, z, ldz, data_model, D.gin_epsilon, (int)d,
+                            input_flag, y, y_dtype, ldy, bias, self_rows,
+                            ld_self, (int)n, relu, out_flag, s);
+    ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
+    ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
+    L->timing_pending = true;
+  });
+}
+
 int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
                              const void* x_host, int32_t dtype, int64_t ldx,
                              int64_t tile_rows, int64_t chunk_rows,
@@ -339,6 +384,7 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
       fail(ATLAS_ECONFIG, "bad tile / chunk rows");
     if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
     if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
+    ensure_records(L);
     use_device(D.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t item = dtype == ATLAS_F32 ? 4 : 2;
@@ -417,6 +463,7 @@ int atlas_layer_timing(atlas_layer* L, float* ms, int32_t n) {
 int atlas_layer_accumulator(atlas_layer* L, float** acc, int64_t* ld) {
   return guarded([&] {
     if (!L) fail(ATLAS_ECONFIG, "null layer");
+    if (!L->gat) ensure_records(L);
     if (acc) *acc = L->acc.ptr;
     if (ld) *ld = L->desc.agg_dim;
   });

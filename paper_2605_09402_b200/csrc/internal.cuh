@@ -175,6 +175,12 @@ void launch_agg_resident(const atlas_graph* g, const void* x, int dtype,
                          int64_t ldx, int model, float gin_epsilon, int d,
                          float* acc, int64_t ldacc, const int32_t* input_flag,
                          cudaStream_t s);
+void launch_agg_resident_epi(const atlas_graph* g, const float* z,
+                             int64_t ldz, int data_model, float gin_epsilon,
+                             int d, const int32_t* input_flag, void* y,
+                             int y_dtype, int64_t ldy, const float* bias,
+                             const float* self_rows, int64_t ld_self, int n,
+                             int relu, int32_t* out_flag, cudaStream_t s);
 void launch_agg_runs(const void* tile, int dtype, int64_t ldx,
                      int64_t tile_lo, const uint32_t* run_dst,
                      const int64_t* run_beg, int64_t nruns,

@@ -161,6 +161,83 @@ struct TcParams {
   int32_t* flag;
 };
 
+// Epilogue warps (8): thread = accumulator row (TMEM lane) for
+// tcgen05.ld; each 32 x 16 block is transposed through a per-warp smem tile
+// so that a warp store covers 8 rows x 64 B (4 lanes x 16 B per row).
+// sscale (per output column, may be null) multiplies the accumulator
+// before the bias (the power-of-two weight scales of the f16 kernel).
+template <typename OutT>
+__device__ __forceinline__ void epilogue_loop(
+    const TcParams& p, int ew, int warp, int lane, int64_t ntiles,
+    uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
+    const float* sbias, const float* sscale, float* stage_out) {
+  const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+  const int cpar = ew >> 2;      // which 16-col blocks this warp takes
+  float* stage = stage_out + ew * 32 * kStageLd;
+  int acc = 0;
+  uint32_t aph[2] = {0, 0};
+  OutT* y = static_cast<OutT*>(p.y);
+  const int rsub = lane >> 2, c4 = (lane & 3) * 4;
+  const bool vec_ok = (p.ldy % 4) == 0 &&
+                      (reinterpret_cast<uintptr_t>(p.y) % (4 * sizeof(OutT))) == 0;
+  int bad = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(&tfull[acc], aph[acc]);
+    aph[acc] ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int64_t row0 = t * BM + quarter * 32;
+    const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                           (uint32_t)(acc * p.BN);
+    for (int c0 = cpar * 16; c0 < p.BN; c0 += 32) {
+      float v[16];
+      tmem_ld16(taddr + c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; j += 4)
+        *reinterpret_cast<float4*>(&stage[lane * kStageLd + j]) =
+            make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      __syncwarp();
+      const int c = c0 + c4;
+      float bias4[4], scale4[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        bias4[j] = sbias[c + j];
+        scale4[j] = sscale ? sscale[c + j] : 1.0f;
+      }
+#pragma unroll
+      for (int rr = 0; rr < 32; rr += 8) {
+        const int r = rr + rsub;
+        const int64_t row = row0 + r;
+        if (row < p.M) {
+          const float4 a = *reinterpret_cast<const float4*>(&stage[r * kStageLd + c4]);
+          const float av[4] = {a.x, a.y, a.z, a.w};
+          OutT q[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            float o = __fadd_rn(sscale ? av[j] * scale4[j] : av[j], bias4[j]);
+            if (p.relu) o = relu_np(o);
+            q[j] = cvt_out<OutT>(o);
+            bad |= (c + j < p.N) ? is_extreme(to_f32(q[j])) : 0;
+          }
+          OutT* dst = y + row * p.ldy + c;
+          if (vec_ok && c + 4 <= p.N) {
+            store4(dst, q);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+              if (c + j < p.N) dst[j] = q[j];
+          }
+        }
+      }
+      __syncwarp();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    mbar_arrive(&tempty[acc]);
+    acc ^= 1;
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0 && p.flag)
+    atomicOr(p.flag, 1);
+}
+
 template <typename TIn, typename OutT, bool RES_W>
 __global__ void __launch_bounds__(kThreads, 1)
     transform_tc_kernel(const __grid_constant__ CUtensorMap map_x,
@@ -375,72 +452,188 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------- epilogue ----------------
-    // thread = accumulator row (TMEM lane) for tcgen05.ld; each 32 x 16
-    // block is transposed through a per-warp smem tile so that a warp store
-    // covers 8 rows x 64 B (4 lanes x 16 B per row)
-    const int ew = warp - 6;
-    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
-    const int cpar = ew >> 2;      // which 16-col blocks this warp takes
-    float* stage = stage_out + ew * 32 * kStageLd;
-    int acc = 0;
-    uint32_t aph[2] = {0, 0};
-    OutT* y = static_cast<OutT*>(p.y);
-    const int rsub = lane >> 2, c4 = (lane & 3) * 4;
-    const bool vec_ok = (p.ldy % 4) == 0 &&
-                        (reinterpret_cast<uintptr_t>(p.y) % (4 * sizeof(OutT))) == 0;
-    int bad = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      mbar_wait(&tfull[acc], aph[acc]);
-      aph[acc] ^= 1;
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int64_t row0 = t * BM + quarter * 32;
-      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
-                             (uint32_t)(acc * p.BN);
-      for (int c0 = cpar * 16; c0 < p.BN; c0 += 32) {
-        float v[16];
-        tmem_ld16(taddr + c0, v);
+    epilogue_loop<OutT>(p, warp - 6, warp, lane, ntiles, tmem_base, tfull,
+                        tempty, sbias, nullptr, stage_out);
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile(
+        "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(
+            tmem_base),
+        "r"(p.tmem_cols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// f16 inputs on kind::f16 (K = 16 per MMA, twice tf32's rate, no splitter):
+// x is consumed as loaded by TMA; W is pre-split per output row n into
+// f16 hi + lo of W[n,:] * 2^k_n (k_n puts the row maximum in [2^14, 2^15),
+// so lo never loses bits to f16's range), both products accumulate in f32
+// in TMEM and the epilogue multiplies by 2^-k_n (exact). W is carried to
+// ~2^-22 relative, x exactly: the same accuracy class as 3xTF32.
+
+constexpr int BKH = 64;                 // 64 f16 = 128 B = one swizzle row
+constexpr int kThreadsH = (2 + kEpiWarps) * 32;
+
+__global__ void split_w_f16(const float* __restrict__ w, int64_t k,
+                            __half* __restrict__ hi, __half* __restrict__ lo,
+                            float* __restrict__ scale) {
+  const int64_t n = blockIdx.x;
+  const float* row = w + n * k;
+  float m = 0.0f;
+  for (int64_t i = threadIdx.x; i < k; i += blockDim.x)
+    m = fmaxf(m, fabsf(row[i]));
+  __shared__ float red[32];
 #pragma unroll
-        for (int j = 0; j < 16; j += 4)
-          *reinterpret_cast<float4*>(&stage[lane * kStageLd + j]) =
-              make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        __syncwarp();
-        const int c = c0 + c4;
-        float bias4[4];
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
 #pragma unroll
-        for (int j = 0; j < 4; j++) bias4[j] = sbias[c + j];
-#pragma unroll
-        for (int rr = 0; rr < 32; rr += 8) {
-          const int r = rr + rsub;
-          const int64_t row = row0 + r;
-          if (row < p.M) {
-            const float4 a = *reinterpret_cast<const float4*>(&stage[r * kStageLd + c4]);
-            const float av[4] = {a.x, a.y, a.z, a.w};
-            OutT q[4];
-#pragma unroll
-            for (int j = 0; j < 4; j++) {
-              float o = __fadd_rn(av[j], bias4[j]);
-              if (p.relu) o = relu_np(o);
-              q[j] = cvt_out<OutT>(o);
-              bad |= (c + j < p.N) ? is_extreme(to_f32(q[j])) : 0;
-            }
-            OutT* dst = y + row * p.ldy + c;
-            if (vec_ok && c + 4 <= p.N) {
-              store4(dst, q);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 4; j++)
-                if (c + j < p.N) dst[j] = q[j];
-            }
+    for (int o = 16; o; o >>= 1)
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) red[0] = m;
+  }
+  __syncthreads();
+  m = red[0];
+  const int e = (m > 0.0f && m <= 3.402823466e38f) ? 14 - ilogbf(m) : 0;
+  const float up = ldexpf(1.0f, e);
+  for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
+    const float v = row[i] * up;  // exact: power-of-two scale
+    const __half h = __float2half_rn(v);
+    hi[n * k + i] = h;
+    lo[n * k + i] = __float2half_rn(v - __half2float(h));
+  }
+  if (threadIdx.x == 0) scale[n] = ldexpf(1.0f, -e);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc,
+                                        uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(
+          tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kThreadsH, 1)
+    transform_h_kernel(const __grid_constant__ CUtensorMap map_x,
+                       const __grid_constant__ CUtensorMap map_whi,
+                       const __grid_constant__ CUtensorMap map_wlo,
+                       TcParams p, const float* __restrict__ wscale) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t x_bytes = BM * BKH * 2;
+  const uint32_t w_bytes = p.BN * BKH * 2;
+  const uint32_t stage_bytes = x_bytes + 2 * w_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + p.stages * stage_bytes);
+  uint64_t* empty = full + p.stages;
+  uint64_t* tfull = empty + p.stages;  // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+  float* sscale = sbias + 256;
+  float* stage_out = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(sscale + 256) + 15) & ~uintptr_t(15));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (p.M + BM - 1) / BM;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; a++) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = threadIdx.x; j < p.BN; j += kThreadsH) {
+    sbias[j] = j < p.N ? p.bias[j] : 0.0f;
+    sscale[j] = j < p.N ? wscale[j] : 0.0f;
+  }
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::
+            "r"(smem_u32(tmem_slot)),
+        "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kb = 0; kb < p.kblocks; kb++) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = base + s * stage_bytes;
+          mbar_expect_tx(&full[s], stage_bytes);
+          tma_load_2d(st, &map_x, &full[s], kb * BKH, (int)(t * BM));
+          tma_load_2d(st + x_bytes, &map_whi, &full[s], kb * BKH, 0);
+          tma_load_2d(st + x_bytes + w_bytes, &map_wlo, &full[s], kb * BKH, 0);
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
           }
         }
-        __syncwarp();
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&tempty[acc]);
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = (1u << 4)                       // D = f32
+                           | (0u << 7) | (0u << 10)        // A, B = f16
+                           | ((uint32_t)(p.BN >> 3) << 17)  // N
+                           | ((uint32_t)(BM >> 4) << 24);   // M
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t aph[2] = {0, 0};
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], aph[acc] ^ 1);
+      aph[acc] ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dt = tmem_base + (uint32_t)(acc * p.BN);
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          uint8_t* st = base + s * stage_bytes;
+          const uint32_t a = smem_u32(st);
+          const uint32_t bh = smem_u32(st + x_bytes);
+          const uint32_t bl = smem_u32(st + x_bytes + w_bytes);
+#pragma unroll
+          for (int k = 0; k < BKH / 16; k++) {  // UMMA_K = 16 f16 = 32 B
+            const uint32_t off = k * 32;
+            const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
+            mma_f16(dt, sw128_desc(a + off), sw128_desc(bl + off), idesc,
+                    first);
+            mma_f16(dt, sw128_desc(a + off), sw128_desc(bh + off), idesc, 1u);
+          }
+          mma_commit(&empty[s]);
+          if (kb == p.kblocks - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
       acc ^= 1;
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0 && p.flag)
-      atomicOr(p.flag, 1);
+  } else {
+    epilogue_loop<OutT>(p, warp - 2, warp, lane, ntiles, tmem_base, tfull,
+                        tempty, sbias, sscale, stage_out);
   }
   __syncthreads();
   if (warp == 1) {
@@ -510,11 +703,95 @@ int num_sms() {
 
 }  // namespace
 
+// 2-D f16 map, box = 64 x box_rows (128-B rows), 128-B swizzle
+bool make_map_h(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols,
+                int64_t ld, int box_rows) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BKH, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr),
+             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// f16 x on kind::f16; false if the shape does not fit (caller falls back)
+bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
+                        const float* w, const float* b, int64_t n, int relu,
+                        void* y, int y_dtype, int64_t ldy, int32_t* flag,
+                        cudaStream_t s) {
+  if (n < 1 || n > 256 || k < 8 || k % 8 != 0 || ldx % 8 != 0 ||
+      (reinterpret_cast<uintptr_t>(x) & 15) != 0)
+    return false;
+  const int BN = (int)((n + 15) / 16 * 16);
+  const int kblocks = (int)((k + BKH - 1) / BKH);
+  const int stage_bytes = BM * BKH * 2 + 2 * BN * BKH * 2;
+  const int fixed = 1024 + 8 * 16 + 16 + 2 * 4 * 256 + 16 +
+                    kEpiWarps * 32 * kStageLd * 4;
+  int stages = (227 * 1024 - fixed) / stage_bytes;
+  if (stages > 6) stages = 6;
+  if (stages < 2) return false;
+  // pre-split W (stream-ordered scratch)
+  __half *whi = nullptr, *wlo = nullptr;
+  float* wsc = nullptr;
+  ATLAS_CUDA(cudaMallocAsync(&whi, n * k * sizeof(__half), s));
+  ATLAS_CUDA(cudaMallocAsync(&wlo, n * k * sizeof(__half), s));
+  ATLAS_CUDA(cudaMallocAsync(&wsc, n * sizeof(float), s));
+  split_w_f16<<<(unsigned)n, 256, 0, s>>>(w, k, whi, wlo, wsc);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  CUtensorMap mx, mhi, mlo;
+  bool ok = make_map_h(&mx, x, rows, k, ldx, BM) &&
+            make_map_h(&mhi, whi, n, k, k, BN) &&
+            make_map_h(&mlo, wlo, n, k, k, BN);
+  if (ok) {
+    const int smem = fixed + stages * stage_bytes;
+    TcParams p{};
+    p.M = rows;
+    p.K = (int)k;
+    p.N = (int)n;
+    p.BN = BN;
+    p.stages = stages;
+    p.kblocks = kblocks;
+    p.relu = relu;
+    p.ldy = ldy;
+    p.bias = b;
+    p.y = y;
+    p.flag = flag;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(2 * BN)) cols <<= 1;
+    p.tmem_cols = cols;
+    const int64_t ntiles = (rows + BM - 1) / BM;
+    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, num_sms());
+    auto launch = [&](auto kern) {
+      ATLAS_CUDA(cudaFuncSetAttribute(
+          kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<grid, kThreadsH, smem, s>>>(mx, mhi, mlo, p, wsc);
+    };
+    if (y_dtype == ATLAS_F32) launch(transform_h_kernel<float>);
+    else if (y_dtype == ATLAS_F16) launch(transform_h_kernel<__half>);
+    else launch(transform_h_kernel<__nv_bfloat16>);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+  }
+  ATLAS_CUDA(cudaFreeAsync(whi, s));
+  ATLAS_CUDA(cudaFreeAsync(wlo, s));
+  ATLAS_CUDA(cudaFreeAsync(wsc, s));
+  return ok;
+}
+
 bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
                          int64_t ldx, const float* w, const float* b,
                          int64_t n, int relu, void* y, int y_dtype,
                          int64_t ldy, int32_t* flag, cudaStream_t s) {
   if (rows <= 0) return true;
+  if (x_dtype == ATLAS_F16 &&
+      launch_transform_h(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
+                         flag, s))
+    return true;
   const int xs = x_dtype == ATLAS_F32 ? 4 : 2;
   if (n < 1 || n > 256 || k < 1 || (ldx * xs) % 16 != 0 || k % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) != 0)

@@ -232,6 +232,22 @@ class DeviceLayer:
             float(negative_slope), y.data_ptr(), torch_dtype_code(y),
             y.stride(0), int(chunk_rows), N.stream_handle(stream)))
 
+    def run_fused(self, graph: DeviceGraph, z, d: int, chunk_rows: int,
+                  bias, y, *, data_model: int, relu: bool, self_col=None,
+                  input_flag=None, out_flag=None, stream=None):
+        """Transform-first pass (atlas_layer_run_fused): aggregate the first
+        d columns of z (V x ldz f32, = h . W_z^T) with ``data_model``'s
+        rule and write y = act(agg + z[:, self_col:] + b) for the range."""
+        if z.shape[0] != self.num_vertices or z.dtype.itemsize != 4:
+            raise ConfigError(f"z {tuple(z.shape)} does not cover the graph")
+        self_ptr = 0 if self_col is None else z.data_ptr() + 4 * self_col
+        N.check(N.load_library().atlas_layer_run_fused(
+            self.handle, graph.handle, z.data_ptr(), z.stride(0),
+            int(data_model), int(d), int(chunk_rows), N.ptr(input_flag),
+            bias.data_ptr(), self_ptr, z.stride(0), y.shape[1], int(relu),
+            y.data_ptr(), torch_dtype_code(y), y.stride(0), N.ptr(out_flag),
+            N.stream_handle(stream)))
+
     def run_streamed(self, graph: DeviceGraph, x_host, chunk_rows: int,
                      tile_bytes: int = 256 << 20, stream=None):
         """x_host: pinned CPU torch tensor (V, embed_dim); streamed to HBM

@@ -76,6 +76,10 @@ class PipelineConfig:
     record_log: bool = False        # keep victim/reload/graduation logs
     force_exact: bool = False       # always replay the exact control engine
     stream_tile_bytes: int = 256 << 20  # host->HBM tile of a streamed input
+    # tcgen05 backend: when a layer's output is narrower than what it
+    # aggregates, transform first and aggregate z = h . W^T (linearity of
+    # the mean / sum); the bit-exact "stable" backend never does
+    transform_first: bool = True
 
     def validate(self) -> None:
         if self.partitions < 1:
@@ -154,15 +158,50 @@ class Engine:
                   for lw in weights.layers]
         self.b = [torch.as_tensor(np.ascontiguousarray(lw.bias)).cuda()
                   for lw in weights.layers]
+        self._wz = {}
         self.last_layers = []
         self._layers = {}
         self.out_flags = {}
+        self.z_flags = {}
 
     def close(self):
         for layer in self._layers.values():
             layer.close()
         self._layers.clear()
         self.graph.close()
+
+    def transform_first(self, l: int) -> bool:
+        """Whether layer l aggregates z = h . W_z^T instead of h: tcgen05
+        backend only, and only when that narrows the aggregated width (the
+        fused ring pass takes up to 128 f32 columns)."""
+        if not self.config.transform_first or \
+                device_code(self.backend) != 1:
+            return False
+        d = self.weights.embedding_dim(l)
+        npad = -(-self.weights.layers[l].out_dim // 4) * 4
+        return npad < d and npad <= 128 and d % 4 == 0
+
+    def _z_weight(self, l: int):
+        """(W_z, zero bias, padded width): W_z = W (GCN/GIN) or [W1; W2]
+        (SAGE's mean half and self half), each padded to a multiple of 4
+        rows so z rows are 16-byte aligned."""
+        import torch
+
+        if l in self._wz:
+            return self._wz[l]
+        lw = self.weights.layers[l]
+        d = self.weights.embedding_dim(l)
+        n = lw.out_dim
+        npad = -(-n // 4) * 4
+        parts = ([lw.weight[:, :d], lw.weight[:, d:]]
+                 if self.kind == ModelKind.SAGE else [lw.weight])
+        wz = np.zeros((npad * len(parts), d), dtype=np.float32)
+        for i, p in enumerate(parts):
+            wz[i * npad:i * npad + n] = p
+        out = (torch.as_tensor(wz).cuda(),
+               torch.zeros(wz.shape[0], device="cuda"), npad)
+        self._wz[l] = out
+        return out
 
     def layer(self, l: int, x, *, chunk_budget=None, input_flag=None,
               defer_metrics: bool = False):
@@ -198,15 +237,18 @@ class Engine:
                 record_log=cfg.record_log, force_exact=cfg.force_exact,
                 device=self.device)
             self._layers[l] = layer
+        nloc = self.hi - self.lo
+        out_dim = w.layers[l].out_dim
+        y = torch.empty((nloc, out_dim), dtype=_torch_dtype(cfg.embed_dtype),
+                        device="cuda")
+        if self.transform_first(l):
+            return self._layer_transform_first(l, x, layer, rows, y, last,
+                                               t0, defer_metrics)
         if x.is_cuda:
             layer.run_resident(self.graph, x, rows, input_flag=input_flag)
         else:  # host (pinned) input: stream it in tiles (K1 streamer)
             layer.run_streamed(self.graph, x, rows,
                                tile_bytes=self.config.stream_tile_bytes)
-        nloc = self.hi - self.lo
-        out_dim = w.layers[l].out_dim
-        y = torch.empty((nloc, out_dim), dtype=_torch_dtype(cfg.embed_dtype),
-                        device="cuda")
         acc_ptr, ld = layer.accumulator_ptr()
         code = device_code(self.backend)
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -232,6 +274,48 @@ class Engine:
             m = metrics_from_device(layer, l)
             m.agg_ms, m.control_ms = layer.timing()
             m.transform_ms = ev0.elapsed_time(ev1)
+            m.gpu_seconds = time.perf_counter() - t0
+            return m
+
+        if defer_metrics:
+            return y, collect, layer
+        return y, collect(), layer
+
+    def _layer_transform_first(self, l, x, layer, rows, y, last, t0,
+                               defer_metrics):
+        """z = h . W_z^T on tcgen05 for every source row, then one fused
+        pass: control plane on the reference chunk plan + ring aggregation
+        of z + bias / SAGE self half / ReLU epilogue (no f32 records)."""
+        import torch
+
+        from .engine import transform_typed
+
+        wz, zb, npad = self._z_weight(l)
+        if not x.is_cuda:
+            x = x.cuda(non_blocking=True)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        z = torch.empty((x.shape[0], wz.shape[0]), dtype=torch.float32,
+                        device="cuda")
+        if l not in self.z_flags:
+            self.z_flags[l] = torch.zeros(1, dtype=torch.int32, device="cuda")
+        transform_typed(x, wz, zb, False, z, 1, flag=self.z_flags[l])
+        ev[1].record()
+        if l not in self.out_flags:
+            self.out_flags[l] = torch.zeros(1, dtype=torch.int32,
+                                            device="cuda")
+        data_model = (ModelKind.GIN if self.kind == ModelKind.GIN
+                      else ModelKind.GCN)
+        layer.run_fused(self.graph, z, npad, rows, self.b[l], y,
+                        data_model=int(data_model), relu=not last,
+                        self_col=npad if self.kind == ModelKind.SAGE else None,
+                        input_flag=self.z_flags[l],
+                        out_flag=self.out_flags[l])
+
+        def collect():
+            m = metrics_from_device(layer, l)
+            m.agg_ms, m.control_ms = layer.timing()
+            m.transform_ms = ev[0].elapsed_time(ev[1])
             m.gpu_seconds = time.perf_counter() - t0
             return m
 

@@ -300,3 +300,42 @@ def test_tcgen05_pipeline_within_tolerance(kind, feat_dtype):
     for a, b in zip(runs["tcgen05"][1], runs["stable"][1]):
         for f in METRICS:
             assert getattr(a, f) == getattr(b, f), f
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("transform_first", [True, False])
+def test_tcgen05_wide_input_transform_first(kind, transform_first):
+    """A wide f16 input layer (256 -> 64 -> 24): with transform_first the
+    tcgen05 backend aggregates z = h . W^T (f16 input on the tensor cores,
+    SAGE's self half added in the fused epilogue); either way every layer
+    is within the stated tolerance of the float64 oracle and the integer
+    metrics equal the bit-exact run's."""
+    from oracle import gather as OG
+    from paper_2605_09402_b200.storage import (ModelKind, random_weights,
+                                               synthetic_in_memory)
+    graph, feats = synthetic_in_memory("uniform", 6000, 7, 256, 21)
+    feats = feats.astype(np.float16)
+    w = random_weights(ModelKind(kind), [256, 64, 24], 5, gin_epsilon=0.25)
+    want = OG.per_layer(graph.num_vertices, graph.offsets, graph.neighbors,
+                        graph.in_degrees, feats.astype(np.float64), kind,
+                        [(lw.weight, lw.bias) for lw in w.layers],
+                        gin_epsilon=w.gin_epsilon)
+    runs = {}
+    for backend in ("tcgen05", "stable"):
+        eng = Engine(graph, w, PipelineConfig(
+            chunk_budget=256 << 10, hot_slots=700, backend=backend,
+            transform_first=transform_first))
+        if backend == "tcgen05":
+            assert [eng.transform_first(l) for l in range(2)] == \
+                [transform_first, transform_first]
+        _, metrics = eng.infer(torch.as_tensor(feats).cuda(),
+                               keep_layers=True)
+        runs[backend] = ([y.double().cpu().numpy() for y in eng.last_layers],
+                         metrics)
+        eng.close()
+    for l, (got, ref) in enumerate(zip(runs["tcgen05"][0], want)):
+        err = float(np.abs(got - ref).max())
+        assert err <= 1e-5 * float(np.abs(ref).max()), (l, err)
+    for a, b in zip(runs["tcgen05"][1], runs["stable"][1]):
+        for f in METRICS:
+            assert getattr(a, f) == getattr(b, f), f
