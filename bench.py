@@ -374,20 +374,36 @@ def main():
     # roofline of the dominant kernel (scatter-aggregate), CUDA events
     in_sizes = [x.element_size()] + [
         {"f32": 4, "f16": 2, "bf16": 2}[cfg.embed_dtype]] * (nlayers - 1)
-    agg_ms = [sum(m.agg_ms for m in step) for step in per_layer]
     if is_gat:
-        agg_b = sum(gat_agg_bytes(graph, weights, eng.layouts,
-                                  (eng.lo, eng.hi), in_sizes[-1]))
+        per_b = gat_agg_bytes(graph, weights, eng.layouts, (eng.lo, eng.hi),
+                              in_sizes[-1])
+        kinds = ["gat_bulk"] * nlayers
     else:
-        agg_b = sum(agg_bytes(graph, weights, (eng.lo, eng.hi), in_sizes,
-                              eng, in_sizes[-1]))
-    achieved = agg_b / (statistics.mean(agg_ms) / 1e3) / 1e9
+        per_b = agg_bytes(graph, weights, (eng.lo, eng.hi), in_sizes, eng,
+                          in_sizes[-1])
+        kinds = ["agg_tf_ring / agg_ring_epi (transform-first)"
+                 if eng.transform_first(l) else
+                 ("agg_bulk" if weights.embedding_dim(l) * in_sizes[l] > 512
+                  else "agg_ring") for l in range(nlayers)]
+    agg_b = sum(per_b)
+    # dominant aggregation kernel: the kind with the most device time;
+    # achieved = its algorithmic bytes / its mean launch time (CUDA events)
+    groups = {}
+    for l, k in enumerate(kinds):
+        ms_l = statistics.mean(step[l].agg_ms for step in per_layer)
+        g = groups.setdefault(k, [0, 0.0, 0])
+        g[0] += per_b[l]
+        g[1] += ms_l
+        g[2] += 1
+    dom = max(groups, key=lambda k: groups[k][1])
+    dom_b, dom_ms, dom_n = groups[dom]
+    achieved = dom_b / (dom_ms / 1e3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
     traffic = None
     prof = ROOT / "profiles" / f"agg_traffic_{args.workload}.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get("bytes_per_launch")
+        traffic = json.loads(prof.read_text()).get(dom)
 
     e2e_line = None
     if not args.no_e2e:
@@ -455,9 +471,14 @@ def main():
                          "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
                          "frac": achieved / peaks.get("hbm_gbs", 6650.0),
                          "traffic": traffic,
-                         "kernel": "scatter-aggregate (agg_ring / agg_bulk / "
-                                   "gat_bulk / agg_tf_narrow; per layer "
-                                   "agg_ms)",
+                         "kernel": dom,
+                         "launches_per_step": dom_n,
+                         "algorithmic_bytes_per_launch": dom_b / dom_n,
+                         "all_kernels": {
+                             k: {"bytes": g[0], "ms": round(g[1], 3),
+                                 "frac": g[0] / (g[1] / 1e3) / 1e9 /
+                                 peaks.get("hbm_gbs", 6650.0)}
+                             for k, g in groups.items()},
                          "algorithmic_bytes_per_step": agg_b},
             "e2e": e2e_line,
             "bit_exact_backend": None if alt is None else {

@@ -438,87 +438,121 @@ __global__ void __launch_bounds__(256, 3)
                                     d, acc, ldacc, self_scale, work, ring);
 }
 
-// transform-first layer, narrow z rows (<= 64 f32): LPD lanes per
-// destination, 32/LPD destinations per warp, each lane with 8 independent
-// 16-byte row loads in flight. Tolerance path (z = h . W^T already
-// reorders the float math), so the mean is sum * RN(1/deg).
+// transform-first layer, narrow z rows (<= 64 f32), streaming version:
+// 32/LPD sub-groups of LPD lanes per warp, each walking its own run of
+// consecutive destinations (one contiguous CSC range) in lockstep with the
+// others: every iteration each sub-group consumes one edge and issues the
+// cp.async of the edge kRing ahead into its lanes' shared-memory ring, so
+// kRing rows per lane stay in flight across destination boundaries and
+// the per-edge instruction cost is shared by 32/LPD destinations.
 template <int LPD, int MODEL, typename OutT>
 __global__ void __launch_bounds__(256, 4)
-    agg_tf_narrow(const float* __restrict__ z, int64_t ldz,
-                  const int64_t* __restrict__ csc_ptr,
-                  const uint32_t* __restrict__ csc_src,
-                  const uint32_t* __restrict__ indeg, int64_t lo, int64_t nloc,
-                  int d, float self_scale, EpiArgs epi) {
-  static_assert(LPD >= 8 && LPD <= 32, "8..32 lanes per destination");
+    agg_tf_ring(const float* __restrict__ z, int64_t ldz,
+                const int64_t* __restrict__ csc_ptr,
+                const uint32_t* __restrict__ csc_src,
+                const uint32_t* __restrict__ indeg, int64_t lo, int64_t nloc,
+                int d, float self_scale, EpiArgs epi,
+                unsigned long long* __restrict__ work) {
   constexpr int DPW = 32 / LPD;
-  constexpr int U = 8;
+  extern __shared__ uint4 ring_smem[];
+  uint4* ring = ring_smem + (threadIdx.x >> 5) * (kRing * 32);
   const int lane = threadIdx.x & 31, sub = lane / LPD, sl = lane % LPD;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t v = warp * DPW + sub;
-  const bool valid = v < nloc;
-  const int64_t beg = valid ? csc_ptr[v] : 0, end = valid ? csc_ptr[v + 1] : 0;
-  const int cnt = (int)(end - beg);
-  int maxcnt = cnt;
-#pragma unroll
-  for (int o = 16; o >= LPD; o >>= 1)
-    maxcnt = max(maxcnt, __shfl_xor_sync(0xffffffffu, maxcnt, o));
   const int col = sl * 4;
-  const bool active = valid && col < d;
-  float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-  // source ids of the next batch are fetched while this batch's rows fly
-  uint32_t next = (sl < U && sl < cnt) ? csc_src[beg + sl] : 0u;
-  for (int b = 0; b < maxcnt; b += U) {
-    const uint32_t id = next;
-    next = (sl < U && b + U + sl < cnt) ? csc_src[beg + b + U + sl] : 0u;
-    float4 f[U];
-#pragma unroll
-    for (int j = 0; j < U; j++) {
-      const uint32_t u = __shfl_sync(0xffffffffu, id, sub * LPD + j);
-      if (active && b + j < cnt)
-        f[j] = __ldg(reinterpret_cast<const float4*>(z + (int64_t)u * ldz +
-                                                     col));
-    }
-#pragma unroll
-    for (int j = 0; j < U; j++)
-      if (active && b + j < cnt) {
-        a[0] += f[j].x;
-        a[1] += f[j].y;
-        a[2] += f[j].z;
-        a[3] += f[j].w;
-      }
-  }
-  if (!valid) return;
-  const int64_t vg = v + lo;
-  if (MODEL == ATLAS_GIN) {
-    if (active) {
-      const float4 me =
-          __ldg(reinterpret_cast<const float4*>(z + vg * ldz + col));
-      a[0] += self_scale * me.x;
-      a[1] += self_scale * me.y;
-      a[2] += self_scale * me.z;
-      a[3] += self_scale * me.w;
-    }
-  } else {
-    const float r = 1.0f / (float)max(1u, indeg[v]);
-#pragma unroll
-    for (int e = 0; e < 4; e++) a[e] *= r;
-  }
+  const bool lane_on = col < d;
   int bad = 0;
-  OutT* yrow = static_cast<OutT*>(epi.y) + v * epi.ldy;
+  while (true) {
+    unsigned long long w0 = 0;
+    if (lane == 0) w0 = atomicAdd(work, (unsigned long long)(kGrab * DPW));
+    w0 = __shfl_sync(0xffffffffu, w0, 0);
+    if ((int64_t)w0 >= nloc) break;
+    // this sub-group's destinations [v, v_end) and edges [e_beg, e_end)
+    int64_t v = min((int64_t)w0 + (int64_t)sub * kGrab, nloc);
+    const int64_t v_end = min(v + kGrab, nloc);
+    const int64_t e_end = csc_ptr[v_end];
+    int64_t ce = csc_ptr[v], pe = ce, ibase = ce;
+    int64_t dend = v < v_end ? csc_ptr[v + 1] : e_end;
+    uint32_t isrc = (pe + sl < e_end) ? csc_src[pe + sl] : 0u;
+    float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    uint32_t n_iss = 0, n_use = 0;  // per-lane ring positions
+    auto issue = [&]() {
+      const bool more = pe < e_end;
+      if (more && pe - ibase == LPD) {
+        ibase = pe;
+        isrc = (pe + sl < e_end) ? csc_src[pe + sl] : 0u;
+      }
+      const uint32_t u =
+          __shfl_sync(0xffffffffu, isrc, (int)(pe - ibase) & (LPD - 1), LPD);
+      if (more) {
+        if (lane_on)
+          cp_async16(&ring[(n_iss % kRing) * 32 + lane],
+                     z + (int64_t)u * ldz + col);
+        n_iss++;
+        pe++;
+      }
+      cp_async_commit();  // one group per lane per iteration, maybe empty
+    };
+    // emit finished destinations (zero-degree ones included)
+    auto flush = [&]() {
+      while (v < v_end && ce == dend) {
+        const int64_t vg = v + lo;
+        float o4[4] = {a[0], a[1], a[2], a[3]};
+        if (MODEL == ATLAS_GIN) {
+          if (lane_on) {
+            const float4 me =
+                __ldg(reinterpret_cast<const float4*>(z + vg * ldz + col));
+            o4[0] += self_scale * me.x;
+            o4[1] += self_scale * me.y;
+            o4[2] += self_scale * me.z;
+            o4[3] += self_scale * me.w;
+          }
+        } else {
+          const float r = 1.0f / (float)max(1u, indeg[v]);
 #pragma unroll
-  for (int e = 0; e < 4; e++) {
-    const int c = col + e;
-    if (c < epi.n) {
-      float o = a[e];
-      if (epi.self_rows) o += epi.self_rows[vg * epi.ld_self + c];
-      o += epi.bias[c];
-      if (epi.relu) o = (o >= 0.0f || o != o) ? o : 0.0f;
-      const OutT q = cvt_from_f32<OutT>(o);
-      bad |= is_extreme(to_f32(q));
-      yrow[c] = q;
+          for (int e = 0; e < 4; e++) o4[e] *= r;
+        }
+        OutT* yrow = static_cast<OutT*>(epi.y) + v * epi.ldy;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const int c = col + e;
+          if (c < epi.n) {
+            float o = o4[e];
+            if (epi.self_rows) o += epi.self_rows[vg * epi.ld_self + c];
+            o += epi.bias[c];
+            if (epi.relu) o = (o >= 0.0f || o != o) ? o : 0.0f;
+            const OutT q = cvt_from_f32<OutT>(o);
+            bad |= is_extreme(to_f32(q));
+            yrow[c] = q;
+          }
+        }
+        a[0] = a[1] = a[2] = a[3] = 0.0f;
+        v++;
+        dend = v < v_end ? csc_ptr[v + 1] : e_end;
+      }
+    };
+#pragma unroll 1
+    for (int k = 0; k < kRing; k++) issue();
+    flush();
+    while (__any_sync(0xffffffffu, ce < e_end)) {
+      cp_async_wait<kRing - 1>();  // the row issued kRing iterations ago
+      if (ce < e_end) {
+        if (lane_on) {
+          const float4 f = *reinterpret_cast<const float4*>(
+              &ring[(n_use % kRing) * 32 + lane]);
+          a[0] += f.x;
+          a[1] += f.y;
+          a[2] += f.z;
+          a[3] += f.w;
+        }
+        n_use++;
+        ce++;
+      }
+      issue();
+      flush();
     }
+    cp_async_wait<0>();
   }
-  if (bad && epi.flag) atomicOr(epi.flag, 1);
+  if (__any_sync(0xffffffffu, bad) && lane == 0 && epi.flag)
+    atomicOr(epi.flag, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -1060,18 +1094,25 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
   EpiArgs epi{y, ldy, bias, self_rows, ld_self, n, relu, out_flag};
   const float e1 = self_scale_of(gin_epsilon);
   if (d <= 64) {  // narrow rows: several destinations per warp
+    g->work.reserve(1);
+    ATLAS_CUDA(cudaMemsetAsync(g->work.ptr, 0, sizeof(unsigned long long), s));
+    const int smem = 8 * kRing * 32 * 16;
     auto narrow = [&](auto lpd_tag, auto model_tag) {
       constexpr int LPD = decltype(lpd_tag)::value;
       constexpr int M = decltype(model_tag)::value;
-      const int64_t warps = ceil_div(g->nloc, 32 / LPD);
-      const unsigned grid = (unsigned)ceil_div(warps, 8);
       auto go = [&](auto kern) {
-        kern<<<grid, 256, 0, s>>>(z, ldz, g->csc_ptr.ptr, g->csc_src.ptr,
-                                  g->indeg.ptr, g->lo, g->nloc, d, e1, epi);
+        ATLAS_CUDA(cudaFuncSetAttribute(
+            kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0;
+        ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, kern, 256, smem));
+        kern<<<kNumSMs * std::max(1, per_sm), 256, smem, s>>>(
+            z, ldz, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
+            g->nloc, d, e1, epi, g->work.ptr);
       };
-      if (y_dtype == ATLAS_F32) go(agg_tf_narrow<LPD, M, float>);
-      else if (y_dtype == ATLAS_F16) go(agg_tf_narrow<LPD, M, __half>);
-      else go(agg_tf_narrow<LPD, M, __nv_bfloat16>);
+      if (y_dtype == ATLAS_F32) go(agg_tf_ring<LPD, M, float>);
+      else if (y_dtype == ATLAS_F16) go(agg_tf_ring<LPD, M, __half>);
+      else go(agg_tf_ring<LPD, M, __nv_bfloat16>);
     };
     auto by_model = [&](auto lpd_tag) {
       if (data_model == ATLAS_GIN)

@@ -22,7 +22,9 @@
 // overlap the MMAs of tile t+1.
 #include <cuda.h>
 
+#include <memory>
 #include <mutex>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -703,6 +705,24 @@ int num_sms() {
 
 }  // namespace
 
+struct SplitScratch {
+  int device;
+  cudaStream_t stream;
+  DevBuf<uint8_t> buf;
+};
+
+SplitScratch& split_scratch(cudaStream_t s) {
+  static std::mutex mu;
+  static std::vector<std::unique_ptr<SplitScratch>> all;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : all)
+    if (e->device == dev && e->stream == s) return *e;
+  all.emplace_back(new SplitScratch{dev, s, {}});
+  return *all.back();
+}
+
 // 2-D f16 map, box = 64 x box_rows (128-B rows), 128-B swizzle
 bool make_map_h(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols,
                 int64_t ld, int box_rows) {
@@ -734,12 +754,14 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
   int stages = (227 * 1024 - fixed) / stage_bytes;
   if (stages > 6) stages = 6;
   if (stages < 2) return false;
-  // pre-split W (stream-ordered scratch)
-  __half *whi = nullptr, *wlo = nullptr;
-  float* wsc = nullptr;
-  ATLAS_CUDA(cudaMallocAsync(&whi, n * k * sizeof(__half), s));
-  ATLAS_CUDA(cudaMallocAsync(&wlo, n * k * sizeof(__half), s));
-  ATLAS_CUDA(cudaMallocAsync(&wsc, n * sizeof(float), s));
+  // pre-split W into the (device, stream)'s grow-only scratch: work on one
+  // stream is ordered, so reusing it across calls is safe without syncs
+  SplitScratch& ws = split_scratch(s);
+  ws.buf.reserve((size_t)(2 * n * k * sizeof(__half) + n * sizeof(float) + 64));
+  __half* whi = reinterpret_cast<__half*>(ws.buf.ptr);
+  __half* wlo = whi + n * k;
+  float* wsc = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(wlo + n * k) + 15) & ~uintptr_t(15));
   split_w_f16<<<(unsigned)n, 256, 0, s>>>(w, k, whi, wlo, wsc);
   count_launch();
   ATLAS_LAUNCH_CHECK();
@@ -777,9 +799,6 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
     count_launch();
     ATLAS_LAUNCH_CHECK();
   }
-  ATLAS_CUDA(cudaFreeAsync(whi, s));
-  ATLAS_CUDA(cudaFreeAsync(wlo, s));
-  ATLAS_CUDA(cudaFreeAsync(wsc, s));
   return ok;
 }
 
