@@ -141,6 +141,12 @@ ATLAS_API void atlas_layer_destroy(atlas_layer* layer);
  * again) without reallocating its device memory */
 ATLAS_API int atlas_layer_reset(atlas_layer* layer, void* stream);
 
+/* atlas_layer_reset after a topology refresh (atlas_graph_update): the
+ * layer takes its in-degrees from the graph's device copy (no host trip),
+ * then re-arms like init_layer */
+ATLAS_API int atlas_layer_bind_graph(atlas_layer* layer,
+                                     const atlas_graph* graph, void* stream);
+
 /* process_chunk: rows (n x embed_dim, dtype) and the chunk CSR slice are
  * HOST pointers (pinned or pageable); the library stages them to HBM. */
 ATLAS_API int atlas_chunk_submit(atlas_layer* layer, int64_t start, int64_t end,
@@ -183,7 +189,9 @@ ATLAS_API int atlas_layer_run_streamed(atlas_layer* layer,
  * y[v] = act(agg + self_rows[v] + b)[:n] (self_rows: SAGE's h_v . W2^T,
  * NULL otherwise). By linearity this is the reference layer up to
  * floating-point order; no f32 records are kept. out_flag (may be NULL)
- * receives y's extremes flag. */
+ * receives y's extremes flag. With y_host (pinned, ldy_host elements per
+ * row) the output also goes to the host in host_slices destination slices,
+ * each copied while the next one aggregates; the stream covers the copies. */
 ATLAS_API int atlas_layer_run_fused(atlas_layer* layer,
                                     const atlas_graph* graph,
                                     const float* z_dev, int64_t ldz,
@@ -195,7 +203,9 @@ ATLAS_API int atlas_layer_run_fused(atlas_layer* layer,
                                     int64_t ld_self, int64_t n,
                                     int32_t relu, void* y_dev,
                                     int32_t y_dtype, int64_t ldy,
-                                    int32_t* out_flag, void* stream);
+                                    int32_t* out_flag, void* y_host,
+                                    int64_t ldy_host, int32_t host_slices,
+                                    void* stream);
 ATLAS_API int atlas_layer_accumulator(atlas_layer* layer, float** acc_dev,
                             int64_t* ld);
 

@@ -76,6 +76,7 @@ def _declare(lib):
        c_vp, ctypes.POINTER(c_vp))
     fn("atlas_layer_destroy", None, c_vp)
     fn("atlas_layer_reset", ctypes.c_int, c_vp, c_vp)
+    fn("atlas_layer_bind_graph", ctypes.c_int, c_vp, c_vp, c_vp)
     fn("atlas_chunk_submit", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_i32,
        c_vp, c_vp, c_i64, c_vp)
     fn("atlas_chunk_graduated", ctypes.c_int, c_vp, c_vp, c_vp, c_i64, P_i64,
@@ -96,7 +97,7 @@ def _declare(lib):
        c_vp, c_i32, c_i64, c_i64, c_vp)
     fn("atlas_layer_run_fused", ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_i32,
        c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_i32,
-       c_i64, c_vp, c_vp)
+       c_i64, c_vp, c_vp, c_i64, c_i32, c_vp)
     fn("atlas_layer_finish", ctypes.c_int, c_vp,
        ctypes.POINTER(LayerMetricsC))
     fn("atlas_layer_chunk_stats", ctypes.c_int, c_vp, c_vp, c_vp, c_i64,
@@ -119,7 +120,7 @@ EXPORTED = [
     "atlas_layer_accumulator", "atlas_transform", "atlas_layer_finish",
     "atlas_layer_chunk_stats", "atlas_layer_log", "atlas_layer_state",
     "atlas_layer_timing", "atlas_reorder", "atlas_transform_typed",
-    "atlas_layer_run_gat", "atlas_layer_run_fused",
+    "atlas_layer_run_gat", "atlas_layer_run_fused", "atlas_layer_bind_graph",
 ]
 
 

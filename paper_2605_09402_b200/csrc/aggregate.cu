@@ -264,6 +264,7 @@ struct EpiArgs {
   int n;                   // output columns
   int relu;
   int32_t* flag;           // extremes flag of y for the next layer
+  int64_t vbeg;            // first destination of this launch's slice
 };
 
 template <typename OutT>
@@ -298,6 +299,7 @@ __device__ __forceinline__ void ring_body(
     unsigned long long v0 = 0;
     if (lane == 0) v0 = atomicAdd(work, (unsigned long long)kGrab);
     v0 = __shfl_sync(0xffffffffu, v0, 0);
+    if constexpr (kEpi) v0 += (unsigned long long)epi.vbeg;
     if ((int64_t)v0 >= nloc) break;
     const int64_t v1 = min((int64_t)v0 + kGrab, nloc);
     const int64_t e0 = csc_ptr[v0], e1 = csc_ptr[v1];
@@ -463,7 +465,7 @@ __global__ void __launch_bounds__(256, 4)
   while (true) {
     unsigned long long w0 = 0;
     if (lane == 0) w0 = atomicAdd(work, (unsigned long long)(kGrab * DPW));
-    w0 = __shfl_sync(0xffffffffu, w0, 0);
+    w0 = __shfl_sync(0xffffffffu, w0, 0) + (unsigned long long)epi.vbeg;
     if ((int64_t)w0 >= nloc) break;
     // this sub-group's destinations [v, v_end) and edges [e_beg, e_end)
     int64_t v = min((int64_t)w0 + (int64_t)sub * kGrab, nloc);
@@ -1085,13 +1087,14 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
                              int d, const int32_t* input_flag, void* y,
                              int y_dtype, int64_t ldy, const float* bias,
                              const float* self_rows, int64_t ld_self, int n,
-                             int relu, int32_t* out_flag, cudaStream_t s) {
-  if (g->nloc == 0) return;
+                             int relu, int32_t* out_flag, int64_t v_begin,
+                             int64_t v_end, cudaStream_t s) {
+  if (v_end <= v_begin) return;
   if (d > 128 || d % 4 != 0 || ldz % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(z) & 15) != 0)
     fail(ATLAS_ECONFIG, "transform-first aggregation needs <= 128 f32 "
                         "columns in 16-byte rows");
-  EpiArgs epi{y, ldy, bias, self_rows, ld_self, n, relu, out_flag};
+  EpiArgs epi{y, ldy, bias, self_rows, ld_self, n, relu, out_flag, v_begin};
   const float e1 = self_scale_of(gin_epsilon);
   if (d <= 64) {  // narrow rows: several destinations per warp
     g->work.reserve(1);
@@ -1108,7 +1111,7 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
             &per_sm, kern, 256, smem));
         kern<<<kNumSMs * std::max(1, per_sm), 256, smem, s>>>(
             z, ldz, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
-            g->nloc, d, e1, epi, g->work.ptr);
+            v_end, d, e1, epi, g->work.ptr);
       };
       if (y_dtype == ATLAS_F32) go(agg_tf_ring<LPD, M, float>);
       else if (y_dtype == ATLAS_F16) go(agg_tf_ring<LPD, M, __half>);
@@ -1143,7 +1146,7 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
     ATLAS_CUDA(cudaFuncSetAttribute(
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<148 * 3, 256, smem, s>>>(z, ldz, g->csc_ptr.ptr, g->csc_src.ptr,
-                                    g->indeg.ptr, g->lo, g->nloc, d, e1, flag,
+                                    g->indeg.ptr, g->lo, v_end, d, e1, flag,
                                     g->work.ptr, epi);
   };
   auto by_out = [&](auto model_tag) {

@@ -40,6 +40,7 @@ static void load_graph(atlas_graph* g, int64_t V, int64_t E,
                        const int64_t* offsets_host,
                        const uint32_t* neighbors_host,
                        const uint32_t* in_degrees_host, cudaStream_t s) {
+  verify_graph(g);  // a pending check of the previous contents
   g->maxpass_cache.clear();
   g->V = V;
   g->E = E;
@@ -86,6 +87,23 @@ static void launch_control(atlas_layer* L, const atlas_graph* g,
   ATLAS_CUDA(cudaEventRecord(L->tev[3], L->ctl_stream));
 }
 
+// side copy stream and its events (created once per layer)
+static void ensure_copy_stream(atlas_layer* L) {
+  if (L->copy_stream) return;
+  ATLAS_CUDA(cudaStreamCreateWithFlags(&L->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; i++) {
+    ATLAS_CUDA(cudaEventCreateWithFlags(&L->ev_ready[i],
+                                        cudaEventDisableTiming));
+    ATLAS_CUDA(cudaEventCreateWithFlags(&L->ev_free[i],
+                                        cudaEventDisableTiming));
+  }
+}
+
+static void ensure_tile_events(atlas_layer* L) {
+  for (auto& e : L->tile_ev)
+    if (!e) ATLAS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
 // the layer's f32 aggregation records (nloc x agg_dim), allocated lazily
 static void ensure_records(atlas_layer* L) {
   const size_t want = (size_t)std::max<int64_t>(L->nloc, 1) * L->desc.agg_dim;
@@ -121,6 +139,7 @@ int atlas_graph_create(int32_t device, int64_t V, int64_t E,
       g->hi = hi;
       g->nloc = hi - lo;
       load_graph(g, V, E, offsets_host, neighbors_host, in_degrees_host, s);
+      verify_graph(g);  // creation reports a bad graph immediately
     } catch (...) {
       delete g;
       throw;
@@ -215,6 +234,32 @@ int atlas_layer_reset(atlas_layer* L, void* stream) {
     use_device(L->desc.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     settle(L);
+    const int64_t nn = std::max<int64_t>(L->nloc, 1);
+    ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
+    L->chunk_reloads.clear();
+    L->chunk_touched.clear();
+    L->fast_path = false;
+    L->chunks_seen = 0;
+    L->stream_step = 0;
+    L->timing_ms[0] = L->timing_ms[1] = 0.f;
+    engine_init(L, s);
+  });
+}
+
+int atlas_layer_bind_graph(atlas_layer* L, const atlas_graph* g,
+                           void* stream) {
+  return guarded([&] {
+    if (!L || !g) fail(ATLAS_ECONFIG, "null argument");
+    const atlas_layer_desc& D = L->desc;
+    if (g->V != D.num_vertices || g->lo != D.dst_lo || g->hi != D.dst_hi)
+      fail(ATLAS_ECONFIG, "graph and layer disagree on the vertex range");
+    use_device(D.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    settle(L);
+    if (L->nloc > 0)
+      ATLAS_CUDA(cudaMemcpyAsync(L->indeg.ptr, g->indeg.ptr,
+                                 L->nloc * sizeof(uint32_t),
+                                 cudaMemcpyDeviceToDevice, s));
     const int64_t nn = std::max<int64_t>(L->nloc, 1);
     ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
     L->chunk_reloads.clear();
@@ -342,7 +387,8 @@ int atlas_layer_run_fused(atlas_layer* L, const atlas_graph* g,
                           const int32_t* input_flag, const float* bias,
                           const float* self_rows, int64_t ld_self, int64_t n,
                           int32_t relu, void* y, int32_t y_dtype, int64_t ldy,
-                          int32_t* out_flag, void* stream) {
+                          int32_t* out_flag, void* y_host, int64_t ldy_host,
+                          int32_t host_slices, void* stream) {
   return guarded([&] {
     if (!L || !g || !z || !bias || !y) fail(ATLAS_ECONFIG, "null argument");
     if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
@@ -362,9 +408,38 @@ int atlas_layer_run_fused(atlas_layer* L, const atlas_graph* g,
     settle(L);
     launch_control(L, g, chunk_rows, s);
     if (out_flag) ATLAS_CUDA(cudaMemsetAsync(out_flag, 0, sizeof(int32_t), s));
-    launch_agg_resident_epi(g, z, ldz, data_model, D.gin_epsilon, (int)d,
-                            input_flag, y, y_dtype, ldy, bias, self_rows,
-                            ld_self, (int)n, relu, out_flag, s);
+    if (!y_host) {
+      launch_agg_resident_epi(g, z, ldz, data_model, D.gin_epsilon, (int)d,
+                              input_flag, y, y_dtype, ldy, bias, self_rows,
+                              ld_self, (int)n, relu, out_flag, 0, L->nloc, s);
+    } else {
+      // the output goes to the host slice by slice: the D2H of slice i
+      // (copy stream) overlaps the aggregation of slice i+1 (stream s)
+      if (ldy_host < n) fail(ATLAS_ECONFIG, "host output too narrow");
+      ensure_copy_stream(L);
+      const size_t es = y_dtype == ATLAS_F32 ? 4 : 2;
+      const int64_t k = std::max<int32_t>(1, host_slices);
+      const int64_t step = ceil_div(std::max<int64_t>(L->nloc, 1), k);
+      for (int64_t a = 0; a < L->nloc; a += step) {
+        const int64_t b = std::min(L->nloc, a + step);
+        launch_agg_resident_epi(g, z, ldz, data_model, D.gin_epsilon, (int)d,
+                                input_flag, y, y_dtype, ldy, bias, self_rows,
+                                ld_self, (int)n, relu, out_flag, a, b, s);
+        ATLAS_CUDA(cudaEventRecord(L->ev_ready[0], s));
+        ATLAS_CUDA(cudaStreamWaitEvent(L->copy_stream, L->ev_ready[0], 0));
+        uint8_t* dst = static_cast<uint8_t*>(y_host) + a * ldy_host * es;
+        const uint8_t* src = static_cast<const uint8_t*>(y) + a * ldy * es;
+        if (ldy == n && ldy_host == n)  // dense rows: one linear DMA
+          ATLAS_CUDA(cudaMemcpyAsync(dst, src, (b - a) * n * es,
+                                     cudaMemcpyDeviceToHost, L->copy_stream));
+        else
+          ATLAS_CUDA(cudaMemcpy2DAsync(dst, ldy_host * es, src, ldy * es,
+                                       n * es, b - a, cudaMemcpyDeviceToHost,
+                                       L->copy_stream));
+      }
+      ATLAS_CUDA(cudaEventRecord(L->ev_ready[1], L->copy_stream));
+      ATLAS_CUDA(cudaStreamWaitEvent(s, L->ev_ready[1], 0));
+    }
     ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
     ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
     L->timing_pending = true;
@@ -391,16 +466,7 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
     const int64_t V = D.num_vertices;
     tile_rows = std::min<int64_t>(tile_rows, std::max<int64_t>(V, 1));
     for (auto& b : L->stream_tile) b.reserve(tile_rows * ldx * item);
-    if (!L->copy_stream) {
-      ATLAS_CUDA(cudaStreamCreateWithFlags(&L->copy_stream,
-                                           cudaStreamNonBlocking));
-      for (int i = 0; i < 2; i++) {
-        ATLAS_CUDA(cudaEventCreateWithFlags(&L->ev_ready[i],
-                                            cudaEventDisableTiming));
-        ATLAS_CUDA(cudaEventCreateWithFlags(&L->ev_free[i],
-                                            cudaEventDisableTiming));
-      }
-    }
+    ensure_copy_stream(L);
     const int64_t nn = std::max<int64_t>(L->nloc, 1);
     L->cursor.reserve(nn);
     if (L->nloc > 0)
@@ -409,26 +475,59 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
                                  cudaMemcpyDeviceToDevice, s));
     ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
     settle(L);
-    launch_control(L, g, chunk_rows, s);  // records tev[0] after the resets
-    // the copy stream may only start once s has the cursor/touched resets
-    ATLAS_CUDA(cudaStreamWaitEvent(L->copy_stream, L->tev[0], 0));
+    // the copy stream starts at once (it overlaps whatever s is still
+    // doing, e.g. a topology refresh); a tile buffer is only refilled after
+    // the kernel that last read it, in this pass or the previous one. The
+    // first two tiles are queued before the control plane, whose launch
+    // may wait on the host for a refreshed graph's chunk statistics.
     const int64_t ntiles = ceil_div(V, tile_rows);
+    // an input of up to 8 GB lands whole in HBM (tile t at its own rows),
+    // so the copy stream never waits for a buffer; larger inputs cycle
+    // through two tile buffers
+    const size_t row_b = (size_t)ldx * item;
+    const bool whole = (size_t)V * row_b <= (size_t(8) << 30);
+    if (whole) L->stream_tile[0].reserve((size_t)V * row_b);
+    auto tile_ptr = [&](int64_t t) -> uint8_t* {
+      return whole ? L->stream_tile[0].ptr + (size_t)(t * tile_rows) * row_b
+                   : L->stream_tile[t & 1].ptr;
+    };
+    auto copy_tile = [&](int64_t t) {
+      const int b = (int)(t & 1);
+      const int64_t r0 = t * tile_rows, r1 = std::min(V, r0 + tile_rows);
+      if (whole ? (t == 0 && L->tile_used[0]) : (t >= 2 || L->tile_used[b]))
+        ATLAS_CUDA(cudaStreamWaitEvent(L->copy_stream,
+                                       L->ev_free[whole ? 0 : b], 0));
+      // whole rows (pitch included) are one contiguous block: a single DMA
+      ATLAS_CUDA(cudaMemcpyAsync(
+          tile_ptr(t), static_cast<const uint8_t*>(x_host) + r0 * row_b,
+          (r1 - r0) * row_b, cudaMemcpyHostToDevice, L->copy_stream));
+      ATLAS_CUDA(cudaEventRecord(whole ? L->tile_ev[t % kTileEvents]
+                                       : L->ev_ready[b],
+                                 L->copy_stream));
+    };
+    if (whole) ensure_tile_events(L);
+    const int64_t ahead = whole ? std::min<int64_t>(kTileEvents, ntiles)
+                                : std::min<int64_t>(2, ntiles);
+    for (int64_t t = 0; t < ahead; t++) copy_tile(t);
+    launch_control(L, g, chunk_rows, s);  // records tev[0] after the resets
     for (int64_t t = 0; t < ntiles; t++) {
       const int b = (int)(t & 1);
       const int64_t r0 = t * tile_rows, r1 = std::min(V, r0 + tile_rows);
-      if (t >= 2) ATLAS_CUDA(cudaStreamWaitEvent(L->copy_stream, L->ev_free[b], 0));
-      // whole rows (pitch included) are one contiguous block: a single DMA
-      ATLAS_CUDA(cudaMemcpyAsync(
-          L->stream_tile[b].ptr,
-          static_cast<const uint8_t*>(x_host) + r0 * ldx * item,
-          (r1 - r0) * ldx * item, cudaMemcpyHostToDevice, L->copy_stream));
-      ATLAS_CUDA(cudaEventRecord(L->ev_ready[b], L->copy_stream));
-      ATLAS_CUDA(cudaStreamWaitEvent(s, L->ev_ready[b], 0));
+      if (t >= ahead) copy_tile(t);
+      ATLAS_CUDA(cudaStreamWaitEvent(
+          s, whole ? L->tile_ev[t % kTileEvents] : L->ev_ready[b], 0));
       if (L->nloc > 0)
-        launch_agg_tile(L->stream_tile[b].ptr, dtype, ldx, r0, r1, g, D.model,
+        launch_agg_tile(tile_ptr(t), dtype, ldx, r0, r1, g, D.model,
                         D.gin_epsilon, (int)D.embed_dim, L->acc.ptr,
                         D.agg_dim, L->cursor.ptr, L->touched.ptr, s);
-      ATLAS_CUDA(cudaEventRecord(L->ev_free[b], s));
+      if (!whole) {
+        ATLAS_CUDA(cudaEventRecord(L->ev_free[b], s));
+        L->tile_used[b] = true;
+      }
+    }
+    if (whole) {
+      ATLAS_CUDA(cudaEventRecord(L->ev_free[0], s));
+      L->tile_used[0] = true;
     }
     ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
     ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
@@ -522,6 +621,7 @@ int atlas_layer_finish(atlas_layer* L, atlas_layer_metrics* m) {
     use_device(L->desc.device);
     cudaStream_t s = nullptr;
     settle(L);
+    verify_graph(L->ctl_graph);
     ATLAS_CUDA(cudaDeviceSynchronize());
     std::memset(m, 0, sizeof(*m));
     finish_spans(L, s);

@@ -44,6 +44,7 @@ struct Error {
 
 constexpr int kWarp = 32;
 constexpr int kNumSMs = 148;
+constexpr int kTileEvents = 64;  // tiles a streamed pass queues ahead
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -232,12 +232,13 @@ __global__ void fill_u64(uint64_t* p, int64_t n, uint64_t val) {
 
 __global__ void span_values(const int64_t* first, const int64_t* last,
                             int64_t n, int64_t* spans,
-                            unsigned long long* sum_count) {
+                            unsigned long long* sum_count,
+                            int64_t sentinel = INT64_MAX) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t my_sum = 0, my_cnt = 0;
   for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const bool got = first[i] >= 0;
-    spans[i] = got ? last[i] - first[i] : INT64_MAX;
+    spans[i] = got ? last[i] - first[i] : sentinel;
     if (got) {
       my_sum += last[i] - first[i];
       my_cnt++;
@@ -267,9 +268,82 @@ unsigned grid_of(int64_t n, int block = 256) {
 
 // spans -> exact integer sum, count and the two order statistics that
 // np.percentile(spans, 99) interpolates between.
+// sum, count and the two order statistics np.percentile(spans, 99)
+// interpolates between (numpy 'linear': virtual index (count - 1) * 0.99)
+__global__ void span_pick(const unsigned long long* sum_count,
+                          const int64_t* sorted, int64_t* out) {
+  const int64_t cnt = (int64_t)sum_count[1];
+  out[0] = (int64_t)sum_count[0];
+  out[1] = cnt;
+  out[2] = out[3] = 0;
+  if (cnt > 0) {
+    const double vi = (double)(cnt - 1) * 0.99;
+    const int64_t lo_i = (int64_t)floor(vi);
+    const int64_t hi_i = min(lo_i + 1, cnt - 1);
+    out[2] = sorted[lo_i];
+    out[3] = sorted[hi_i];
+  }
+}
+
+// Whole-layer passes: the spans' reductions are queued on the control
+// stream right behind the walk that produced first/last positions, so
+// finalize_layer only reads four pinned integers.
+void queue_spans(atlas_layer* L, const atlas_graph* g, cudaStream_t s) {
+  const int64_t n = L->nloc;
+  L->span_pin.reserve(4);
+  L->span_dev.reserve(4);
+  if (!L->span_ev)
+    ATLAS_CUDA(cudaEventCreateWithFlags(&L->span_ev, cudaEventDisableTiming));
+  if (n == 0) {
+    ATLAS_CUDA(cudaMemsetAsync(L->span_dev.ptr, 0, 4 * sizeof(int64_t), s));
+  } else {
+    // spans are < E + V + 1 stream positions; the sentinel of vertices
+    // without a step sorts last within the same bit width
+    int bits = 1;
+    while (bits < 62 && (int64_t(1) << bits) <= g->E + g->V + 2) bits++;
+    bits++;
+    const int64_t sentinel = (int64_t(1) << bits) - 1;
+    DevBuf<int64_t>& spans = L->span_buf;
+    DevBuf<int64_t>& sorted = L->span_sorted;
+    DevBuf<unsigned long long>& sc = L->span_acc;
+    spans.reserve(n);
+    sorted.reserve(n);
+    sc.reserve(2);
+    ATLAS_CUDA(cudaMemsetAsync(sc.ptr, 0, 2 * sizeof(unsigned long long), s));
+    span_values<<<grid_of(n), 256, 0, s>>>(L->first_pos.ptr, L->last_pos.ptr,
+                                           n, spans.ptr, sc.ptr, sentinel);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+    size_t tmp_bytes = 0;
+    ATLAS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, spans.ptr,
+                                              sorted.ptr, n, 0, bits, s));
+    DevBuf<uint8_t>& tmp = L->span_tmp;
+    tmp.reserve(tmp_bytes);
+    ATLAS_CUDA(cub::DeviceRadixSort::SortKeys(tmp.ptr, tmp_bytes, spans.ptr,
+                                              sorted.ptr, n, 0, bits, s));
+    count_launch();
+    span_pick<<<1, 1, 0, s>>>(sc.ptr, sorted.ptr, L->span_dev.ptr);
+    count_launch();
+    ATLAS_LAUNCH_CHECK();
+  }
+  ATLAS_CUDA(cudaMemcpyAsync(L->span_pin.ptr, L->span_dev.ptr,
+                             4 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  ATLAS_CUDA(cudaEventRecord(L->span_ev, s));
+  L->spans_queued = true;
+}
+
 void finish_spans(atlas_layer* L, cudaStream_t s) {
   const int64_t n = L->nloc;
   L->span_count = L->span_sum = L->span_q_lo = L->span_q_hi = 0;
+  if (L->spans_queued) {
+    L->spans_queued = false;
+    ATLAS_CUDA(cudaEventSynchronize(L->span_ev));
+    L->span_sum = L->span_pin.ptr[0];
+    L->span_count = L->span_pin.ptr[1];
+    L->span_q_lo = L->span_pin.ptr[2];
+    L->span_q_hi = L->span_pin.ptr[3];
+    return;
+  }
   if (n == 0) return;
   DevBuf<int64_t>& spans = L->span_buf;
   DevBuf<int64_t>& sorted = L->span_sorted;
@@ -491,6 +565,7 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
     ATLAS_CUDA(cudaMemcpyAsync(h.data(), hist.ptr, h.size() * sizeof(h[0]),
                                cudaMemcpyDeviceToHost, s));
     ATLAS_CUDA(cudaStreamSynchronize(s));
+    queue_spans(L, g, s);
     if (!fast_verdict(L, g, R, h.data())) exact_replay(L, g, R, s);
     return;
   }
@@ -504,6 +579,7 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
   ATLAS_CUDA(cudaMemcpyAsync(L->pin_hist.ptr, hist.ptr,
                              7 * nchunks * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
+  queue_spans(L, g, s);
   L->ctl_deferred = true;
   L->ctl_graph = g;
   L->ctl_R = R;

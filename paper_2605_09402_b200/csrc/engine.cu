@@ -587,6 +587,7 @@ int64_t phys_slots_of(const atlas_layer* L) {
 }
 
 void engine_init(atlas_layer* L, cudaStream_t s) {
+  L->spans_queued = false;
   const int64_t n = L->nloc;
   const int64_t phys = phys_slots_of(L);
   const int64_t nn = n > 0 ? n : 1;

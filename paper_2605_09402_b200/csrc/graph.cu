@@ -166,14 +166,28 @@ void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs,
                                              g->csc_ptr.ptr + 1, g->nloc, s));
     count_launch();
   }
-  int64_t total = 0;
-  ATLAS_CUDA(cudaMemcpyAsync(&total, g->csc_ptr.ptr + g->nloc,
+  // the consistency total is read back without stalling the host: the
+  // next layer can be queued (and its input copies start) right away
+  g->chk.reserve(1);
+  if (!g->chk_ev)
+    ATLAS_CUDA(cudaEventCreateWithFlags(&g->chk_ev, cudaEventDisableTiming));
+  ATLAS_CUDA(cudaMemcpyAsync(g->chk.ptr, g->csc_ptr.ptr + g->nloc,
                              sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  ATLAS_CUDA(cudaStreamSynchronize(s));
-  if (total != n)
+  ATLAS_CUDA(cudaEventRecord(g->chk_ev, s));
+  g->chk_pending = true;
+  g->chk_expect = n;
+}
+
+void verify_graph(const atlas_graph* g) {
+  if (!g || !g->chk_pending) return;
+  ATLAS_CUDA(cudaEventSynchronize(g->chk_ev));
+  g->chk_pending = false;
+  const int64_t total = g->chk.ptr[0];
+  if (total != g->chk_expect)
     fail(ATLAS_EINVARIANT, "in-degrees disagree with adjacency (" +
                                std::to_string(total) + " vs " +
-                               std::to_string(n) + " in-range edges)");
+                               std::to_string(g->chk_expect) +
+                               " in-range edges)");
 }
 
 }  // namespace atlas

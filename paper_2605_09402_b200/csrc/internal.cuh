@@ -28,6 +28,15 @@ struct atlas_graph {
       ws_sel;
   atlas::DevBuf<int64_t> ws_nsel;
   atlas::DevBuf<uint8_t> ws_tmp;
+  // deferred consistency check of the last CSC build (in-degrees vs
+  // adjacency): the device total lands in chk, verified by verify_graph
+  mutable atlas::PinnedBuf<int64_t> chk;
+  mutable cudaEvent_t chk_ev = nullptr;
+  mutable bool chk_pending = false;
+  int64_t chk_expect = 0;
+  ~atlas_graph() {
+    if (chk_ev) cudaEventDestroy(chk_ev);
+  }
 };
 
 namespace atlas {
@@ -146,17 +155,28 @@ struct atlas_layer {
   atlas::DevBuf<int64_t> span_buf, span_sorted;
   atlas::DevBuf<unsigned long long> span_acc;
   atlas::DevBuf<uint8_t> span_tmp;
+  // spans reduced on the control stream (whole-layer passes)
+  atlas::DevBuf<int64_t> span_dev;
+  atlas::PinnedBuf<int64_t> span_pin;
+  cudaEvent_t span_ev = nullptr;
+  bool spans_queued = false;
   // chunk streamer (host -> HBM double buffer)
   atlas::DevBuf<uint8_t> stream_tile[2];
   atlas::DevBuf<int64_t> cursor;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_ready[2] = {nullptr, nullptr};
   cudaEvent_t ev_free[2] = {nullptr, nullptr};
+  bool tile_used[2] = {false, false};  // ev_free[b] was recorded
+  // whole-input streaming: one ready event per in-flight tile
+  cudaEvent_t tile_ev[atlas::kTileEvents] = {};
   ~atlas_layer() {
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ctl_stream) cudaStreamDestroy(ctl_stream);
     for (auto& e : tev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : tile_ev)
+      if (e) cudaEventDestroy(e);
+    if (span_ev) cudaEventDestroy(span_ev);
     for (int i = 0; i < 2; i++) {
       if (ev_ready[i]) cudaEventDestroy(ev_ready[i]);
       if (ev_free[i]) cudaEventDestroy(ev_free[i]);
@@ -169,6 +189,8 @@ namespace atlas {
 // graph.cu
 void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs_dev,
                const uint32_t* indeg_host, cudaStream_t s);
+// raise the deferred in-degree/adjacency mismatch of the last build, if any
+void verify_graph(const atlas_graph* g);
 
 // aggregate.cu
 void launch_agg_resident(const atlas_graph* g, const void* x, int dtype,
@@ -180,7 +202,8 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
                              int d, const int32_t* input_flag, void* y,
                              int y_dtype, int64_t ldy, const float* bias,
                              const float* self_rows, int64_t ld_self, int n,
-                             int relu, int32_t* out_flag, cudaStream_t s);
+                             int relu, int32_t* out_flag, int64_t v_begin,
+                             int64_t v_end, cudaStream_t s);
 void launch_agg_runs(const void* tile, int dtype, int64_t ldx,
                      int64_t tile_lo, const uint32_t* run_dst,
                      const int64_t* run_beg, int64_t nruns,

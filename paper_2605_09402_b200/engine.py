@@ -84,6 +84,7 @@ class DeviceGraph:
         N.check(N.load_library().atlas_graph_csc(self.handle, None, None,
                                                  ctypes.byref(n)))
         self.local_edges = n.value
+        self.version = getattr(self, "version", 0) + 1
 
     def close(self):
         if getattr(self, "handle", None):
@@ -167,6 +168,12 @@ class DeviceLayer:
         N.check(N.load_library().atlas_layer_reset(self.handle,
                                                    N.stream_handle(stream)))
 
+    def bind_graph(self, graph: DeviceGraph, stream=None):
+        """reset() after a topology refresh: in-degrees come from the
+        graph's device copy."""
+        N.check(N.load_library().atlas_layer_bind_graph(
+            self.handle, graph.handle, N.stream_handle(stream)))
+
     # -- operator path ------------------------------------------------------
     def submit_chunk(self, start, end, rows, local_offsets, neighbors,
                      stream=None):
@@ -234,10 +241,13 @@ class DeviceLayer:
 
     def run_fused(self, graph: DeviceGraph, z, d: int, chunk_rows: int,
                   bias, y, *, data_model: int, relu: bool, self_col=None,
-                  input_flag=None, out_flag=None, stream=None):
+                  input_flag=None, out_flag=None, host_out=None,
+                  host_slices: int = 8, stream=None):
         """Transform-first pass (atlas_layer_run_fused): aggregate the first
         d columns of z (V x ldz f32, = h . W_z^T) with ``data_model``'s
-        rule and write y = act(agg + z[:, self_col:] + b) for the range."""
+        rule and write y = act(agg + z[:, self_col:] + b) for the range.
+        ``host_out`` (pinned CPU tensor like y) also receives y, slice by
+        slice, each D2H overlapping the next slice's aggregation."""
         if z.shape[0] != self.num_vertices or z.dtype.itemsize != 4:
             raise ConfigError(f"z {tuple(z.shape)} does not cover the graph")
         self_ptr = 0 if self_col is None else z.data_ptr() + 4 * self_col
@@ -246,7 +256,8 @@ class DeviceLayer:
             int(data_model), int(d), int(chunk_rows), N.ptr(input_flag),
             bias.data_ptr(), self_ptr, z.stride(0), y.shape[1], int(relu),
             y.data_ptr(), torch_dtype_code(y), y.stride(0), N.ptr(out_flag),
-            N.stream_handle(stream)))
+            N.ptr(host_out), 0 if host_out is None else host_out.stride(0),
+            int(host_slices), N.stream_handle(stream)))
 
     def run_streamed(self, graph: DeviceGraph, x_host, chunk_rows: int,
                      tile_bytes: int = 256 << 20, stream=None):

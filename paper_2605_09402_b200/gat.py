@@ -278,8 +278,13 @@ class GATEngine:
         from . import _native as N
 
         layer = self._layers.get(l)
+        gv = getattr(self.graph, "version", 0)
         if layer is not None and layer.handle:
-            layer.reset()
+            if layer.graph_version == gv:
+                layer.reset()
+            else:
+                layer.bind_graph(self.graph)
+                layer.graph_version = gv
             return layer
         cfg = self.config
         hf = lay.heads * lay.head_dim
@@ -293,8 +298,16 @@ class GATEngine:
                             dst_range=(self.lo, self.hi),
                             record_log=cfg.record_log,
                             force_exact=cfg.force_exact, device=self.device)
+        layer.graph_version = 0
+        if gv:
+            layer.bind_graph(self.graph)
+            layer.graph_version = gv
         self._layers[l] = layer
         return layer
+
+    def update_graph(self, offsets, neighbors, in_degrees):
+        """Topology refresh (see runtime.Engine.update_graph)."""
+        self.graph.update(offsets, neighbors, in_degrees)
 
     def gather(self, z_local):
         if self.world == 1:
@@ -352,9 +365,10 @@ class GATEngine:
             return y, collect, layer
         return y, collect(), layer
 
-    def infer(self, x, keep_layers: bool = False):
-        """All layers; x is the full (V, in) feature matrix on the device.
-        Returns (final local output, [LayerMetrics])."""
+    def infer(self, x, keep_layers: bool = False, host_out=None):
+        """All layers; x is the full (V, in) feature matrix (device, or
+        pinned host). Returns (final local output, [LayerMetrics]);
+        ``host_out`` (pinned) also receives the final output."""
         import torch
 
         pending, outs = [], []
@@ -370,6 +384,8 @@ class GATEngine:
             if keep_layers:
                 outs.append(y)
             h = y
+        if host_out is not None:
+            host_out.copy_(y, non_blocking=True)
         metrics = [collect() for collect in pending]
         self.last_layers = outs
         return y, metrics

@@ -204,7 +204,7 @@ class Engine:
         return out
 
     def layer(self, l: int, x, *, chunk_budget=None, input_flag=None,
-              defer_metrics: bool = False):
+              defer_metrics: bool = False, host_out=None):
         """One layer: x (V, d) CUDA tensor (or pinned host tensor, streamed)
         -> (y (V or range, out), metrics, device layer handle).
         ``input_flag``: extremes flag of the transform that produced x; the
@@ -225,8 +225,11 @@ class Engine:
         rows = plan_rows(self.num_vertices, d, _plan_dtype(x),
                          chunk_budget or cfg.chunk_budget)
         layer = self._layers.get(l)
+        gv = getattr(self.graph, "version", 0)
         if layer is not None and layer.handle:
-            layer.reset()  # same descriptor: reuse the device workspaces
+            # same descriptor: reuse the device workspaces
+            if layer.graph_version == gv:
+                layer.reset()
         else:
             budget = slot_budget(w, l, cfg.hot_budget, cfg.hot_slots)
             layer = DeviceLayer(
@@ -237,13 +240,18 @@ class Engine:
                 record_log=cfg.record_log, force_exact=cfg.force_exact,
                 device=self.device)
             self._layers[l] = layer
+            layer.graph_version = 0  # built from the initial host degrees
+        if layer.graph_version != gv:
+            # topology refreshed since: in-degrees from the device graph
+            layer.bind_graph(self.graph)
+            layer.graph_version = gv
         nloc = self.hi - self.lo
         out_dim = w.layers[l].out_dim
         y = torch.empty((nloc, out_dim), dtype=_torch_dtype(cfg.embed_dtype),
                         device="cuda")
         if self.transform_first(l):
             return self._layer_transform_first(l, x, layer, rows, y, last,
-                                               t0, defer_metrics)
+                                               t0, defer_metrics, host_out)
         if x.is_cuda:
             layer.run_resident(self.graph, x, rows, input_flag=input_flag)
         else:  # host (pinned) input: stream it in tiles (K1 streamer)
@@ -269,6 +277,8 @@ class Engine:
                     agg, w.layers[l], apply_activation=not last,
                     backend=self.backend)))
         ev1.record()
+        if host_out is not None:
+            host_out.copy_(y, non_blocking=True)
 
         def collect():
             m = metrics_from_device(layer, l)
@@ -282,7 +292,7 @@ class Engine:
         return y, collect(), layer
 
     def _layer_transform_first(self, l, x, layer, rows, y, last, t0,
-                               defer_metrics):
+                               defer_metrics, host_out=None):
         """z = h . W_z^T on tcgen05 for every source row, then one fused
         pass: control plane on the reference chunk plan + ring aggregation
         of z + bias / SAGE self half / ReLU epilogue (no f32 records)."""
@@ -310,7 +320,7 @@ class Engine:
                         data_model=int(data_model), relu=not last,
                         self_col=npad if self.kind == ModelKind.SAGE else None,
                         input_flag=self.z_flags[l],
-                        out_flag=self.out_flags[l])
+                        out_flag=self.out_flags[l], host_out=host_out)
 
         def collect():
             m = metrics_from_device(layer, l)
@@ -323,21 +333,32 @@ class Engine:
             return y, collect, layer
         return y, collect(), layer
 
+    def update_graph(self, offsets, neighbors, in_degrees):
+        """Refresh the topology (same vertex count and range) without
+        reallocating; cached layers re-read their in-degrees from the
+        device graph on their next pass (atlas_layer_bind_graph)."""
+        self.graph.update(offsets, neighbors, in_degrees)
+
     def gather(self, y_local):
         """All ranks' ranges -> full (V, out) next-layer input (NCCL)."""
         if self.world == 1:
             return y_local
         return gather_ranges(y_local, self.ranges, self.group)
 
-    def infer(self, x, keep_layers: bool = False):
-        """All layers; returns (final local output, [LayerMetrics])."""
+    def infer(self, x, keep_layers: bool = False, host_out=None):
+        """All layers; returns (final local output, [LayerMetrics]).
+        ``host_out`` (pinned CPU tensor of the output's shape and dtype)
+        receives the final output too; a transform-first last layer copies
+        it out slice by slice while it is still being computed."""
         pending, outs = [], []
         h, flag = x, None
-        for l in range(len(self.weights.layers)):
+        nl = len(self.weights.layers)
+        for l in range(nl):
             # every layer is queued before any metric is read back, so the
             # host never stalls the device between layers
-            y, collect, _ = self.layer(l, h, input_flag=flag,
-                                       defer_metrics=True)
+            y, collect, _ = self.layer(
+                l, h, input_flag=flag, defer_metrics=True,
+                host_out=host_out if l == nl - 1 else None)
             pending.append(collect)
             if keep_layers:
                 outs.append(y)

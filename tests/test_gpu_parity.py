@@ -339,3 +339,47 @@ def test_tcgen05_wide_input_transform_first(kind, transform_first):
     for a, b in zip(runs["tcgen05"][1], runs["stable"][1]):
         for f in METRICS:
             assert getattr(a, f) == getattr(b, f), f
+
+
+def test_topology_refresh_rebinds_layers():
+    """Engine.update_graph with a different graph of the same size: the
+    cached layers take the new in-degrees from the device graph and the
+    result equals a fresh engine's, bit for bit (stable backend)."""
+    from paper_2605_09402_b200.storage import (ModelKind, random_weights,
+                                               synthetic_in_memory)
+    g1, feats = synthetic_in_memory("uniform", 5000, 6, 16, 3)
+    g2, _ = synthetic_in_memory("uniform", 5000, 9, 16, 4)
+    w = random_weights(ModelKind.SAGE, [16, 12, 8], 5)
+    cfg = dict(chunk_budget=32 << 10, hot_slots=300)
+    x = torch.as_tensor(feats).cuda()
+    eng = Engine(g1, w, PipelineConfig(**cfg))
+    eng.infer(x)
+    eng.update_graph(g2.offsets, g2.neighbors, g2.in_degrees)
+    y, m = eng.infer(x)
+    fresh = Engine(g2, w, PipelineConfig(**cfg))
+    y2, m2 = fresh.infer(x)
+    assert torch.equal(y, y2)
+    for a, b in zip(m, m2):
+        for f in METRICS:
+            assert getattr(a, f) == getattr(b, f), f
+    eng.close()
+    fresh.close()
+
+
+@pytest.mark.parametrize("transform_first", [True, False])
+def test_host_output_slices(transform_first):
+    """infer(..., host_out=pinned): the final output reaches the host
+    (sliced D2H behind a transform-first last layer) bit-identical to the
+    device result."""
+    from paper_2605_09402_b200.storage import (ModelKind, random_weights,
+                                               synthetic_in_memory)
+    graph, feats = synthetic_in_memory("uniform", 7001, 5, 32, 9)
+    w = random_weights(ModelKind.GCN, [32, 16, 6], 5)
+    eng = Engine(graph, w, PipelineConfig(backend="tcgen05", hot_slots=7001,
+                                          transform_first=transform_first))
+    assert eng.transform_first(1) == transform_first
+    host = torch.empty((7001, 6), dtype=torch.float32).pin_memory()
+    y, _ = eng.infer(torch.as_tensor(feats).pin_memory(), host_out=host)
+    torch.cuda.synchronize()
+    assert torch.equal(host, y.cpu())
+    eng.close()

@@ -1,4 +1,6 @@
-"""Stage timings of the end-to-end path (diagnostic; not part of bench)."""
+"""Stage timings of the end-to-end path (diagnostic; not part of bench):
+host enqueue time of each stage and device time between the events
+recorded after each stage, for the bench's e2e loop."""
 
 import sys
 import time
@@ -13,15 +15,12 @@ from paper_2605_09402_b200 import storage as S  # noqa: E402
 from paper_2605_09402_b200.runtime import Engine, PipelineConfig  # noqa: E402
 
 
-def t():
-    torch.cuda.synchronize()
-    return time.perf_counter()
-
-
-def main(v=2_400_000, deg=26, dim=100):
+def main(v=2_400_000, deg=26, dim=100, tile_mb=256):
     graph, feats = S.synthetic_in_memory("uniform", v, deg, dim, 7)
     w = S.random_weights(S.ModelKind.GCN, [dim, 128, 128, 47], 5)
-    cfg = PipelineConfig(chunk_budget=8 << 20, hot_slots=v, backend="tcgen05")
+    cfg = PipelineConfig(chunk_budget=8 << 20, hot_slots=v, backend="tcgen05",
+                         stream_tile_bytes=tile_mb << 20)
+    print("tile MB", tile_mb)
     eng = Engine(graph, w, cfg)
     pinned = torch.from_numpy(feats).pin_memory()
     pin_off = torch.from_numpy(graph.offsets).pin_memory()
@@ -29,29 +28,45 @@ def main(v=2_400_000, deg=26, dim=100):
         graph.neighbors.astype(np.uint32).view(np.int32)).pin_memory()
     pin_deg = torch.from_numpy(
         graph.in_degrees.astype(np.uint32).view(np.int32)).pin_memory()
-    xd = pinned.cuda()
-    for it in range(3):
-        a = t()
-        eng.graph.update(pin_off, pin_nb, pin_deg)
-        b = t()
-        y0, m0, _ = eng.layer(0, pinned)
-        c = t()
-        y0r, m0r, _ = eng.layer(0, xd)
-        d = t()
-        x2 = pinned.cuda(non_blocking=True)
-        e = t()
-        y, ms = eng.infer(xd)
-        f = t()
-        out = y.cpu()
-        g = t()
-        print(f"iter {it}: graph_update {1e3*(b-a):.1f} ms | layer0 streamed "
-              f"{1e3*(c-b):.1f} (agg {m0.agg_ms:.1f} ctl {m0.control_ms:.1f}"
-              f" tr {m0.transform_ms:.1f}) | layer0 resident {1e3*(d-c):.1f} "
-              f"(agg {m0r.agg_ms:.1f}) | H2D feats {1e3*(e-d):.1f} | infer "
-              f"{1e3*(f-e):.1f} | D2H {1e3*(g-f):.1f}", flush=True)
-        assert torch.equal(y0.cpu(), y0r.cpu())
+    host_out = torch.empty((v, 47), dtype=torch.float32).pin_memory()
+    names = ["graph", "layer0", "layer1", "layer2", "d2h"]
+    for it in range(4):
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        hs = [time.perf_counter()]
+        evs[0].record()
+        eng.update_graph(pin_off, pin_nb, pin_deg)
+        evs[1].record()
+        hs.append(time.perf_counter())
+        h = pinned
+        pend = []
+        for l in range(3):
+            y, collect, _ = eng.layer(
+                l, h, defer_metrics=True,
+                host_out=host_out if (l == 2 and SLICED) else None)
+            pend.append(collect)
+            evs[2 + l].record()
+            hs.append(time.perf_counter())
+            h = y
+        if not SLICED:
+            host_out.copy_(y, non_blocking=True)
+        evs[5].record()
+        hs.append(time.perf_counter())
+        torch.cuda.synchronize()
+        end = time.perf_counter()
+        ms = [c() for c in pend]
+        dev = [evs[i].elapsed_time(evs[i + 1]) for i in range(5)]
+        host = [1e3 * (hs[i + 1] - hs[i]) for i in range(5)]
+        print(f"iter {it}: total {1e3 * (end - hs[0]):.1f} ms | " + " | ".join(
+            f"{n} host {a:.1f} dev {b:.1f}" for n, a, b in zip(names, host, dev))
+            + " | " + " ".join(f"L{m.layer}: agg {m.agg_ms:.1f} ctl "
+                               f"{m.control_ms:.1f} tr {m.transform_ms:.1f}"
+                               for m in ms), flush=True)
     eng.close()
 
 
 if __name__ == "__main__":
-    main()
+    for SLICED in (False, True):
+        print("sliced D2H", SLICED)
+        for mb in (sys.argv[1:] or ["256"]):
+            main(tile_mb=int(mb))
