@@ -263,6 +263,10 @@ def main():
     ap.add_argument("--backend", default="tcgen05")
     ap.add_argument("--workload", default="cfg2",
                     choices=["cfg2"] + sorted(EXTRA))
+    ap.add_argument("--embed-dtype", default="f32",
+                    choices=["f32", "f16", "bf16"],
+                    help="storage type of intermediate embeddings (GAT: "
+                         "of z); f32 keeps the reference's f32 semantics")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true",
@@ -290,7 +294,8 @@ def main():
         x = torch.from_numpy(feats).cuda()
         workload, dtype = WORKLOAD, "f32"
         cfg = PipelineConfig(chunk_budget=CHUNK_BUDGET, hot_slots=V,
-                             backend=args.backend, device=local)
+                             backend=args.backend, device=local,
+                             embed_dtype=args.embed_dtype)
     else:
         kind, dims = EXTRA[args.workload]
         graph, x, weights = build_igb(kind, dims)
@@ -300,9 +305,11 @@ def main():
                     f"degree {IGB_DEG}, device Philox seed {SEED}), "
                     f"{IGB_DIM}-d f16 features, 8 MiB reference chunk plan, "
                     f"hot_slots=V")
-        dtype = "f16 in / f32 accumulate"
+        dtype = (f"f16 in / f32 accumulate / {args.embed_dtype} "
+                 f"intermediate embeddings")
         cfg = PipelineConfig(chunk_budget=CHUNK_BUDGET, hot_slots=IGB_V,
-                             backend=args.backend, device=local)
+                             backend=args.backend, device=local,
+                             embed_dtype=args.embed_dtype)
     gen_s = time.perf_counter() - t_gen
     is_gat = args.workload.endswith("-gat")
     if is_gat:

@@ -246,6 +246,20 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
+// same, with a precomputed shared-space destination address
+__device__ __forceinline__ void cp_async16_s(uint32_t smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds16(uint32_t smem) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem)
+               : "memory");
+  return v;
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -295,6 +309,13 @@ __device__ __forceinline__ void ring_body(
   const int lane = threadIdx.x & 31;
   const int col = lane * VEC;
   const bool active = col < d;
+  // lanes past the row's end copy (and ignore) the last chunk instead of
+  // branching around the copy, so the hot loop has no divergence
+  const int colc = active ? col : d - VEC;
+  // this lane's column of the ring as a shared-space address; slot k is
+  // 32 lanes x 16 B, so it starts kRing-periodically at k * 512 B
+  const uint32_t ring_lane =
+      (uint32_t)__cvta_generic_to_shared(ring) + (uint32_t)lane * 16u;
   while (true) {
     unsigned long long v0 = 0;
     if (lane == 0) v0 = atomicAdd(work, (unsigned long long)kGrab);
@@ -303,19 +324,20 @@ __device__ __forceinline__ void ring_body(
     if ((int64_t)v0 >= nloc) break;
     const int64_t v1 = min((int64_t)v0 + kGrab, nloc);
     const int64_t e0 = csc_ptr[v0], e1 = csc_ptr[v1];
-    // issue side: edges [pe, e1) not yet requested; src ids 32 at a time
-    int64_t pe = e0, ibase = e0;
-    uint32_t isrc = (e0 + lane < e1) ? csc_src[e0 + lane] : 0u;
+    // edges of the grab, relative to e0 (a grab holds < 2^31 edges)
+    const int ne = (int)(e1 - e0);
+    const uint32_t* __restrict__ src0 = csc_src + e0;
+    const T* __restrict__ xc = x + colc;
+    // issue side: edges [pe, ne) not yet requested; src ids 32 at a time
+    int pe = 0;
+    uint32_t isrc = lane < ne ? src0[lane] : 0u;
     auto issue = [&]() {
-      if (pe < e1) {
-        if (pe - ibase == 32) {
-          ibase = pe;
-          isrc = (pe + lane < e1) ? csc_src[pe + lane] : 0u;
-        }
-        const uint32_t s = __shfl_sync(0xffffffffu, isrc, (int)(pe - ibase));
-        if (active)
-          cp_async16(&ring[(pe % kRing) * 32 + lane],
-                     x + (int64_t)s * ldx + col);
+      if (pe < ne) {
+        if ((pe & 31) == 0 && pe != 0)
+          isrc = pe + lane < ne ? src0[pe + lane] : 0u;
+        const uint32_t s = __shfl_sync(0xffffffffu, isrc, pe & 31);
+        cp_async16_s(ring_lane + ((uint32_t)(pe & (kRing - 1)) << 9),
+                     xc + (int64_t)s * ldx);
         pe++;
       }
       cp_async_commit();  // empty groups keep the wait count uniform
@@ -323,10 +345,10 @@ __device__ __forceinline__ void ring_body(
 #pragma unroll 1
     for (int k = 0; k < kRing; k++) issue();
     // consume side (GIN needs the source id to place its self term)
-    int64_t ce = e0, cbase = e0;
-    uint32_t csrc = isrc;
+    int ce = 0;
+    uint32_t csrc = lane < ne ? src0[lane] : 0u;
     for (int64_t v = (int64_t)v0; v < v1; v++) {
-      const int64_t dend = csc_ptr[v + 1];
+      const int dend = (int)(csc_ptr[v + 1] - e0);
       const uint32_t vg = (uint32_t)(v + lo);
       const float denom = kMean ? (float)max(1u, indeg[v]) : 1.0f;
       const float rcp = kMean ? __frcp_rn(denom) : 1.0f;
@@ -336,11 +358,9 @@ __device__ __forceinline__ void ring_body(
       bool self_pending = MODEL == ATLAS_GIN;
       for (; ce < dend; ce++) {
         if (MODEL == ATLAS_GIN) {
-          if (ce - cbase == 32) {
-            cbase = ce;
-            csrc = (ce + lane < e1) ? csc_src[ce + lane] : 0u;
-          }
-          const uint32_t s = __shfl_sync(0xffffffffu, csrc, (int)(ce - cbase));
+          if ((ce & 31) == 0 && ce != 0)
+            csrc = ce + lane < ne ? src0[ce + lane] : 0u;
+          const uint32_t s = __shfl_sync(0xffffffffu, csrc, ce & 31);
           if (self_pending && s >= vg) {
             self_pending = false;
             if (active) {
@@ -351,12 +371,9 @@ __device__ __forceinline__ void ring_body(
           }
         }
         cp_async_wait<kRing - 1>();  // this lane's copy of edge ce landed
-        if (active) {
-          F f;
-          f.raw = *reinterpret_cast<const typename F::Raw*>(
-              &ring[(ce % kRing) * 32 + lane]);
-          add_msg<T, VEC, kMean, GUARD>(a, f, false, denom, rcp, 1.0f);
-        }
+        F f;
+        f.raw = lds16(ring_lane + ((uint32_t)(ce & (kRing - 1)) << 9));
+        add_msg<T, VEC, kMean, GUARD>(a, f, false, denom, rcp, 1.0f);
         issue();  // refill the slot just consumed
       }
       if (MODEL == ATLAS_GIN && self_pending && active) {
