@@ -474,38 +474,40 @@ __global__ void __launch_bounds__(256, 4)
                 unsigned long long* __restrict__ work) {
   constexpr int DPW = 32 / LPD;
   extern __shared__ uint4 ring_smem[];
-  uint4* ring = ring_smem + (threadIdx.x >> 5) * (kRing * 32);
   const int lane = threadIdx.x & 31, sub = lane / LPD, sl = lane % LPD;
   const int col = sl * 4;
   const bool lane_on = col < d;
+  const int colc = lane_on ? col : d - 4;  // clamped: branch-free copies
+  const uint32_t ring_lane =
+      (uint32_t)__cvta_generic_to_shared(ring_smem + (threadIdx.x >> 5) *
+                                                         (kRing * 32)) +
+      (uint32_t)lane * 16u;
+  const float* __restrict__ zc = z + colc;
   int bad = 0;
   while (true) {
     unsigned long long w0 = 0;
     if (lane == 0) w0 = atomicAdd(work, (unsigned long long)(kGrab * DPW));
     w0 = __shfl_sync(0xffffffffu, w0, 0) + (unsigned long long)epi.vbeg;
     if ((int64_t)w0 >= nloc) break;
-    // this sub-group's destinations [v, v_end) and edges [e_beg, e_end)
+    // this sub-group's destinations [v, v_end) and its edges, relative to
+    // e_beg: [0, ne)
     int64_t v = min((int64_t)w0 + (int64_t)sub * kGrab, nloc);
     const int64_t v_end = min(v + kGrab, nloc);
-    const int64_t e_end = csc_ptr[v_end];
-    int64_t ce = csc_ptr[v], pe = ce, ibase = ce;
-    int64_t dend = v < v_end ? csc_ptr[v + 1] : e_end;
-    uint32_t isrc = (pe + sl < e_end) ? csc_src[pe + sl] : 0u;
+    const int64_t e_beg = csc_ptr[v];
+    const int ne = (int)(csc_ptr[v_end] - e_beg);
+    const uint32_t* __restrict__ src0 = csc_src + e_beg;
+    int ce = 0, pe = 0;
+    int dend = v < v_end ? (int)(csc_ptr[v + 1] - e_beg) : ne;
+    uint32_t isrc = sl < ne ? src0[sl] : 0u;
     float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    uint32_t n_iss = 0, n_use = 0;  // per-lane ring positions
     auto issue = [&]() {
-      const bool more = pe < e_end;
-      if (more && pe - ibase == LPD) {
-        ibase = pe;
-        isrc = (pe + sl < e_end) ? csc_src[pe + sl] : 0u;
-      }
-      const uint32_t u =
-          __shfl_sync(0xffffffffu, isrc, (int)(pe - ibase) & (LPD - 1), LPD);
+      const bool more = pe < ne;
+      if (more && (pe & (LPD - 1)) == 0 && pe != 0)
+        isrc = pe + sl < ne ? src0[pe + sl] : 0u;
+      const uint32_t u = __shfl_sync(0xffffffffu, isrc, pe & (LPD - 1), LPD);
       if (more) {
-        if (lane_on)
-          cp_async16(&ring[(n_iss % kRing) * 32 + lane],
-                     z + (int64_t)u * ldz + col);
-        n_iss++;
+        cp_async16_s(ring_lane + ((uint32_t)(pe & (kRing - 1)) << 9),
+                     zc + (int64_t)u * ldz);
         pe++;
       }
       cp_async_commit();  // one group per lane per iteration, maybe empty
@@ -545,24 +547,20 @@ __global__ void __launch_bounds__(256, 4)
         }
         a[0] = a[1] = a[2] = a[3] = 0.0f;
         v++;
-        dend = v < v_end ? csc_ptr[v + 1] : e_end;
+        dend = v < v_end ? (int)(csc_ptr[v + 1] - e_beg) : ne;
       }
     };
 #pragma unroll 1
     for (int k = 0; k < kRing; k++) issue();
     flush();
-    while (__any_sync(0xffffffffu, ce < e_end)) {
+    while (__any_sync(0xffffffffu, ce < ne)) {
       cp_async_wait<kRing - 1>();  // the row issued kRing iterations ago
-      if (ce < e_end) {
-        if (lane_on) {
-          const float4 f = *reinterpret_cast<const float4*>(
-              &ring[(n_use % kRing) * 32 + lane]);
-          a[0] += f.x;
-          a[1] += f.y;
-          a[2] += f.z;
-          a[3] += f.w;
-        }
-        n_use++;
+      if (ce < ne) {
+        const uint4 r = lds16(ring_lane + ((uint32_t)(ce & (kRing - 1)) << 9));
+        a[0] += __uint_as_float(r.x);
+        a[1] += __uint_as_float(r.y);
+        a[2] += __uint_as_float(r.z);
+        a[3] += __uint_as_float(r.w);
         ce++;
       }
       issue();
