@@ -647,12 +647,11 @@ __device__ __forceinline__ void bulk_body(
             self_term();
           }
         }
-        const uint4* row = reinterpret_cast<const uint4*>(feed.wait());
+        const uint32_t row = feed.wait();
         F f[CH];
 #pragma unroll
         for (int j = 0; j < CH; j++)
-          if (act[j]) f[j].raw = *reinterpret_cast<const typename F::Raw*>(
-                          &row[j * 32 + lane]);
+          if (act[j]) f[j].raw = lds_v4(row + (uint32_t)(j * 32 + lane) * 16u);
 #pragma unroll
         for (int j = 0; j < CH; j++)
           if (act[j])

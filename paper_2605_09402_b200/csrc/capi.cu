@@ -64,8 +64,15 @@ static void ensure_ctl(atlas_layer* L) {
 }
 
 // take any deferred control verdict and the pending pass timings
-static void settle(atlas_layer* L) {
+// read_timing=false (a new pass is starting): an unread timing of the
+// previous pass is dropped without waiting for the device, so queueing
+// pass after pass never stalls the host on the data plane
+static void settle(atlas_layer* L, bool read_timing = false) {
   settle_control(L);
+  if (L->timing_pending && !read_timing) {
+    L->timing_pending = false;
+    L->timing_ms[0] = L->timing_ms[1] = 0.f;
+  }
   if (L->timing_pending) {
     L->timing_pending = false;
     ATLAS_CUDA(cudaEventSynchronize(L->tev[1]));
@@ -554,7 +561,7 @@ int atlas_layer_timing(atlas_layer* L, float* ms, int32_t n) {
   return guarded([&] {
     if (!L || !ms) fail(ATLAS_ECONFIG, "null argument");
     use_device(L->desc.device);
-    settle(L);
+    settle(L, true);
     for (int i = 0; i < n && i < 2; i++) ms[i] = L->timing_ms[i];
   });
 }
@@ -620,7 +627,7 @@ int atlas_layer_finish(atlas_layer* L, atlas_layer_metrics* m) {
     if (!L || !m) fail(ATLAS_ECONFIG, "null argument");
     use_device(L->desc.device);
     cudaStream_t s = nullptr;
-    settle(L);
+    settle(L, true);
     verify_graph(L->ctl_graph);
     ATLAS_CUDA(cudaDeviceSynchronize());
     std::memset(m, 0, sizeof(*m));
@@ -676,7 +683,7 @@ int atlas_layer_state(atlas_layer* L, uint32_t* pending, uint8_t* state,
   return guarded([&] {
     if (!L) fail(ATLAS_ECONFIG, "null layer");
     use_device(L->desc.device);
-    settle(L);
+    settle(L, true);
     ATLAS_CUDA(cudaDeviceSynchronize());
     const int64_t n = L->nloc;
     if (n == 0) return;
@@ -706,7 +713,7 @@ int atlas_layer_chunk_stats(atlas_layer* L, int64_t* reloads, int64_t* touched,
   return guarded([&] {
     if (!L) fail(ATLAS_ECONFIG, "null layer");
     use_device(L->desc.device);
-    settle(L);
+    settle(L, true);
     const int64_t n = (int64_t)L->chunk_reloads.size();
     if (count) *count = n;
     if (!reloads && !touched) return;
@@ -724,7 +731,7 @@ int atlas_layer_log(atlas_layer* L, int32_t which, int64_t* out, int64_t cap,
     if (!L) fail(ATLAS_ECONFIG, "null layer");
     if (!L->desc.record_log) fail(ATLAS_ECONFIG, "layer was not logging");
     use_device(L->desc.device);
-    settle(L);
+    settle(L, true);
     EngineScalars sc = read_scalars(L, nullptr);
     DevBuf<int64_t>* buf;
     int64_t used;

@@ -119,17 +119,18 @@ __global__ void __launch_bounds__(kGatWarps * 32,
         for (int e = 0; e < EPC; e++) acc[j][e] = 0.0f;
       }
       for (; ce < dend; ce++) {
-        const uint8_t* row = feed.wait();
-        const ZT* rel = reinterpret_cast<const ZT*>(row) + a.el_col;
+        const uint32_t row = feed.wait();
+        const uint32_t rel = row + (uint32_t)(a.el_col * sizeof(ZT));
 #pragma unroll
         for (int j = 0; j < CH; j++) {
           if (!act[j]) continue;
           ZChunk<ZT> f;
-          f.raw = reinterpret_cast<const uint4*>(row)[j * 32 + lane];
+          f.raw = lds_v4(row + (uint32_t)(j * 32 + lane) * 16u);
           // online softmax, one exp per (edge, head): with d = x - m,
           // t = exp(-|d|) rescales the old state (d > 0) or weighs the new
           // edge (d <= 0)
-          float x = to_f32(rel[head[j]]) + er_s[head[j]];
+          float x = lds_as_f32<ZT>(rel + (uint32_t)(head[j] * sizeof(ZT))) +
+                    er_s[head[j]];
           x = x >= 0.0f ? x : a.slope * x;
           const float d = x - m[j];
           const float t = __expf(-fabsf(d));

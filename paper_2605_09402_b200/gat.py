@@ -365,7 +365,8 @@ class GATEngine:
             return y, collect, layer
         return y, collect(), layer
 
-    def infer(self, x, keep_layers: bool = False, host_out=None):
+    def infer(self, x, keep_layers: bool = False, host_out=None,
+              metrics: bool = True):
         """All layers; x is the full (V, in) feature matrix (device, or
         pinned host). Returns (final local output, [LayerMetrics]);
         ``host_out`` (pinned) also receives the final output."""
@@ -386,9 +387,10 @@ class GATEngine:
             h = y
         if host_out is not None:
             host_out.copy_(y, non_blocking=True)
-        metrics = [collect() for collect in pending]
         self.last_layers = outs
-        return y, metrics
+        if not metrics:
+            return y, None
+        return y, [collect() for collect in pending]
 
 
 __all__ = ["GATLayerWeights", "GATWeights", "random_gat_weights",

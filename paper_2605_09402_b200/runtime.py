@@ -345,11 +345,15 @@ class Engine:
             return y_local
         return gather_ranges(y_local, self.ranges, self.group)
 
-    def infer(self, x, keep_layers: bool = False, host_out=None):
+    def infer(self, x, keep_layers: bool = False, host_out=None,
+              metrics: bool = True):
         """All layers; returns (final local output, [LayerMetrics]).
         ``host_out`` (pinned CPU tensor of the output's shape and dtype)
         receives the final output too; a transform-first last layer copies
-        it out slice by slice while it is still being computed."""
+        it out slice by slice while it is still being computed. With
+        ``metrics=False`` nothing waits for the device (metrics None): the
+        control plane's verdicts are still taken when the layers are
+        re-armed, but their counters are not read back."""
         pending, outs = [], []
         h, flag = x, None
         nl = len(self.weights.layers)
@@ -369,9 +373,10 @@ class Engine:
                     import torch.distributed as dist
                     dist.all_reduce(flag, op=dist.ReduceOp.MAX,
                                     group=self.group)
-        metrics = [collect() for collect in pending]
         self.last_layers = outs
-        return y, metrics
+        if not metrics:
+            return y, None
+        return y, [collect() for collect in pending]
 
 
 def gather_ranges(y_local, ranges, group=None):
