@@ -291,6 +291,52 @@ class Engine:
             return y, collect, layer
         return y, collect(), layer
 
+    def _transform_rows(self, l, x, wz, zb):
+        """z = x . W_z^T (f32) on tcgen05; a pinned host x streams to HBM
+        in double-buffered row tiles on a side stream, each tile
+        transformed as soon as it lands (layer-input ingest overlaps the
+        GEMM). Leaves z's extremes flag in self.z_flags[l]."""
+        import torch
+
+        from .engine import transform_typed
+
+        if l not in self.z_flags:
+            self.z_flags[l] = torch.zeros(1, dtype=torch.int32, device="cuda")
+        n = x.shape[0]
+        z = torch.empty((n, wz.shape[0]), dtype=torch.float32, device="cuda")
+        if x.is_cuda:
+            if n:
+                transform_typed(x, wz, zb, False, z, 1, flag=self.z_flags[l])
+            else:
+                self.z_flags[l].zero_()
+            return z
+        row_b = x.stride(0) * x.element_size()
+        tile = max(128, (self.config.stream_tile_bytes // row_b) // 128 * 128)
+        ntiles = -(-n // tile)
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream()
+        copy, cur = self._copy_stream, torch.cuda.current_stream()
+        bufs = [torch.empty((min(tile, n), x.shape[1]), dtype=x.dtype,
+                            device="cuda") for _ in range(min(2, ntiles))]
+        flags = torch.zeros(max(1, ntiles), dtype=torch.int32, device="cuda")
+        freed = [None, None]
+        for t in range(ntiles):
+            b, r0 = t & 1, t * tile
+            r1 = min(n, r0 + tile)
+            with torch.cuda.stream(copy):
+                if freed[b] is not None:
+                    copy.wait_event(freed[b])
+                bufs[b][:r1 - r0].copy_(x[r0:r1], non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(copy)
+            cur.wait_event(ready)
+            transform_typed(bufs[b][:r1 - r0], wz, zb, False, z[r0:r1], 1,
+                            flag=flags[t:t + 1])
+            freed[b] = torch.cuda.Event()
+            freed[b].record(cur)
+        torch.amax(flags, dim=0, keepdim=True, out=self.z_flags[l])
+        return z
+
     def _layer_transform_first(self, l, x, layer, rows, y, last, t0,
                                defer_metrics, host_out=None):
         """z = h . W_z^T on tcgen05 for every source row, then one fused
@@ -301,16 +347,19 @@ class Engine:
         from .engine import transform_typed
 
         wz, zb, npad = self._z_weight(l)
-        if not x.is_cuda:
-            x = x.cuda(non_blocking=True)
+        # with G ranks each rank transforms its own rows and the z rows are
+        # all-gathered (z is narrower than h, so this is the cheap exchange)
+        if self.world > 1 and x.shape[0] == self.num_vertices:
+            x = x[self.lo:self.hi]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ev[0].record()
-        z = torch.empty((x.shape[0], wz.shape[0]), dtype=torch.float32,
-                        device="cuda")
-        if l not in self.z_flags:
-            self.z_flags[l] = torch.zeros(1, dtype=torch.int32, device="cuda")
-        transform_typed(x, wz, zb, False, z, 1, flag=self.z_flags[l])
+        z = self._transform_rows(l, x, wz, zb)
         ev[1].record()
+        if self.world > 1:
+            z = self.gather(z)
+            import torch.distributed as dist
+            dist.all_reduce(self.z_flags[l], op=dist.ReduceOp.MAX,
+                            group=self.group)
         if l not in self.out_flags:
             self.out_flags[l] = torch.zeros(1, dtype=torch.int32,
                                             device="cuda")
@@ -367,7 +416,10 @@ class Engine:
             if keep_layers:
                 outs.append(y)
             if l != len(self.weights.layers) - 1:
-                h = self.gather(y)
+                # a transform-first next layer gathers its (narrower) z
+                # instead of this layer's output
+                h = y if (self.world > 1 and self.transform_first(l + 1)) \
+                    else self.gather(y)
                 flag = self.out_flags.get(l)
                 if flag is not None and self.world > 1:
                     import torch.distributed as dist

@@ -383,3 +383,24 @@ def test_host_output_slices(transform_first):
     torch.cuda.synchronize()
     assert torch.equal(host, y.cpu())
     eng.close()
+
+
+def test_transform_first_streams_host_input():
+    """A pinned-host f16 input of a transform-first layer streams to HBM in
+    row tiles, each transformed as it lands: outputs and metrics equal the
+    device-resident input's, bit for bit."""
+    from paper_2605_09402_b200.storage import (ModelKind, random_weights,
+                                               synthetic_in_memory)
+    graph, feats = synthetic_in_memory("uniform", 9000, 6, 256, 17)
+    feats = feats.astype(np.float16)
+    w = random_weights(ModelKind.SAGE, [256, 32, 8], 5)
+    cfg = dict(backend="tcgen05", hot_slots=9000, chunk_budget=64 << 10)
+    eng = Engine(graph, w, PipelineConfig(stream_tile_bytes=700 * 512, **cfg))
+    assert eng.transform_first(0)
+    y_host, m_host = eng.infer(torch.as_tensor(feats).pin_memory())
+    y_dev, m_dev = eng.infer(torch.as_tensor(feats).cuda())
+    assert torch.equal(y_host, y_dev)
+    for a, b in zip(m_host, m_dev):
+        for f in METRICS:
+            assert getattr(a, f) == getattr(b, f), f
+    eng.close()
