@@ -184,10 +184,10 @@ ATLAS_API int atlas_layer_run_streamed(atlas_layer* layer,
  * source (V rows, ldz); the pass runs the layer's control plane on the
  * reference chunk plan (chunk_rows rows, as for the layer's own input) and
  * aggregates the first d columns of z with data_model's rule (ATLAS_GCN =
- * mean, for GCN and SAGE; ATLAS_GIN = sum + (1+eps) self, in stream
- * order, exact division as in atlas_layer_run_resident), then writes
- * y[v] = act(agg + self_rows[v] + b)[:n] (self_rows: SAGE's h_v . W2^T,
- * NULL otherwise). By linearity this is the reference layer up to
+ * mean, for GCN and SAGE; ATLAS_GIN = sum + (1+eps) self), then writes
+ * y[v] = act(agg + self_rows[v] + b)[:n] (self_rows: SAGE's h_v . W2^T for
+ * the range's destinations, row v = local destination v; NULL otherwise).
+ * By linearity this is the reference layer up to
  * floating-point order; no f32 records are kept. out_flag (may be NULL)
  * receives y's extremes flag. With y_host (pinned, ldy_host elements per
  * row) the output also goes to the host in host_slices destination slices,

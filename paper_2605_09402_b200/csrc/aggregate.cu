@@ -267,8 +267,8 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // Fused epilogue of the transform-first layer (tcgen05 backend): the ring
 // aggregates z = h . W_z^T instead of h, then writes the layer output
-// y[v] = act(agg(z)[v] + self[v] + b) straight away (self = the SAGE
-// z2 = h_v . W2^T part of the same z row, or none).
+// y[v] = act(agg(z)[v] + self[v] + b) straight away (self = SAGE's
+// z2 = h_v . W2^T, indexed by the LOCAL destination, or none).
 struct EpiArgs {
   void* y;
   int64_t ldy;
@@ -389,7 +389,7 @@ __device__ __forceinline__ void ring_body(
           const int c = col + e;
           if (c < epi.n) {
             float o = a[e];
-            if (epi.self_rows) o += epi.self_rows[(int64_t)vg * epi.ld_self + c];
+            if (epi.self_rows) o += epi.self_rows[v * epi.ld_self + c];
             o += epi.bias[c];
             if (epi.relu) o = (o >= 0.0f || o != o) ? o : 0.0f;
             const O q = cvt_from_f32<O>(o);
@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(256, 4)
           const int c = col + e;
           if (c < epi.n) {
             float o = o4[e];
-            if (epi.self_rows) o += epi.self_rows[vg * epi.ld_self + c];
+            if (epi.self_rows) o += epi.self_rows[v * epi.ld_self + c];
             o += epi.bias[c];
             if (epi.relu) o = (o >= 0.0f || o != o) ? o : 0.0f;
             const OutT q = cvt_from_f32<OutT>(o);

@@ -240,21 +240,26 @@ class DeviceLayer:
             y.stride(0), int(chunk_rows), N.stream_handle(stream)))
 
     def run_fused(self, graph: DeviceGraph, z, d: int, chunk_rows: int,
-                  bias, y, *, data_model: int, relu: bool, self_col=None,
+                  bias, y, *, data_model: int, relu: bool, self_rows=None,
                   input_flag=None, out_flag=None, host_out=None,
                   host_slices: int = 8, stream=None):
         """Transform-first pass (atlas_layer_run_fused): aggregate the first
         d columns of z (V x ldz f32, = h . W_z^T) with ``data_model``'s
-        rule and write y = act(agg + z[:, self_col:] + b) for the range.
+        rule and write y = act(agg + self_rows + b) for the range
+        (self_rows: SAGE's h_v . W2^T, one f32 row per local destination).
         ``host_out`` (pinned CPU tensor like y) also receives y, slice by
         slice, each D2H overlapping the next slice's aggregation."""
         if z.shape[0] != self.num_vertices or z.dtype.itemsize != 4:
             raise ConfigError(f"z {tuple(z.shape)} does not cover the graph")
-        self_ptr = 0 if self_col is None else z.data_ptr() + 4 * self_col
+        if self_rows is not None and (self_rows.shape[0] != self.hi - self.lo
+                                      or self_rows.stride(1) != 1):
+            raise ConfigError("self rows must cover the destination range")
         N.check(N.load_library().atlas_layer_run_fused(
             self.handle, graph.handle, z.data_ptr(), z.stride(0),
             int(data_model), int(d), int(chunk_rows), N.ptr(input_flag),
-            bias.data_ptr(), self_ptr, z.stride(0), y.shape[1], int(relu),
+            bias.data_ptr(), N.ptr(self_rows),
+            0 if self_rows is None else self_rows.stride(0), y.shape[1],
+            int(relu),
             y.data_ptr(), torch_dtype_code(y), y.stride(0), N.ptr(out_flag),
             N.ptr(host_out), 0 if host_out is None else host_out.stride(0),
             int(host_slices), N.stream_handle(stream)))

@@ -353,13 +353,18 @@ class Engine:
             x = x[self.lo:self.hi]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ev[0].record()
-        z = self._transform_rows(l, x, wz, zb)
+        zp = self._transform_rows(l, x, wz, zb)
         ev[1].record()
+        sage = self.kind == ModelKind.SAGE
+        # SAGE's self half z2 = h_v . W2^T is needed for local rows only
+        self_rows = None
+        if sage:
+            self_rows = zp[:, npad:] if self.world > 1 else \
+                zp[self.lo:self.hi, npad:]
+        z = zp
         if self.world > 1:
-            z = self.gather(z)
-            import torch.distributed as dist
-            dist.all_reduce(self.z_flags[l], op=dist.ReduceOp.MAX,
-                            group=self.group)
+            z = self.gather(zp[:, :npad].contiguous() if sage else zp)
+            self.allreduce_max(self.z_flags[l])
         if l not in self.out_flags:
             self.out_flags[l] = torch.zeros(1, dtype=torch.int32,
                                             device="cuda")
@@ -367,7 +372,7 @@ class Engine:
                       else ModelKind.GCN)
         layer.run_fused(self.graph, z, npad, rows, self.b[l], y,
                         data_model=int(data_model), relu=not last,
-                        self_col=npad if self.kind == ModelKind.SAGE else None,
+                        self_rows=self_rows,
                         input_flag=self.z_flags[l],
                         out_flag=self.out_flags[l], host_out=host_out)
 
@@ -387,6 +392,11 @@ class Engine:
         reallocating; cached layers re-read their in-degrees from the
         device graph on their next pass (atlas_layer_bind_graph)."""
         self.graph.update(offsets, neighbors, in_degrees)
+
+    def allreduce_max(self, t):
+        """Element-wise max over ranks (the extremes flags)."""
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
 
     def gather(self, y_local):
         """All ranks' ranges -> full (V, out) next-layer input (NCCL)."""
@@ -422,9 +432,7 @@ class Engine:
                     else self.gather(y)
                 flag = self.out_flags.get(l)
                 if flag is not None and self.world > 1:
-                    import torch.distributed as dist
-                    dist.all_reduce(flag, op=dist.ReduceOp.MAX,
-                                    group=self.group)
+                    self.allreduce_max(flag)
         self.last_layers = outs
         if not metrics:
             return y, None
