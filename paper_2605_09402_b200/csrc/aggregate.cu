@@ -127,12 +127,42 @@ __global__ void scan_extremes(const T* __restrict__ x, int64_t rows, int d,
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
        r < rows; r += nwarps) {
     const T* row = x + r * ldx;
-    for (int c = lane; c < d; c += 32) {
-      const float v = fabsf(to_f32(row[c]));
-      bad |= (v < 0x1p-100f && v != 0.0f) || !(v <= 3.402823466e38f);
-    }
+    for (int c = lane; c < d; c += 32) bad |= is_extreme(to_f32(row[c]));
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+// dense rows (ldx == d): one flat pass with 16-byte loads
+template <typename T>
+__global__ void scan_extremes_flat(const T* __restrict__ x, int64_t n,
+                                   int* __restrict__ flag) {
+  constexpr int EPC = 16 / sizeof(T);
+  const int64_t nvec = n / EPC;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += stride) {
+    const uint4 raw = __ldg(reinterpret_cast<const uint4*>(x) + i);
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int k = 0; k < EPC; k++) bad |= is_extreme(to_f32(e[k]));
+  }
+  for (int64_t i = nvec * EPC + blockIdx.x * (int64_t)blockDim.x +
+                   threadIdx.x;
+       i < n; i += stride)
+    bad |= is_extreme(to_f32(x[i]));
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+template <typename T>
+void launch_scan(const T* x, int64_t rows, int d, int64_t ldx, int* flag,
+                 cudaStream_t s) {
+  if (ldx == d && (reinterpret_cast<uintptr_t>(x) & 15) == 0)
+    scan_extremes_flat<T><<<148 * 8, 256, 0, s>>>(x, rows * d, flag);
+  else
+    scan_extremes<T><<<148 * 8, 256, 0, s>>>(x, rows, d, ldx, flag);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------------------
@@ -901,10 +931,7 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
   const int* flag = g->known_flag;
   if (!flag) {
     ATLAS_CUDA(cudaMemsetAsync(g->scan_flag.ptr, 0, sizeof(int), s));
-    scan_extremes<T><<<148 * 8, 256, 0, s>>>(x, g->V, d, ldx,
-                                             g->scan_flag.ptr);
-    count_launch();
-    ATLAS_LAUNCH_CHECK();
+    launch_scan<T>(x, g->V, d, ldx, g->scan_flag.ptr, s);
     flag = g->scan_flag.ptr;
   }
   if constexpr (VEC * sizeof(T) == 16) if (d <= 32 * VEC) {
@@ -1147,10 +1174,7 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
   if (!flag) {
     g->scan_flag.reserve(1);
     ATLAS_CUDA(cudaMemsetAsync(g->scan_flag.ptr, 0, sizeof(int), s));
-    scan_extremes<float><<<148 * 8, 256, 0, s>>>(z, g->V, d, ldz,
-                                                 g->scan_flag.ptr);
-    count_launch();
-    ATLAS_LAUNCH_CHECK();
+    launch_scan<float>(z, g->V, d, ldz, g->scan_flag.ptr, s);
     flag = g->scan_flag.ptr;
   }
   g->work.reserve(1);

@@ -1,6 +1,7 @@
 // C-ABI edge of libatlas_b200.so (include/atlas_b200.h).
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -104,6 +105,17 @@ static void ensure_copy_stream(atlas_layer* L) {
     ATLAS_CUDA(cudaEventCreateWithFlags(&L->ev_free[i],
                                         cudaEventDisableTiming));
   }
+}
+
+// inputs up to this many bytes land whole in HBM during a streamed pass;
+// ATLAS_STREAM_WHOLE_MAX_BYTES overrides the 8 GiB default (tests set 0 to
+// exercise the two-buffer tile path)
+static size_t stream_whole_max() {
+  static const size_t v = [] {
+    const char* e = std::getenv("ATLAS_STREAM_WHOLE_MAX_BYTES");
+    return e ? (size_t)std::strtoull(e, nullptr, 10) : (size_t(8) << 30);
+  }();
+  return v;
 }
 
 static void ensure_tile_events(atlas_layer* L) {
@@ -492,7 +504,7 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
     // so the copy stream never waits for a buffer; larger inputs cycle
     // through two tile buffers
     const size_t row_b = (size_t)ldx * item;
-    const bool whole = (size_t)V * row_b <= (size_t(8) << 30);
+    const bool whole = (size_t)V * row_b <= stream_whole_max();
     if (whole) L->stream_tile[0].reserve((size_t)V * row_b);
     auto tile_ptr = [&](int64_t t) -> uint8_t* {
       return whole ? L->stream_tile[0].ptr + (size_t)(t * tile_rows) * row_b

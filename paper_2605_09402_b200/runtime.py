@@ -303,7 +303,10 @@ class Engine:
         if l not in self.z_flags:
             self.z_flags[l] = torch.zeros(1, dtype=torch.int32, device="cuda")
         n = x.shape[0]
-        z = torch.empty((n, wz.shape[0]), dtype=torch.float32, device="cuda")
+        # row pitch: whole 64-byte units, so a narrow z row never straddles
+        # more DRAM bursts than it needs (the GEMM writes wz.shape[0] cols)
+        z = torch.empty((n, -(-wz.shape[0] // 16) * 16), dtype=torch.float32,
+                        device="cuda")
         if x.is_cuda:
             if n:
                 transform_typed(x, wz, zb, False, z, 1, flag=self.z_flags[l])
@@ -363,7 +366,13 @@ class Engine:
                 zp[self.lo:self.hi, npad:]
         z = zp
         if self.world > 1:
-            z = self.gather(zp[:, :npad].contiguous() if sage else zp)
+            if sage:  # gather z1 only, in its own 64-byte-pitch rows
+                z1 = torch.zeros((zp.shape[0], -(-npad // 16) * 16),
+                                 dtype=zp.dtype, device="cuda")
+                z1[:, :npad] = zp[:, :npad]
+                z = self.gather(z1)
+            else:
+                z = self.gather(zp)
             self.allreduce_max(self.z_flags[l])
         if l not in self.out_flags:
             self.out_flags[l] = torch.zeros(1, dtype=torch.int32,

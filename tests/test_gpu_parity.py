@@ -87,6 +87,41 @@ OPERATOR_CASES = [c for c in CASES if golden_manifest()[c]["dataset"]
                                                    "cfg1_sage"])
 @pytest.mark.parametrize("tile_rows", [1, 7, 1000])
 def test_streamed_layers_bit_exact(case, tile_rows):
+    _streamed_case(case, tile_rows)
+
+
+TILE_PATH = r"""
+import sys
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+import test_gpu_parity as T
+for case in %r:
+    for rows in (7, 1000):
+        T._streamed_case(case, rows)
+print("ok")
+"""
+
+
+def test_streamed_two_buffer_tile_path_bit_exact():
+    """Inputs above ATLAS_STREAM_WHOLE_MAX_BYTES cycle through two tile
+    buffers with per-tile aggregation (agg_tile, per-destination cursors);
+    forced here on small inputs (fresh process: the limit is read once)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    here = Path(__file__).resolve().parent
+    cases = ["small_gcn_tight", "small_sage", "small_gin_tight",
+             "half_sage_slots300", "uniform_gin", "pa_sage_10pct"]
+    env = dict(os.environ, ATLAS_STREAM_WHOLE_MAX_BYTES="0")
+    out = subprocess.run([sys.executable, "-c",
+                          TILE_PATH % (str(here.parent), str(here), cases)],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert out.stdout.strip().endswith("ok")
+
+
+def _streamed_case(case, tile_rows):
     """Host-resident input streamed to HBM in tiles (double-buffered side
     stream): outputs and integers identical to the reference."""
     if tile_rows == 1 and golden_manifest()[case]["dataset"] in ("pa", "cfg1",
