@@ -1,0 +1,120 @@
+"""Ablation harness parity (oocgnn/bench.py).
+
+CPU: scenario parsing and the gather-pattern replay against the reference's
+own functions (imported read-only when /root/reference is present) and its
+hand-graph known answers (gather 5 rows vs broadcast 6,
+tests/test_bench.py:92-96).
+
+GPU: the reference's acceptance criteria 4, 5, 6 and 11 re-run through
+this engine on the reference's PA desk dataset (generate_synthetic("pa",
+100_000, 10, 64, seed 12), GCN [64, 32, 16]); every integer must equal the
+reference's shipped run (pkg/test_output.txt:314-321).
+"""
+
+import sys
+
+import numpy as np
+import pytest
+
+from helpers import REFERENCE_SRC, fig2_graph
+from paper_2605_09402_b200 import ablation as A
+from paper_2605_09402_b200 import storage as S
+from paper_2605_09402_b200.errors import ConfigError, FormatError
+
+
+def test_parse_scenario(tmp_path):
+    p = tmp_path / "sc.txt"
+    p.write_text("# budget sweep\nname = sweep1\nsweep=budget\n"
+                 "graph = pa\nvertices=500\nbudget_pcts = 2,5,10\n"
+                 "layers_out=16,8\nevictions=lru,rnd\ndirect_io=0\n")
+    sc = A.parse_scenario(p)
+    assert (sc.name, sc.sweep, sc.graph, sc.vertices) == ("sweep1", "budget",
+                                                          "pa", 500)
+    assert sc.budget_pcts == [2.0, 5.0, 10.0]
+    assert sc.layers_out == [16, 8] and sc.evictions == ["lru", "rnd"]
+    assert sc.direct_io is False
+    p.write_text("bogus=1\n")
+    with pytest.raises(FormatError):
+        A.parse_scenario(p)
+    p.write_text("sweep=sideways\n")
+    with pytest.raises(ConfigError):
+        A.parse_scenario(p)
+
+
+def test_gather_replay_hand_graph():
+    g = fig2_graph()
+    assert A.simulate_gather_rows(g, cache_rows=0, block_rows=1) == 5
+    assert A.broadcast_rows(g) == 6
+
+
+@pytest.mark.skipif(not REFERENCE_SRC.exists(), reason="reference absent")
+@pytest.mark.parametrize("cache,block", [(0, 1), (50, 1), (64, 4), (7, 3)])
+def test_gather_replay_matches_reference(cache, block):
+    sys.path.insert(0, str(REFERENCE_SRC))
+    from oocgnn import bench as RB
+    from oocgnn.storage import GraphCSR as RG
+    g, _ = S.synthetic_in_memory("pa", 2000, 5, 4, 12)
+    rg = RG(g.num_vertices, g.num_edges, g.offsets, g.neighbors,
+            g.in_degrees)
+    assert A.simulate_gather_rows(g, cache, block) == \
+        RB.simulate_gather_rows(rg, cache_rows=cache, block_rows=block)
+    off, src = A.reverse_csr(g)
+    roff, rsrc = RB.reverse_csr(rg)
+    np.testing.assert_array_equal(off, roff)
+    np.testing.assert_array_equal(src, rsrc)
+
+
+@pytest.fixture(scope="module")
+def pa_dir(tmp_path_factory):
+    d = tmp_path_factory.mktemp("ablation") / "pa"
+    S.generate_synthetic("pa", 100_000, 10, 64, 12, d)
+    return d
+
+
+def _scenario(pa_dir, **kw):
+    return A.Scenario(name="acc", graph=str(pa_dir), model="gcn",
+                      layers_out=[32, 16], seed=5, **kw)
+
+
+@pytest.mark.gpu
+def test_criterion_4_min_pending_beats_other_policies(pa_dir, tmp_path):
+    rows = A.run_ablation(_scenario(pa_dir, sweep="eviction"), tmp_path)
+    means = {p: np.mean([r["reloads"] for r in rows if r["variant"] == p])
+             for p in ("minpend", "lru", "rnd")}
+    # reference: "minpend 172165 < lru 177053 < rnd 176824" (means, .0f)
+    assert round(means["minpend"]) == 172165
+    assert round(means["lru"]) == 177053
+    assert round(means["rnd"]) == 176824
+
+
+@pytest.mark.gpu
+def test_criterion_6_reloads_fall_monotonically_with_budget(pa_dir,
+                                                            tmp_path):
+    rows = A.run_ablation(_scenario(pa_dir, sweep="budget"), tmp_path)
+    assert [r["hot_slots"] for r in rows] == [2000, 5000, 10000, 50000,
+                                              100000]
+    assert [r["reloads"] for r in rows] == [178370, 172165, 161944, 43315, 0]
+
+
+@pytest.mark.gpu
+def test_criterion_5_reordering_spans_and_reloads(pa_dir, tmp_path):
+    rows = A.run_ablation(_scenario(pa_dir, sweep="ordering"), tmp_path)
+    by = {r["variant"]: r for r in rows}
+    assert by["original"]["reloads"] == 172165
+    assert by["greedy"]["reloads"] == 99548
+    # reference: "mean span 588768 -> 400330 (1.47x)" (the known-red 1.5x)
+    assert round(float(by["original"]["mean_span"])) == 588768
+    assert round(float(by["greedy"]["mean_span"])) == 400330
+
+
+@pytest.mark.gpu
+def test_criterion_11_gather_reads_more_than_broadcast(pa_dir, tmp_path):
+    from paper_2605_09402_b200.runtime import PipelineConfig, run_inference
+    g = S.read_csr(pa_dir)
+    w = S.random_weights(S.ModelKind.GCN, [64, 32, 16], 5)
+    report = run_inference(pa_dir, w, PipelineConfig(), tmp_path / "run")
+    broadcast = report.layers[0].feature_bytes_read
+    gather = A.simulate_gather_rows(g, cache_rows=g.num_vertices // 4) * 64 * 4
+    # reference: "gather 198 MB > broadcast 26 MB at 25% cache"
+    assert round(gather / 1e6) == 198
+    assert round(broadcast / 1e6) == 26
