@@ -56,7 +56,10 @@ enum {
   ATLAS_ECOVERAGE = -6,    /* CoverageError */
   ATLAS_EFORMAT = -7,      /* FormatError */
   ATLAS_EDEVICE = -8,      /* CUDA/NCCL failure (DeviceError) */
-  ATLAS_EINVARIANT = -9    /* InvariantError */
+  ATLAS_EINVARIANT = -9,   /* InvariantError */
+  ATLAS_EMAGIC = -10,      /* BadMagicError (a FormatError) */
+  ATLAS_ETRUNCATED = -11,  /* TruncatedFileError (a FormatError) */
+  ATLAS_EVERSION = -12     /* VersionMismatchError (a FormatError) */
 };
 
 /* ModelKind (oocgnn/storage.py:498) + GAT, which the reference lacks
@@ -278,6 +281,29 @@ ATLAS_API int atlas_reorder(int32_t device, int64_t num_vertices,
                             int64_t* new_offsets, uint32_t* new_neighbors,
                             uint32_t* new_in_degrees, double* scores,
                             void* stream);
+
+/* ---- layer-directory spill I/O (host only) -- */
+/* read the ASPL spill files of a layer directory (oocgnn/storage.py:
+ * 257-357; the reference reads them through SpillSet, oocgnn/chunks.py:
+ * 103-201) into a dense row-major host buffer (num_vertices x dim, pinned
+ * for the K1 streamer), files in parallel on `threads` host threads (0 =
+ * all cores). Every id must arrive exactly once (ATLAS_ECOVERAGE
+ * otherwise; delivery_out, may be NULL, receives the per-id counts like
+ * the reference's delivery counters, oocgnn/chunks.py:145-147). */
+ATLAS_API int atlas_spill_read(const char* const* paths, int32_t n_files,
+                               int32_t dtype, int64_t dim,
+                               int64_t num_vertices, void* rows_out,
+                               uint16_t* delivery_out, int32_t threads,
+                               int64_t* bytes_read);
+/* write rows [id_lo, id_hi) of a dense host matrix (ld elements per row,
+ * row 0 = id_lo) as one partition directory's spill files spill_0..k of
+ * spill_rows rows each plus its manifest -- the bytes
+ * oocgnn/storage.py:write_matrix_as_layer / writer.py produce */
+ATLAS_API int atlas_spill_write(const char* part_dir, const void* rows,
+                                int32_t dtype, int64_t dim, int64_t ld,
+                                int64_t id_lo, int64_t id_hi,
+                                int64_t spill_rows, int32_t threads,
+                                int64_t* bytes_written);
 
 /* number of kernels this library launched since load (evidence counter) */
 ATLAS_API int64_t atlas_kernel_launches(void);

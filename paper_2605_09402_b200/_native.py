@@ -107,6 +107,10 @@ def _declare(lib):
     fn("atlas_layer_timing", ctypes.c_int, c_vp, c_vp, c_i32)
     fn("atlas_reorder", ctypes.c_int, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp,
        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
+    fn("atlas_spill_read", ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
+       c_i32, c_i32, c_i64, c_i64, c_vp, c_vp, c_i32, P_i64)
+    fn("atlas_spill_write", ctypes.c_int, ctypes.c_char_p, c_vp, c_i32, c_i64,
+       c_i64, c_i64, c_i64, c_i64, c_i32, P_i64)
 
 
 EXPORTED = [
@@ -121,6 +125,7 @@ EXPORTED = [
     "atlas_layer_chunk_stats", "atlas_layer_log", "atlas_layer_state",
     "atlas_layer_timing", "atlas_reorder", "atlas_transform_typed",
     "atlas_layer_run_gat", "atlas_layer_run_fused", "atlas_layer_bind_graph",
+    "atlas_spill_read", "atlas_spill_write",
 ]
 
 

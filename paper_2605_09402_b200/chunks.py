@@ -4,9 +4,9 @@
   (oocgnn/chunks.py:36-48): rows = max(1, budget // row_bytes).
 * ``Chunk`` is the operator-path payload (oocgnn/chunks.py:204-220).
 * ``load_layer_input`` replaces the merge-on-read spill reader
-  (oocgnn/chunks.py:103-260) for the HBM-resident path: one sequential
-  pass over the layer directory's spills into a pinned host buffer, ready
-  for a single host->HBM copy. Every row is checked to arrive exactly once
+  (oocgnn/chunks.py:103-260): the library reads the layer directory's
+  spill files in parallel straight into a pinned host buffer, the source of
+  the K1 host->HBM streamer. Every row is checked to arrive exactly once
   (the reference's delivery counters, criterion 2).
 """
 
@@ -61,31 +61,80 @@ def chunk_from_csr(graph, features, start: int, end: int) -> Chunk:
                  np.asarray(graph.neighbors[lo:hi], dtype=np.int64))
 
 
-def load_layer_input(layer_dir, out=None):
-    """Dense (V, dim) rows of a layer dir in their stored dtype.
+def _pinned_rows(shape, dtype):
+    """A page-locked host buffer for the K1 streamer when CUDA is usable,
+    else plain memory (host-only use, e.g. format tools)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            t = torch.empty(shape, dtype={np.dtype(np.float32): torch.float32,
+                                          np.dtype(np.float16): torch.float16}
+                            [np.dtype(dtype)], pin_memory=True)
+            return t.numpy()
+    except Exception:  # noqa: BLE001 - no torch / no device: plain memory
+        pass
+    return np.empty(shape, dtype=dtype)
+
+
+def load_layer_input(layer_dir, out=None, threads: int = 0):
+    """Dense (V, dim) rows of a layer dir in their stored dtype, read by
+    the library's parallel spill reader (csrc/spillio.cu) straight into a
+    pinned buffer (the source of the K1 host->HBM streamer); replaces the
+    reference's merge-on-read SpillSet (oocgnn/chunks.py:103-260).
 
     Returns (meta, rows, bytes_read, delivery) where delivery counts how
     often each id arrived (all ones, or CoverageError)."""
+    import ctypes
+
+    from . import _native as N
+
     meta = read_layer_meta(layer_dir)
     dtype = NP_DTYPES[meta.dtype]
-    rows = out if out is not None else np.empty(
-        (meta.num_vertices, meta.dim), dtype=dtype)
+    rows = out if out is not None else _pinned_rows(
+        (meta.num_vertices, meta.dim), dtype)
+    if rows.shape != (meta.num_vertices, meta.dim) or rows.dtype != dtype \
+            or not rows.flags.c_contiguous:
+        raise ConsistencyError(f"{layer_dir}: output buffer does not match "
+                               f"({meta.num_vertices}, {meta.dim}) "
+                               f"{meta.dtype}")
+    paths = [str(part_dir(layer_dir, k) / name)
+             for k in range(meta.partitions)
+             for name in read_manifest(part_dir(layer_dir, k))]
+    arr = (ctypes.c_char_p * max(1, len(paths)))(
+        *[p.encode() for p in paths])
     delivery = np.zeros(meta.num_vertices, dtype=np.uint16)
-    nbytes = 0
-    for k in range(meta.partitions):
+    nbytes = ctypes.c_int64()
+    N.check(N.load_library().atlas_spill_read(
+        arr, len(paths), N.F32 if meta.dtype == "f32" else N.F16, meta.dim,
+        meta.num_vertices, rows.ctypes.data, delivery.ctypes.data,
+        int(threads), ctypes.byref(nbytes)))
+    return meta, rows, int(nbytes.value), delivery
+
+
+def write_layer_output(layer_dir, matrix: np.ndarray, partitions: int = 1,
+                       dtype: str = "f32", threads: int = 0) -> int:
+    """Write a (V, dim) output matrix as a partitioned layer directory with
+    the library's parallel spill writer (csrc/spillio.cu): one spill per
+    partition, the bytes storage.write_matrix_as_layer produces
+    (oocgnn/storage.py:468-491, tested byte-for-byte). Returns the bytes
+    written."""
+    import ctypes
+
+    from . import _native as N
+    from .storage import LayerMeta, partition_ranges, write_layer_meta
+
+    rows = np.ascontiguousarray(matrix, dtype=NP_DTYPES[dtype])
+    v, dim = rows.shape
+    write_layer_meta(layer_dir, LayerMeta(v, dim, dtype, partitions))
+    lib = N.load_library()
+    total = 0
+    for k, (lo, hi) in enumerate(partition_ranges(v, partitions)):
         pdir = part_dir(layer_dir, k)
-        for name in read_manifest(pdir):
-            ids, block = read_spill_file(pdir / name)
-            if block.shape[1] != meta.dim or block.dtype != dtype:
-                raise ConsistencyError(
-                    f"{pdir / name}: shape {block.shape[1]}/{block.dtype} "
-                    f"does not match layer meta {meta.dim}/{meta.dtype}")
-            rows[ids] = block
-            delivery[ids] += 1
-            nbytes += block.nbytes + ids.nbytes
-    if not np.all(delivery == 1):
-        bad = np.flatnonzero(delivery != 1)
-        raise CoverageError(
-            f"{layer_dir}: {bad.size} ids not delivered exactly once, "
-            f"first {bad[:8].tolist()}")
-    return meta, rows, nbytes, delivery
+        pdir.mkdir(parents=True, exist_ok=True)
+        nb = ctypes.c_int64()
+        N.check(lib.atlas_spill_write(
+            str(pdir).encode(), rows[lo:hi].ctypes.data if hi > lo else None,
+            N.F32 if dtype == "f32" else N.F16, dim, dim, lo, hi,
+            max(1, hi - lo), int(threads), ctypes.byref(nb)))
+        total += int(nb.value)
+    return total

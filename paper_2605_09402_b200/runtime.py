@@ -30,7 +30,7 @@ from pathlib import Path
 import numpy as np
 
 from .chunks import chunk_rows as plan_rows
-from .chunks import load_layer_input
+from .chunks import load_layer_input, write_layer_output
 from .compute import device_code, get_backend
 from .engine import DeviceGraph, DeviceLayer, transform_device
 from .errors import ConfigError
@@ -489,8 +489,8 @@ def _write_output(layer_dir, y, config, num_vertices) -> int:
     dtype = "f16" if config.embed_dtype == "f16" else "f32"
     if layer_dir.exists():
         shutil.rmtree(layer_dir)
-    return write_matrix_as_layer(layer_dir, host, partitions=config.partitions,
-                                 dtype=dtype)
+    return write_layer_output(layer_dir, host, partitions=config.partitions,
+                              dtype=dtype)
 
 
 def _upload(rows):
