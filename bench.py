@@ -312,6 +312,10 @@ class ClockSampler:
         self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
 
+    def reset(self):
+        """Drop the samples taken so far (before the timed region)."""
+        self.sm, self.reasons = [], set()
+
     def _sample(self):
         nv = self.nv
         self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
@@ -477,11 +481,14 @@ def main():
         if world > 1:
             dist.barrier()
 
+    # the NVML sampler thread starts (and takes its first samples) during
+    # the warm-up; only samples from the timed region are kept
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         eng.infer(x)
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.reset()
     launches0 = N.kernel_launches()
     start, stop = torch.cuda.Event(True), torch.cuda.Event(True)
     marks = [torch.cuda.Event(True) for _ in range(args.steps)]
