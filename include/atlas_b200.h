@@ -239,7 +239,11 @@ ATLAS_API int atlas_transform_typed(int32_t backend, const void* x_dev,
  * the control plane of a layer created with model ATLAS_GAT (GCN rules:
  * pending = in-degree) on the reference chunk plan of chunk_rows rows, and
  * the edge-softmax aggregation of the range with bias, head concat (+ReLU)
- * or head mean fused, written to y (nloc x ldy). No reference counterpart
+ * or head mean fused, written to y (nloc x ldy). attn_l_dev (may be NULL):
+ * a_l laid out like the z columns (heads x head_stride, zero pads); given
+ * it, f32 z of <= 128 columns is aggregated moving only the z part of each source row, el_u = a_l . z_u
+ * recomputed per edge (4 DRAM lines per edge instead of 5-6 when the z
+ * rows start on 128-byte lines). No reference counterpart
  * (SPEC.md:8); oracle/gat.py defines the result. */
 ATLAS_API int atlas_layer_run_gat(atlas_layer* layer, const atlas_graph* graph,
                                   const void* z_dev, int32_t z_dtype,
@@ -250,6 +254,7 @@ ATLAS_API int atlas_layer_run_gat(atlas_layer* layer, const atlas_graph* graph,
                                   int32_t mean_heads, int32_t relu,
                                   float negative_slope, void* y_dev,
                                   int32_t y_dtype, int64_t ldy,
+                                  const float* attn_l_dev,
                                   int64_t chunk_rows, void* stream);
 
 ATLAS_API int atlas_layer_finish(atlas_layer* layer, atlas_layer_metrics* out);

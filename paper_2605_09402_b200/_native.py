@@ -94,7 +94,7 @@ def _declare(lib):
        c_vp)
     fn("atlas_layer_run_gat", ctypes.c_int, c_vp, c_vp, c_vp, c_i32, c_i64,
        c_i32, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, ctypes.c_float,
-       c_vp, c_i32, c_i64, c_i64, c_vp)
+       c_vp, c_i32, c_i64, c_vp, c_i64, c_vp)
     fn("atlas_layer_run_fused", ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_i32,
        c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_i32,
        c_i64, c_vp, c_vp, c_i64, c_i32, c_vp)

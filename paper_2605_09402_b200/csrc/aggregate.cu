@@ -267,34 +267,6 @@ __global__ void __launch_bounds__(256, 6)
 constexpr int kRing = 16;
 constexpr int kGrab = 32;  // destinations per work grab
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(smem)),
-               "l"(gmem)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-// same, with a precomputed shared-space destination address
-__device__ __forceinline__ void cp_async16_s(uint32_t smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem),
-               "l"(gmem)
-               : "memory");
-}
-__device__ __forceinline__ uint4 lds16(uint32_t smem) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "r"(smem)
-               : "memory");
-  return v;
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 // Fused epilogue of the transform-first layer (tcgen05 backend): the ring
 // aggregates z = h . W_z^T instead of h, then writes the layer output
 // y[v] = act(agg(z)[v] + self[v] + b) straight away (self = SAGE's

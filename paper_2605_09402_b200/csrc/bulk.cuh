@@ -1,6 +1,7 @@
-// Row-granular bulk copies (TMA engine, cp.async.bulk -> UBLKCP) completed
-// on shared-memory mbarriers: the staging primitive of the wide-row
-// aggregation kernels (aggregate.cu agg_bulk, gat.cu gat_bulk).
+// Staging primitives of the aggregation kernels: row-granular bulk copies
+// (TMA engine, cp.async.bulk -> UBLKCP) completed on shared-memory
+// mbarriers (aggregate.cu agg_bulk, gat.cu gat_bulk) and per-lane 16-byte
+// cp.async copies (LDGSTS) waited on per lane (the ring kernels).
 #pragma once
 
 #include "internal.cuh"
@@ -91,6 +92,30 @@ __device__ __forceinline__ float lds_as_f32<__nv_bfloat16>(uint32_t smem) {
   return __bfloat162float(__ushort_as_bfloat16(v));
 }
 
+// per-lane 16-byte asynchronous copies (LDGSTS) into shared memory
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+// same, with a precomputed shared-space destination address
+__device__ __forceinline__ void cp_async16_s(uint32_t smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds16(uint32_t smem) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem)
+               : "memory");
+  return v;
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+
 // Feeds the rows of a contiguous edge range [e0, e1) of a CSC source list
 // through a per-warp ring of SLOTS shared-memory row buffers. Refills go
 // out in groups of G: lanes 0..G-1 each issue one row copy (source ids come
@@ -156,10 +181,25 @@ struct RowFeeder {
   // the row from wait() is consumed by every lane: refill when G are free
   template <typename T>
   __device__ __forceinline__ void release(const T* base, int64_t ld) {
-    n_used++;
+    release_n(1, base, ld);
+  }
+  // the k-th row after the next one (k = 0: wait()), not consumed yet
+  __device__ __forceinline__ uint32_t wait_k(uint32_t k) {
+    const uint32_t n = n_used + k;
+    const uint32_t slot = n & (SLOTS - 1);
+    mbar_wait_parity_s(bars + slot * 8u, (n / SLOTS) & 1u);
+    return ring + slot * row_bytes;
+  }
+  // n rows consumed by every lane; refill while whole groups are free
+  template <typename T>
+  __device__ __forceinline__ void release_n(uint32_t n, const T* base,
+                                            int64_t ld) {
+    n_used += n;
     if (pe < ne && n_issued - n_used <= SLOTS - G) {
       __syncwarp();  // every lane is done with the slots being refilled
-      issue_group(base, ld);
+      do {
+        issue_group(base, ld);
+      } while (pe < ne && n_issued - n_used <= SLOTS - G);
     }
   }
 };

@@ -378,7 +378,8 @@ int atlas_layer_run_gat(atlas_layer* L, const atlas_graph* g, const void* z,
                         int32_t el_col, int32_t er_col,
                         const float* bias, int32_t mean_heads, int32_t relu,
                         float negative_slope, void* y, int32_t y_dtype,
-                        int64_t ldy, int64_t chunk_rows, void* stream) {
+                        int64_t ldy, const float* attn_l,
+                        int64_t chunk_rows, void* stream) {
   return guarded([&] {
     if (!L || !g || !z || !bias || !y) fail(ATLAS_ECONFIG, "null argument");
     if (!L->gat) fail(ATLAS_ECONFIG, "layer was not created as GAT");
@@ -393,7 +394,7 @@ int atlas_layer_run_gat(atlas_layer* L, const atlas_graph* g, const void* z,
     launch_control(L, g, chunk_rows, s);
     launch_gat_aggregate(g, z, z_dtype, ldz, heads, head_dim, head_stride,
                          el_col, er_col, bias, mean_heads, relu,
-                         negative_slope, y, y_dtype, ldy, s);
+                         negative_slope, y, y_dtype, ldy, attn_l, s);
     ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
     ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
     L->timing_pending = true;

@@ -226,7 +226,7 @@ void launch_gat_aggregate(const atlas_graph* g, const void* z, int z_dtype,
                           int head_stride, int el_col, int er_col,
                           const float* bias, int mean_heads, int relu,
                           float slope, void* y, int y_dtype, int64_t ldy,
-                          cudaStream_t s);
+                          const float* attn_l, cudaStream_t s);
 
 // transform.cu
 void launch_transform_stable(const float* x, int64_t rows, int64_t k,

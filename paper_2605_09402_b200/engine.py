@@ -225,10 +225,12 @@ class DeviceLayer:
 
     def run_gat(self, graph: DeviceGraph, z, layout, bias, y, *,
                 mean_heads: bool, relu: bool, chunk_rows: int,
-                negative_slope: float = 0.2, stream=None):
+                negative_slope: float = 0.2, attn_l=None, stream=None):
         """GAT pass B (atlas_layer_run_gat): z (V, ldz) CUDA tensor laid
         out as ``layout`` (gat.ZLayout) -> y (range rows) with bias, head
-        concat/ReLU or head mean fused; control plane on the chunk plan."""
+        concat/ReLU or head mean fused; control plane on the chunk plan.
+        ``attn_l`` (f32 CUDA, heads x head_stride, zero pads) lets
+        line-aligned f32 z (layout.line_rows) recompute el per edge."""
         if z.shape[0] != self.num_vertices or z.stride(1) != 1:
             raise ConfigError(f"z {tuple(z.shape)} does not cover the graph")
         N.check(N.load_library().atlas_layer_run_gat(
@@ -237,7 +239,8 @@ class DeviceLayer:
             layout.el_col, layout.er_col, bias.data_ptr(), int(mean_heads),
             int(relu),
             float(negative_slope), y.data_ptr(), torch_dtype_code(y),
-            y.stride(0), int(chunk_rows), N.stream_handle(stream)))
+            y.stride(0), N.ptr(attn_l), int(chunk_rows),
+            N.stream_handle(stream)))
 
     def run_fused(self, graph: DeviceGraph, z, d: int, chunk_rows: int,
                   bias, y, *, data_model: int, relu: bool, self_rows=None,

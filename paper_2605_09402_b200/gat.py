@@ -198,16 +198,30 @@ class ZLayout:
         return self.el_col + self.heads
 
     @property
-    def ldz(self) -> int:
+    def ncols(self) -> int:
+        """columns pass A writes (z, el, er, chunk padding)"""
         return self._up(self.er_col + self.heads)
+
+    @property
+    def line_rows(self) -> bool:
+        """f32 z of <= 128 columns: pass B moves only the z part of a source
+        row and recomputes el from it (csrc/gat.cu gat_ring), so rows start
+        on 128-byte lines and a z part costs whole DRAM lines, not a
+        [z | el] straddle."""
+        return self.itemsize == 4 and self.el_col <= 128
+
+    @property
+    def ldz(self) -> int:
+        n = self.ncols
+        return -(-n // 32) * 32 if self.line_rows else n
 
 
 def extended_weight(lw: GATLayerWeights, layout: ZLayout) -> np.ndarray:
-    """W_ext (ldz x in): the heads of W at their strided rows, then
+    """W_ext (ncols x in): the heads of W at their strided rows, then
     a_l[h]^T W_h and a_r[h]^T W_h, zero elsewhere (computed in float64,
     stored f32), so z_ext = h . W_ext^T carries z, el and er."""
     w = lw.weight.astype(np.float64).reshape(lw.heads, lw.head_dim, lw.in_dim)
-    ext = np.zeros((layout.ldz, lw.in_dim), dtype=np.float64)
+    ext = np.zeros((layout.ncols, lw.in_dim), dtype=np.float64)
     for h in range(lw.heads):
         r = h * layout.head_stride
         ext[r:r + lw.head_dim] = w[h]
@@ -258,12 +272,19 @@ class GATEngine:
         self.zt = _torch_dtype(config.embed_dtype)
         item = torch.empty(0, dtype=self.zt).element_size()
         self.layouts, self.w_ext, self.zero_b, self.bias = [], [], [], []
+        self.attn_l = []  # a_l at the strided z columns (line_rows layouts)
         for lw in weights.layers:
             lay = ZLayout(lw.heads, lw.head_dim, item)
             self.layouts.append(lay)
             self.w_ext.append(torch.as_tensor(extended_weight(lw, lay)).cuda())
-            self.zero_b.append(torch.zeros(lay.ldz, device="cuda"))
+            self.zero_b.append(torch.zeros(lay.ncols, device="cuda"))
             self.bias.append(torch.as_tensor(lw.bias).cuda())
+            al = None
+            if lay.line_rows:
+                al = np.zeros((lw.heads, lay.head_stride), dtype=np.float32)
+                al[:, :lw.head_dim] = lw.attn_l
+                al = torch.as_tensor(al.reshape(-1)).cuda()
+            self.attn_l.append(al)
         self._layers = {}
         self.last_layers = []
 
@@ -339,7 +360,7 @@ class GATEngine:
                               device="cuda")
         if h_local.shape[0]:
             transform_typed(h_local, self.w_ext[l], self.zero_b[l], False,
-                            z_local, 1)
+                            z_local[:, :lay.ncols], 1)
         ev[1].record()
         z = self.gather(z_local)
         rows = plan_rows(self.num_vertices, lay.ldz,
@@ -347,12 +368,14 @@ class GATEngine:
                          self.config.chunk_budget)
         layer = self._device_layer(l, lay)
         out_dim = lw.head_dim if last else lw.hf
-        y = torch.empty((nloc, out_dim),
-                        dtype=torch.float32 if last else self.zt,
-                        device="cuda")
+        yt = torch.float32 if last else self.zt
+        # 16-byte row pitch: the next layer's pass A reads y through TMA
+        pitch = -(-out_dim // 8) * 8
+        y = torch.empty((nloc, pitch), dtype=yt, device="cuda")[:, :out_dim]
         layer.run_gat(self.graph, z, lay, self.bias[l], y, mean_heads=last,
                       relu=not last, chunk_rows=rows,
-                      negative_slope=w.negative_slope)
+                      negative_slope=w.negative_slope,
+                      attn_l=self.attn_l[l])
 
         def collect():
             m = metrics_from_device(layer, l)

@@ -33,7 +33,8 @@ def hub_graph(v=3000, seed=4):
 @pytest.mark.parametrize("zdtype", ["f32", "f16"])
 @pytest.mark.parametrize("feat_dtype", ["f32", "f16"])
 @pytest.mark.parametrize("heads,dims", [(4, [64, 128, 128, 19]),
-                                        (2, [24, 16, 5]), (1, [16, 8, 8])])
+                                        (2, [24, 16, 5]), (1, [16, 8, 8]),
+                                        (1, [16, 100, 12])])
 def test_gat_matches_f64_oracle(zdtype, feat_dtype, heads, dims):
     g = hub_graph()
     w = G.random_gat_weights(dims, heads, seed=5)
