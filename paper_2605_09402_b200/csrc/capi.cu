@@ -83,16 +83,25 @@ static void settle(atlas_layer* L, bool read_timing = false) {
   }
 }
 
-// queue the control plane of a whole-layer pass on the control stream,
-// ordered after everything already queued on the launch stream s
-static void launch_control(atlas_layer* L, const atlas_graph* g,
-                           int64_t chunk_rows, cudaStream_t s) {
+// The control plane of a whole-layer pass runs on the control stream,
+// ordered after everything queued on the launch stream s before
+// control_begin. It is queued (control_queue) only after the data plane:
+// queueing it may wait on the host for a refreshed graph's chunk
+// statistics, and the data plane (tile copies, aggregation) must already
+// be in flight by then.
+static void control_begin(atlas_layer* L, cudaStream_t s) {
   ensure_ctl(L);
   ATLAS_CUDA(cudaEventRecord(L->tev[0], s));
   ATLAS_CUDA(cudaStreamWaitEvent(L->ctl_stream, L->tev[0], 0));
   ATLAS_CUDA(cudaEventRecord(L->tev[2], L->ctl_stream));
+}
+
+// queue the control plane and make s wait for it
+static void control_queue(atlas_layer* L, const atlas_graph* g,
+                          int64_t chunk_rows, cudaStream_t s) {
   resident_control(L, g, chunk_rows, L->ctl_stream);
   ATLAS_CUDA(cudaEventRecord(L->tev[3], L->ctl_stream));
+  ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
 }
 
 // side copy stream and its events (created once per layer)
@@ -359,15 +368,15 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
     use_device(D.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     settle(L);
-    // control plane first (own stream, runs beside the data plane), then
-    // the scatter-aggregate; s waits for the control plane at the end
-    launch_control(L, g, chunk_rows, s);
+    // control plane on its own stream beside the scatter-aggregate; s
+    // waits for it at the end
+    control_begin(L, s);
     if (L->nloc > 0)
       launch_agg_resident(g, x, dtype, ldx, D.model, D.gin_epsilon,
                           (int)D.embed_dim, L->acc.ptr, D.agg_dim,
                           input_flag, s);
     ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
-    ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
+    control_queue(L, g, chunk_rows, s);
     L->timing_pending = true;
   });
 }
@@ -391,12 +400,12 @@ int atlas_layer_run_gat(atlas_layer* L, const atlas_graph* g, const void* z,
     use_device(D.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     settle(L);
-    launch_control(L, g, chunk_rows, s);
+    control_begin(L, s);
     launch_gat_aggregate(g, z, z_dtype, ldz, heads, head_dim, head_stride,
                          el_col, er_col, bias, mean_heads, relu,
                          negative_slope, y, y_dtype, ldy, attn_l, s);
     ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
-    ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
+    control_queue(L, g, chunk_rows, s);
     L->timing_pending = true;
   });
 }
@@ -426,7 +435,7 @@ int atlas_layer_run_fused(atlas_layer* L, const atlas_graph* g,
     use_device(D.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     settle(L);
-    launch_control(L, g, chunk_rows, s);
+    control_begin(L, s);
     if (out_flag) ATLAS_CUDA(cudaMemsetAsync(out_flag, 0, sizeof(int32_t), s));
     if (!y_host) {
       launch_agg_resident_epi(g, z, ldz, data_model, D.gin_epsilon, (int)d,
@@ -461,7 +470,7 @@ int atlas_layer_run_fused(atlas_layer* L, const atlas_graph* g,
       ATLAS_CUDA(cudaStreamWaitEvent(s, L->ev_ready[1], 0));
     }
     ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
-    ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
+    control_queue(L, g, chunk_rows, s);
     L->timing_pending = true;
   });
 }
@@ -497,23 +506,25 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
     settle(L);
     // the copy stream starts at once (it overlaps whatever s is still
     // doing, e.g. a topology refresh); a tile buffer is only refilled after
-    // the kernel that last read it, in this pass or the previous one. The
-    // first two tiles are queued before the control plane, whose launch
-    // may wait on the host for a refreshed graph's chunk statistics.
-    const int64_t ntiles = ceil_div(V, tile_rows);
-    // an input of up to 8 GB lands whole in HBM (tile t at its own rows),
-    // so the copy stream never waits for a buffer; larger inputs cycle
-    // through two tile buffers
+    // the kernel that last read it, in this pass or the previous one.
+    // An input of up to 8 GB lands whole in HBM (each tile at its own
+    // rows), so the copy stream never waits for a buffer and every copy is
+    // queued before any kernel; larger inputs cycle through two buffers.
     const size_t row_b = (size_t)ldx * item;
     const bool whole = (size_t)V * row_b <= stream_whole_max();
     if (whole) L->stream_tile[0].reserve((size_t)V * row_b);
+    // Tile boundaries (uniform: a tapered tail measured slower, every
+    // extra tile re-reads and re-writes the whole accumulator)
+    std::vector<int64_t> bnd{0};
+    for (int64_t r = 0; r < V;) bnd.push_back(r = std::min(V, r + tile_rows));
+    const int64_t ntiles = (int64_t)bnd.size() - 1;
     auto tile_ptr = [&](int64_t t) -> uint8_t* {
-      return whole ? L->stream_tile[0].ptr + (size_t)(t * tile_rows) * row_b
+      return whole ? L->stream_tile[0].ptr + (size_t)bnd[t] * row_b
                    : L->stream_tile[t & 1].ptr;
     };
     auto copy_tile = [&](int64_t t) {
       const int b = (int)(t & 1);
-      const int64_t r0 = t * tile_rows, r1 = std::min(V, r0 + tile_rows);
+      const int64_t r0 = bnd[t], r1 = bnd[t + 1];
       if (whole ? (t == 0 && L->tile_used[0]) : (t >= 2 || L->tile_used[b]))
         ATLAS_CUDA(cudaStreamWaitEvent(L->copy_stream,
                                        L->ev_free[whole ? 0 : b], 0));
@@ -529,10 +540,10 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
     const int64_t ahead = whole ? std::min<int64_t>(kTileEvents, ntiles)
                                 : std::min<int64_t>(2, ntiles);
     for (int64_t t = 0; t < ahead; t++) copy_tile(t);
-    launch_control(L, g, chunk_rows, s);  // records tev[0] after the resets
+    control_begin(L, s);  // tev[0] after the resets
     for (int64_t t = 0; t < ntiles; t++) {
       const int b = (int)(t & 1);
-      const int64_t r0 = t * tile_rows, r1 = std::min(V, r0 + tile_rows);
+      const int64_t r0 = bnd[t], r1 = bnd[t + 1];
       if (t >= ahead) copy_tile(t);
       ATLAS_CUDA(cudaStreamWaitEvent(
           s, whole ? L->tile_ev[t % kTileEvents] : L->ev_ready[b], 0));
@@ -550,7 +561,7 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
       L->tile_used[0] = true;
     }
     ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
-    ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
+    control_queue(L, g, chunk_rows, s);
     L->timing_pending = true;
   });
 }

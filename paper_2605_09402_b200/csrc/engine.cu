@@ -586,6 +586,8 @@ int64_t phys_slots_of(const atlas_layer* L) {
   return std::max<int64_t>(1, std::min<int64_t>(L->desc.slot_count, L->nloc));
 }
 
+__global__ void set_scalars(EngineScalars* dst, EngineScalars v) { *dst = v; }
+
 void engine_init(atlas_layer* L, cudaStream_t s) {
   L->spans_queued = false;
   const int64_t n = L->nloc;
@@ -627,11 +629,11 @@ void engine_init(atlas_layer* L, cudaStream_t s) {
   sc.rng_state_lo = L->desc.rnd_state[1];
   sc.rng_inc_hi = L->desc.rnd_state[2];
   sc.rng_inc_lo = L->desc.rnd_state[3];
-  L->pin_scalars.reserve(1);
-  *L->pin_scalars.ptr = sc;
-  ATLAS_CUDA(cudaMemcpyAsync(L->scalars.ptr, L->pin_scalars.ptr, sizeof(sc),
-                             cudaMemcpyHostToDevice, s));
-  ATLAS_CUDA(cudaStreamSynchronize(s));
+  // by value through the launch: no staging buffer, no host wait (a
+  // topology refresh re-arms every layer while the device still works)
+  set_scalars<<<1, 1, 0, s>>>(L->scalars.ptr, sc);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
   L->engine_initialized = true;
 }
 
@@ -649,6 +651,7 @@ static void grow_log(DevBuf<int64_t>& buf, int64_t used, int64_t need,
 }
 
 EngineScalars read_scalars(atlas_layer* L, cudaStream_t s) {
+  L->pin_scalars.reserve(1);
   ATLAS_CUDA(cudaMemcpyAsync(L->pin_scalars.ptr, L->scalars.ptr,
                              sizeof(EngineScalars), cudaMemcpyDeviceToHost,
                              s));

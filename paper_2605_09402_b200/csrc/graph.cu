@@ -92,6 +92,14 @@ void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs,
   DevBuf<uint32_t>& keys_out = g->ws_keys_out;
   DevBuf<uint8_t>& tmp = g->ws_tmp;
   src_of_edge.reserve(e1);
+  // every host->device copy goes first: one queued behind the sort would
+  // wait in the copy engine behind whatever input copies the next layer
+  // queues meanwhile
+  g->indeg.reserve(g->nloc > 0 ? g->nloc : 1);
+  if (g->nloc > 0)
+    ATLAS_CUDA(cudaMemcpyAsync(g->indeg.ptr, indeg_host + g->lo,
+                               g->nloc * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, s));
   if (E > 0) {
     expand_sources<<<grid_for(V * 32, 256), 256, 0, s>>>(g->offsets.ptr, V,
                                                         src_of_edge.ptr);
@@ -151,13 +159,9 @@ void build_csc(atlas_graph* g, DevBuf<uint32_t>& nbrs,
     ATLAS_LAUNCH_CHECK();
   }
   // csc_ptr = exclusive scan of local in-degrees
-  g->indeg.reserve(g->nloc > 0 ? g->nloc : 1);
   g->csc_ptr.reserve(g->nloc + 1);
   ATLAS_CUDA(cudaMemsetAsync(g->csc_ptr.ptr, 0, sizeof(int64_t), s));
   if (g->nloc > 0) {
-    ATLAS_CUDA(cudaMemcpyAsync(g->indeg.ptr, indeg_host + g->lo,
-                               g->nloc * sizeof(uint32_t),
-                               cudaMemcpyHostToDevice, s));
     size_t tmp_bytes = 0;
     ATLAS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, g->indeg.ptr,
                                              g->csc_ptr.ptr + 1, g->nloc, s));

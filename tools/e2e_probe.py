@@ -15,6 +15,24 @@ from paper_2605_09402_b200 import storage as S  # noqa: E402
 from paper_2605_09402_b200.runtime import Engine, PipelineConfig  # noqa: E402
 
 
+HOST_MS = {}
+
+
+def _trace(cls, names):
+    """accumulate host time spent inside cls.<name> (blocking calls show)"""
+    for n in names:
+        f = getattr(cls, n)
+
+        def wrap(*a, _f=f, _n=n, **k):
+            t = time.perf_counter()
+            try:
+                return _f(*a, **k)
+            finally:
+                HOST_MS[_n] = HOST_MS.get(_n, 0.0) + 1e3 * (
+                    time.perf_counter() - t)
+        setattr(cls, n, wrap)
+
+
 def main(v=2_400_000, deg=26, dim=100, tile_mb=256):
     graph, feats = S.synthetic_in_memory("uniform", v, deg, dim, 7)
     w = S.random_weights(S.ModelKind.GCN, [dim, 128, 128, 47], 5)
@@ -37,6 +55,8 @@ def main(v=2_400_000, deg=26, dim=100, tile_mb=256):
         evs[0].record()
         eng.update_graph(pin_off, pin_nb, pin_deg)
         evs[1].record()
+        if SYNC_GRAPH:
+            torch.cuda.synchronize()
         hs.append(time.perf_counter())
         h = pinned
         pend = []
@@ -57,6 +77,8 @@ def main(v=2_400_000, deg=26, dim=100, tile_mb=256):
         ms = [c() for c in pend]
         dev = [evs[i].elapsed_time(evs[i + 1]) for i in range(5)]
         host = [1e3 * (hs[i + 1] - hs[i]) for i in range(5)]
+        print("  host ms in:", {k: round(x, 2) for k, x in HOST_MS.items()})
+        HOST_MS.clear()
         print(f"iter {it}: total {1e3 * (end - hs[0]):.1f} ms | " + " | ".join(
             f"{n} host {a:.1f} dev {b:.1f}" for n, a, b in zip(names, host, dev))
             + " | " + " ".join(f"L{m.layer}: agg {m.agg_ms:.1f} ctl "
@@ -65,8 +87,15 @@ def main(v=2_400_000, deg=26, dim=100, tile_mb=256):
     eng.close()
 
 
+SYNC_GRAPH = False
+from paper_2605_09402_b200 import engine as _E  # noqa: E402
+
+_trace(_E.DeviceLayer, ["reset", "bind_graph", "run_streamed",
+                        "accumulator_ptr"])
+_trace(_E.DeviceGraph, ["update"])
+
 if __name__ == "__main__":
-    for SLICED in (False, True):
-        print("sliced D2H", SLICED)
+    for SLICED, SYNC_GRAPH in ((True, False),):
+        print("sliced D2H", SLICED, "sync after graph", SYNC_GRAPH)
         for mb in (sys.argv[1:] or ["256"]):
             main(tile_mb=int(mb))
