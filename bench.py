@@ -61,8 +61,19 @@ GAT_HEADS = 4
 # host memory. The other ranks' rows of every all-gathered tensor are
 # stand-ins filled once outside the timed region; the NVLink all-gather
 # bytes are reported, not timed.
-LARGE_V, LARGE_G, LARGE_DEG = 100_000_000, 8, 12
-SLICE = {"igb-large-sage-rank0of8": ("SAGE", [1024, 128, 128, 19])}
+# BASELINE configs[3] likewise: the ogbn-papers100M-shaped graph (111M
+# vertices, avg degree 15 -> ~1.67B edges; the generator takes integer
+# degrees, 15 is the nearer to 1.6B), 128-d f16, 3-layer SAGE
+# [128,128,128,172], rank 0 of 8.
+# name -> (model, dims, V, avg degree, feature dim, hot-slot fraction of
+# the rank's range)
+LARGE_G = 8
+SLICE = {
+    "igb-large-sage-rank0of8": ("SAGE", [1024, 128, 128, 19], 100_000_000,
+                                12, 1024, 1.0),
+    "papers100m-sage-rank0of8": ("SAGE", [128, 128, 128, 172], 111_000_000,
+                                 15, 128, 1.0),
+}
 
 
 def build_inputs():
@@ -106,32 +117,32 @@ def build_igb(kind, dims, seed=SEED):
     return graph, feats, weights
 
 
-def build_large_slice(kind, dims, seed=SEED):
-    """Rank 0's edges of a uniform IGB-Large-shaped graph: the E/G edges
+def build_large_slice(kind, dims, big_v, deg, dim, seed=SEED):
+    """Rank 0's edges of a uniform graph of big_v vertices: the E/G edges
     whose destination is in [0, V/G), sources over all V (generated on the
     device; multi-edges removed, rows ascending)."""
     import torch
 
     from paper_2605_09402_b200 import storage as S
 
-    lo, hi = S.partition_ranges(LARGE_V, LARGE_G)[0]
+    lo, hi = S.partition_ranges(big_v, LARGE_G)[0]
     gen = torch.Generator(device="cuda")
     gen.manual_seed(seed)
-    m = LARGE_V * LARGE_DEG // LARGE_G
-    src = torch.randint(0, LARGE_V, (m,), generator=gen, device="cuda")
+    m = big_v * deg // LARGE_G
+    src = torch.randint(0, big_v, (m,), generator=gen, device="cuda")
     dst = torch.randint(lo, hi, (m,), generator=gen, device="cuda")
     key = torch.unique(src * hi + dst)
     del src, dst
     s, t = key // hi, key % hi
     del key
-    offsets = torch.zeros(LARGE_V + 1, dtype=torch.int64, device="cuda")
-    offsets[1:] = torch.cumsum(torch.bincount(s, minlength=LARGE_V), 0)
-    indeg = torch.bincount(t, minlength=LARGE_V)
-    graph = S.GraphCSR(LARGE_V, int(t.numel()), offsets.cpu().numpy(),
+    offsets = torch.zeros(big_v + 1, dtype=torch.int64, device="cuda")
+    offsets[1:] = torch.cumsum(torch.bincount(s, minlength=big_v), 0)
+    indeg = torch.bincount(t, minlength=big_v)
+    graph = S.GraphCSR(big_v, int(t.numel()), offsets.cpu().numpy(),
                        t.to(torch.int32).cpu().numpy().view(np.uint32),
                        indeg.cpu().numpy())
     del s, t, offsets, indeg
-    own = torch.empty((hi - lo, IGB_DIM), dtype=torch.float16, device="cuda")
+    own = torch.empty((hi - lo, dim), dtype=torch.float16, device="cuda")
     own.uniform_(-1.0, 1.0, generator=gen)
     feats = own.cpu().pin_memory()
     del own
@@ -179,11 +190,13 @@ def run_slice(args):
     from paper_2605_09402_b200 import _native as N
     from paper_2605_09402_b200.runtime import PipelineConfig
 
-    kind, dims = SLICE[args.workload]
+    kind, dims, big_v, deg, dim, hot_frac = SLICE[args.workload]
     t_gen = time.perf_counter()
-    graph, feats, weights = build_large_slice(kind, dims)
+    graph, feats, weights = build_large_slice(kind, dims, big_v, deg, dim)
     gen_s = time.perf_counter() - t_gen
-    cfg = PipelineConfig(chunk_budget=CHUNK_BUDGET, hot_slots=LARGE_V // LARGE_G,
+    rng = -(-big_v // LARGE_G)
+    cfg = PipelineConfig(chunk_budget=CHUNK_BUDGET,
+                         hot_slots=max(1, int(rng * hot_frac)),
                          backend=args.backend, embed_dtype=args.embed_dtype)
     eng = slice_engine_class()(graph, weights, cfg, rank=0, world=LARGE_G)
     for _ in range(args.warmup):
@@ -217,15 +230,18 @@ def run_slice(args):
         "dtype": f"f16 in / f32 accumulate / {args.embed_dtype} embeddings",
         "data": "synthetic",
         "config": {"workload": f"{args.workload}: 3-layer {kind} {dims} on "
-                   f"rank 0 of {LARGE_G} of a uniform graph V={LARGE_V:,}, "
-                   f"avg degree {LARGE_DEG} (rank edges {e_rank:,}), "
-                   f"1024-d f16 own feature rows streamed from pinned host",
+                   f"rank 0 of {LARGE_G} of a uniform graph V={big_v:,}, "
+                   f"avg degree {deg} (rank edges {e_rank:,}), "
+                   f"{dim}-d f16 own feature rows streamed from pinned host, "
+                   f"hot_slots={cfg.hot_slots:,} ({hot_frac:.0%} of the "
+                   "range)",
                    "parallelism": f"dst-range rank 0/{LARGE_G}",
                    "transform_backend": args.backend},
         "per_layer": [{"layer": m.layer, "agg_ms": round(m.agg_ms, 3),
                        "control_ms": round(m.control_ms, 3),
                        "transform_ms": round(m.transform_ms, 3),
-                       "fast_path": m.fast_path, "messages": m.messages}
+                       "fast_path": m.fast_path, "messages": m.messages,
+                       "evictions": m.evictions, "reloads": m.reloads}
                       for m in metrics],
         "ingest": {"h2d_bytes_per_step": h2d,
                    "gb_per_s_if_ingest_bound": h2d / (ms / 1e3) / 1e9},
@@ -409,15 +425,20 @@ def main():
     ap.add_argument("--backend", default="tcgen05")
     ap.add_argument("--workload", default="cfg2",
                     choices=["cfg2"] + sorted(EXTRA) + sorted(SLICE))
-    ap.add_argument("--embed-dtype", default="f32",
+    ap.add_argument("--embed-dtype", default=None,
                     choices=["f32", "f16", "bf16"],
                     help="storage type of intermediate embeddings (GAT: "
-                         "of z); f32 keeps the reference's f32 semantics")
+                         "of z); f32 (default) keeps the reference's f32 "
+                         "semantics; the 8-GPU rank slices default to f16 "
+                         "(SURVEY.md §8d: layer inputs >= 2 are fp16 for "
+                         "configs 4/5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true",
                     help="skip the bit-exact (stable) backend re-run")
     args = ap.parse_args()
+    if args.embed_dtype is None:
+        args.embed_dtype = "f16" if args.workload in SLICE else "f32"
     if args.impl == "reference":
         run_reference(args)
         return

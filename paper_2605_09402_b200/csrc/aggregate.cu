@@ -47,6 +47,17 @@ struct Frag {
     const T* t = reinterpret_cast<const T*>(&raw);
     return to_f32(t[e]);
   }
+  // elements e, e+1 (e even) as a float2 (exact widening)
+  __device__ __forceinline__ float2 get2(int e) const {
+    const T* t = reinterpret_cast<const T*>(&raw);
+    if constexpr (std::is_same<T, __half>::value)
+      return __half22float2(*reinterpret_cast<const __half2*>(t + e));
+    else if constexpr (std::is_same<T, __nv_bfloat16>::value)
+      return __bfloat1622float2(
+          *reinterpret_cast<const __nv_bfloat162*>(t + e));
+    else
+      return make_float2(t[e], t[e + 1]);
+  }
 };
 
 template <int VEC>
@@ -100,19 +111,43 @@ __device__ __forceinline__ float div_rn(float m, float d, float r) {
 }
 
 // a += (self ? m * self_scale : (MEAN ? m / denom : m)), per element.
+// Unguarded even widths run on the packed f32x2 pipe (FMUL2/FFMA2/FADD2:
+// two IEEE round-to-nearest results per instruction, the same bits as the
+// scalar sequence; e = m - q d is formed as fma(q, -d, m), equal to
+// fma(-q, d, m) since negation is exact).
 template <typename T, int VEC, bool MEAN, bool GUARD = true>
 __device__ __forceinline__ void add_msg(float (&a)[VEC],
                                         const Frag<T, VEC>& f, bool self,
                                         float denom, float rcp,
                                         float self_scale) {
+  if constexpr (VEC % 2 == 0 && !GUARD) {
+    const float2 r2 = make_float2(rcp, rcp);
+    const float2 nd2 = make_float2(-denom, -denom);
+    const float2 s2 = make_float2(self_scale, self_scale);
 #pragma unroll
-  for (int e = 0; e < VEC; e++) {
-    float m = f.get(e);
-    if (self)
-      m = __fmul_rn(m, self_scale);
-    else if (MEAN)
-      m = div_rn<GUARD>(m, denom, rcp);
-    a[e] = __fadd_rn(a[e], m);
+    for (int e = 0; e < VEC; e += 2) {
+      float2 m = f.get2(e);
+      if (self) {
+        m = __fmul2_rn(m, s2);
+      } else if (MEAN) {
+        const float2 q = __fmul2_rn(m, r2);
+        const float2 r = __ffma2_rn(q, nd2, m);
+        m = __ffma2_rn(r, r2, q);
+      }
+      const float2 o = __fadd2_rn(make_float2(a[e], a[e + 1]), m);
+      a[e] = o.x;
+      a[e + 1] = o.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; e++) {
+      float m = f.get(e);
+      if (self)
+        m = __fmul_rn(m, self_scale);
+      else if (MEAN)
+        m = div_rn<GUARD>(m, denom, rcp);
+      a[e] = __fadd_rn(a[e], m);
+    }
   }
 }
 
@@ -457,6 +492,161 @@ __global__ void __launch_bounds__(256, 3)
   else
     ring_body<T, VEC, MODEL, false>(x, ldx, csc_ptr, csc_src, indeg, lo, nloc,
                                     d, acc, ldacc, self_scale, work, ring);
+}
+
+// Bit-exact ring for narrow rows (<= 16 chunks of 16 B: 128-d f16, 64-d
+// f32): 32/LPD sub-groups of LPD lanes per warp, each walking its own run
+// of consecutive destinations (a contiguous CSC range) in lockstep with the
+// others -- the agg_tf_ring schedule with ring_body's arithmetic. Each
+// destination's sources are still folded one at a time in ascending order
+// (same rounded divide and add per column), so records are the bits of
+// agg_ring; the warp just keeps every lane busy instead of idling the
+// half (or more) of it a narrow row does not cover.
+// shallower ring than agg_ring's: 32/LPD runs share a warp's rows in
+// flight, and the smaller footprint leaves room for more blocks per SM
+constexpr int kSubRing = 8;
+constexpr int kSubBlocks = 4;  // per SM (64 registers: no address remat)
+
+template <typename T, int LPD, int MODEL, bool GUARD>
+__device__ __forceinline__ void sub_ring_body(
+    const T* __restrict__ x, int64_t ldx, const int64_t* __restrict__ csc_ptr,
+    const uint32_t* __restrict__ csc_src, const uint32_t* __restrict__ indeg,
+    int64_t lo, int64_t nloc, int d, float* __restrict__ acc, int64_t ldacc,
+    float self_scale, unsigned long long* __restrict__ work,
+    uint4* __restrict__ ring) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int DPW = 32 / LPD;
+  constexpr bool kMean = MODEL != ATLAS_GIN;
+  using F = Frag<T, VEC>;
+  const int lane = threadIdx.x & 31, sub = lane / LPD, sl = lane % LPD;
+  const int col = sl * VEC;
+  const bool lane_on = col < d;
+  const int colc = lane_on ? col : d - VEC;  // clamped: branch-free copies
+  const uint32_t ring_lane =
+      (uint32_t)__cvta_generic_to_shared(ring) + (uint32_t)lane * 16u;
+  // source row address = xbase + u * pitch (one IMAD.WIDE per edge)
+  const uint64_t xbase = reinterpret_cast<uint64_t>(x + colc);
+  const uint32_t pitch = (uint32_t)(ldx * (int64_t)sizeof(T));
+  while (true) {
+    unsigned long long w0 = 0;
+    if (lane == 0) w0 = atomicAdd(work, (unsigned long long)(kGrab * DPW));
+    w0 = __shfl_sync(0xffffffffu, w0, 0);
+    if ((int64_t)w0 >= nloc) break;
+    // this sub-group's destinations [v, v_end) and its edges [0, ne)
+    // relative to e_beg
+    int64_t v = min((int64_t)w0 + (int64_t)sub * kGrab, nloc);
+    const int64_t v_end = min(v + kGrab, nloc);
+    const int64_t e_beg = csc_ptr[v];
+    const int ne = (int)(csc_ptr[v_end] - e_beg);
+    const uint32_t* __restrict__ src0 = csc_src + e_beg;
+    int ce = 0, pe = 0;
+    int dend = 0;
+    float denom = 1.0f, rcp = 1.0f;
+    bool self_pending = false;
+    uint32_t isrc = sl < ne ? src0[sl] : 0u;
+    uint32_t csrc = isrc;  // GIN: consume-side source ids, LPD at a time
+    float a[VEC];
+    auto start_dest = [&]() {  // arm destination v (v < v_end)
+      dend = (int)(csc_ptr[v + 1] - e_beg);
+      if (kMean) {
+        denom = (float)max(1u, indeg[v]);
+        rcp = __frcp_rn(denom);
+      }
+      self_pending = MODEL == ATLAS_GIN;
+#pragma unroll
+      for (int e = 0; e < VEC; e++) a[e] = 0.0f;
+    };
+    auto add_self = [&]() {
+      if (lane_on) {
+        F me;
+        me.load(x + (v + lo) * ldx + col);
+        add_msg<T, VEC, false>(a, me, true, 1.0f, 1.0f, self_scale);
+      }
+    };
+    auto issue = [&]() {
+      const bool more = pe < ne;
+      if (more && (pe & (LPD - 1)) == 0 && pe != 0)
+        isrc = pe + sl < ne ? src0[pe + sl] : 0u;
+      const uint32_t u = __shfl_sync(0xffffffffu, isrc, pe & (LPD - 1), LPD);
+      if (more) {
+        cp_async16_s(ring_lane + ((uint32_t)(pe & (kSubRing - 1)) << 9),
+                     reinterpret_cast<const void*>(
+                         xbase + (uint64_t)u * pitch));
+        pe++;
+      }
+      cp_async_commit();  // one group per lane per iteration, maybe empty
+    };
+    // write out finished destinations (zero-degree ones included)
+    auto flush = [&]() {
+      while (v < v_end && ce == dend) {
+        if (MODEL == ATLAS_GIN && self_pending) add_self();
+        if (lane_on) {
+          float* out = acc + v * ldacc;
+          store_f32<VEC>(out + col, a);
+          if (MODEL == ATLAS_SAGE) {
+            F me;
+            me.load(x + (v + lo) * ldx + col);
+            float h[VEC];
+#pragma unroll
+            for (int e = 0; e < VEC; e++) h[e] = me.get(e);
+            store_f32<VEC>(out + d + col, h);
+          }
+        }
+        v++;
+        if (v < v_end) start_dest();
+      }
+    };
+    if (v < v_end) start_dest();
+#pragma unroll 1
+    for (int k = 0; k < kSubRing; k++) issue();
+    flush();
+    while (__any_sync(0xffffffffu, ce < ne)) {
+      const bool on = ce < ne;
+      if (MODEL == ATLAS_GIN) {
+        // GIN's self term goes before the first source >= v (its stream
+        // position); ids of the consumed edges, LPD at a time
+        if (on && (ce & (LPD - 1)) == 0 && ce != 0)
+          csrc = ce + sl < ne ? src0[ce + sl] : 0u;
+        const uint32_t s =
+            __shfl_sync(0xffffffffu, csrc, ce & (LPD - 1), LPD);
+        if (on && self_pending && s >= (uint32_t)(v + lo)) {
+          self_pending = false;
+          add_self();
+        }
+      }
+      cp_async_wait<kSubRing - 1>();  // the row issued kSubRing iterations ago
+      if (on) {
+        F f;
+        f.raw = lds16(ring_lane + ((uint32_t)(ce & (kSubRing - 1)) << 9));
+        add_msg<T, VEC, kMean, GUARD>(a, f, false, denom, rcp, 1.0f);
+        ce++;
+      }
+      issue();
+      flush();
+    }
+    cp_async_wait<0>();
+  }
+}
+
+template <typename T, int LPD, int MODEL>
+__global__ void __launch_bounds__(256, kSubBlocks)
+    agg_sub_ring(const T* __restrict__ x, int64_t ldx,
+                 const int64_t* __restrict__ csc_ptr,
+                 const uint32_t* __restrict__ csc_src,
+                 const uint32_t* __restrict__ indeg, int64_t lo, int64_t nloc,
+                 int d, float* __restrict__ acc, int64_t ldacc,
+                 float self_scale, const int* __restrict__ guard_flag,
+                 unsigned long long* __restrict__ work) {
+  extern __shared__ uint4 ring_smem[];
+  uint4* ring = ring_smem + (threadIdx.x >> 5) * (kSubRing * 32);
+  if (*guard_flag)
+    sub_ring_body<T, LPD, MODEL, true>(x, ldx, csc_ptr, csc_src, indeg, lo,
+                                       nloc, d, acc, ldacc, self_scale, work,
+                                       ring);
+  else
+    sub_ring_body<T, LPD, MODEL, false>(x, ldx, csc_ptr, csc_src, indeg, lo,
+                                        nloc, d, acc, ldacc, self_scale, work,
+                                        ring);
 }
 
 // transform-first layer, narrow z rows (<= 64 f32), streaming version:
@@ -907,7 +1097,8 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
     flag = g->scan_flag.ptr;
   }
   if constexpr (VEC * sizeof(T) == 16) if (d <= 32 * VEC) {
-    // ring kernel: persistent warps, dynamic destination batches
+    // ring kernel: persistent warps, dynamic destination batches; rows of
+    // <= 16 chunks run 32/LPD destination runs per warp in lockstep
     g->work.reserve(1);
     ATLAS_CUDA(cudaMemsetAsync(g->work.ptr, 0, sizeof(unsigned long long), s));
     const int smem = 8 * kRing * 32 * 16;
@@ -918,9 +1109,29 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
           x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
           g->nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
     };
-    if (model == ATLAS_GCN) ring(agg_ring<T, VEC, ATLAS_GCN>);
-    else if (model == ATLAS_SAGE) ring(agg_ring<T, VEC, ATLAS_SAGE>);
-    else ring(agg_ring<T, VEC, ATLAS_GIN>);
+    if (d <= 16 * VEC) {
+      const int sub_smem = 8 * kSubRing * 32 * 16;
+      auto sub = [&](auto kern) {
+        ATLAS_CUDA(cudaFuncSetAttribute(
+            kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sub_smem));
+        kern<<<148 * kSubBlocks, 256, sub_smem, s>>>(
+            x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
+            g->nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
+      };
+      if (d <= 8 * VEC) {
+        if (model == ATLAS_GCN) sub(agg_sub_ring<T, 8, ATLAS_GCN>);
+        else if (model == ATLAS_SAGE) sub(agg_sub_ring<T, 8, ATLAS_SAGE>);
+        else sub(agg_sub_ring<T, 8, ATLAS_GIN>);
+      } else {
+        if (model == ATLAS_GCN) sub(agg_sub_ring<T, 16, ATLAS_GCN>);
+        else if (model == ATLAS_SAGE) sub(agg_sub_ring<T, 16, ATLAS_SAGE>);
+        else sub(agg_sub_ring<T, 16, ATLAS_GIN>);
+      }
+    } else {
+      if (model == ATLAS_GCN) ring(agg_ring<T, VEC, ATLAS_GCN>);
+      else if (model == ATLAS_SAGE) ring(agg_ring<T, VEC, ATLAS_SAGE>);
+      else ring(agg_ring<T, VEC, ATLAS_GIN>);
+    }
     count_launch();
     ATLAS_LAUNCH_CHECK();
     return;

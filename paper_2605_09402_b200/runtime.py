@@ -252,6 +252,12 @@ class Engine:
         if self.transform_first(l):
             return self._layer_transform_first(l, x, layer, rows, y, last,
                                                t0, defer_metrics, host_out)
+        if not x.is_cuda and self.world > 1 and x.shape[0] == nloc \
+                and nloc != self.num_vertices:
+            # a rank holding only its own rows (its partition of the layer
+            # input): upload them and all-gather the full input (SURVEY.md
+            # §8e: every source row reaches every rank once per layer)
+            x = self.gather(x.to("cuda", non_blocking=True))
         if x.is_cuda:
             layer.run_resident(self.graph, x, rows, input_flag=input_flag)
         else:  # host (pinned) input: stream it in tiles (K1 streamer)

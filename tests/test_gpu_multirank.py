@@ -51,7 +51,7 @@ def _engine(model, graph, w, backend, rank, world, group=None):
     return Engine(graph, w, cfg, rank=rank, world=world, dist_group=group)
 
 
-def _worker(rank, world, port, model, backend, q):
+def _worker(rank, world, port, model, backend, q, own=False):
     sys.path.insert(0, str(HERE.parent))
     sys.path.insert(0, str(HERE))
     import torch
@@ -64,7 +64,11 @@ def _worker(rank, world, port, model, backend, q):
         graph, feats, w = _case(model)
         eng = _engine(model, graph, w, backend, rank, world,
                       dist.group.WORLD)
-        y, metrics = eng.infer(torch.as_tensor(feats).cuda())
+        # own=True: the rank holds only its partition of the input, in
+        # pinned host memory (the engine uploads and all-gathers it)
+        x = torch.as_tensor(feats[eng.lo:eng.hi]).pin_memory() if own \
+            else torch.as_tensor(feats).cuda()
+        y, metrics = eng.infer(x)
         full = gather_ranges(y, eng.ranges)
         q.put((rank, full.cpu().numpy() if rank == 0 else None,
                sum(m.messages for m in metrics)))
@@ -74,17 +78,20 @@ def _worker(rank, world, port, model, backend, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("model,backend", [("gcn", "stable"),
-                                           ("sage", "tcgen05"),
-                                           ("gin", "tcgen05"),
-                                           ("gat", "tcgen05")])
-def test_two_ranks_on_one_gpu_match_single_rank(model, backend):
+@pytest.mark.parametrize("model,backend,own", [("gcn", "stable", False),
+                                               ("sage", "tcgen05", False),
+                                               ("gin", "tcgen05", False),
+                                               ("gat", "tcgen05", False),
+                                               ("gcn", "tcgen05", True),
+                                               ("sage", "tcgen05", True)])
+def test_two_ranks_on_one_gpu_match_single_rank(model, backend, own):
     import torch
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, model, backend, q))
+    procs = [ctx.Process(target=_worker,
+                         args=(r, 2, port, model, backend, q, own))
              for r in range(2)]
     for p in procs:
         p.start()
