@@ -71,6 +71,10 @@ LARGE_G = 8
 SLICE = {
     "igb-large-sage-rank0of8": ("SAGE", [1024, 128, 128, 19], 100_000_000,
                                 12, 1024, 1.0),
+    # the same with a hot budget of 10 % of the range: min-pending eviction
+    # fires on every chunk and the control plane replays it exactly
+    "igb-large-sage-rank0of8-evict": ("SAGE", [1024, 128, 128, 19],
+                                      100_000_000, 12, 1024, 0.1),
     "papers100m-sage-rank0of8": ("SAGE", [128, 128, 128, 172], 111_000_000,
                                  15, 128, 1.0),
 }
@@ -218,7 +222,12 @@ def run_slice(args):
     clk = clocks.stop()
     ms = start.elapsed_time(stop) / args.steps
     remote = eng.remote_bytes / args.steps
+    # one more step with its metrics taken at once (every layer's verdict
+    # and, under eviction, its exact replay inside this wall-clock window)
+    t_m = time.perf_counter()
     _, metrics = eng.infer(feats)
+    torch.cuda.synchronize()
+    metrics_wall = time.perf_counter() - t_m
     e_rank = graph.num_edges
     nl = len(weights.layers)
     h2d = feats.numel() * feats.element_size()
@@ -248,6 +257,7 @@ def run_slice(args):
         "allgather_bytes_received_per_step": remote,
         "projected_8gpu_edges_per_s_excluding_allgather":
             LARGE_G * nl * e_rank / (ms / 1e3),
+        "step_with_metrics_wall_s": metrics_wall,
         "gpu_launches": launches, "clocks": clk, "generate_s": gen_s}),
         flush=True)
     eng.close()

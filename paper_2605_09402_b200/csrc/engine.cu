@@ -50,6 +50,7 @@ struct EngineArgs {
   int64_t* chunk_touched;
   int64_t phys_slots;
   int32_t keep_chunk_grad;
+  GridSync* gs;  // victim-selection jobs shared with the helper CTAs
 };
 
 struct Smem {
@@ -173,28 +174,126 @@ __device__ int64_t block_sum(Smem& sm, int64_t x) {
   return r;
 }
 
-__device__ uint64_t block_or(Smem& sm, uint64_t x) {
-  // reduce via warp shuffles + smem
-  for (int o = 16; o > 0; o >>= 1) x |= __shfl_xor_sync(0xffffffffu, x, o);
-  __shared__ uint64_t part[32];
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = x;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    uint64_t y = part[threadIdx.x];
-    for (int o = 16; o > 0; o >>= 1) y |= __shfl_xor_sync(0xffffffffu, y, o);
-    if (threadIdx.x == 0) sm.bcast[1] = (int64_t)y;
-  }
-  __syncthreads();
-  uint64_t r = (uint64_t)sm.bcast[1];
-  __syncthreads();
-  return r;
-}
-
 __device__ void log_push(int64_t* log, int64_t& n, int64_t cap, int64_t x,
                          int32_t& overflow) {
   if (n < cap) log[n] = x;
   else overflow = 1;
   n++;
+}
+
+// ---- grid jobs: scans of the hot list shared by all CTAs -------------
+
+constexpr int kJobOr = 1, kJobHist = 2, kJobCollect = 3, kJobExit = 4;
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// this CTA's slices of the hot list (1024-entry blocks, round robin over
+// the grid); OR of keys, 256-bin histogram of the masked-prefix keys, or
+// the victims (keys <= prefix) appended through gs->nv
+__device__ void job_slice(const EngineArgs& A, int type, int byte,
+                          uint64_t prefix, uint64_t mask, int32_t* victims,
+                          uint32_t* shist) {
+  GridSync* gs = A.gs;
+  if (type == kJobHist) {
+    for (int j = threadIdx.x; j < 256; j += kThreads) shist[j] = 0;
+    __syncthreads();
+  }
+  uint64_t o = 0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+       j < A.phys_slots; j += stride) {
+    const int32_t v = A.st.hot_list[j];
+    if (v < 0) continue;
+    const uint64_t key = vkey(A, v);
+    if (type == kJobOr) {
+      o |= key;
+    } else if (type == kJobHist) {
+      if ((key & mask) == prefix)
+        atomicAdd(&shist[(key >> (8 * byte)) & 255u], 1u);
+    } else if (key <= prefix) {
+      victims[atomicAdd(&gs->nv, 1)] = v;
+    }
+  }
+  if (type == kJobOr) {
+    for (int s2 = 16; s2 > 0; s2 >>= 1) o |= __shfl_xor_sync(0xffffffffu, o, s2);
+    if ((threadIdx.x & 31) == 0 && o)
+      atomicOr(reinterpret_cast<unsigned long long*>(&gs->anybits),
+               (unsigned long long)o);
+  } else if (type == kJobHist) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < 256; j += kThreads)
+      if (shist[j]) atomicAdd(&gs->hist[j], shist[j]);
+  }
+  __syncthreads();
+}
+
+// CTA 0: post a job, take its own slice, wait for the helpers; returns
+// the OR of keys (kJobOr) or the victim count (kJobCollect)
+__device__ uint64_t grid_job(const EngineArgs& A, Smem& sm, int type,
+                             int byte, uint64_t prefix, uint64_t mask,
+                             int32_t* victims) {
+  GridSync* gs = A.gs;
+  const unsigned helpers = gridDim.x - 1;
+  if (threadIdx.x == 0) {
+    if (type == kJobOr) gs->anybits = 0;
+    if (type == kJobCollect) gs->nv = 0;
+    gs->type = type;
+    gs->byte = byte;
+    gs->prefix = prefix;
+    gs->mask = mask;
+  }
+  if (type == kJobHist)
+    for (int j = threadIdx.x; j < 256; j += kThreads) gs->hist[j] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&gs->job, 1u);  // publish
+  }
+  job_slice(A, type, byte, prefix, mask, victims, sm.hist);
+  if (threadIdx.x == 0) {
+    const unsigned want = helpers * ld_volatile(&gs->job);
+    while (ld_volatile(&gs->done) < want) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+  uint64_t r = 0;
+  if (type == kJobOr)
+    r = *reinterpret_cast<const volatile uint64_t*>(&gs->anybits);
+  else if (type == kJobCollect)
+    r = (uint64_t)*reinterpret_cast<const volatile int32_t*>(&gs->nv);
+  __syncthreads();
+  return r;
+}
+
+// helper CTAs: run every posted job on their slices until kJobExit
+__device__ void helper_loop(const EngineArgs& A) {
+  __shared__ uint32_t shist[256];
+  __shared__ unsigned posted;
+  GridSync* gs = A.gs;
+  unsigned seen = 0;
+  while (true) {
+    if (threadIdx.x == 0) {
+      unsigned j;
+      while ((j = ld_volatile(&gs->job)) == seen) __nanosleep(64);
+      __threadfence();
+      posted = j;
+    }
+    __syncthreads();
+    seen = posted;
+    const int type = *reinterpret_cast<const volatile int32_t*>(&gs->type);
+    if (type == kJobExit) return;
+    const int byte = *reinterpret_cast<const volatile int32_t*>(&gs->byte);
+    const uint64_t prefix =
+        *reinterpret_cast<const volatile uint64_t*>(&gs->prefix);
+    const uint64_t mask = *reinterpret_cast<const volatile uint64_t*>(&gs->mask);
+    job_slice(A, type, byte, prefix, mask, A.st.scratch_b, shist);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&gs->done, 1u);
+    }
+  }
 }
 
 // evict(k) (oocgnn/memstore.py:397-411)
@@ -223,36 +322,22 @@ __device__ void evict(const EngineArgs& A, Smem& sm, int64_t k) {
     }
     __syncthreads();
   } else {
-    // radix-select the k-th smallest key over the hot list
-    const uint64_t anybits = [&] {
-      uint64_t o = 0;
-      for (int64_t j = threadIdx.x; j < A.phys_slots; j += kThreads) {
-        const int32_t v = A.st.hot_list[j];
-        if (v >= 0) o |= vkey(A, v);
-      }
-      return block_or(sm, o);
-    }();
+    // radix-select the k-th smallest key over the hot list; every scan
+    // of the hot list is a grid job (all CTAs of the launch take slices)
+    const uint64_t anybits = grid_job(A, sm, kJobOr, 0, 0, 0, victims);
     int top = 0;
     while (top < 7 && (anybits >> (8 * (top + 1))) != 0) top++;
     uint64_t prefix = 0, mask = 0;
     int64_t remaining = k;
     for (int byte = top; byte >= 0; byte--) {
-      for (int j = threadIdx.x; j < 256; j += kThreads) sm.hist[j] = 0;
-      __syncthreads();
-      for (int64_t j = threadIdx.x; j < A.phys_slots; j += kThreads) {
-        const int32_t v = A.st.hot_list[j];
-        if (v < 0) continue;
-        const uint64_t key = vkey(A, v);
-        if ((key & mask) == prefix)
-          atomicAdd(&sm.hist[(key >> (8 * byte)) & 255u], 1u);
-      }
-      __syncthreads();
+      grid_job(A, sm, kJobHist, byte, prefix, mask, victims);
       if (threadIdx.x == 0) {
         int64_t cum = 0;
         int dd = 0;
         for (; dd < 256; dd++) {
-          if (cum + sm.hist[dd] >= remaining) break;
-          cum += sm.hist[dd];
+          const uint32_t h = ld_volatile(&A.gs->hist[dd]);
+          if (cum + h >= remaining) break;
+          cum += h;
         }
         sm.bcast[2] = dd;
         sm.bcast[3] = remaining - cum;
@@ -265,14 +350,8 @@ __device__ void evict(const EngineArgs& A, Smem& sm, int64_t k) {
       __syncthreads();
     }
     // keys are unique: the victims are exactly the keys <= prefix
-    __shared__ int32_t nv;
-    if (threadIdx.x == 0) nv = 0;
-    __syncthreads();
-    for (int64_t j = threadIdx.x; j < A.phys_slots; j += kThreads) {
-      const int32_t v = A.st.hot_list[j];
-      if (v >= 0 && vkey(A, v) <= prefix) victims[atomicAdd(&nv, 1)] = v;
-    }
-    __syncthreads();
+    const int64_t nv = (int64_t)grid_job(A, sm, kJobCollect, 0, prefix, 0,
+                                         victims);
     if (threadIdx.x == 0 && nv != k) set_err(sm, ATLAS_EINVARIANT, nv, k);
     __syncthreads();
     if (sm.err) return;
@@ -494,6 +573,10 @@ __device__ int64_t run_pass(const EngineArgs& A, Smem& sm, const PassView& P,
 }
 
 __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineArgs A) {
+  if (blockIdx.x != 0) {
+    helper_loop(A);
+    return;
+  }
   __shared__ Smem sm;
   if (threadIdx.x == 0) {
     sm.sc = *A.sc;
@@ -546,6 +629,11 @@ __global__ void __launch_bounds__(kThreads, 1) engine_kernel(EngineArgs A) {
   if (threadIdx.x == 0) {
     if (sm.err) s.err = sm.err;
     *A.sc = s;
+    if (gridDim.x > 1) {  // release the helpers
+      A.gs->type = kJobExit;
+      __threadfence();
+      atomicAdd(&A.gs->job, 1u);
+    }
   }
 }
 
@@ -713,7 +801,36 @@ void engine_run_chunks(atlas_layer* L, const uint64_t* runs,
   A.chunk_touched = stats.ptr + std::max<int64_t>(nchunks, 1);
   A.phys_slots = phys_slots_of(L);
   A.keep_chunk_grad = nchunks == 1 ? 1 : 0;
-  engine_kernel<<<1, kThreads, 0, s>>>(A);
+  // helper CTAs share the victim scans; a cooperative launch guarantees
+  // they are co-resident with CTA 0 (which spins on them). Scans of a
+  // small hot list stay on CTA 0.
+  L->grid_sync.reserve(1);
+  ATLAS_CUDA(cudaMemsetAsync(L->grid_sync.ptr, 0, sizeof(GridSync), s));
+  A.gs = L->grid_sync.ptr;
+  int grid = 1;
+  if (A.phys_slots > 8 * kThreads && L->desc.policy != ATLAS_RND) {
+    int dev = 0, sms = 0, coop = 0, per_sm = 0;
+    ATLAS_CUDA(cudaGetDevice(&dev));
+    ATLAS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount,
+                                      dev));
+    ATLAS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch,
+                                      dev));
+    ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, engine_kernel, kThreads, 0));
+    const int64_t want = ceil_div(A.phys_slots, 4 * kThreads);
+    if (coop && per_sm > 0)
+      grid = (int)std::max<int64_t>(
+          1, std::min<int64_t>(std::min<int64_t>(want, (int64_t)sms * per_sm),
+                               64));
+  }
+  if (grid > 1) {
+    void* args[] = {&A};
+    ATLAS_CUDA(cudaLaunchCooperativeKernel((const void*)engine_kernel,
+                                           dim3(grid), dim3(kThreads), args,
+                                           0, s));
+  } else {
+    engine_kernel<<<1, kThreads, 0, s>>>(A);
+  }
   count_launch();
   ATLAS_LAUNCH_CHECK();
   std::vector<int64_t> h(2 * std::max<int64_t>(nchunks, 1));

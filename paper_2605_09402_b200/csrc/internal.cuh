@@ -85,6 +85,18 @@ struct EngineScalars {
   int64_t err_info[4];
 };
 
+// Victim selection is a grid job: CTA 0 (the state machine) posts a scan
+// of the hot list and helper CTAs of the same cooperative launch share it.
+struct GridSync {
+  unsigned job;   // posted job count (CTA 0)
+  unsigned done;  // helper completions, cumulative
+  int32_t type, byte;
+  uint64_t prefix, mask;
+  uint64_t anybits;
+  uint32_t hist[256];
+  int32_t nv;
+};
+
 struct EngineConfig {
   int64_t lo, hi, nloc;
   int64_t slot_count, evict_batch, sub_batch;
@@ -114,6 +126,7 @@ struct atlas_layer {
   atlas::DevBuf<int32_t> chunk_grad;
   atlas::DevBuf<int64_t> chunk_grad_batches;
   atlas::DevBuf<atlas::EngineScalars> scalars;
+  atlas::DevBuf<atlas::GridSync> grid_sync;
   atlas::DevBuf<int64_t> first_pos, last_pos;  // spans (per local vertex)
   std::vector<int64_t> chunk_reloads, chunk_touched;
   bool engine_initialized = false;
