@@ -264,18 +264,54 @@ def run_slice(args):
 
 
 def gat_agg_bytes(graph, weights, layouts, rank_range, zsize):
-    """GAT pass B per layer: per in-edge the source's z part (H*F) and its
-    el sector (32 B), its u32 id; per destination CSC/degree (12 B), its er
-    sector, and the output row written once."""
+    """GAT pass B per layer: per in-edge the source's z part (H*F) and,
+    unless el is recomputed from z (line-aligned f32 rows, gat_ring), its
+    el sector (32 B), its u32 id; per destination CSC/degree (12 B), its
+    er sector, and the output row written once."""
     lo, hi = rank_range
     e_g, v_g = int(graph.offsets[-1]), hi - lo
     out = []
     for l, (lw, lay) in enumerate(zip(weights.layers, layouts)):
         last = l == len(weights.layers) - 1
         osz = 4 if last else zsize
-        out.append(e_g * (lw.hf * zsize + 32) + 4 * e_g + 12 * v_g + 32 * v_g
-                   + v_g * weights.out_dim(l) * osz)
+        el = 0 if lay.line_rows else 32
+        out.append(e_g * (lw.hf * zsize + el) + 4 * e_g + 12 * v_g
+                   + 32 * v_g + v_g * weights.out_dim(l) * osz)
     return out
+
+
+def transform_roofline(weights, eng, per_layer, in_sizes, peaks, nloc,
+                       nrows):
+    """The dense transform per layer (tcgen05 GEMM): algorithmic HBM bytes
+    (input rows once, output rows once, W once) and flops 2*rows*K*N over
+    the layer's measured transform time. Aggregate-first: the f32 records
+    (nloc x agg_dim) -> out. Transform-first: the layer input (all rows)
+    -> z (npad per half, f32)."""
+    out = []
+    for l, lw in enumerate(weights.layers):
+        t_ms = statistics.mean(step[l].transform_ms for step in per_layer)
+        last = l == len(weights.layers) - 1
+        if getattr(eng, "transform_first", lambda _: False)(l):
+            k = weights.embedding_dim(l)
+            npad = -(-lw.out_dim // 4) * 4
+            n = npad * (2 if weights.kind == 1 else 1)
+            rows = nrows
+            b = rows * k * in_sizes[l] + rows * n * 4 + n * k * 4
+        else:
+            k, n = weights.agg_dim(l), lw.out_dim
+            rows = nloc
+            osz = 4 if last else in_sizes[min(l + 1, len(in_sizes) - 1)]
+            b = rows * k * 4 + rows * n * osz + n * k * 4
+        fl = 2.0 * rows * k * n
+        gbs = b / (t_ms / 1e3) / 1e9 if t_ms > 0 else None
+        out.append({"layer": l, "rows": rows, "k": k, "n": n,
+                    "ms": round(t_ms, 3), "bytes": b,
+                    "hbm_gbs": gbs and round(gbs, 1),
+                    "hbm_frac": gbs and round(gbs / peaks["hbm_gbs"], 3),
+                    "tflops": t_ms and round(fl / (t_ms / 1e3) / 1e12, 1)})
+    return {"bound": "hbm", "note": "3xTF32 (f32 input) or hi/lo f16 "
+            "(f16 input) on tcgen05; intensity <= 64 flop/B, below the "
+            "ridge, so HBM bytes are the roofline", "layers": out}
 
 
 def agg_bytes(graph, weights, rank_range, in_sizes, eng=None, out_size=4):
@@ -574,14 +610,19 @@ def main():
     if is_gat:
         per_b = gat_agg_bytes(graph, weights, eng.layouts, (eng.lo, eng.hi),
                               in_sizes[-1])
-        kinds = ["gat_bulk"] * nlayers
+        kinds = ["gat_ring" if eng.layouts[l].line_rows else "gat_bulk"
+                 for l in range(nlayers)]
     else:
         per_b = agg_bytes(graph, weights, (eng.lo, eng.hi), in_sizes, eng,
                           in_sizes[-1])
-        kinds = ["agg_tf_ring / agg_ring_epi (transform-first)"
-                 if eng.transform_first(l) else
-                 ("agg_bulk" if weights.embedding_dim(l) * in_sizes[l] > 512
-                  else "agg_ring") for l in range(nlayers)]
+
+        def kind_of(l):
+            if eng.transform_first(l):
+                return "agg_tf_ring / agg_ring_epi (transform-first)"
+            row = weights.embedding_dim(l) * in_sizes[l]
+            return ("agg_bulk" if row > 512 else
+                    "agg_ring" if row > 256 else "agg_sub_ring")
+        kinds = [kind_of(l) for l in range(nlayers)]
     agg_b = sum(per_b)
     # dominant aggregation kernel: the kind with the most device time;
     # achieved = its algorithmic bytes / its mean launch time (CUDA events)
@@ -680,6 +721,9 @@ def main():
                                  peaks.get("hbm_gbs", 6650.0)}
                              for k, g in groups.items()},
                          "algorithmic_bytes_per_step": agg_b},
+            "transform": None if is_gat else transform_roofline(
+                weights, eng, per_layer, in_sizes, peaks, eng.hi - eng.lo,
+                graph.num_vertices),
             "e2e": e2e_line,
             "bit_exact_backend": None if alt is None else {
                 "backend": alt, "ms_per_step": alt_ms,
