@@ -830,7 +830,7 @@ bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
   const bool res_w = w_res + 2 * x_stage <= budget;
   const int stage_bytes = res_w ? x_stage : x_stage + 2 * BN * BK * 4;
   int stages = (budget - (res_w ? w_res : 0)) / stage_bytes;
-  if (stages > 4) stages = 4;
+  if (stages > 8) stages = 8;
   if (stages < 2) return false;
   const int smem = 1024 + (res_w ? w_res : 0) + stages * stage_bytes +
                    8 * (3 * stages + 6) + 16 + 4 * 256 + 16 +
