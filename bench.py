@@ -453,7 +453,10 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value,
         "unit": "edges/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": None,
+        "warmup": args.warmup,
+        # one full step (3 layers over all E edges) at the sampled rate
+        "ms_per_step": len(weights.layers) * graph.num_edges / value * 1e3,
+        "ms_per_step_note": "extrapolated from the bounded samples",
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "parallelism": "host, 1 thread"},
