@@ -51,6 +51,8 @@ struct EngineArgs {
   int64_t phys_slots;
   int32_t keep_chunk_grad;
   GridSync* gs;  // victim-selection jobs shared with the helper CTAs
+  int64_t grid_min;  // sub-batches of at least this many elements run as
+                     // grid jobs (when the launch has helper CTAs)
 };
 
 struct Smem {
@@ -184,9 +186,138 @@ __device__ void log_push(int64_t* log, int64_t& n, int64_t cap, int64_t x,
 // ---- grid jobs: scans of the hot list shared by all CTAs -------------
 
 constexpr int kJobOr = 1, kJobHist = 2, kJobCollect = 3, kJobExit = 4;
+// sub-batch jobs (large sub-batches only; the element order of every
+// compaction is kept by per-CTA contiguous slices placed by their counts)
+constexpr int kJobClassify = 5, kJobCount2 = 6, kJobWrite2 = 7,
+              kJobAdmit = 8, kJobDeliver = 9, kJobCount0 = 10,
+              kJobWrite0 = 11, kJobRelease = 12;
 
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
   return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+__device__ __forceinline__ void warp_add(unsigned long long* dst, int64_t x) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0 && x)
+    atomicAdd(dst, (unsigned long long)x);
+}
+
+// this CTA's part of a sub-batch job (see GridSync)
+__device__ void pass_slice(const EngineArgs& A, int type) {
+  GridSync* gs = A.gs;
+  const PassView P{gs->pkind, static_cast<const uint64_t*>(gs->pptr),
+                   static_cast<const int32_t*>(gs->pptr), gs->pfirst};
+  const int64_t lo = gs->lo, n = gs->n;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t first = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (type == kJobClassify) {
+    int64_t need = 0, bad = 0;
+    for (int64_t i = first; i < n; i += stride) {
+      const uint8_t st = A.st.state[P.v(lo + i)];
+      need += st != HOT;
+      bad += st > COLD;
+    }
+    warp_add(&gs->sum[0], need);
+    warp_add(&gs->sum[1], bad);
+  } else if (type == kJobAdmit) {
+    const int64_t ftop0 = gs->base;
+    for (int64_t i = first; i < n; i += stride) {
+      const int32_t v = gs->list[i];
+      const int32_t slot = A.st.free_stack[ftop0 - 1 - i];
+      A.st.state[v] = HOT;
+      A.st.slot_of[v] = slot;
+      A.st.hot_list[slot] = v;
+      if (gs->flag) A.st.unique_reloaded[v] = 1;
+    }
+  } else if (type == kJobDeliver) {
+    int64_t msgs = 0, bad = 0;
+    const uint64_t seq0 = (uint64_t)gs->base;
+    for (int64_t i = first; i < n; i += stride) {
+      const int32_t v = P.v(lo + i);
+      const uint32_t c = P.cnt(lo + i);
+      const uint32_t p = A.st.pending[v];
+      if (p < c) {
+        bad++;
+        continue;
+      }
+      A.st.pending[v] = p - c;
+      A.st.seq[v] = (uint32_t)(seq0 + (uint64_t)i);
+      msgs += c;
+    }
+    warp_add(&gs->sum[0], msgs);
+    warp_add(&gs->sum[1], bad);
+  } else if (type == kJobRelease) {
+    const int64_t ftop0 = gs->base;
+    for (int64_t i = first; i < n; i += stride) {
+      const int32_t v = gs->list[i];
+      const int32_t slot = A.st.slot_of[v];
+      A.st.state[v] = COMPLETED;
+      A.st.slot_of[v] = -1;
+      A.st.hot_list[slot] = -1;
+      A.st.free_stack[ftop0 + i] = slot;
+      if (A.keep_chunk_grad) A.st.chunk_grad[gs->base2 + i] = v;
+    }
+  } else {
+    // ordered compactions: CTA b owns elements [b*slice, (b+1)*slice)
+    __shared__ BlockScan::TempStorage scan;
+    __shared__ int64_t tot[2];
+    const int64_t s0 = (int64_t)blockIdx.x * gs->slice;
+    const int64_t s1 = min(n, s0 + gs->slice);
+    const bool two = type == kJobCount2 || type == kJobWrite2;
+    // predicate q of element i: 0 = fresh / done, 1 = cold
+    auto pred = [&](int64_t i, int q) -> bool {
+      const int32_t v = P.v(lo + i);
+      if (!two) return A.st.pending[v] == 0;
+      const uint8_t st = A.st.state[v];
+      return q == 0 ? st == NOT_STARTED : st == COLD;
+    };
+    if (type == kJobCount2 || type == kJobCount0) {
+      int64_t c[2] = {0, 0};
+      for (int64_t i = s0 + threadIdx.x; i < s1; i += kThreads) {
+        c[0] += pred(i, 0);
+        if (two) c[1] += pred(i, 1);
+      }
+      if (threadIdx.x == 0) tot[0] = tot[1] = 0;
+      __syncthreads();
+      for (int q = 0; q < (two ? 2 : 1); q++) {
+        int64_t x = c[q];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) == 0 && x)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&tot[q]),
+                    (unsigned long long)x);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        gs->cnt[blockIdx.x][0] = tot[0];
+        gs->cnt[blockIdx.x][1] = tot[1];
+      }
+    } else {  // kJobWrite2 / kJobWrite0: place this slice's matches
+      int64_t off[2] = {0, 0}, all0 = 0;
+      for (int b = 0; b < (int)gridDim.x; b++) {
+        const int64_t c0 = *reinterpret_cast<volatile int64_t*>(&gs->cnt[b][0]);
+        const int64_t c1 = *reinterpret_cast<volatile int64_t*>(&gs->cnt[b][1]);
+        if (b < (int)blockIdx.x) {
+          off[0] += c0;
+          off[1] += c1;
+        }
+        all0 += c0;
+      }
+      off[1] += all0;  // cold entries follow all fresh ones
+      for (int q = 0; q < (two ? 2 : 1); q++) {
+        int64_t base = off[q];
+        for (int64_t t0 = s0; t0 < s1; t0 += kThreads) {
+          const int64_t i = t0 + threadIdx.x;
+          const int64_t f = (i < s1 && pred(i, q)) ? 1 : 0;
+          int64_t pos, total;
+          BlockScan(scan).ExclusiveSum(f, pos, total);
+          if (f) gs->out[base + pos] = P.v(lo + i);
+          base += total;
+          __syncthreads();
+        }
+      }
+    }
+  }
+  __syncthreads();
 }
 
 // this CTA's slices of the hot list (1024-entry blocks, round robin over
@@ -196,6 +327,10 @@ __device__ void job_slice(const EngineArgs& A, int type, int byte,
                           uint64_t prefix, uint64_t mask, int32_t* victims,
                           uint32_t* shist) {
   GridSync* gs = A.gs;
+  if (type >= kJobClassify) {
+    pass_slice(A, type);
+    return;
+  }
   if (type == kJobHist) {
     for (int j = threadIdx.x; j < 256; j += kThreads) shist[j] = 0;
     __syncthreads();
@@ -265,6 +400,31 @@ __device__ uint64_t grid_job(const EngineArgs& A, Smem& sm, int type,
     r = (uint64_t)*reinterpret_cast<const volatile int32_t*>(&gs->nv);
   __syncthreads();
   return r;
+}
+
+// CTA 0: run a sub-batch job whose GridSync fields thread 0 has set
+__device__ void pass_job(const EngineArgs& A, Smem& sm, int type) {
+  GridSync* gs = A.gs;
+  if (threadIdx.x == 0) {
+    gs->type = type;
+    if (type == kJobClassify || type == kJobDeliver)
+      gs->sum[0] = gs->sum[1] = 0;
+    __threadfence();
+    atomicAdd(&gs->job, 1u);  // publish
+  }
+  __syncthreads();
+  job_slice(A, type, 0, 0, 0, nullptr, sm.hist);
+  if (threadIdx.x == 0) {
+    const unsigned want = (gridDim.x - 1) * ld_volatile(&gs->job);
+    while (ld_volatile(&gs->done) < want) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int64_t gs_sum(const GridSync* gs, int k) {
+  return (int64_t)*reinterpret_cast<const volatile unsigned long long*>(
+      &gs->sum[k]);
 }
 
 // helper CTAs: run every posted job on their slices until kJobExit
@@ -563,11 +723,140 @@ __device__ void sub_batch(const EngineArgs& A, Smem& sm, const PassView& P,
   release(A, sm, A.st.scratch_a, nd);
 }
 
+// sub_batch() with every pass over the batch as a grid job (large
+// sub-batches, MINPEND/LRU without logs): the same steps in the same order;
+// compactions keep element order through per-CTA contiguous slices
+__device__ void sub_batch_grid(const EngineArgs& A, Smem& sm,
+                               const PassView& P, int64_t lo, int64_t n) {
+  EngineScalars& s = sm.sc;
+  GridSync* gs = A.gs;
+  auto pass_fields = [&]() {
+    if (threadIdx.x == 0) {
+      gs->pkind = P.kind;
+      gs->pptr = P.kind == EDGEPASS ? static_cast<const void*>(P.runs)
+                                    : static_cast<const void*>(P.list);
+      gs->pfirst = P.first;
+      gs->lo = lo;
+      gs->n = n;
+      gs->slice = ((n + gridDim.x - 1) / gridDim.x + kThreads - 1) /
+                  kThreads * kThreads;
+      gs->out = A.st.scratch_a;
+    }
+  };
+  auto counts = [&](int64_t& c0, int64_t& c1) {
+    if (threadIdx.x == 0) {
+      int64_t a = 0, b = 0;
+      for (int k = 0; k < (int)gridDim.x; k++) {
+        a += *reinterpret_cast<volatile int64_t*>(&gs->cnt[k][0]);
+        b += *reinterpret_cast<volatile int64_t*>(&gs->cnt[k][1]);
+      }
+      sm.bcast[2] = a;
+      sm.bcast[3] = b;
+    }
+    __syncthreads();
+    c0 = sm.bcast[2];
+    c1 = sm.bcast[3];
+    __syncthreads();
+  };
+  // classify; evict until the non-hot part fits
+  while (true) {
+    pass_fields();
+    pass_job(A, sm, kJobClassify);
+    const int64_t need = gs_sum(gs, 0), bad = gs_sum(gs, 1);
+    if (bad) {
+      if (threadIdx.x == 0) set_err(sm, ATLAS_ESTATE, bad, 0);
+      __syncthreads();
+      return;
+    }
+    const int64_t free = A.cfg.slot_count - s.hot_pop;
+    if (need <= free) break;
+    if (need > A.cfg.slot_count) {
+      if (threadIdx.x == 0) set_err(sm, ATLAS_ECONFIG, need, A.cfg.slot_count);
+      __syncthreads();
+      return;
+    }
+    while (A.cfg.slot_count - s.hot_pop < need) {
+      const int64_t deficit = need - (A.cfg.slot_count - s.hot_pop);
+      evict(A, sm, deficit > A.cfg.evict_batch ? deficit : A.cfg.evict_batch);
+      if (sm.err) return;
+    }
+  }
+  // fresh then cold, each in batch order, into scratch_a
+  pass_fields();
+  pass_job(A, sm, kJobCount2);
+  int64_t nf, nc;
+  counts(nf, nc);
+  pass_job(A, sm, kJobWrite2);
+  for (int r = 0; r < 2; r++) {
+    const int64_t m = r ? nc : nf;
+    if (m == 0) continue;
+    if (threadIdx.x == 0) {
+      gs->list = A.st.scratch_a + (r ? nf : 0);
+      gs->n = m;
+      gs->base = s.free_top;
+      gs->flag = r;
+    }
+    pass_job(A, sm, kJobAdmit);
+    if (threadIdx.x == 0) {
+      s.free_top -= m;
+      s.hot_pop += m;
+      s.admissions += m;
+      if (s.hot_pop > s.hot_peak) s.hot_peak = s.hot_pop;
+      if (s.hot_pop > A.cfg.slot_count) set_err(sm, ATLAS_EBUDGET, s.hot_pop, 0);
+      if (r) s.reloads += m;
+    }
+    __syncthreads();
+    if (sm.err) return;
+  }
+  // deliveries: pending -= cnt, seq = message index
+  pass_fields();
+  if (threadIdx.x == 0) gs->base = (int64_t)s.seq_ctr;
+  pass_job(A, sm, kJobDeliver);
+  const int64_t msgs = gs_sum(gs, 0), bad = gs_sum(gs, 1);
+  if (bad) {
+    if (threadIdx.x == 0) set_err(sm, ATLAS_ECONSISTENCY, bad, 0);
+    __syncthreads();
+    return;
+  }
+  if (threadIdx.x == 0) {
+    s.messages += msgs;
+    s.seq_ctr += (uint64_t)n;
+  }
+  __syncthreads();
+  // graduation: pending == 0 in batch order
+  pass_fields();
+  pass_job(A, sm, kJobCount0);
+  int64_t nd, unused;
+  counts(nd, unused);
+  pass_job(A, sm, kJobWrite0);
+  if (nd == 0) return;
+  if (threadIdx.x == 0) {
+    gs->list = A.st.scratch_a;
+    gs->n = nd;
+    gs->base = s.free_top;
+    gs->base2 = s.chunk_grad_n;
+  }
+  pass_job(A, sm, kJobRelease);
+  if (threadIdx.x == 0) {
+    s.free_top += nd;
+    s.hot_pop -= nd;
+    s.graduations += nd;
+    if (A.keep_chunk_grad) {
+      s.chunk_grad_n += nd;
+      A.st.chunk_grad_batches[s.chunk_grad_batches_n++] = nd;
+    }
+  }
+  __syncthreads();
+}
+
 __device__ int64_t run_pass(const EngineArgs& A, Smem& sm, const PassView& P,
                             int64_t n) {
+  const bool grid_ok = gridDim.x > 1 && P.kind != PREPASS &&
+                       A.cfg.policy != ATLAS_RND && !A.cfg.record_log;
   for (int64_t lo = 0; lo < n && !sm.err; lo += A.cfg.sub_batch) {
     const int64_t m = min(A.cfg.sub_batch, n - lo);
-    sub_batch(A, sm, P, lo, m);
+    if (grid_ok && m >= A.grid_min) sub_batch_grid(A, sm, P, lo, m);
+    else sub_batch(A, sm, P, lo, m);
   }
   return n;
 }
@@ -807,8 +1096,15 @@ void engine_run_chunks(atlas_layer* L, const uint64_t* runs,
   L->grid_sync.reserve(1);
   ATLAS_CUDA(cudaMemsetAsync(L->grid_sync.ptr, 0, sizeof(GridSync), s));
   A.gs = L->grid_sync.ptr;
+  // ATLAS_ENGINE_GRID_MIN (tests): smallest sub-batch run as grid jobs
+  static const int64_t grid_min = [] {
+    const char* e = getenv("ATLAS_ENGINE_GRID_MIN");
+    return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)16384;
+  }();
+  A.grid_min = grid_min;
   int grid = 1;
-  if (A.phys_slots > 8 * kThreads && L->desc.policy != ATLAS_RND) {
+  if ((A.phys_slots > 8 * kThreads || grid_min < 16384) &&
+      L->desc.policy != ATLAS_RND) {
     int dev = 0, sms = 0, coop = 0, per_sm = 0;
     ATLAS_CUDA(cudaGetDevice(&dev));
     ATLAS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount,
@@ -817,7 +1113,8 @@ void engine_run_chunks(atlas_layer* L, const uint64_t* runs,
                                       dev));
     ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &per_sm, engine_kernel, kThreads, 0));
-    const int64_t want = ceil_div(A.phys_slots, 4 * kThreads);
+    const int64_t want = std::max<int64_t>(
+        ceil_div(A.phys_slots, 4 * kThreads), grid_min < 16384 ? 8 : 1);
     if (coop && per_sm > 0)
       grid = (int)std::max<int64_t>(
           1, std::min<int64_t>(std::min<int64_t>(want, (int64_t)sms * per_sm),

@@ -95,6 +95,19 @@ struct GridSync {
   uint64_t anybits;
   uint32_t hist[256];
   int32_t nv;
+  // sub-batch jobs over pass elements [lo, lo + n) (engine.cu pass_slice)
+  int32_t pkind;
+  const void* pptr;  // runs (EDGEPASS) or vertex list (PREPASS)
+  int64_t pfirst;    // SELFPASS first vertex
+  int64_t lo, n;
+  int64_t base;      // admit / release: free-stack top; deliver: seq base
+  int64_t base2;     // release: chunk_grad fill
+  int32_t flag;      // admit: reload
+  const int32_t* list;
+  int32_t* out;
+  int64_t slice;     // elements per CTA slice of an ordered compaction
+  unsigned long long sum[2];
+  int64_t cnt[64][2];  // per-CTA counts (<= 64 CTAs)
 };
 
 struct EngineConfig {
