@@ -227,6 +227,7 @@ __device__ void pass_slice(const EngineArgs& A, int type) {
       A.st.state[v] = HOT;
       A.st.slot_of[v] = slot;
       A.st.hot_list[slot] = v;
+      A.st.slot_key[slot] = vkey(A, v);
       if (gs->flag) A.st.unique_reloaded[v] = 1;
     }
   } else if (type == kJobDeliver) {
@@ -242,6 +243,7 @@ __device__ void pass_slice(const EngineArgs& A, int type) {
       }
       A.st.pending[v] = p - c;
       A.st.seq[v] = (uint32_t)(seq0 + (uint64_t)i);
+      A.st.slot_key[A.st.slot_of[v]] = vkey(A, v);
       msgs += c;
     }
     warp_add(&gs->sum[0], msgs);
@@ -254,6 +256,7 @@ __device__ void pass_slice(const EngineArgs& A, int type) {
       A.st.state[v] = COMPLETED;
       A.st.slot_of[v] = -1;
       A.st.hot_list[slot] = -1;
+      A.st.slot_key[slot] = ~0ull;
       A.st.free_stack[ftop0 + i] = slot;
       if (A.keep_chunk_grad) A.st.chunk_grad[gs->base2 + i] = v;
     }
@@ -337,18 +340,19 @@ __device__ void job_slice(const EngineArgs& A, int type, int byte,
   }
   uint64_t o = 0;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
+  // keys by slot: a coalesced 8-byte read per slot (free slots hold ~0,
+  // which no real key reaches: seq < 2^32, pending < 2^32)
   for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x;
        j < A.phys_slots; j += stride) {
-    const int32_t v = A.st.hot_list[j];
-    if (v < 0) continue;
-    const uint64_t key = vkey(A, v);
+    const uint64_t key = A.st.slot_key[j];
+    if (key == ~0ull) continue;
     if (type == kJobOr) {
       o |= key;
     } else if (type == kJobHist) {
       if ((key & mask) == prefix)
         atomicAdd(&shist[(key >> (8 * byte)) & 255u], 1u);
     } else if (key <= prefix) {
-      victims[atomicAdd(&gs->nv, 1)] = v;
+      victims[atomicAdd(&gs->nv, 1)] = A.st.hot_list[j];
     }
   }
   if (type == kJobOr) {
@@ -524,6 +528,7 @@ __device__ void evict(const EngineArgs& A, Smem& sm, int64_t k) {
     A.st.state[v] = COLD;
     A.st.slot_of[v] = -1;
     A.st.hot_list[slot] = -1;
+    A.st.slot_key[slot] = ~0ull;
     A.st.free_stack[ftop0 + i] = slot;
   }
   __syncthreads();
@@ -558,6 +563,7 @@ __device__ void admit(const EngineArgs& A, Smem& sm, const int32_t* list,
     A.st.state[v] = HOT;
     A.st.slot_of[v] = slot;
     A.st.hot_list[slot] = v;
+    A.st.slot_key[slot] = vkey(A, v);
     if (reload) A.st.unique_reloaded[v] = 1;
     if (A.cfg.policy == ATLAS_RND) {
       A.st.rnd_members[rnd0 + i] = v;
@@ -598,6 +604,7 @@ __device__ void release(const EngineArgs& A, Smem& sm, const int32_t* list,
     A.st.state[v] = COMPLETED;
     A.st.slot_of[v] = -1;
     A.st.hot_list[slot] = -1;
+    A.st.slot_key[slot] = ~0ull;
     A.st.free_stack[ftop0 + i] = slot;
     if (A.keep_chunk_grad) A.st.chunk_grad[s.chunk_grad_n + i] = v;
   }
@@ -699,6 +706,7 @@ __device__ void sub_batch(const EngineArgs& A, Smem& sm, const PassView& P,
     }
     A.st.pending[v] = p - c;
     A.st.seq[v] = (uint32_t)(s.seq_ctr + (uint64_t)i);
+    A.st.slot_key[A.st.slot_of[v]] = vkey(A, v);
     msgs += c;
   }
   msgs = block_sum(sm, msgs);
@@ -942,11 +950,12 @@ __global__ void init_state(uint32_t* pending, uint8_t* state, uint32_t* seq,
   }
 }
 
-__global__ void init_slots(int32_t* hot_list, int32_t* free_stack,
-                           int64_t phys) {
+__global__ void init_slots(int32_t* hot_list, uint64_t* slot_key,
+                           int32_t* free_stack, int64_t phys) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (; i < phys; i += (int64_t)gridDim.x * blockDim.x) {
     hot_list[i] = -1;
+    slot_key[i] = ~0ull;
     free_stack[i] = (int32_t)(phys - 1 - i);
   }
 }
@@ -978,6 +987,7 @@ void engine_init(atlas_layer* L, cudaStream_t s) {
   L->first_pos.alloc(nn);
   L->last_pos.alloc(nn);
   L->hot_list.alloc(phys);
+  L->slot_key.alloc(phys);
   L->free_stack.alloc(phys);
   L->scratch_a.alloc(std::max(phys, nn) + kThreads);
   L->scratch_b.alloc(phys + kThreads + nn + kThreads);
@@ -996,7 +1006,7 @@ void engine_init(atlas_layer* L, cudaStream_t s) {
     count_launch();
     ATLAS_LAUNCH_CHECK();
   }
-  init_slots<<<grid_of(phys), 256, 0, s>>>(L->hot_list.ptr,
+  init_slots<<<grid_of(phys), 256, 0, s>>>(L->hot_list.ptr, L->slot_key.ptr,
                                            L->free_stack.ptr, phys);
   count_launch();
   ATLAS_LAUNCH_CHECK();
@@ -1060,6 +1070,7 @@ void engine_run_chunks(atlas_layer* L, const uint64_t* runs,
   A.st.slot_of = L->slot_of.ptr;
   A.st.unique_reloaded = L->unique_reloaded.ptr;
   A.st.hot_list = L->hot_list.ptr;
+  A.st.slot_key = L->slot_key.ptr;
   A.st.free_stack = L->free_stack.ptr;
   A.st.scratch_a = L->scratch_a.ptr;
   A.st.scratch_b = L->scratch_b.ptr;

@@ -51,6 +51,7 @@ struct EngineState {
   uint8_t* unique_reloaded;
   // hot set
   int32_t* hot_list;   // slot -> local vertex or -1
+  uint64_t* slot_key;  // slot -> its vertex's eviction key, or ~0 if free
   int32_t* free_stack; // LIFO of free slots
   // scratch (size >= slot_count + 1024)
   int32_t* scratch_a;
@@ -134,6 +135,7 @@ struct atlas_layer {
   atlas::DevBuf<int32_t> slot_of;
   atlas::DevBuf<uint8_t> unique_reloaded;
   atlas::DevBuf<int32_t> hot_list, free_stack, scratch_a, scratch_b;
+  atlas::DevBuf<uint64_t> slot_key;
   atlas::DevBuf<int32_t> rnd_members, rnd_pos;
   atlas::DevBuf<int64_t> log_victims, log_reloads, log_grad;
   atlas::DevBuf<int32_t> chunk_grad;
