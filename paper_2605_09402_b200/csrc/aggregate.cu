@@ -653,11 +653,19 @@ __global__ void __launch_bounds__(256, kSubBlocks)
 // 32/LPD sub-groups of LPD lanes per warp, each walking its own run of
 // consecutive destinations (one contiguous CSC range) in lockstep with the
 // others: every iteration each sub-group consumes one edge and issues the
-// cp.async of the edge kRing ahead into its lanes' shared-memory ring, so
-// kRing rows per lane stay in flight across destination boundaries and
-// the per-edge instruction cost is shared by 32/LPD destinations.
+// cp.async of the edge kTfRing ahead into its lanes' shared-memory ring,
+// so kTfRing rows per lane stay in flight across destination boundaries
+// and the per-edge instruction cost is shared by 32/LPD destinations.
+// ring depth / blocks per SM by sub-group width (measured: 8-lane groups,
+// e.g. 20-wide z, are latency-bound at 16 deep x 3 blocks; 16-lane groups
+// are issue-bound and keep the deeper ring)
+template <int LPD>
+constexpr int kTfRing = LPD == 8 ? 8 : 16;
+template <int LPD>
+constexpr int kTfBlocks = LPD == 8 ? 5 : 4;
+
 template <int LPD, int MODEL, typename OutT>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, kTfBlocks<LPD>)
     agg_tf_ring(const float* __restrict__ z, int64_t ldz,
                 const int64_t* __restrict__ csc_ptr,
                 const uint32_t* __restrict__ csc_src,
@@ -672,7 +680,7 @@ __global__ void __launch_bounds__(256, 4)
   const int colc = lane_on ? col : d - 4;  // clamped: branch-free copies
   const uint32_t ring_lane =
       (uint32_t)__cvta_generic_to_shared(ring_smem + (threadIdx.x >> 5) *
-                                                         (kRing * 32)) +
+                                                         (kTfRing<LPD> * 32)) +
       (uint32_t)lane * 16u;
   const float* __restrict__ zc = z + colc;
   int bad = 0;
@@ -698,7 +706,7 @@ __global__ void __launch_bounds__(256, 4)
         isrc = pe + sl < ne ? src0[pe + sl] : 0u;
       const uint32_t u = __shfl_sync(0xffffffffu, isrc, pe & (LPD - 1), LPD);
       if (more) {
-        cp_async16_s(ring_lane + ((uint32_t)(pe & (kRing - 1)) << 9),
+        cp_async16_s(ring_lane + ((uint32_t)(pe & (kTfRing<LPD> - 1)) << 9),
                      zc + (int64_t)u * ldz);
         pe++;
       }
@@ -743,12 +751,12 @@ __global__ void __launch_bounds__(256, 4)
       }
     };
 #pragma unroll 1
-    for (int k = 0; k < kRing; k++) issue();
+    for (int k = 0; k < kTfRing<LPD>; k++) issue();
     flush();
     while (__any_sync(0xffffffffu, ce < ne)) {
-      cp_async_wait<kRing - 1>();  // the row issued kRing iterations ago
+      cp_async_wait<kTfRing<LPD> - 1>();  // the row issued kTfRing<LPD> iterations ago
       if (ce < ne) {
-        const uint4 r = lds16(ring_lane + ((uint32_t)(ce & (kRing - 1)) << 9));
+        const uint4 r = lds16(ring_lane + ((uint32_t)(ce & (kTfRing<LPD> - 1)) << 9));
         a[0] += __uint_as_float(r.x);
         a[1] += __uint_as_float(r.y);
         a[2] += __uint_as_float(r.z);
@@ -1323,10 +1331,10 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
   if (d <= 64) {  // narrow rows: several destinations per warp
     g->work.reserve(1);
     ATLAS_CUDA(cudaMemsetAsync(g->work.ptr, 0, sizeof(unsigned long long), s));
-    const int smem = 8 * kRing * 32 * 16;
     auto narrow = [&](auto lpd_tag, auto model_tag) {
       constexpr int LPD = decltype(lpd_tag)::value;
       constexpr int M = decltype(model_tag)::value;
+      const int smem = 8 * kTfRing<LPD> * 32 * 16;
       auto go = [&](auto kern) {
         ATLAS_CUDA(cudaFuncSetAttribute(
             kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
