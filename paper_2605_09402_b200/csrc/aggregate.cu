@@ -1241,6 +1241,120 @@ void runs_typed(const void* tile, int64_t ldx, const uint32_t* run_dst,
   }
 }
 
+// ---------------------------------------------------------------------------
+// streamed front end, LAST tile of a whole-input stream (GCN, f32 rows of
+// <= 512 B): every edge a destination still has, [cursor[v], end_v), has its
+// source in this tile, so the remaining work is each destination's edge
+// SUFFIX. Persistent warps take 32 destinations, concatenate their suffixes
+// (warp scan of the lengths) and stream the rows through the per-lane
+// cp.async ring of agg_ring across destination boundaries; each record is
+// resumed from acc when an earlier tile touched it, folded in source order
+// exactly like agg_tile (same guarded divide and add), and stored. This is
+// the part of the stream left after the last copy lands, so it is what the
+// end-to-end time sees; agg_tile (a warp per destination, ~6 edges per
+// tile) runs it at a third of the DRAM rate.
+template <int VEC>
+__global__ void __launch_bounds__(256, 3)
+    agg_suffix_ring(const float* __restrict__ tile, int64_t ldx,
+                    int64_t tile_lo, const int64_t* __restrict__ csc_ptr,
+                    const uint32_t* __restrict__ csc_src,
+                    const uint32_t* __restrict__ indeg, int64_t lo,
+                    int64_t nloc, int d, float* __restrict__ acc,
+                    int64_t ldacc, const int64_t* __restrict__ cursor,
+                    uint8_t* __restrict__ touched,
+                    unsigned long long* __restrict__ work) {
+  using F = Frag<float, VEC>;
+  extern __shared__ uint4 ring_smem[];
+  const int lane = threadIdx.x & 31;
+  const int col = lane * VEC;
+  const bool active = col < d;
+  const int colc = active ? col : d - VEC;
+  const uint32_t ring_lane =
+      (uint32_t)__cvta_generic_to_shared(ring_smem +
+                                         (threadIdx.x >> 5) * (kRing * 32)) +
+      (uint32_t)lane * 16u;
+  const float* __restrict__ xc = tile + colc;
+  while (true) {
+    unsigned long long v0 = 0;
+    if (lane == 0) v0 = atomicAdd(work, (unsigned long long)kGrab);
+    v0 = __shfl_sync(0xffffffffu, v0, 0);
+    if ((int64_t)v0 >= nloc) break;
+    const int64_t v1 = min((int64_t)v0 + kGrab, nloc);
+    // lane j: destination v0 + j, its suffix [b_j, b_j + n_j), its place
+    // off_j in the grab's concatenated edge list
+    const int64_t vj = (int64_t)v0 + lane;
+    int64_t b_j = 0;
+    int n_j = 0;
+    uint32_t dg_j = 0, tch_j = 0;  // in-degree, touched flag of v0 + j
+    if (vj < v1) {
+      b_j = cursor[vj];
+      n_j = (int)(csc_ptr[vj + 1] - b_j);
+      dg_j = indeg[vj];
+      tch_j = touched[vj];
+    }
+    int off_j = n_j;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, off_j, o);
+      if (lane >= o) off_j += y;
+    }
+    const int ne = __shfl_sync(0xffffffffu, off_j, 31);
+    off_j -= n_j;  // exclusive
+    // source id of grab edge k: the last destination j with off_j <= k
+    auto src_of = [&](int k) -> uint32_t {
+      int j = 0;
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1) {
+        const int oc = __shfl_sync(0xffffffffu, off_j, (j + st) & 31);
+        if (j + st < 32 && oc <= k) j += st;
+      }
+      const int64_t bj = __shfl_sync(0xffffffffu, b_j, j);
+      const int oj = __shfl_sync(0xffffffffu, off_j, j);
+      return k < ne ? csc_src[bj + (k - oj)] : 0u;
+    };
+    int pe = 0;
+    uint32_t isrc = src_of(lane);
+    auto issue = [&]() {
+      if (pe < ne) {
+        if ((pe & 31) == 0 && pe != 0) isrc = src_of(pe + lane);
+        const uint32_t u = __shfl_sync(0xffffffffu, isrc, pe & 31);
+        cp_async16_s(ring_lane + ((uint32_t)(pe & (kRing - 1)) << 9),
+                     xc + ((int64_t)u - tile_lo) * ldx);
+        pe++;
+      }
+      cp_async_commit();
+    };
+#pragma unroll 1
+    for (int k = 0; k < kRing; k++) issue();
+    int ce = 0;
+    for (int j = 0; j < (int)(v1 - (int64_t)v0); j++) {
+      const int64_t v = (int64_t)v0 + j;
+      const int nj = __shfl_sync(0xffffffffu, n_j, j);
+      const uint32_t dg = __shfl_sync(0xffffffffu, dg_j, j);
+      const bool zero_row = dg == 0 && v + lo >= tile_lo;
+      if (nj == 0 && !zero_row) continue;
+      const float denom = (float)max(1u, dg);
+      const float rcp = __frcp_rn(denom);
+      float a[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; e++) a[e] = 0.0f;
+      const bool resume = __shfl_sync(0xffffffffu, tch_j, j) != 0;
+      float* out = acc + v * ldacc;
+      if (resume && active) load_f32<VEC>(out + col, a);
+      for (int c = 0; c < nj; c++, ce++) {
+        cp_async_wait<kRing - 1>();
+        F f;
+        f.raw = lds16(ring_lane + ((uint32_t)(ce & (kRing - 1)) << 9));
+        add_msg<float, VEC, true>(a, f, false, denom, rcp, 1.0f);
+        issue();
+      }
+      if (active) store_f32<VEC>(out + col, a);
+      if (lane == 0) touched[v] = 1;
+    }
+    cp_async_wait<0>();
+  }
+}
+
 struct TileArgs {
   int64_t ldx, tile_lo, tile_hi;
   const atlas_graph* g;
@@ -1295,6 +1409,30 @@ void launch_agg_tile(const void* tile, int dtype, int64_t ldx, int64_t tile_lo,
   if (dtype == ATLAS_F32) tile_typed<float>(tile, a, s);
   else if (dtype == ATLAS_F16) tile_typed<__half>(tile, a, s);
   else tile_typed<__nv_bfloat16>(tile, a, s);
+}
+
+bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
+                       int64_t tile_lo, const atlas_graph* g, int model,
+                       int d, float* acc, int64_t ldacc, int64_t* cursor,
+                       uint8_t* touched, cudaStream_t s) {
+  if (model != ATLAS_GCN || dtype != ATLAS_F32 || d % 4 != 0 || d > 128 ||
+      ldx % 4 != 0 || ldacc % 4 != 0 ||
+      (reinterpret_cast<uintptr_t>(tile) & 15) != 0)
+    return false;
+  if (g->nloc == 0) return true;
+  g->work.reserve(1);
+  ATLAS_CUDA(cudaMemsetAsync(g->work.ptr, 0, sizeof(unsigned long long), s));
+  const int smem = 8 * kRing * 32 * 16;
+  auto kern = agg_suffix_ring<4>;
+  ATLAS_CUDA(cudaFuncSetAttribute(
+      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<148 * 3, 256, smem, s>>>(
+      static_cast<const float*>(tile), ldx, tile_lo, g->csc_ptr.ptr,
+      g->csc_src.ptr, g->indeg.ptr, g->lo, g->nloc, d, acc, ldacc, cursor,
+      touched, g->work.ptr);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  return true;
 }
 
 // numpy: np.float32(1.0) + np.float32(eps), rounded to f32

@@ -547,7 +547,12 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
       if (t >= ahead) copy_tile(t);
       ATLAS_CUDA(cudaStreamWaitEvent(
           s, whole ? L->tile_ev[t % kTileEvents] : L->ev_ready[b], 0));
-      if (L->nloc > 0)
+      const bool suffix =
+          whole && t == ntiles - 1 && t > 0 && L->nloc > 0 &&
+          launch_agg_suffix(tile_ptr(t), dtype, ldx, r0, g, D.model,
+                            (int)D.embed_dim, L->acc.ptr, D.agg_dim,
+                            L->cursor.ptr, L->touched.ptr, s);
+      if (L->nloc > 0 && !suffix)
         launch_agg_tile(tile_ptr(t), dtype, ldx, r0, r1, g, D.model,
                         D.gin_epsilon, (int)D.embed_dim, L->acc.ptr,
                         D.agg_dim, L->cursor.ptr, L->touched.ptr, s);

@@ -238,6 +238,12 @@ void launch_agg_runs(const void* tile, int dtype, int64_t ldx,
                      const uint32_t* ent_src, const uint32_t* indeg,
                      int model, float gin_epsilon, int d, float* acc,
                      int64_t ldacc, uint8_t* touched, cudaStream_t s);
+// last tile of a whole-input stream: the remaining edge suffixes on the
+// cp.async ring (GCN, f32 rows <= 512 B); false if the shape does not fit
+bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
+                       int64_t tile_lo, const atlas_graph* g, int model,
+                       int d, float* acc, int64_t ldacc, int64_t* cursor,
+                       uint8_t* touched, cudaStream_t s);
 void launch_agg_tile(const void* tile, int dtype, int64_t ldx, int64_t tile_lo,
                      int64_t tile_hi, const atlas_graph* g, int model,
                      float gin_epsilon, int d, float* acc, int64_t ldacc,
