@@ -1256,11 +1256,12 @@ void runs_typed(const void* tile, int64_t ldx, const uint32_t* run_dst,
 template <int VEC>
 __global__ void __launch_bounds__(256, 3)
     agg_suffix_ring(const float* __restrict__ tile, int64_t ldx,
-                    int64_t tile_lo, const int64_t* __restrict__ csc_ptr,
+                    int64_t tile_lo, int64_t tile_hi, int64_t V,
+                    const int64_t* __restrict__ csc_ptr,
                     const uint32_t* __restrict__ csc_src,
                     const uint32_t* __restrict__ indeg, int64_t lo,
                     int64_t nloc, int d, float* __restrict__ acc,
-                    int64_t ldacc, const int64_t* __restrict__ cursor,
+                    int64_t ldacc, int64_t* __restrict__ cursor,
                     uint8_t* __restrict__ touched,
                     unsigned long long* __restrict__ work) {
   using F = Frag<float, VEC>;
@@ -1288,7 +1289,17 @@ __global__ void __launch_bounds__(256, 3)
     uint32_t dg_j = 0, tch_j = 0;  // in-degree, touched flag of v0 + j
     if (vj < v1) {
       b_j = cursor[vj];
-      n_j = (int)(csc_ptr[vj + 1] - b_j);
+      int64_t e = csc_ptr[vj + 1];
+      if (tile_hi < V) {  // the ascending sources below tile_hi
+        int64_t a = b_j;
+        while (a < e) {
+          const int64_t m = (a + e) >> 1;
+          if ((int64_t)csc_src[m] < tile_hi) a = m + 1;
+          else e = m;
+        }
+        cursor[vj] = e;  // the next tile resumes here
+      }
+      n_j = (int)(e - b_j);
       dg_j = indeg[vj];
       tch_j = touched[vj];
     }
@@ -1331,7 +1342,7 @@ __global__ void __launch_bounds__(256, 3)
       const int64_t v = (int64_t)v0 + j;
       const int nj = __shfl_sync(0xffffffffu, n_j, j);
       const uint32_t dg = __shfl_sync(0xffffffffu, dg_j, j);
-      const bool zero_row = dg == 0 && v + lo >= tile_lo;
+      const bool zero_row = dg == 0 && v + lo >= tile_lo && v + lo < tile_hi;
       if (nj == 0 && !zero_row) continue;
       const float denom = (float)max(1u, dg);
       const float rcp = __frcp_rn(denom);
@@ -1412,9 +1423,10 @@ void launch_agg_tile(const void* tile, int dtype, int64_t ldx, int64_t tile_lo,
 }
 
 bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
-                       int64_t tile_lo, const atlas_graph* g, int model,
-                       int d, float* acc, int64_t ldacc, int64_t* cursor,
-                       uint8_t* touched, cudaStream_t s) {
+                       int64_t tile_lo, int64_t tile_hi,
+                       const atlas_graph* g, int model, int d, float* acc,
+                       int64_t ldacc, int64_t* cursor, uint8_t* touched,
+                       cudaStream_t s) {
   if (model != ATLAS_GCN || dtype != ATLAS_F32 || d % 4 != 0 || d > 128 ||
       ldx % 4 != 0 || ldacc % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(tile) & 15) != 0)
@@ -1427,7 +1439,8 @@ bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
   ATLAS_CUDA(cudaFuncSetAttribute(
       kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<148 * 3, 256, smem, s>>>(
-      static_cast<const float*>(tile), ldx, tile_lo, g->csc_ptr.ptr,
+      static_cast<const float*>(tile), ldx, tile_lo, tile_hi, g->V,
+      g->csc_ptr.ptr,
       g->csc_src.ptr, g->indeg.ptr, g->lo, g->nloc, d, acc, ldacc, cursor,
       touched, g->work.ptr);
   count_launch();

@@ -548,8 +548,8 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
       ATLAS_CUDA(cudaStreamWaitEvent(
           s, whole ? L->tile_ev[t % kTileEvents] : L->ev_ready[b], 0));
       const bool suffix =
-          whole && t == ntiles - 1 && t > 0 && L->nloc > 0 &&
-          launch_agg_suffix(tile_ptr(t), dtype, ldx, r0, g, D.model,
+          whole && L->nloc > 0 &&
+          launch_agg_suffix(tile_ptr(t), dtype, ldx, r0, r1, g, D.model,
                             (int)D.embed_dim, L->acc.ptr, D.agg_dim,
                             L->cursor.ptr, L->touched.ptr, s);
       if (L->nloc > 0 && !suffix)

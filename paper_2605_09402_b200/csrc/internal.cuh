@@ -241,9 +241,10 @@ void launch_agg_runs(const void* tile, int dtype, int64_t ldx,
 // last tile of a whole-input stream: the remaining edge suffixes on the
 // cp.async ring (GCN, f32 rows <= 512 B); false if the shape does not fit
 bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
-                       int64_t tile_lo, const atlas_graph* g, int model,
-                       int d, float* acc, int64_t ldacc, int64_t* cursor,
-                       uint8_t* touched, cudaStream_t s);
+                       int64_t tile_lo, int64_t tile_hi,
+                       const atlas_graph* g, int model, int d, float* acc,
+                       int64_t ldacc, int64_t* cursor, uint8_t* touched,
+                       cudaStream_t s);
 void launch_agg_tile(const void* tile, int dtype, int64_t ldx, int64_t tile_lo,
                      int64_t tile_hi, const atlas_graph* g, int model,
                      float gin_epsilon, int d, float* acc, int64_t ldacc,
