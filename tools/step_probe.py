@@ -13,7 +13,29 @@ x = torch.from_numpy(f).cuda()
 for _ in range(3):
     eng.infer(x)
 torch.cuda.synchronize()
-for trial in range(2):
+HOST = {}
+
+
+def _trace(cls, names):
+    for n in names:
+        f = getattr(cls, n)
+
+        def wrap(*a, _f=f, _n=n, **k):
+            t = time.perf_counter()
+            try:
+                return _f(*a, **k)
+            finally:
+                HOST.setdefault(_n, []).append(
+                    round(1e3 * (time.perf_counter() - t), 2))
+        setattr(cls, n, wrap)
+
+
+from paper_2605_09402_b200 import engine as _E  # noqa: E402
+_trace(_E.DeviceLayer, ["reset", "run_resident", "run_fused",
+                        "accumulator_ptr"])
+_trace(_E, ["transform_device", "transform_typed"])
+for trial in range(4):
+    HOST.clear()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
     hs = []
     evs[0].record()
@@ -25,3 +47,4 @@ for trial in range(2):
     torch.cuda.synchronize()
     print("host ms", [round(h, 2) for h in hs])
     print("dev ms ", [round(evs[i].elapsed_time(evs[i + 1]), 2) for i in range(6)])
+    print("  per call host ms:", {k: v for k, v in HOST.items()})
