@@ -1254,7 +1254,7 @@ void runs_typed(const void* tile, int64_t ldx, const uint32_t* run_dst,
 // end-to-end time sees; agg_tile (a warp per destination, ~6 edges per
 // tile) runs it at a third of the DRAM rate.
 template <int VEC>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, kSubBlocks + 1)
     agg_suffix_ring(const float* __restrict__ tile, int64_t ldx,
                     int64_t tile_lo, int64_t tile_hi, int64_t V,
                     const int64_t* __restrict__ csc_ptr,
@@ -1272,7 +1272,7 @@ __global__ void __launch_bounds__(256, 3)
   const int colc = active ? col : d - VEC;
   const uint32_t ring_lane =
       (uint32_t)__cvta_generic_to_shared(ring_smem +
-                                         (threadIdx.x >> 5) * (kRing * 32)) +
+                                         (threadIdx.x >> 5) * (kSubRing * 32)) +
       (uint32_t)lane * 16u;
   const float* __restrict__ xc = tile + colc;
   while (true) {
@@ -1329,14 +1329,14 @@ __global__ void __launch_bounds__(256, 3)
       if (pe < ne) {
         if ((pe & 31) == 0 && pe != 0) isrc = src_of(pe + lane);
         const uint32_t u = __shfl_sync(0xffffffffu, isrc, pe & 31);
-        cp_async16_s(ring_lane + ((uint32_t)(pe & (kRing - 1)) << 9),
+        cp_async16_s(ring_lane + ((uint32_t)(pe & (kSubRing - 1)) << 9),
                      xc + ((int64_t)u - tile_lo) * ldx);
         pe++;
       }
       cp_async_commit();
     };
 #pragma unroll 1
-    for (int k = 0; k < kRing; k++) issue();
+    for (int k = 0; k < kSubRing; k++) issue();
     int ce = 0;
     for (int j = 0; j < (int)(v1 - (int64_t)v0); j++) {
       const int64_t v = (int64_t)v0 + j;
@@ -1353,9 +1353,9 @@ __global__ void __launch_bounds__(256, 3)
       float* out = acc + v * ldacc;
       if (resume && active) load_f32<VEC>(out + col, a);
       for (int c = 0; c < nj; c++, ce++) {
-        cp_async_wait<kRing - 1>();
+        cp_async_wait<kSubRing - 1>();
         F f;
-        f.raw = lds16(ring_lane + ((uint32_t)(ce & (kRing - 1)) << 9));
+        f.raw = lds16(ring_lane + ((uint32_t)(ce & (kSubRing - 1)) << 9));
         add_msg<float, VEC, true>(a, f, false, denom, rcp, 1.0f);
         issue();
       }
@@ -1434,11 +1434,11 @@ bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
   if (g->nloc == 0) return true;
   g->work.reserve(1);
   ATLAS_CUDA(cudaMemsetAsync(g->work.ptr, 0, sizeof(unsigned long long), s));
-  const int smem = 8 * kRing * 32 * 16;
+  const int smem = 8 * kSubRing * 32 * 16;
   auto kern = agg_suffix_ring<4>;
   ATLAS_CUDA(cudaFuncSetAttribute(
       kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<148 * 3, 256, smem, s>>>(
+  kern<<<148 * (kSubBlocks + 1), 256, smem, s>>>(
       static_cast<const float*>(tile), ldx, tile_lo, tile_hi, g->V,
       g->csc_ptr.ptr,
       g->csc_src.ptr, g->indeg.ptr, g->lo, g->nloc, d, acc, ldacc, cursor,
