@@ -310,6 +310,17 @@ ATLAS_API int atlas_spill_write(const char* part_dir, const void* rows,
                                 int64_t spill_rows, int32_t threads,
                                 int64_t* bytes_written);
 
+/* Gather-pattern replay (ablation criterion 11): rows a destination-major
+ * gather engine loads in one layer through an LRU cache of cache_rows rows
+ * fetched in block_rows blocks (0 cache rows: every touch loads). Replaces
+ * oocgnn/bench.py:282-305 simulate_gather_rows; exact LRU via reuse
+ * distances. Host-only. */
+ATLAS_API int atlas_gather_replay(int64_t num_vertices, int64_t num_edges,
+                                  const int64_t* offsets,
+                                  const uint32_t* neighbors,
+                                  int64_t cache_rows, int64_t block_rows,
+                                  int64_t* rows_loaded);
+
 /* number of kernels this library launched since load (evidence counter) */
 ATLAS_API int64_t atlas_kernel_launches(void);
 

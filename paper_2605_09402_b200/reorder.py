@@ -113,15 +113,21 @@ class SpanStats:
 
 
 def compute_span(graph: GraphCSR) -> SpanStats:
-    """oocgnn/reorder.py:168-187 (offline analysis helper)."""
-    if graph.num_edges == 0:
+    """Per-destination message spans of the source-order walk
+    (oocgnn/reorder.py:168-187, an offline analysis helper).
+
+    Message t of the walk is CSR edge t, so a destination's first and last
+    steps are the smallest and largest CSR positions holding its id: a
+    stable sort of the neighbour array groups each destination's positions
+    in ascending order, and the run ends give both. Spans come out in
+    ascending destination order, as the reference's masked arrays do."""
+    nbrs = np.asarray(graph.neighbors)
+    if nbrs.size == 0:
         return SpanStats(0.0, 0.0, 0.0)
-    steps = np.arange(graph.num_edges, dtype=np.int64)
-    first = np.full(graph.num_vertices, np.iinfo(np.int64).max)
-    last = np.full(graph.num_vertices, -1, dtype=np.int64)
-    np.minimum.at(first, graph.neighbors, steps)
-    np.maximum.at(last, graph.neighbors, steps)
-    got = last >= 0
-    spans = (last[got] - first[got]).astype(np.float64)
+    pos = np.argsort(nbrs, kind="stable")
+    grouped = nbrs[pos]
+    heads = np.flatnonzero(np.r_[True, grouped[1:] != grouped[:-1]])
+    tails = np.r_[heads[1:], grouped.size] - 1
+    spans = (pos[tails] - pos[heads]).astype(np.float64)
     return SpanStats(float(spans.mean()), float(np.percentile(spans, 99)),
                      float(spans.max()))

@@ -120,6 +120,30 @@ METRIC_FIELDS = ["messages", "evictions", "reloads", "unique_reloads",
                  "hot_slot_count"]
 
 
+def metrics_rows(path):
+    """metrics.csv as written by the reference (oocgnn/runtime.py:98-111),
+    minus the wall_seconds column (timing)."""
+    import csv
+    with open(path, newline="") as f:
+        rows = list(csv.reader(f))
+    return [r[:-1] for r in rows]
+
+
+def dir_digest(layer_dir):
+    """sha256 over the sorted (relative path, bytes) of a layer directory,
+    plus its file count and total bytes."""
+    layer_dir = Path(layer_dir)
+    h = hashlib.sha256()
+    n = total = 0
+    for p in sorted(q for q in layer_dir.rglob("*") if q.is_file()):
+        data = p.read_bytes()
+        h.update(str(p.relative_to(layer_dir)).encode() + b"\0")
+        h.update(data)
+        n += 1
+        total += len(data)
+    return {"sha": h.hexdigest(), "files": n, "bytes": total}
+
+
 def fig2_dataset(root):
     edges = [(0, 1), (0, 3), (2, 3), (4, 1), (4, 3)]
     g = edges_to_csr(np.array([e[0] for e in edges]),
@@ -218,6 +242,9 @@ def main(only=None):
             if full:
                 arrays[f"L{l}_out"] = y
             entry["layers"].append(lay)
+        entry["metrics_csv"] = metrics_rows(out / "metrics.csv")
+        entry["layer_dirs"] = [dir_digest(out / f"layer_{l}")
+                               for l in range(len(report.layers))]
         entry["oracle64_sha"] = digest_array(ref64)
         arrays["oracle64"] = ref64 if full else ref64[:64]
         entry["oracle64_absmax"] = float(np.abs(ref64).max())
@@ -236,6 +263,76 @@ def main(only=None):
     old = json.loads(path.read_text()) if (only and path.exists()) else {}
     old.update(manifest)
     path.write_text(json.dumps(old, indent=1, sort_keys=True))
+
+
+# --- benchmark-scale case (BASELINE configs[1] = cfg2) -------------------
+# One reference run at the headline configuration: 3-layer GCN
+# [100,128,128,47] on the uniform V=2.4M / E=62,399,647 graph (seed 7),
+# 8 MiB chunks (115 at layer 1), hot_slots = V. ~20 min on one core here.
+# Stored in its own manifest (golden_scale.json) so the per-case parity
+# suites do not pick it up: per-layer output sha256 and metrics, the
+# graduation log digest, metrics.csv, the layer-dir digests, and the
+# reference oracle (oocgnn/oracle.py:26-55) per layer on SAMPLE_ROWS
+# sampled rows (the truncated model l+1 layers deep, ReLU applied on
+# hidden layers as the full model does) with each layer's max |y|.
+SCALE_DATASETS = {"cfg2": ("uniform", 2_400_000, 26, 100, 7, "f32")}
+SCALE_CASES = [("cfg2_gcn", "cfg2", ModelKind.GCN, [100, 128, 128, 47], 5,
+                0.0, 1.0, dict(hot_slots=2_400_000))]
+SAMPLE_ROWS = 2048
+
+
+def scale_goldens():
+    from oocgnn.storage import ModelWeights
+    work = Path(tempfile.mkdtemp(prefix="golden_scale_"))
+    path = OUT / "golden_scale.json"
+    manifest = json.loads(path.read_text()) if path.exists() else {}
+    for case, ds, kind, dims, wseed, eps, gain, cfg in SCALE_CASES:
+        gk, v, deg, dim, seed, dt = SCALE_DATASETS[ds]
+        dsdir = work / ds
+        generate_synthetic(gk, v, deg, dim, seed, dsdir, dtype=dt)
+        weights = random_weights(kind, dims, wseed, gin_epsilon=eps,
+                                 gain=gain)
+        REC.layers.clear()
+        out = work / f"run_{case}"
+        report = rt.run_inference(dsdir, weights, rt.PipelineConfig(**cfg),
+                                  out)
+        graph = read_csr(dsdir)
+        feats = load_layer_matrix(dsdir / "features")
+        rows = np.sort(np.random.default_rng(0).choice(v, SAMPLE_ROWS,
+                                                       replace=False))
+        entry = {"dataset": ds, "dataset_spec": SCALE_DATASETS[ds],
+                 "model": int(kind), "dims": dims, "weight_seed": wseed,
+                 "gin_epsilon": eps, "gain": gain, "config": cfg,
+                 "num_edges": int(graph.num_edges), "layers": []}
+        arrays = {"rows": rows}
+        last = len(weights.layers) - 1
+        for l, m in enumerate(report.layers):
+            y = load_layer_matrix(out / f"layer_{l}")
+            log = REC.layers[l]
+            lay = {f: getattr(m, f) for f in METRIC_FIELDS}
+            lay["output_sha"] = digest_array(y)
+            lay["output_absmax"] = float(np.abs(y).max())
+            for key in ("victims", "reloads", "graduated"):
+                flat = flatten_events(log[key])
+                lay[f"{key}_sha"] = digest_array(flat)
+                lay[f"{key}_events"] = len(log[key])
+            arrays[f"L{l}_out_rows"] = y[rows]
+            trunc = ModelWeights(kind, weights.layers[:l + 1], eps)
+            ref = oracle_inference(graph, feats, trunc, memory_cap=32 << 30)
+            if l != last:
+                np.maximum(ref, 0.0, out=ref)
+            lay["oracle_absmax"] = float(np.abs(ref).max())
+            arrays[f"L{l}_oracle_rows"] = ref[rows]
+            del ref
+            entry["layers"].append(lay)
+            print(case, l, lay["messages"], lay["output_sha"][:12],
+                  flush=True)
+        entry["metrics_csv"] = metrics_rows(out / "metrics.csv")
+        entry["layer_dirs"] = [dir_digest(out / f"layer_{l}")
+                               for l in range(len(report.layers))]
+        manifest[case] = entry
+        np.savez_compressed(OUT / f"{case}.npz", **arrays)
+        path.write_text(json.dumps(manifest, indent=1, sort_keys=True))
 
 
 def reorder_goldens():
@@ -272,5 +369,7 @@ def reorder_goldens():
 if __name__ == "__main__":
     if sys.argv[1:] == ["reorder"]:
         reorder_goldens()
+    elif sys.argv[1:] == ["scale"]:
+        scale_goldens()
     else:
         main(set(sys.argv[1:]) or None)

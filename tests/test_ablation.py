@@ -64,6 +64,52 @@ def test_gather_replay_matches_reference(cache, block):
     np.testing.assert_array_equal(src, rsrc)
 
 
+def test_gather_replay_criterion_11_rows():
+    """The reference's shipped criterion-11 figure, host-only: a gather
+    engine with a 25 % row cache reads 198 MB of 64-d f32 rows on the PA
+    desk graph (pkg/test_output.txt:321)."""
+    g, _ = S.synthetic_in_memory("pa", 100_000, 10, 4, 12)
+    rows = A.simulate_gather_rows(g, cache_rows=g.num_vertices // 4)
+    assert round(rows * 64 * 4 / 1e6) == 198
+
+
+@pytest.mark.parametrize("block", [1, 2, 5])
+def test_gather_replay_matches_python_lru(block):
+    """Reuse-distance count == a literal LRU walk, across cache sizes."""
+    from collections import OrderedDict
+    g, _ = S.synthetic_in_memory("uniform", 3000, 6, 4, 2)
+    off, src = A.reverse_csr(g)
+    for cache in (0, 1, 7, 64, 500, 3000):
+        cap = cache // block
+        lru, loads = OrderedDict(), 0
+        for b in (src // block).tolist():
+            if cap and b in lru:
+                lru.move_to_end(b)
+                continue
+            loads += 1
+            if cap:
+                lru[b] = None
+                if len(lru) > cap:
+                    lru.popitem(last=False)
+        assert A.simulate_gather_rows(g, cache, block) == loads * block
+
+
+def test_scenario_defaults_and_codecs(tmp_path):
+    sc = A.Scenario()
+    assert sc.budget_pcts == [2, 5, 10, 50, 100] and sc.direct_io is True
+    assert A.Scenario().layers_out is not sc.layers_out
+    p = tmp_path / "s.txt"
+    p.write_text("seeds = 4, 5,\nbudget_pct=2.5\nvertices = x\n")
+    with pytest.raises(FormatError):
+        A.parse_scenario(p)
+    p.write_text("no equals sign\n")
+    with pytest.raises(FormatError):
+        A.parse_scenario(p)
+    p.write_text("seeds = 4, 5,\nbudget_pct=2.5  # inline\n")
+    sc = A.parse_scenario(p)
+    assert sc.seeds == [4, 5] and sc.budget_pct == 2.5
+
+
 @pytest.fixture(scope="module")
 def pa_dir(tmp_path_factory):
     d = tmp_path_factory.mktemp("ablation") / "pa"
