@@ -21,10 +21,11 @@ reproduce bit-exactly: the victim list of every
 eviction, the reload list of every admission batch, and the graduation
 order with its sub-batch grouping.
 
-Pinned against the reference: tests/test_oracle_pinning.py compares every
-output of this module with the unmodified reference (imported from
-/root/reference when present) and with the committed fixtures under
-tests/golden/ (generated by tests/golden/make_golden.py).
+Pinned against the reference: tests/test_cpu_boundary.py
+(``test_oracle_pinned_to_reference_goldens``) compares every output, metric
+and event log of this module with the committed fixtures under
+tests/golden/, which tests/golden/make_golden.py produced by running the
+unmodified reference.
 """
 
 from __future__ import annotations

@@ -4,7 +4,13 @@ Restates ``oracle_inference`` (oocgnn/oracle.py:18-55): a scipy CSR
 (dst, src) matrix product per layer in float64, mean = sum * 1/max(1,d_in),
 SAGE concat [mean || self], GIN sum + (1+eps) self, ReLU on every layer
 but the last. ``per_layer`` returns every layer's post-activation output
-(the reference returns only the last)."""
+(the reference returns only the last).
+
+Pinned: tests/test_cpu_boundary.py::test_gather_oracle_pinned_to_reference_oracle
+checks the last layer, rounded to f32, equals the reference's
+``oracle_inference`` output stored by make_golden for every golden case
+(bit-exact); the cfg2-scale golden adds the reference's per-layer outputs
+on sampled rows."""
 
 import numpy as np
 import scipy.sparse as sp

@@ -7,8 +7,9 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from helpers import (REFERENCE_SRC, digest_array, flatten_events,
-                     golden_manifest, oracle_case)
+from helpers import (REFERENCE_SRC, case_weights, dataset, digest_array,
+                     flatten_events, golden_arrays, golden_manifest,
+                     oracle_case)
 from paper_2605_09402_b200 import _native as N
 from paper_2605_09402_b200 import storage as S
 from paper_2605_09402_b200.chunks import plan_chunks
@@ -164,3 +165,32 @@ def test_markstein_division(tmp_path):
     out = subprocess.run([str(exe)], check=True, capture_output=True,
                          text=True).stdout
     assert out.strip().endswith("bad(normal results)=0"), out
+
+
+GATHER_CASES = [c for c in golden_manifest() if not c.startswith("_")]
+
+
+@pytest.mark.parametrize("case", GATHER_CASES)
+def test_gather_oracle_pinned_to_reference_oracle(case):
+    """oracle/gather.py (the f64 oracle behind every tolerance test) equals
+    the reference's own ``oracle_inference`` (oocgnn/oracle.py:26-55) as
+    make_golden stored it: the last layer rounded to f32, every row for the
+    small cases and the first 64 rows otherwise. Same CSR construction,
+    same f64 operation order, so the f32 roundings must agree exactly."""
+    from oracle import gather as G
+
+    entry = golden_manifest()[case]
+    graph, feats = dataset(entry["dataset"])
+    w = case_weights(entry)
+    outs = G.per_layer(graph.num_vertices, graph.offsets, graph.neighbors,
+                       graph.in_degrees, feats, int(w.kind),
+                       [(lw.weight, lw.bias) for lw in w.layers],
+                       gin_epsilon=w.gin_epsilon)
+    want = golden_arrays(case)["oracle64"]
+    got = outs[-1].astype(np.float32)[:len(want)]
+    np.testing.assert_array_equal(got, want)
+    if len(want) == graph.num_vertices:
+        assert digest_array(outs[-1].astype(np.float32)) == \
+            entry["oracle64_sha"]
+    assert float(np.abs(outs[-1]).max().astype(np.float32)) == \
+        entry["oracle64_absmax"]
