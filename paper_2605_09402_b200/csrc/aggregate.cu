@@ -193,9 +193,9 @@ template <typename T>
 void launch_scan(const T* x, int64_t rows, int d, int64_t ldx, int* flag,
                  cudaStream_t s) {
   if (ldx == d && (reinterpret_cast<uintptr_t>(x) & 15) == 0)
-    scan_extremes_flat<T><<<148 * 8, 256, 0, s>>>(x, rows * d, flag);
+    scan_extremes_flat<T><<<num_sms() * 8, 256, 0, s>>>(x, rows * d, flag);
   else
-    scan_extremes<T><<<148 * 8, 256, 0, s>>>(x, rows, d, ldx, flag);
+    scan_extremes<T><<<num_sms() * 8, 256, 0, s>>>(x, rows, d, ldx, flag);
   count_launch();
   ATLAS_LAUNCH_CHECK();
 }
@@ -505,7 +505,8 @@ __global__ void __launch_bounds__(256, 3)
 // shallower ring than agg_ring's: 32/LPD runs share a warp's rows in
 // flight, and the smaller footprint leaves room for more blocks per SM
 constexpr int kSubRing = 8;
-constexpr int kSubBlocks = 4;  // per SM (64 registers: no address remat)
+constexpr int kSubBlocks = 4;  // agg_sub_ring blocks per SM (64 registers
+                                // each: no address rematerialisation)
 
 template <typename T, int LPD, int MODEL, bool GUARD>
 __device__ __forceinline__ void sub_ring_body(
@@ -1113,7 +1114,7 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
     auto ring = [&](auto kern) {
       ATLAS_CUDA(cudaFuncSetAttribute(
           kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      kern<<<148 * 3, 256, smem, s>>>(
+      kern<<<num_sms() * 3, 256, smem, s>>>(
           x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
           g->nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
     };
@@ -1122,7 +1123,7 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
       auto sub = [&](auto kern) {
         ATLAS_CUDA(cudaFuncSetAttribute(
             kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sub_smem));
-        kern<<<148 * kSubBlocks, 256, sub_smem, s>>>(
+        kern<<<num_sms() * kSubBlocks, 256, sub_smem, s>>>(
             x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
             g->nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
       };
@@ -1158,7 +1159,7 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
       int per_sm = 0;
       ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &per_sm, kern, kBulkWarps * 32, smem));
-      kern<<<kNumSMs * std::max(1, per_sm), kBulkWarps * 32, smem, s>>>(
+      kern<<<num_sms() * std::max(1, per_sm), kBulkWarps * 32, smem, s>>>(
           x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
           g->nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
     };
@@ -1253,6 +1254,9 @@ void runs_typed(const void* tile, int64_t ldx, const uint32_t* run_dst,
 // the part of the stream left after the last copy lands, so it is what the
 // end-to-end time sees; agg_tile (a warp per destination, ~6 edges per
 // tile) runs it at a third of the DRAM rate.
+// Occupancy: 5 blocks/SM caps registers at 51; ptxas -v reports 42 and no
+// spills for VEC=4 (the 64-register note on kSubBlocks is for
+// agg_sub_ring's lockstep sub-groups, not this kernel).
 template <int VEC>
 __global__ void __launch_bounds__(256, kSubBlocks + 1)
     agg_suffix_ring(const float* __restrict__ tile, int64_t ldx,
@@ -1438,7 +1442,7 @@ bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
   auto kern = agg_suffix_ring<4>;
   ATLAS_CUDA(cudaFuncSetAttribute(
       kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<148 * (kSubBlocks + 1), 256, smem, s>>>(
+  kern<<<num_sms() * (kSubBlocks + 1), 256, smem, s>>>(
       static_cast<const float*>(tile), ldx, tile_lo, tile_hi, g->V,
       g->csc_ptr.ptr,
       g->csc_src.ptr, g->indeg.ptr, g->lo, g->nloc, d, acc, ldacc, cursor,
@@ -1492,7 +1496,7 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
         int per_sm = 0;
         ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, kern, 256, smem));
-        kern<<<kNumSMs * std::max(1, per_sm), 256, smem, s>>>(
+        kern<<<num_sms() * std::max(1, per_sm), 256, smem, s>>>(
             z, ldz, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
             v_end, d, e1, epi, g->work.ptr);
       };
@@ -1525,7 +1529,7 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
   auto go = [&](auto kern) {
     ATLAS_CUDA(cudaFuncSetAttribute(
         kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<148 * 3, 256, smem, s>>>(z, ldz, g->csc_ptr.ptr, g->csc_src.ptr,
+    kern<<<num_sms() * 3, 256, smem, s>>>(z, ldz, g->csc_ptr.ptr, g->csc_src.ptr,
                                     g->indeg.ptr, g->lo, v_end, d, e1, flag,
                                     g->work.ptr, epi);
   };

@@ -314,6 +314,7 @@ int atlas_chunk_submit(atlas_layer* L, int64_t start, int64_t end,
       // records start at zero; later chunks resume via touched flags
       ATLAS_CUDA(cudaMemsetAsync(L->acc.ptr, 0, L->acc.bytes(), s));
     }
+    L->submit_stream = s;
     submit_chunk(L, start, end, rows_host, dtype, off, nbrs, m, s);
   });
 }
@@ -324,7 +325,10 @@ int atlas_chunk_graduated(atlas_layer* L, int64_t* ids, float* rows,
   return guarded([&] {
     if (!L) fail(ATLAS_ECONFIG, "null layer");
     use_device(L->desc.device);
-    cudaStream_t s = nullptr;
+    // the chunk's work was queued on the caller's stream (often a
+    // non-blocking torch stream): wait for it there, then read back on it
+    cudaStream_t s = L->submit_stream;
+    ATLAS_CUDA(cudaStreamSynchronize(s));
     EngineScalars sc = read_scalars(L, s);
     const int64_t n = sc.chunk_grad_n, nb = sc.chunk_grad_batches_n;
     if (count) *count = n;
@@ -346,8 +350,10 @@ int atlas_chunk_graduated(atlas_layer* L, int64_t* ids, float* rows,
       L->grad_rows.reserve(n * w);
       launch_gather_rows(L->acc.ptr, w, L->chunk_grad.ptr, n, w,
                          L->grad_rows.ptr, s);
-      ATLAS_CUDA(cudaMemcpy(rows, L->grad_rows.ptr, n * w * sizeof(float),
-                            cudaMemcpyDeviceToHost));
+      ATLAS_CUDA(cudaMemcpyAsync(rows, L->grad_rows.ptr,
+                                 n * w * sizeof(float),
+                                 cudaMemcpyDeviceToHost, s));
+      ATLAS_CUDA(cudaStreamSynchronize(s));
     }
   });
 }
@@ -761,7 +767,8 @@ int atlas_layer_log(atlas_layer* L, int32_t which, int64_t* out, int64_t cap,
     if (!L->desc.record_log) fail(ATLAS_ECONFIG, "layer was not logging");
     use_device(L->desc.device);
     settle(L, true);
-    EngineScalars sc = read_scalars(L, nullptr);
+    ATLAS_CUDA(cudaStreamSynchronize(L->submit_stream));
+    EngineScalars sc = read_scalars(L, L->submit_stream);
     DevBuf<int64_t>* buf;
     int64_t used;
     if (which == ATLAS_LOG_VICTIMS) {

@@ -97,7 +97,7 @@ struct IsRun {
 
 unsigned grid_of(int64_t n, int block = 256) {
   int64_t g = ceil_div(n, block);
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > num_sms() * 16) g = num_sms() * 16;
   return (unsigned)(g < 1 ? 1 : g);
 }
 
@@ -149,8 +149,8 @@ void submit_chunk(atlas_layer* L, int64_t start, int64_t end,
   L->vals_a.reserve(mmx);
   L->vals_b.reserve(mmx);
   L->ent_src.reserve(mmx);
-  DevBuf<uint32_t> srcrow;
-  srcrow.alloc(mmx);
+  DevBuf<uint32_t>& srcrow = L->op_srcrow;
+  srcrow.reserve(mmx);
   int64_t nruns = 0;
   const int64_t lo = D.dst_lo, hi = D.dst_hi;
   if (mm > 0 && n > 0) {
@@ -168,8 +168,8 @@ void submit_chunk(atlas_layer* L, int64_t start, int64_t end,
     L->run_dst.reserve(mmx + 1);
     L->run_beg.reserve(mmx + 2);
     L->misc64.reserve(2);
-    DevBuf<int64_t> counts;
-    counts.alloc(mmx + 1);
+    DevBuf<int64_t>& counts = L->op_counts;
+    counts.reserve(mmx + 1);
     cub_call(L->sort_tmp, [&](void* t, size_t& b) {
       return cub::DeviceRunLengthEncode::Encode(t, b, L->keys_b.ptr,
                                                 L->run_dst.ptr, counts.ptr,
@@ -224,11 +224,12 @@ void submit_chunk(atlas_layer* L, int64_t start, int64_t end,
   L->stream_step = edge_base + mm;
 
   // 5. appearance order + engine
-  DevBuf<uint64_t> at_first, ordered;
-  DevBuf<int64_t> nsel;
-  at_first.alloc(mmx);
-  ordered.alloc(std::max<int64_t>(nruns, 1));
-  nsel.alloc(1);
+  DevBuf<uint64_t>& at_first = L->op_at_first;
+  DevBuf<uint64_t>& ordered = L->op_ordered;
+  DevBuf<int64_t>& nsel = L->op_nsel;
+  at_first.reserve(mmx);
+  ordered.reserve(std::max<int64_t>(nruns, 1));
+  nsel.reserve(1);
   if (nruns > 0) {
     fill_u64<<<grid_of(mm), 256, 0, s>>>(at_first.ptr, mm, ~0ull);
     count_launch();
@@ -245,8 +246,8 @@ void submit_chunk(atlas_layer* L, int64_t start, int64_t end,
   }
   int64_t h_off[2] = {0, nruns};
   int64_t h_bounds[2] = {start, end};
-  DevBuf<int64_t> dv;
-  dv.alloc(4);
+  DevBuf<int64_t>& dv = L->op_dv;
+  dv.reserve(4);
   ATLAS_CUDA(cudaMemcpyAsync(dv.ptr, h_off, sizeof(h_off),
                              cudaMemcpyHostToDevice, s));
   ATLAS_CUDA(cudaMemcpyAsync(dv.ptr + 2, h_bounds, sizeof(h_bounds),

@@ -43,7 +43,20 @@ struct Error {
 #define ATLAS_LAUNCH_CHECK() ATLAS_CUDA(cudaGetLastError())
 
 constexpr int kWarp = 32;
-constexpr int kNumSMs = 148;
+// SM count of the current device (148 on B200), queried once per device;
+// persistent grids are sized from it, never from a literal.
+inline int num_sms() {
+  static int cached[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
 constexpr int kTileEvents = 64;  // tiles a streamed pass queues ahead
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -260,7 +260,7 @@ struct NotNoRun {
 
 unsigned grid_of(int64_t n, int block = 256) {
   int64_t g = ceil_div(n, block);
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > num_sms() * 16) g = num_sms() * 16;
   return (unsigned)(g < 1 ? 1 : g);
 }
 
@@ -461,7 +461,7 @@ static void exact_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   const size_t hbytes = 7 * (size_t)nchunks * 4;
   const int use_smem = hbytes <= 48 * 1024 ? 1 : 0;
   const unsigned blocks = (unsigned)std::min<int64_t>(
-      148 * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
+      num_sms() * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
   L->fast_path = false;
   const int64_t npos = g->E + (model == ATLAS_GCN ? 0 : V) + 1;
   DevBuf<uint64_t> at_pos, runs;
@@ -552,7 +552,7 @@ void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
   const size_t hbytes = 7 * (size_t)nchunks * 4;
   const int use_smem = hbytes <= 48 * 1024 ? 1 : 0;
   const unsigned blocks = (unsigned)std::min<int64_t>(
-      148 * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
+      num_sms() * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
   L->chunks_seen += nchunks;
   if (need_runs) {
     walk_destinations<<<blocks, 256, use_smem ? hbytes : 0, s>>>(

@@ -962,7 +962,7 @@ __global__ void init_slots(int32_t* hot_list, uint64_t* slot_key,
 
 unsigned grid_of(int64_t n) {
   int64_t g = ceil_div(n, 256);
-  if (g > 148 * 8) g = 148 * 8;
+  if (g > num_sms() * 8) g = num_sms() * 8;
   return (unsigned)(g < 1 ? 1 : g);
 }
 

@@ -371,7 +371,7 @@ void gat_typed(const atlas_graph* g, const void* z, void* y, const GatArgs& a,
     int per_sm = 0;
     ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &per_sm, kern, kGatWarps * 32, smem));
-    kern<<<kNumSMs * std::max(1, per_sm), kGatWarps * 32, smem, s>>>(
+    kern<<<num_sms() * std::max(1, per_sm), kGatWarps * 32, smem, s>>>(
         static_cast<const ZT*>(z), g->csc_ptr.ptr, g->csc_src.ptr,
         static_cast<OutT*>(y), a, g->work.ptr);
   };
@@ -393,7 +393,7 @@ void gat_typed(const atlas_graph* g, const void* z, void* y, const GatArgs& a,
     int per_sm = 0;
     ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &per_sm, kern, kGatRingWarps * 32, rsmem));
-    kern<<<kNumSMs * std::max(1, per_sm), kGatRingWarps * 32, rsmem, s>>>(
+    kern<<<num_sms() * std::max(1, per_sm), kGatRingWarps * 32, rsmem, s>>>(
         reinterpret_cast<const float*>(z), g->csc_ptr.ptr, g->csc_src.ptr,
         static_cast<OutT*>(y), a, g->work.ptr);
   } else if (a.heads * a.head_stride <= 16 * EPC)

@@ -68,7 +68,7 @@ struct InRange {
 
 int grid_for(int64_t n, int block) {
   int64_t g = ceil_div(n, block);
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > num_sms() * 16) g = num_sms() * 16;
   return (int)(g < 1 ? 1 : g);
 }
 

@@ -161,6 +161,13 @@ struct atlas_layer {
   atlas::DevBuf<uint32_t> run_dst, ent_src;
   atlas::DevBuf<int64_t> misc64;
   atlas::DevBuf<float> grad_rows;
+  // per-chunk workspaces of the operator path, grow-only across chunks
+  atlas::DevBuf<uint32_t> op_srcrow;
+  atlas::DevBuf<int64_t> op_counts, op_nsel, op_dv;
+  atlas::DevBuf<uint64_t> op_at_first, op_ordered;
+  // stream the last atlas_chunk_submit queued on: read-backs of the
+  // chunk's results (graduated ids/rows, logs) synchronise on it
+  cudaStream_t submit_stream = nullptr;
   atlas::PinnedBuf<int64_t> pin64;
   atlas::PinnedBuf<atlas::EngineScalars> pin_scalars;
   // fast-path metrics

@@ -81,7 +81,7 @@ __global__ void relabel_rows(const int64_t* __restrict__ off,
 
 unsigned grid_of(int64_t n) {
   int64_t g = ceil_div(n, 256);
-  if (g > 148 * 16) g = 148 * 16;
+  if (g > num_sms() * 16) g = num_sms() * 16;
   return (unsigned)(g < 1 ? 1 : g);
 }
 

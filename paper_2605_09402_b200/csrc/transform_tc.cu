@@ -692,17 +692,6 @@ bool make_map(CUtensorMap* m, const void* ptr, int dtype, int64_t rows,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = kNumSMs;
-  }
-  return n;
-}
-
 }  // namespace
 
 struct SplitScratch {

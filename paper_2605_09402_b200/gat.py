@@ -239,6 +239,18 @@ def _torch_dtype(name):
             "bf16": torch.bfloat16}[name]
 
 
+def _reference_row_dtype(layer_index, x) -> str:
+    """Row format a layer's input has in the reference's layer directories
+    (what plan_chunks sizes chunks by, oocgnn/chunks.py:36-48): the dataset
+    dtype for layer 0 (2-byte features plan as f16), f32 afterwards
+    (oocgnn/writer.py:60-62 always writes f32)."""
+    import torch
+
+    if layer_index > 0:
+        return "f32"
+    return "f32" if x.dtype == torch.float32 else "f16"
+
+
 class GATEngine:
     """Device-resident GAT inference over one destination range (the GAT
     counterpart of runtime.Engine; same PipelineConfig knobs).
@@ -363,8 +375,12 @@ class GATEngine:
                             z_local[:, :lay.ncols], 1)
         ev[1].record()
         z = self.gather(z_local)
-        rows = plan_rows(self.num_vertices, lay.ldz,
-                         "f32" if self.zt == torch.float32 else "f16",
+        # the control plane's chunk plan follows the layer INPUT's format
+        # (in_dim rows; layer 0 in the dataset dtype, later layers f32 as
+        # the reference writer emits them), never the z storage layout, so
+        # pending / eviction / span integers depend only on model and graph
+        rows = plan_rows(self.num_vertices, lw.in_dim,
+                         _reference_row_dtype(l, h_local),
                          self.config.chunk_budget)
         layer = self._device_layer(l, lay)
         out_dim = lw.head_dim if last else lw.hf

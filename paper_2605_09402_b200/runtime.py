@@ -121,9 +121,16 @@ def _torch_dtype(name):
             "bf16": torch.bfloat16}[name]
 
 
-def _plan_dtype(x) -> str:
+def _plan_dtype(layer_index: int, x) -> str:
+    """Row format the reference's chunk plan sizes layer ``layer_index`` by
+    (oocgnn/chunks.py:36-48 over the layer directory it reads): the dataset
+    dtype for layer 0, f32 for every later layer because the reference's
+    writer always emits f32 (oocgnn/writer.py:60-62) -- whatever dtype this
+    engine keeps the embeddings in (``embed_dtype``)."""
     import torch
 
+    if layer_index > 0:
+        return "f32"
     return "f32" if x.dtype == torch.float32 else "f16"
 
 
@@ -222,7 +229,7 @@ class Engine:
         if x.shape[1] != d:
             raise ConfigError(
                 f"layer {l} expects {d}-wide rows, input holds {x.shape[1]}")
-        rows = plan_rows(self.num_vertices, d, _plan_dtype(x),
+        rows = plan_rows(self.num_vertices, d, _plan_dtype(l, x),
                          chunk_budget or cfg.chunk_budget)
         layer = self._layers.get(l)
         gv = getattr(self.graph, "version", 0)

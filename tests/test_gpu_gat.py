@@ -51,10 +51,12 @@ def test_gat_matches_f64_oracle(zdtype, feat_dtype, heads, dims):
         got = y.double().cpu().numpy()
         err = float(np.abs(got - ref).max())
         assert err <= TOL[zdtype] * float(np.abs(ref).max()), (l, err)
-    # control plane: GCN rules on the z-row chunk plan
+    # control plane: GCN rules on the layer input's chunk plan (in_dim
+    # rows; the dataset dtype at layer 0, f32 afterwards) -- independent of
+    # the z storage dtype and padding
     for l, (m, lw) in enumerate(zip(metrics, w.layers)):
-        lay = eng.layouts[l]
-        rows = max(1, (16 << 10) // (lay.ldz * lay.itemsize))
+        item = 2 if (l == 0 and feat_dtype == "f16") else 4
+        rows = max(1, (16 << 10) // (lw.in_dim * item))
         _, om, _ = OE.run_layer(
             g.offsets, g.neighbors, g.in_degrees,
             np.zeros((g.num_vertices, 1), np.float32), OE.GCN,
