@@ -162,6 +162,10 @@ def slice_engine_class():
         """Rank 0 of G on one GPU: the other ranks' rows of each gathered
         tensor are stand-ins (filled once), the own block is copied in."""
 
+        def __init__(self, *a, **k):
+            super().__init__(*a, **k)
+            self.exchange = None  # one GPU: no peers to broadcast with
+
         def gather(self, y_local):
             import torch
 
@@ -467,6 +471,30 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0}}), flush=True)
 
 
+def self_launch(n: int) -> int:
+    """``bench.py --gpus N`` without a launcher: start N ranks with
+    torch.distributed.run on 127.0.0.1 (NCCL inside), pass their output
+    through, return the launcher's exit code."""
+    import socket
+    import subprocess
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} needs {n} visible GPUs, "
+                          f"found {have}"}), flush=True)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.run(cmd, check=False).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -490,6 +518,10 @@ def main():
     args = ap.parse_args()
     if args.embed_dtype is None:
         args.embed_dtype = "f16" if args.workload in SLICE else "f32"
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ \
+            and args.impl != "reference":
+        # one process per GPU: re-launch this script under torchrun
+        sys.exit(self_launch(args.gpus))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -565,6 +597,8 @@ def main():
         y, _ = eng.infer(x)
     barrier()
     clocks.reset()
+    if eng.exchange is not None:
+        eng.exchange.bytes_received = 0
     launches0 = N.kernel_launches()
     start, stop = torch.cuda.Event(True), torch.cuda.Event(True)
     marks = [torch.cuda.Event(True) for _ in range(args.steps)]
@@ -581,6 +615,14 @@ def main():
     gc.enable()
     launches = N.kernel_launches() - launches0
     clk = clocks.stop()
+    exchange = None
+    if eng.exchange is not None:
+        exchange = {
+            "kind": "owner broadcasts (NCCL) into each layer's input "
+                    "buffer, folded in piece by piece",
+            "pieces_per_rank": eng.exchange.pieces_per_rank,
+            "bytes_received_per_step_rank0":
+                eng.exchange.bytes_received / args.steps}
     # one more (untimed) step with its metrics: per-layer kernel times from
     # CUDA events on the launching stream, and the integer counters
     y, metrics = eng.infer(x)
@@ -742,6 +784,7 @@ def main():
                         "tolerance (tests/test_gpu_parity.py)"},
             "gpu_launches": launches,
             "gpu_launches_per_step": launches / max(1, args.steps),
+            "exchange": exchange,
             "clocks": clk,
             "setup_s": setup_s, "generate_s": gen_s,
         }

@@ -182,6 +182,19 @@ ATLAS_API int atlas_layer_run_streamed(atlas_layer* layer,
                                        const void* x_host, int32_t dtype,
                                        int64_t ldx, int64_t tile_rows,
                                        int64_t chunk_rows, void* stream);
+/* whole-layer pass over a DEVICE input that arrives in pieces: rows
+ * [bounds[t], bounds[t+1]) of x (ldx elements per row) become valid when
+ * the CUDA event ready[t] completes (NULL entries: already valid). Pieces
+ * tile [0, V) in ascending order -- the multi-GPU exchange (SURVEY.md §8e:
+ * each source piece broadcast by its owner, rank order) -- and each is
+ * aggregated as soon as it lands, so the exchange overlaps the
+ * aggregation. Records are bit-identical to atlas_layer_run_resident. */
+ATLAS_API int atlas_layer_run_pieces(atlas_layer* layer,
+                                     const atlas_graph* graph, const void* x,
+                                     int32_t dtype, int64_t ldx,
+                                     const int64_t* bounds, int32_t npieces,
+                                     void* const* ready, int64_t chunk_rows,
+                                     void* stream);
 /* transform-first layer pass (tcgen05 backend, out_dim < aggregated
  * width): z = h . W_z^T was computed by atlas_transform_typed for every
  * source (V rows, ldz); the pass runs the layer's control plane on the

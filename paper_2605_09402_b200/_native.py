@@ -85,6 +85,8 @@ def _declare(lib):
        c_i64, c_i64, c_vp, c_vp)
     fn("atlas_layer_run_streamed", ctypes.c_int, c_vp, c_vp, c_vp, c_i32,
        c_i64, c_i64, c_i64, c_vp)
+    fn("atlas_layer_run_pieces", ctypes.c_int, c_vp, c_vp, c_vp, c_i32,
+       c_i64, c_vp, c_i32, c_vp, c_i64, c_vp)
     fn("atlas_layer_accumulator", ctypes.c_int, c_vp, ctypes.POINTER(c_vp),
        P_i64)
     fn("atlas_transform", ctypes.c_int, c_i32, c_vp, c_i64, c_i64, c_i64,
@@ -122,7 +124,7 @@ EXPORTED = [
     "atlas_layer_create", "atlas_layer_destroy", "atlas_layer_reset",
     "atlas_chunk_submit",
     "atlas_chunk_graduated", "atlas_layer_run_resident",
-    "atlas_layer_run_streamed",
+    "atlas_layer_run_streamed", "atlas_layer_run_pieces",
     "atlas_layer_accumulator", "atlas_transform", "atlas_layer_finish",
     "atlas_layer_chunk_stats", "atlas_layer_log", "atlas_layer_state",
     "atlas_layer_timing", "atlas_reorder", "atlas_transform_typed",

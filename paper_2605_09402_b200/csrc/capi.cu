@@ -577,6 +577,65 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
   });
 }
 
+int atlas_layer_run_pieces(atlas_layer* L, const atlas_graph* g,
+                           const void* x, int32_t dtype, int64_t ldx,
+                           const int64_t* bounds, int32_t npieces,
+                           void* const* ready, int64_t chunk_rows,
+                           void* stream) {
+  return guarded([&] {
+    if (!L || !g || !x || !bounds || npieces < 1)
+      fail(ATLAS_ECONFIG, "null argument");
+    const atlas_layer_desc& D = L->desc;
+    if (g->V != D.num_vertices || g->lo != D.dst_lo || g->hi != D.dst_hi)
+      fail(ATLAS_ECONFIG, "graph and layer disagree on the vertex range");
+    if (chunk_rows < 1 || ldx < D.embed_dim)
+      fail(ATLAS_ECONFIG, "bad pitch / chunk rows");
+    if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
+    if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
+    if (bounds[0] != 0 || bounds[npieces] != D.num_vertices)
+      fail(ATLAS_ECONFIG, "pieces must tile [0, V)");
+    for (int32_t t = 0; t < npieces; t++)
+      if (bounds[t + 1] < bounds[t])
+        fail(ATLAS_ECONFIG, "piece bounds must ascend");
+    ensure_records(L);
+    use_device(D.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t row_b = (size_t)ldx * (dtype == ATLAS_F32 ? 4 : 2);
+    const int64_t nn = std::max<int64_t>(L->nloc, 1);
+    L->cursor.reserve(nn);
+    if (L->nloc > 0)
+      ATLAS_CUDA(cudaMemcpyAsync(L->cursor.ptr, g->csc_ptr.ptr,
+                                 L->nloc * sizeof(int64_t),
+                                 cudaMemcpyDeviceToDevice, s));
+    ATLAS_CUDA(cudaMemsetAsync(L->touched.ptr, 0, nn, s));
+    settle(L);
+    control_begin(L, s);
+    // pieces arrive in ascending source order (the owners' broadcasts);
+    // each is folded into the records as soon as its event fires, resuming
+    // every destination's ascending source list from its cursor, so the
+    // records are the resident pass's bits whatever the piece boundaries
+    const uint8_t* base = static_cast<const uint8_t*>(x);
+    for (int32_t t = 0; t < npieces; t++) {
+      const int64_t r0 = bounds[t], r1 = bounds[t + 1];
+      if (ready && ready[t])
+        ATLAS_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ready[t]),
+                                       0));
+      if (r1 == r0 || L->nloc == 0) continue;
+      const uint8_t* tile = base + (size_t)r0 * row_b;
+      const bool suffix = launch_agg_suffix(
+          tile, dtype, ldx, r0, r1, g, D.model, (int)D.embed_dim, L->acc.ptr,
+          D.agg_dim, L->cursor.ptr, L->touched.ptr, s);
+      if (!suffix)
+        launch_agg_tile(tile, dtype, ldx, r0, r1, g, D.model, D.gin_epsilon,
+                        (int)D.embed_dim, L->acc.ptr, D.agg_dim,
+                        L->cursor.ptr, L->touched.ptr, s);
+    }
+    ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
+    control_queue(L, g, chunk_rows, s);
+    L->timing_pending = true;
+  });
+}
+
 int atlas_reorder(int32_t device, int64_t V, int64_t E, const int64_t* off,
                   const uint32_t* nbrs, const uint32_t* indeg,
                   int64_t* old_to_new, int64_t* new_off, uint32_t* new_nbrs,

@@ -282,6 +282,24 @@ class DeviceLayer:
             torch_dtype_code(x_host), x_host.stride(0), int(tile_rows),
             int(chunk_rows), N.stream_handle(stream)))
 
+    def run_pieces(self, graph: DeviceGraph, x, bounds, events,
+                   chunk_rows: int, stream=None):
+        """x: CUDA tensor (V, embed_dim) whose rows [bounds[t], bounds[t+1])
+        land when torch.cuda.Event ``events[t]`` fires (None: already
+        there); each piece is aggregated as soon as it lands
+        (atlas_layer_run_pieces)."""
+        if x.shape[1] != self.embed_dim or x.shape[0] != self.num_vertices:
+            raise ConfigError(f"input {tuple(x.shape)} does not match "
+                              f"layer ({self.num_vertices}, {self.embed_dim})")
+        b = np.ascontiguousarray(bounds, dtype=np.int64)
+        n = len(b) - 1
+        handles = (ctypes.c_void_p * max(1, n))(
+            *[(e.cuda_event if e is not None else None) for e in events])
+        N.check(N.load_library().atlas_layer_run_pieces(
+            self.handle, graph.handle, x.data_ptr(), torch_dtype_code(x),
+            x.stride(0), b.ctypes.data, n, handles, int(chunk_rows),
+            N.stream_handle(stream)))
+
     def accumulator_ptr(self):
         p, ld = ctypes.c_void_p(), ctypes.c_int64()
         N.check(N.load_library().atlas_layer_accumulator(

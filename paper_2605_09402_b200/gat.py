@@ -299,6 +299,12 @@ class GATEngine:
             self.attn_l.append(al)
         self._layers = {}
         self.last_layers = []
+        self.exchange = None
+        if world > 1:
+            from .exchange import RangeExchange
+            self.exchange = RangeExchange(graph.num_vertices, self.ranges,
+                                          rank, dist_group,
+                                          config.exchange_pieces)
 
     def close(self):
         for layer in self._layers.values():
@@ -343,10 +349,11 @@ class GATEngine:
         self.graph.update(offsets, neighbors, in_degrees)
 
     def gather(self, z_local):
+        """All ranks' rows -> full tensor (owner broadcasts, in place)."""
         if self.world == 1:
             return z_local
-        from .runtime import gather_ranges
-        return gather_ranges(z_local, self.ranges, self.group)
+        return self.exchange.gather(z_local, key=("in", z_local.shape[1],
+                                                  z_local.dtype))
 
     def layer(self, l: int, h_local, defer_metrics: bool = False):
         """h_local: this rank's rows [lo, hi) of the layer input (CUDA
@@ -368,13 +375,25 @@ class GATEngine:
                               f"input holds {h_local.shape[1]}")
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ev[0].record()
-        z_local = torch.empty((h_local.shape[0], lay.ldz), dtype=self.zt,
-                              device="cuda")
+        ex = self.exchange
+        if ex is not None:
+            # pass A writes this rank's z rows straight into its slice of
+            # the exchange buffer; the owners' broadcasts fill the rest
+            zfull = ex.buffer(("z", l), lay.ldz, self.zt, "cuda")
+            z_local = ex.own(zfull)
+        else:
+            z_local = torch.empty((h_local.shape[0], lay.ldz), dtype=self.zt,
+                                  device="cuda")
         if h_local.shape[0]:
             transform_typed(h_local, self.w_ext[l], self.zero_b[l], False,
                             z_local[:, :lay.ncols], 1)
         ev[1].record()
-        z = self.gather(z_local)
+        if ex is not None:
+            _, events = ex.start(zfull)
+            ex.finish(events)
+            z = zfull
+        else:
+            z = z_local
         # the control plane's chunk plan follows the layer INPUT's format
         # (in_dim rows; layer 0 in the dataset dtype, later layers f32 as
         # the reference writer emits them), never the z storage layout, so

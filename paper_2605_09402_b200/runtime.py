@@ -34,6 +34,7 @@ from .chunks import load_layer_input, write_layer_output
 from .compute import device_code, get_backend
 from .engine import DeviceGraph, DeviceLayer, transform_device
 from .errors import ConfigError
+from .exchange import gather_ranges
 from .iostats import IOCounters
 from .orchestrator import CSV_FIELDS, LayerMetrics, metrics_from_device
 from .orchestrator import slot_budget
@@ -80,6 +81,9 @@ class PipelineConfig:
     # aggregates, transform first and aggregate z = h . W^T (linearity of
     # the mean / sum); the bit-exact "stable" backend never does
     transform_first: bool = True
+    # multi-GPU exchange: each owner range is broadcast in up to this many
+    # pieces, and the next layer folds every piece in as it lands
+    exchange_pieces: int = 4
 
     def validate(self) -> None:
         if self.partitions < 1:
@@ -165,6 +169,12 @@ class Engine:
                   for lw in weights.layers]
         self.b = [torch.as_tensor(np.ascontiguousarray(lw.bias)).cuda()
                   for lw in weights.layers]
+        self.exchange = None
+        if world > 1:
+            from .exchange import RangeExchange
+            self.exchange = RangeExchange(graph.num_vertices, self.ranges,
+                                          rank, dist_group,
+                                          config.exchange_pieces)
         self._wz = {}
         self.last_layers = []
         self._layers = {}
@@ -211,11 +221,15 @@ class Engine:
         return out
 
     def layer(self, l: int, x, *, chunk_budget=None, input_flag=None,
-              defer_metrics: bool = False, host_out=None):
+              defer_metrics: bool = False, host_out=None, out=None,
+              pieces=None):
         """One layer: x (V, d) CUDA tensor (or pinned host tensor, streamed)
         -> (y (V or range, out), metrics, device layer handle).
         ``input_flag``: extremes flag of the transform that produced x; the
-        output's flag is left in ``self.out_flags[l]``.
+        output's flag is left in ``self.out_flags[l]``. ``out``: where to
+        write the (nloc, out) output (a rank's slice of the next layer's
+        exchange buffer). ``pieces``: (bounds, events) of an input that is
+        still arriving from the other ranks (RangeExchange.start).
         With ``defer_metrics`` nothing waits for the device: the second
         element is a callable that collects the metrics later (the layer's
         control-plane verdict and timings are taken then)."""
@@ -254,8 +268,9 @@ class Engine:
             layer.graph_version = gv
         nloc = self.hi - self.lo
         out_dim = w.layers[l].out_dim
-        y = torch.empty((nloc, out_dim), dtype=_torch_dtype(cfg.embed_dtype),
-                        device="cuda")
+        y = out if out is not None else torch.empty(
+            (nloc, out_dim), dtype=_torch_dtype(cfg.embed_dtype),
+            device="cuda")
         if self.transform_first(l):
             return self._layer_transform_first(l, x, layer, rows, y, last,
                                                t0, defer_metrics, host_out)
@@ -265,7 +280,9 @@ class Engine:
             # input): upload them and all-gather the full input (SURVEY.md
             # §8e: every source row reaches every rank once per layer)
             x = self.gather(x.to("cuda", non_blocking=True))
-        if x.is_cuda:
+        if x.is_cuda and pieces is not None:
+            layer.run_pieces(self.graph, x, pieces[0], pieces[1], rows)
+        elif x.is_cuda:
             layer.run_resident(self.graph, x, rows, input_flag=input_flag)
         else:  # host (pinned) input: stream it in tiles (K1 streamer)
             layer.run_streamed(self.graph, x, rows,
@@ -304,7 +321,7 @@ class Engine:
             return y, collect, layer
         return y, collect(), layer
 
-    def _transform_rows(self, l, x, wz, zb):
+    def _transform_rows(self, l, x, wz, zb, out=None):
         """z = x . W_z^T (f32) on tcgen05; a pinned host x streams to HBM
         in double-buffered row tiles on a side stream, each tile
         transformed as soon as it lands (layer-input ingest overlaps the
@@ -318,8 +335,8 @@ class Engine:
         n = x.shape[0]
         # row pitch: whole 64-byte units, so a narrow z row never straddles
         # more DRAM bursts than it needs (the GEMM writes wz.shape[0] cols)
-        z = torch.empty((n, -(-wz.shape[0] // 16) * 16), dtype=torch.float32,
-                        device="cuda")
+        z = out if out is not None else torch.empty(
+            (n, z_pitch(wz.shape[0])), dtype=torch.float32, device="cuda")
         if x.is_cuda:
             if n:
                 transform_typed(x, wz, zb, False, z, 1, flag=self.z_flags[l])
@@ -367,25 +384,41 @@ class Engine:
         # all-gathered (z is narrower than h, so this is the cheap exchange)
         if self.world > 1 and x.shape[0] == self.num_vertices:
             x = x[self.lo:self.hi]
+        sage = self.kind == ModelKind.SAGE
+        ex = self.exchange
+        zfull = None
+        if ex is not None and not sage:
+            # the GEMM writes this rank's z rows straight into its slice of
+            # the exchange buffer; the owners' broadcasts fill the rest
+            zfull = ex.buffer(("z", l), z_pitch(wz.shape[0]), torch.float32,
+                              "cuda")
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ev[0].record()
-        zp = self._transform_rows(l, x, wz, zb)
+        zp = self._transform_rows(
+            l, x, wz, zb, out=None if zfull is None else ex.own(zfull))
         ev[1].record()
-        sage = self.kind == ModelKind.SAGE
         # SAGE's self half z2 = h_v . W2^T is needed for local rows only
         self_rows = None
         if sage:
             self_rows = zp[:, npad:] if self.world > 1 else \
                 zp[self.lo:self.hi, npad:]
         z = zp
-        if self.world > 1:
-            if sage:  # gather z1 only, in its own 64-byte-pitch rows
-                z1 = torch.zeros((zp.shape[0], -(-npad // 16) * 16),
+        if ex is not None:
+            if sage:  # exchange z1 only, in its own 64-byte-pitch rows
+                zfull = ex.buffer(("z1", l), z_pitch(npad), torch.float32,
+                                  "cuda")
+                ex.own(zfull)[:, :npad].copy_(zp[:, :npad])
+            _, events = ex.start(zfull)
+            ex.finish(events)
+            z = zfull
+        elif self.world > 1:  # a subclass's own gather (bench rank slice)
+            if sage:
+                z1 = torch.zeros((zp.shape[0], z_pitch(npad)),
                                  dtype=zp.dtype, device="cuda")
                 z1[:, :npad] = zp[:, :npad]
-                z = self.gather(z1)
-            else:
-                z = self.gather(zp)
+                zp = z1
+            z = self.gather(zp)
+        if self.world > 1:
             self.allreduce_max(self.z_flags[l])
         if l not in self.out_flags:
             self.out_flags[l] = torch.zeros(1, dtype=torch.int32,
@@ -421,10 +454,12 @@ class Engine:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
 
     def gather(self, y_local):
-        """All ranks' ranges -> full (V, out) next-layer input (NCCL)."""
+        """All ranks' ranges -> full (V, out) tensor, by owner broadcasts
+        into one buffer (exchange.RangeExchange; NCCL on GPUs)."""
         if self.world == 1:
             return y_local
-        return gather_ranges(y_local, self.ranges, self.group)
+        return self.exchange.gather(y_local, key=("in", y_local.shape[1],
+                                                  y_local.dtype))
 
     def infer(self, x, keep_layers: bool = False, host_out=None,
               metrics: bool = True):
@@ -435,54 +470,56 @@ class Engine:
         ``metrics=False`` nothing waits for the device (metrics None): the
         control plane's verdicts are still taken when the layers are
         re-armed, but their counters are not read back."""
+        import torch
+
         pending, outs = [], []
-        h, flag = x, None
+        h, flag, pieces = x, None, None
         nl = len(self.weights.layers)
+        ex = self.exchange
         for l in range(nl):
+            # with G ranks an aggregate-first next layer reads every rank's
+            # rows: this layer writes its own rows straight into the next
+            # layer's input buffer, whose other rows arrive by broadcast
+            nxt = None
+            if ex is not None and l != nl - 1 and \
+                    not self.transform_first(l + 1):
+                nxt = ex.buffer(("h", l + 1), self.weights.layers[l].out_dim,
+                                _torch_dtype(self.config.embed_dtype), "cuda")
             # every layer is queued before any metric is read back, so the
             # host never stalls the device between layers
             y, collect, _ = self.layer(
                 l, h, input_flag=flag, defer_metrics=True,
-                host_out=host_out if l == nl - 1 else None)
+                host_out=host_out if l == nl - 1 else None,
+                out=None if nxt is None else ex.own(nxt), pieces=pieces)
             pending.append(collect)
             if keep_layers:
                 outs.append(y)
-            if l != len(self.weights.layers) - 1:
-                # a transform-first next layer gathers its (narrower) z
-                # instead of this layer's output
-                h = y if (self.world > 1 and self.transform_first(l + 1)) \
-                    else self.gather(y)
+            pieces = None
+            if l != nl - 1:
                 flag = self.out_flags.get(l)
                 if flag is not None and self.world > 1:
                     self.allreduce_max(flag)
+                if nxt is not None:
+                    # the owners' pieces in ascending row order; the next
+                    # layer folds each one in as soon as it lands
+                    h, pieces = nxt, ex.start(nxt)
+                elif self.world > 1 and not self.transform_first(l + 1):
+                    h = self.gather(y)  # a subclass's own gather
+                else:
+                    # a transform-first next layer (or one rank) needs only
+                    # this rank's rows: it exchanges its narrower z instead
+                    h = y
         self.last_layers = outs
         if not metrics:
             return y, None
         return y, [collect() for collect in pending]
 
 
-def gather_ranges(y_local, ranges, group=None):
-    """Reassemble the next layer's full input from every rank's
-    destination range (partition_ranges order). One all-gather of
-    equal-size padded blocks: NCCL over NVLink on GPUs, gloo on CPU."""
-    import torch
-    import torch.distributed as dist
-
-    world = len(ranges)
-    w = max(h - l for l, h in ranges)
-    pad = torch.zeros((w, y_local.shape[1]), dtype=y_local.dtype,
-                      device=y_local.device)
-    pad[:y_local.shape[0]] = y_local
-    if dist.get_backend(group) == "nccl":
-        full = torch.empty((w * world, y_local.shape[1]), dtype=y_local.dtype,
-                           device=y_local.device)
-        dist.all_gather_into_tensor(full, pad, group=group)
-        blocks = [full[g * w:(g + 1) * w] for g in range(world)]
-    else:
-        blocks = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(blocks, pad, group=group)
-    return torch.cat([blocks[g][:h - l] for g, (l, h) in enumerate(ranges)],
-                     dim=0)
+def z_pitch(cols: int) -> int:
+    """Row pitch (f32 elements) of a transform-first z buffer: whole
+    64-byte units, so a narrow z row never straddles more DRAM bursts than
+    it needs."""
+    return -(-cols // 16) * 16
 
 
 def _load_graph(topology_path, in_degrees):

@@ -1,0 +1,143 @@
+"""Parity at the benchmark scale: BASELINE configs[1] (cfg2), the workload
+bench.py times -- 3-layer GCN [100,128,128,47] on the uniform V=2,400,000 /
+E=62,399,647 graph (seed 7), 8 MiB chunks (115 at layer 1), hot_slots=V.
+
+tests/golden/golden_scale.json + cfg2_gcn.npz come from ONE run of the
+unmodified reference at this size (tests/golden/make_golden.py scale, ~20
+minutes of CPU): per-layer output sha256, every metric, the graduation-log
+digest, and the reference's own oracle (oocgnn/oracle.py:26-55, float64,
+rounded to f32) per layer on 2048 sampled rows, with each layer's max |y|.
+
+* ``stable`` backend: every layer's output (full sha256), every metric and
+  the graduation order are bit-exact -- resident, streamed from pinned host
+  (the e2e path) and with the exact control engine logging.
+* ``tcgen05`` backend with transform-first layers (the headline bench
+  configuration): per layer max |y - oracle| <= 1e-5 * max |oracle| on the
+  sampled rows; integers bit-exact.
+"""
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import GOLDEN, digest_array
+from paper_2605_09402_b200 import _native as N
+from paper_2605_09402_b200 import storage as S
+from paper_2605_09402_b200.runtime import Engine, PipelineConfig
+
+pytestmark = pytest.mark.gpu
+
+CASE = "cfg2_gcn"
+TOL = 1e-5  # relative to the layer's max |oracle|
+METRICS = ("messages", "evictions", "reloads", "unique_reloads",
+           "mean_span", "p99_span", "mean_reload_pct", "hot_peak",
+           "hot_slot_count")
+
+
+@pytest.fixture(scope="module")
+def golden():
+    man = json.loads((GOLDEN / "golden_scale.json").read_text())[CASE]
+    arrays = dict(np.load(GOLDEN / f"{CASE}.npz"))
+    return man, arrays
+
+
+@pytest.fixture(scope="module")
+def cfg2(golden):
+    man, _ = golden
+    kind, v, deg, dim, seed, dtype = man["dataset_spec"]
+    graph, feats = S.synthetic_in_memory(kind, v, deg, dim, seed, dtype)
+    assert graph.num_edges == man["num_edges"]
+    w = S.random_weights(S.ModelKind(man["model"]), man["dims"],
+                         man["weight_seed"])
+    return graph, feats, w
+
+
+def _config(man, **kw):
+    return PipelineConfig(chunk_budget=8 << 20,
+                          hot_slots=man["config"]["hot_slots"], **kw)
+
+
+def _check_metrics(metrics, man):
+    for l, (m, g) in enumerate(zip(metrics, man["layers"])):
+        for f in METRICS:
+            assert getattr(m, f) == g[f], (l, f, getattr(m, f), g[f])
+
+
+def test_cfg2_stable_resident_bit_exact(golden, cfg2):
+    man, _ = golden
+    graph, feats, w = cfg2
+    eng = Engine(graph, w, _config(man, backend="stable"))
+    _, metrics = eng.infer(torch.as_tensor(feats).cuda(), keep_layers=True)
+    for l, y in enumerate(eng.last_layers):
+        assert digest_array(y.cpu().numpy()) == \
+            man["layers"][l]["output_sha"], l
+    _check_metrics(metrics, man)
+    eng.close()
+
+
+def test_cfg2_stable_streamed_from_host_bit_exact(golden, cfg2):
+    """The e2e path: features streamed from pinned host in tiles."""
+    man, _ = golden
+    graph, feats, w = cfg2
+    eng = Engine(graph, w, _config(man, backend="stable",
+                                   stream_tile_bytes=64 << 20))
+    _, metrics = eng.infer(torch.as_tensor(feats).pin_memory(),
+                           keep_layers=True)
+    for l, y in enumerate(eng.last_layers):
+        assert digest_array(y.cpu().numpy()) == \
+            man["layers"][l]["output_sha"], l
+    _check_metrics(metrics, man)
+    eng.close()
+
+
+def test_cfg2_graduation_order_bit_exact(golden, cfg2):
+    """The exact control engine with logs: the graduation order of all
+    2.4M destinations per layer equals the reference's."""
+    man, _ = golden
+    graph, feats, w = cfg2
+    eng = Engine(graph, w, _config(man, backend="stable", record_log=True))
+    h = torch.as_tensor(feats).cuda()
+    for l, g in enumerate(man["layers"]):
+        y, m, layer = eng.layer(l, h)
+        assert digest_array(layer.log(N.LOG_GRADUATED)) == \
+            g["graduated_sha"], l
+        assert digest_array(layer.log(N.LOG_VICTIMS)) == g["victims_sha"]
+        for f in METRICS:
+            assert getattr(m, f) == g[f], (l, f)
+        layer.close()
+        h = y
+    eng.close()
+
+
+def test_cfg2_tcgen05_within_tolerance(golden, cfg2):
+    """Headline backend (3xTF32 tcgen05, transform-first last layer)
+    against the reference's per-layer oracle at benchmark scale."""
+    man, arrays = golden
+    graph, feats, w = cfg2
+    eng = Engine(graph, w, _config(man, backend="tcgen05"))
+    assert eng.transform_first(2) and not eng.transform_first(0)
+    _, metrics = eng.infer(torch.as_tensor(feats).cuda(), keep_layers=True)
+    rows = torch.as_tensor(arrays["rows"]).cuda()
+    for l, y in enumerate(eng.last_layers):
+        got = y[rows].double().cpu().numpy()
+        ref = arrays[f"L{l}_oracle_rows"].astype(np.float64)
+        bound = TOL * man["layers"][l]["oracle_absmax"]
+        err = float(np.abs(got - ref).max())
+        assert err <= bound, (l, err, bound)
+        # and the whole layer's extremes agree with the oracle's
+        assert abs(float(y.abs().max()) - man["layers"][l]["oracle_absmax"]) \
+            <= bound
+    _check_metrics(metrics, man)
+    eng.close()
+
+
+def test_cfg2_reference_engine_rows_agree_with_its_oracle(golden):
+    """Sanity of the fixture itself: the reference engine's f32 rows are
+    within the reference's own 1e-4 bar of its oracle rows."""
+    man, arrays = golden
+    for l in range(len(man["layers"])):
+        d = np.abs(arrays[f"L{l}_out_rows"].astype(np.float64)
+                   - arrays[f"L{l}_oracle_rows"])
+        assert d.max() <= 1e-4
