@@ -323,6 +323,18 @@ ATLAS_API int atlas_spill_write(const char* part_dir, const void* rows,
                                 int64_t spill_rows, int32_t threads,
                                 int64_t* bytes_written);
 
+/* Writes one output partition as the reference's writer lays it out
+ * (oocgnn/writer.py:40-115: partition buffers filled in graduation order,
+ * each flush sorted by id): spill f holds ids[spill_start[f] ..
+ * spill_start[f+1]) (ascending), rows gathered from the dense matrix
+ * `rows` (row of id v at v * ld elements), plus the manifest. */
+ATLAS_API int atlas_spill_write_runs(const char* part_dir, const void* rows,
+                                     int32_t dtype, int64_t dim, int64_t ld,
+                                     const int64_t* ids,
+                                     const int64_t* spill_start,
+                                     int64_t nspills, int32_t threads,
+                                     int64_t* bytes_written);
+
 /* Gather-pattern replay (ablation criterion 11): rows a destination-major
  * gather engine loads in one layer through an LRU cache of cache_rows rows
  * fetched in block_rows blocks (0 cache rows: every touch loads). Replaces

@@ -113,6 +113,8 @@ def _declare(lib):
        c_i32, c_i32, c_i64, c_i64, c_vp, c_vp, c_i32, P_i64)
     fn("atlas_spill_write", ctypes.c_int, ctypes.c_char_p, c_vp, c_i32, c_i64,
        c_i64, c_i64, c_i64, c_i64, c_i32, P_i64)
+    fn("atlas_spill_write_runs", ctypes.c_int, ctypes.c_char_p, c_vp, c_i32,
+       c_i64, c_i64, c_vp, c_vp, c_i64, c_i32, P_i64)
     fn("atlas_gather_replay", ctypes.c_int, c_i64, c_i64, c_vp, c_vp, c_i64,
        c_i64, P_i64)
 
@@ -130,6 +132,7 @@ EXPORTED = [
     "atlas_layer_timing", "atlas_reorder", "atlas_transform_typed",
     "atlas_layer_run_gat", "atlas_layer_run_fused", "atlas_layer_bind_graph",
     "atlas_spill_read", "atlas_spill_write", "atlas_gather_replay",
+    "atlas_spill_write_runs",
 ]
 
 

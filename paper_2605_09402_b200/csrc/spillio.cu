@@ -183,6 +183,86 @@ int default_threads(int32_t threads) {
   return (int)std::max(1u, std::min(h, 32u));
 }
 
+// Writes nfiles spills spill_0.. into dir plus its manifest. ids_of(f, v)
+// fills spill f's ascending id list; rows are gathered from src, the row of
+// id v at v * ld elements (ld >= dim; the spill stores dim columns). Runs
+// of consecutive ids go out as one write. Returns an ATLAS status.
+template <typename IdsOf>
+int write_spills(const char* part_dir, const uint8_t* src, int32_t dtype,
+                 int64_t dim, int64_t ld, int64_t nfiles, IdsOf ids_of,
+                 int32_t threads, int64_t* bytes_written) {
+  const int64_t item = dtype == ATLAS_F32 ? 4 : 2;
+  const int64_t row_b = dim * item;
+  const std::string dir(part_dir);
+  std::atomic<int64_t> bytes{0};
+  FirstError err;
+  run_pool(nfiles, default_threads(threads), [&](int64_t f) {
+    std::vector<uint64_t> ids;
+    ids_of(f, ids);
+    const int64_t nr = (int64_t)ids.size();
+    const int64_t ids_pos = kAlign;
+    const int64_t rows_pos = ids_pos + align_up(nr * 8);
+    const int64_t size = align_up(rows_pos + nr * row_b);
+    const std::string path = dir + "/spill_" + std::to_string(f);
+    const int fd = ::open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (fd < 0) {
+      err.set(ATLAS_EFORMAT, path + ": cannot create");
+      return;
+    }
+    std::vector<uint8_t> head(kAlign, 0);
+    const uint32_t ver = 1, d32 = (uint32_t)dim;
+    const uint64_t ulo = ids.front(), uhi = ids.back(), unr = (uint64_t)nr;
+    std::memcpy(head.data(), "ASPL", 4);
+    std::memcpy(head.data() + 4, &ver, 4);
+    std::memcpy(head.data() + 8, &ulo, 8);
+    std::memcpy(head.data() + 16, &uhi, 8);
+    std::memcpy(head.data() + 24, &unr, 8);
+    std::memcpy(head.data() + 32, &d32, 4);
+    head[36] = dtype == ATLAS_F32 ? 0 : 1;
+    std::vector<uint64_t> idblk((size_t)(rows_pos - ids_pos) / 8, 0);
+    std::copy(ids.begin(), ids.end(), idblk.begin());
+    bool ok = pwrite_all(fd, head.data(), kAlign, 0) &&
+              pwrite_all(fd, idblk.data(), rows_pos - ids_pos, ids_pos);
+    for (int64_t i = 0; ok && i < nr;) {
+      int64_t j = i + 1;
+      if (ld == dim)
+        while (j < nr && ids[j] == ids[j - 1] + 1) j++;
+      ok = pwrite_all(fd, src + (int64_t)ids[i] * ld * item, (j - i) * row_b,
+                      rows_pos + i * row_b);
+      i = j;
+    }
+    const int64_t tail = size - (rows_pos + nr * row_b);
+    if (ok && tail > 0) {
+      std::vector<uint8_t> zeros((size_t)tail, 0);
+      ok = pwrite_all(fd, zeros.data(), tail, rows_pos + nr * row_b);
+    }
+    ::close(fd);
+    if (!ok) {
+      err.set(ATLAS_EFORMAT, path + ": write failed");
+      return;
+    }
+    bytes.fetch_add(size, std::memory_order_relaxed);
+  });
+  if (err.code != ATLAS_OK) {
+    set_error(err.msg);
+    return err.code;
+  }
+  // the manifest lists the files in order, like append_manifest
+  std::string manifest;
+  for (int64_t f = 0; f < nfiles; f++)
+    manifest += "spill_" + std::to_string(f) + "\n";
+  const std::string mpath = dir + "/manifest.txt";
+  const int fd = ::open(mpath.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+  if (fd < 0 || !pwrite_all(fd, manifest.data(), manifest.size(), 0)) {
+    if (fd >= 0) ::close(fd);
+    set_error(mpath + ": write failed");
+    return ATLAS_EFORMAT;
+  }
+  ::close(fd);
+  if (bytes_written) *bytes_written = bytes.load();
+  return ATLAS_OK;
+}
+
 }  // namespace
 }  // namespace atlas
 
@@ -249,78 +329,56 @@ int atlas_spill_write(const char* part_dir, const void* rows, int32_t dtype,
     const int64_t n = id_hi - id_lo;
     const int64_t step = spill_rows > 0 ? spill_rows : std::max<int64_t>(n, 1);
     const int64_t nfiles = n > 0 ? ceil_div(n, step) : 0;
-    const int64_t item = dtype == ATLAS_F32 ? 4 : 2;
-    const int64_t row_b = dim * item;
-    const std::string dir(part_dir);
-    std::atomic<int64_t> bytes{0};
-    FirstError err;
-    run_pool(nfiles, default_threads(threads), [&](int64_t f) {
-      const int64_t lo = id_lo + f * step, hi = std::min(id_hi, lo + step);
-      const int64_t nr = hi - lo;
-      const int64_t ids_pos = kAlign;
-      const int64_t rows_pos = ids_pos + align_up(nr * 8);
-      const int64_t size = align_up(rows_pos + nr * row_b);
-      const std::string path = dir + "/spill_" + std::to_string(f);
-      const int fd = ::open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
-      if (fd < 0) {
-        err.set(ATLAS_EFORMAT, path + ": cannot create");
-        return;
-      }
-      std::vector<uint8_t> head(kAlign, 0);
-      const uint32_t ver = 1, d32 = (uint32_t)dim;
-      const uint64_t ulo = (uint64_t)lo, uhi = (uint64_t)(hi - 1),
-                     unr = (uint64_t)nr;
-      std::memcpy(head.data(), "ASPL", 4);
-      std::memcpy(head.data() + 4, &ver, 4);
-      std::memcpy(head.data() + 8, &ulo, 8);
-      std::memcpy(head.data() + 16, &uhi, 8);
-      std::memcpy(head.data() + 24, &unr, 8);
-      std::memcpy(head.data() + 32, &d32, 4);
-      head[36] = dtype == ATLAS_F32 ? 0 : 1;
-      std::vector<uint64_t> ids((size_t)(rows_pos - ids_pos) / 8, 0);
-      for (int64_t i = 0; i < nr; i++) ids[i] = (uint64_t)(lo + i);
-      bool ok = pwrite_all(fd, head.data(), kAlign, 0) &&
-                pwrite_all(fd, ids.data(), rows_pos - ids_pos, ids_pos);
-      const auto* src = static_cast<const uint8_t*>(rows);
-      if (ok && ld == dim) {
-        ok = pwrite_all(fd, src + (lo - id_lo) * row_b, nr * row_b, rows_pos);
-      } else {
-        for (int64_t i = 0; ok && i < nr; i++)
-          ok = pwrite_all(fd, src + (lo - id_lo + i) * ld * item, row_b,
-                          rows_pos + i * row_b);
-      }
-      const int64_t tail = size - (rows_pos + nr * row_b);
-      if (ok && tail > 0) {
-        std::vector<uint8_t> zeros((size_t)tail, 0);
-        ok = pwrite_all(fd, zeros.data(), tail, rows_pos + nr * row_b);
-      }
-      ::close(fd);
-      if (!ok) {
-        err.set(ATLAS_EFORMAT, path + ": write failed");
-        return;
-      }
-      bytes.fetch_add(size, std::memory_order_relaxed);
-    });
-    if (err.code != ATLAS_OK) {
-      set_error(err.msg);
-      return err.code;
-    }
-    // the manifest lists the files in order, like append_manifest
-    std::string manifest;
-    for (int64_t f = 0; f < nfiles; f++)
-      manifest += "spill_" + std::to_string(f) + "\n";
-    const std::string mpath = dir + "/manifest.txt";
-    const int fd = ::open(mpath.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
-    if (fd < 0 || !pwrite_all(fd, manifest.data(), manifest.size(), 0)) {
-      if (fd >= 0) ::close(fd);
-      set_error(mpath + ": write failed");
-      return ATLAS_EFORMAT;
-    }
-    ::close(fd);
-    if (bytes_written) *bytes_written = bytes.load();
-    return ATLAS_OK;
+    // rows holds ids [id_lo, id_hi): row of id v at (v - id_lo) * ld
+    const auto* src = static_cast<const uint8_t*>(rows) -
+                      id_lo * ld * (dtype == ATLAS_F32 ? 4 : 2);
+    return write_spills(
+        part_dir, src, dtype, dim, ld, nfiles,
+        [&](int64_t f, std::vector<uint64_t>& ids) {
+          const int64_t lo = id_lo + f * step, hi = std::min(id_hi, lo + step);
+          ids.resize(hi - lo);
+          for (int64_t i = 0; i < hi - lo; i++) ids[i] = (uint64_t)(lo + i);
+        },
+        threads, bytes_written);
   } catch (const std::exception& e) {
     set_error(std::string("atlas_spill_write: ") + e.what());
+    return ATLAS_EINVARIANT;
+  }
+}
+
+int atlas_spill_write_runs(const char* part_dir, const void* rows,
+                           int32_t dtype, int64_t dim, int64_t ld,
+                           const int64_t* ids, const int64_t* spill_start,
+                           int64_t nspills, int32_t threads,
+                           int64_t* bytes_written) {
+  try {
+    if (!part_dir || dim < 1 || ld < dim || nspills < 0 ||
+        (nspills && (!rows || !ids || !spill_start)) ||
+        (dtype != ATLAS_F32 && dtype != ATLAS_F16)) {
+      set_error("atlas_spill_write_runs: bad arguments");
+      return ATLAS_ECONFIG;
+    }
+    for (int64_t f = 0; f < nspills; f++) {
+      const int64_t a = spill_start[f], b = spill_start[f + 1];
+      if (b <= a) {
+        set_error("atlas_spill_write_runs: empty spill");
+        return ATLAS_EINVARIANT;
+      }
+      for (int64_t i = a; i < b; i++)
+        if (ids[i] < 0 || (i > a && ids[i] <= ids[i - 1])) {
+          set_error("atlas_spill_write_runs: spill ids must ascend");
+          return ATLAS_EINVARIANT;
+        }
+    }
+    return write_spills(
+        part_dir, static_cast<const uint8_t*>(rows), dtype, dim, ld, nspills,
+        [&](int64_t f, std::vector<uint64_t>& out) {
+          const int64_t a = spill_start[f], b = spill_start[f + 1];
+          out.assign(ids + a, ids + b);
+        },
+        threads, bytes_written);
+  } catch (const std::exception& e) {
+    set_error(std::string("atlas_spill_write_runs: ") + e.what());
     return ATLAS_EINVARIANT;
   }
 }

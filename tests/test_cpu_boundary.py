@@ -194,3 +194,23 @@ def test_gather_oracle_pinned_to_reference_oracle(case):
             entry["oracle64_sha"]
     assert float(np.abs(outs[-1]).max().astype(np.float32)) == \
         entry["oracle64_absmax"]
+
+
+def test_cfg2_scale_golden_is_self_consistent():
+    """The benchmark-scale golden (make_golden.py scale, one run of the
+    unmodified reference at cfg2): the reference engine's f32 rows sit
+    within the reference's own 1e-4 bar of its float64 oracle rows
+    (tests/test_acceptance.py:43), and the row sample and metrics are the
+    shape the GPU tests expect."""
+    import json
+    from helpers import GOLDEN
+    man = json.loads((GOLDEN / "golden_scale.json").read_text())["cfg2_gcn"]
+    arrays = dict(np.load(GOLDEN / "cfg2_gcn.npz"))
+    assert man["num_edges"] == 62_399_647 and len(man["layers"]) == 3
+    assert len(arrays["rows"]) == 2048
+    for l, lay in enumerate(man["layers"]):
+        assert lay["messages"] == man["num_edges"]
+        d = np.abs(arrays[f"L{l}_out_rows"].astype(np.float64)
+                   - arrays[f"L{l}_oracle_rows"])
+        assert d.max() <= 1e-4
+        assert abs(lay["output_absmax"] - lay["oracle_absmax"]) <= 1e-6
