@@ -138,3 +138,62 @@ def write_layer_output(layer_dir, matrix: np.ndarray, partitions: int = 1,
             max(1, hi - lo), int(threads), ctypes.byref(nb)))
         total += int(nb.value)
     return total
+
+
+def graduation_spills(grad_order, num_vertices: int, partitions: int,
+                      dim: int, spill_buffer: int):
+    """The reference writer's file layout for one layer output
+    (oocgnn/writer.py:40-115): per partition, a buffer of
+    ``max(1, spill_buffer // partitions // (dim*4 + 8))`` rows fills in
+    graduation order and every full buffer (and the final partial one) is
+    flushed as one spill sorted by id. Returns, per partition, (ids int64
+    laid out spill after spill, spill_start int64[nspills+1])."""
+    from .storage import partition_width
+
+    order = np.asarray(grad_order, dtype=np.int64)
+    if order.shape != (num_vertices,):
+        raise ConsistencyError(f"graduation order holds {order.size} ids, "
+                               f"expected {num_vertices}")
+    width = partition_width(num_vertices, partitions)
+    per = max(1, spill_buffer // max(1, partitions) // (dim * 4 + 8))
+    part = order // width
+    out = []
+    for k in range(partitions):
+        seq = order[part == k]            # graduation order within k
+        spill = np.arange(seq.size, dtype=np.int64) // per
+        ids = seq[np.lexsort((seq, spill))]
+        nsp = -(-seq.size // per)
+        start = np.minimum(np.arange(nsp + 1, dtype=np.int64) * per,
+                           seq.size)
+        out.append((ids, start))
+    return out
+
+
+def write_graduation_layout(layer_dir, matrix: np.ndarray, grad_order,
+                            partitions: int, spill_buffer: int,
+                            threads: int = 0) -> int:
+    """Write a (V, dim) layer output exactly as the reference's writer
+    stage would have (same spill files, bytes and manifests, f32 rows --
+    oocgnn/writer.py:60-62), given the layer's graduation order. Returns
+    the spill bytes written (IOCounters.spill_bytes_written)."""
+    import ctypes
+
+    from . import _native as N
+    from .storage import LayerMeta, write_layer_meta
+
+    rows = np.ascontiguousarray(matrix, dtype=np.float32)
+    v, dim = rows.shape
+    layout = graduation_spills(grad_order, v, partitions, dim, spill_buffer)
+    write_layer_meta(layer_dir, LayerMeta(v, dim, "f32", partitions))
+    lib = N.load_library()
+    total = 0
+    for k, (ids, start) in enumerate(layout):
+        pdir = part_dir(layer_dir, k)
+        pdir.mkdir(parents=True, exist_ok=True)
+        nb = ctypes.c_int64()
+        N.check(lib.atlas_spill_write_runs(
+            str(pdir).encode(), rows.ctypes.data, N.F32, dim, dim,
+            ids.ctypes.data, start.ctypes.data, len(start) - 1,
+            int(threads), ctypes.byref(nb)))
+        total += int(nb.value)
+    return total

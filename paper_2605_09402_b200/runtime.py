@@ -533,22 +533,44 @@ def _load_graph(topology_path, in_degrees):
                     indeg), topo_bytes
 
 
-def _write_output(layer_dir, y, config, num_vertices) -> int:
-    """One layer's output to its layer directory: a D2H copy into pinned
-    memory (full PCIe rate; a pageable .cpu() runs at a few GB/s), then the
-    library's parallel spill writer."""
+def _graduation_order(layer) -> np.ndarray:
+    """The layer's graduation order (every destination once), from the
+    control plane's graduation log ([n, ids..] per sub-batch)."""
+    from . import _native as N
+
+    flat = layer.log(N.LOG_GRADUATED)
+    keep = np.ones(flat.size, dtype=bool)
+    i = 0
+    while i < flat.size:  # drop the per-batch counts
+        keep[i] = False
+        i += 1 + int(flat[i])
+    return flat[keep]
+
+
+def _write_output(layer_dir, y, config, grad_order) -> int:
+    """One layer's output to its layer directory, laid out exactly as the
+    reference's writer stage lays it out (oocgnn/writer.py:40-115: f32
+    rows, partition buffers of spill_buffer bytes filled in graduation
+    order, each flush sorted by id), so the directory is byte-identical to
+    the reference's. y goes D2H into pinned memory first (a pageable .cpu()
+    runs at a few GB/s). A failed write leaves no partial directory
+    (oocgnn/writer.py:119-121). Returns the spill bytes written."""
     import torch
 
-    if config.embed_dtype == "bf16":
-        y = y.float()
-    pinned = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+    from .chunks import write_graduation_layout
+
+    pinned = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
     pinned.copy_(y)
-    host = pinned.numpy()
-    dtype = "f16" if config.embed_dtype == "f16" else "f32"
+    layer_dir = Path(layer_dir)
     if layer_dir.exists():
         shutil.rmtree(layer_dir)
-    return write_layer_output(layer_dir, host, partitions=config.partitions,
-                              dtype=dtype)
+    try:
+        return write_graduation_layout(layer_dir, pinned.numpy(), grad_order,
+                                       config.partitions,
+                                       config.spill_buffer)
+    except BaseException:
+        shutil.rmtree(layer_dir, ignore_errors=True)
+        raise
 
 
 def _upload(rows):
@@ -573,13 +595,15 @@ def run_layer(topology_path, in_degrees: np.ndarray, input_dir, output_dir,
                           f"input holds {meta.dim}")
     graph, topo_bytes = _load_graph(topology_path, in_degrees)
     _, rows, feat_bytes, delivery = load_layer_input(input_dir)
-    eng = Engine(graph, weights, config)
+    # the graduation log fixes the output's spill layout
+    eng = Engine(graph, weights, replace(config, record_log=True))
     try:
         y, m, layer = eng.layer(layer_index, _upload(rows))
+        order = _graduation_order(layer)
         layer.close()
     finally:
         eng.close()
-    written = _write_output(Path(output_dir), y, config, graph.num_vertices)
+    written = _write_output(Path(output_dir), y, config, order)
     m.feature_bytes_read = feat_bytes
     m.bytes_read += feat_bytes + topo_bytes
     m.bytes_written += written
@@ -610,7 +634,8 @@ def run_inference(graph_dir, weights, config: PipelineConfig, out_dir,
                      in_degrees)
     topo_bytes = offsets.nbytes + nbrs.nbytes
     _, rows, feat_bytes, delivery = load_layer_input(features_dir)
-    eng = Engine(graph, weights, config)
+    # the graduation log fixes each output's spill layout
+    eng = Engine(graph, weights, replace(config, record_log=True))
     layers = []
     prev_dir = None
     try:
@@ -618,10 +643,10 @@ def run_inference(graph_dir, weights, config: PipelineConfig, out_dir,
         for l in range(len(weights.layers)):
             tl = time.perf_counter()
             y, m, layer = eng.layer(l, h)
+            order = _graduation_order(layer)
             layer.close()
             layer_out = out_dir / f"layer_{l}"
-            m.bytes_written += _write_output(layer_out, y, config,
-                                             hdr.num_vertices)
+            m.bytes_written += _write_output(layer_out, y, config, order)
             if l == 0:
                 m.feature_bytes_read = feat_bytes
                 m.bytes_read += feat_bytes + topo_bytes
