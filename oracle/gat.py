@@ -102,3 +102,36 @@ def gat_per_layer(offsets, neighbors, features, layers, slope=0.2):
             h = np.maximum(h, 0.0)
         outs.append(h)
     return outs
+
+
+def gat_layer_at(dests, in_offsets, in_sources, h_src, h_dst, weight, attn_l,
+                 attn_r, bias, heads, concat, slope=0.2):
+    """The same layer for a SUBSET of destinations (float64), for checks at
+    scales where whole layers do not fit the host: ``dests`` (n,) sampled
+    destinations, ``in_offsets`` (n+1,) / ``in_sources`` their in-edges as
+    row indices into ``h_src`` (the source rows the sample needs), ``h_dst``
+    (n, in) the destinations' own rows (for er). Returns (n, H*F) or (n, F)
+    -- ``gat_layer``'s rows for ``dests`` when h_src/h_dst are the layer
+    input's rows."""
+    w = np.asarray(weight, np.float64)
+    hf = w.shape[0]
+    f = hf // heads
+    al, ar = np.asarray(attn_l, np.float64), np.asarray(attn_r, np.float64)
+    zs = (np.asarray(h_src, np.float64) @ w.T).reshape(-1, heads, f)
+    zd = (np.asarray(h_dst, np.float64) @ w.T).reshape(-1, heads, f)
+    el = np.einsum("vhf,hf->vh", zs, al)
+    er = np.einsum("vhf,hf->vh", zd, ar)
+    n = len(dests)
+    deg = np.diff(in_offsets)
+    dst = np.repeat(np.arange(n), deg)
+    src = np.asarray(in_sources, np.int64)
+    e = leaky(el[src] + er[dst], slope)
+    emax = np.full((n, heads), -np.inf)
+    np.maximum.at(emax, dst, e)
+    p = np.exp(e - emax[dst])
+    s = np.zeros((n, heads))
+    np.add.at(s, dst, p)
+    out = np.zeros((n, heads, f))
+    np.add.at(out, dst, (p / s[dst])[:, :, None] * zs[src])
+    out += np.asarray(bias, np.float64).reshape(heads, f)
+    return out.reshape(n, hf) if concat else out.mean(axis=1)

@@ -99,3 +99,27 @@ def test_extended_weight_emits_el_er(itemsize):
                                atol=1e-5)
     np.testing.assert_allclose(zx[:, lay.er_col:lay.er_col + 4], er,
                                atol=1e-5)
+
+
+def test_gat_subset_oracle_matches_whole_layer():
+    """oracle.gat.gat_layer_at (destination subsets, used by the IGB-Medium
+    scale check) == gat_layer's rows for those destinations."""
+    import numpy as np
+    from oracle import gat as OG
+    from paper_2605_09402_b200 import storage as S
+    from paper_2605_09402_b200.gat import random_gat_weights
+    g, _ = S.synthetic_in_memory("uniform", 500, 6, 4, 3)
+    w = random_gat_weights([12, 16, 5], 4, seed=2).layers[0]
+    h = np.random.default_rng(1).uniform(-1, 1, (500, 12))
+    full = OG.gat_layer(g.offsets, g.neighbors, h, w.weight, w.attn_l,
+                        w.attn_r, w.bias, w.heads, concat=True)
+    dests = np.array([0, 7, 99, 250, 499])
+    src = np.repeat(np.arange(500), np.diff(g.offsets))
+    dst = np.asarray(g.neighbors, np.int64)
+    lists = [src[dst == t] for t in dests]
+    offs = np.concatenate([[0], np.cumsum([len(x) for x in lists])])
+    srcs = np.concatenate(lists)
+    uniq, inv = np.unique(srcs, return_inverse=True)
+    got = OG.gat_layer_at(dests, offs, inv, h[uniq], h[dests], w.weight,
+                          w.attn_l, w.attn_r, w.bias, w.heads, concat=True)
+    np.testing.assert_allclose(got, full[dests], rtol=0, atol=1e-12)

@@ -131,3 +131,91 @@ def test_cfg2_tcgen05_within_tolerance(golden, cfg2):
             <= bound
     _check_metrics(metrics, man)
     eng.close()
+
+
+def test_cfg2_disk_to_disk_reproduces_reference_directories(golden,
+                                                            tmp_path):
+    """run_inference from a dataset directory (written by this repo's
+    reference-identical generator) to layer directories: every layer_l/ is
+    byte-identical to the reference's (sha256 over all files) and
+    metrics.csv equals the reference's except bytes_read."""
+    import csv
+
+    from test_disk_api import dir_digest
+    from paper_2605_09402_b200.runtime import run_inference
+
+    man, _ = golden
+    kind, v, deg, dim, seed, dtype = man["dataset_spec"]
+    ds = tmp_path / "cfg2"
+    S.generate_synthetic(kind, v, deg, dim, seed, ds, dtype=dtype)
+    w = S.random_weights(S.ModelKind(man["model"]), man["dims"],
+                         man["weight_seed"])
+    out = tmp_path / "out"
+    run_inference(ds, w, PipelineConfig(**man["config"], backend="stable"),
+                  out)
+    for l, want in enumerate(man["layer_dirs"]):
+        assert dir_digest(out / f"layer_{l}") == want, l
+    with open(out / "metrics.csv", newline="") as f:
+        got = [r[:-1] for r in csv.reader(f)]
+    for g, r in zip(got, man["metrics_csv"]):
+        assert g[:8] + g[9:] == r[:8] + r[9:], (g, r)
+
+
+def test_igb_medium_gat_sampled_destinations():
+    """BASELINE configs[2] at full size (the bench's IGB-Medium GAT: 10M
+    vertices, ~120M edges, 1024-d f16, 4 heads x 32, [1024,128,128,19],
+    f32 z): for 100,000 sampled destinations per layer, the device output
+    equals the float64 GAT oracle (oracle/gat.py ``gat_layer_at``, parity
+    unpinned: the reference has no GAT) applied to the SAME layer input,
+    within 2e-5 of the sample's max |y| -- a layer-local
+    check of pass A (tcgen05) and pass B (gat_ring) at scale."""
+    import bench
+    from oracle import gat as OG
+    from paper_2605_09402_b200.gat import GATEngine
+
+    graph, x, w = bench.build_igb("GAT", [1024, 128, 128, 19])
+    v = graph.num_vertices
+    eng = GATEngine(graph, w, PipelineConfig(chunk_budget=8 << 20,
+                                             hot_slots=v,
+                                             backend="tcgen05"))
+    _, metrics = eng.infer(x, keep_layers=True)
+    assert sum(m.messages for m in metrics) == 3 * graph.num_edges
+    rng = np.random.default_rng(11)
+    dests = np.sort(rng.choice(v, 100_000, replace=False))
+    mark = np.zeros(v, dtype=bool)
+    mark[dests] = True
+    nbrs = np.asarray(graph.neighbors, dtype=np.int64)
+    sel = mark[nbrs]
+    src = np.repeat(np.arange(v, dtype=np.int64),
+                    np.diff(graph.offsets))[sel]
+    dst = nbrs[sel]
+    del sel, nbrs
+    order = np.lexsort((src, dst))
+    src, dst = src[order], dst[order]
+    pos = np.searchsorted(dests, dst)
+    offs = np.concatenate([[0], np.cumsum(np.bincount(pos,
+                                                      minlength=len(dests)))])
+    inputs = [x] + eng.last_layers[:-1]
+    nl = len(w.layers)
+    for l, lw in enumerate(w.layers):
+        h, y = inputs[l], eng.last_layers[l]
+        errs, peak = [], 0.0
+        for b0 in range(0, len(dests), 10_000):
+            b1 = min(len(dests), b0 + 10_000)
+            e0, e1 = offs[b0], offs[b1]
+            uniq, inv = np.unique(src[e0:e1], return_inverse=True)
+            take = torch.as_tensor
+            h_src = h[take(uniq).cuda()].double().cpu().numpy()
+            h_dst = h[take(dests[b0:b1]).cuda()].double().cpu().numpy()
+            ref = OG.gat_layer_at(dests[b0:b1], offs[b0:b1 + 1] - e0, inv,
+                                  h_src, h_dst, lw.weight, lw.attn_l,
+                                  lw.attn_r, lw.bias, lw.heads,
+                                  concat=l != nl - 1,
+                                  slope=w.negative_slope)
+            if l != nl - 1:
+                ref = np.maximum(ref, 0.0)
+            got = y[take(dests[b0:b1]).cuda()].double().cpu().numpy()
+            errs.append(float(np.abs(got - ref).max()))
+            peak = max(peak, float(np.abs(ref).max()))
+        assert max(errs) <= 2e-5 * peak, (l, max(errs), peak)
+    eng.close()
