@@ -443,6 +443,51 @@ def cpu_baseline(graph, feats, weights, seconds=20.0):
                       f"of {os.cpu_count()} host cores"}
 
 
+def gat_cpu_baseline(graph, x, weights, seconds=15.0, block=50_000,
+                     batch=2000):
+    """The reference has no GAT, so there is no reference
+    CPU path for configs[2]: this times this repo's float64 GAT oracle
+    (oracle/gat.py ``gat_layer_at``, the CPU restatement the GPU is checked
+    against) on layer 1, destination batch after batch over the first
+    ``block`` destinations; edges/s extrapolates linearly like the
+    reference arm. The in-edge lists and source rows are prepared once,
+    outside the timed calls."""
+    import torch
+
+    from oracle import gat as OG
+
+    lw = weights.layers[0]
+    nbrs = np.asarray(graph.neighbors, dtype=np.int64)
+    sel = np.flatnonzero(nbrs < block)
+    src = np.searchsorted(graph.offsets, sel, side="right") - 1
+    dst = nbrs[sel]
+    order = np.lexsort((src, dst))
+    src, dst = src[order], dst[order]
+    offs = np.concatenate([[0], np.cumsum(np.bincount(dst,
+                                                      minlength=block))])
+    uniq, inv = np.unique(src, return_inverse=True)
+    rows = x[torch.as_tensor(uniq).cuda()].cpu().numpy()
+    own = x[:block].cpu().numpy()
+    t0 = time.perf_counter()
+    edges = done = 0
+    while done < block and time.perf_counter() - t0 < seconds:
+        b1 = min(block, done + batch)
+        e0, e1 = offs[done], offs[b1]
+        u, k = np.unique(inv[e0:e1], return_inverse=True)
+        OG.gat_layer_at(np.arange(done, b1), offs[done:b1 + 1] - e0, k,
+                        rows[u], own[done:b1], lw.weight, lw.attn_l,
+                        lw.attn_r, lw.bias, lw.heads, concat=True)
+        edges += e1 - e0
+        done = b1
+    dt = time.perf_counter() - t0
+    return {"value": edges / dt, "unit": "edges/s", "cores": os.cpu_count(),
+            "kind": "port",
+            "sample": f"NO reference CPU path exists for GAT (the reference "
+                      f"has none); this repo's float64 GAT oracle on layer 1 "
+                      f"(1024 -> 4x32): destinations [0, {done}), {edges} "
+                      f"in-edges in {dt:.1f} s, numpy + multi-threaded BLAS"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -512,6 +557,9 @@ def main():
                          "(SURVEY.md §8d: layer inputs >= 2 are fp16 for "
                          "configs 4/5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg3", action="store_true",
+                    help="skip the IGB-Medium GAT (BASELINE configs[2]) "
+                         "measurement the default cfg2 run nests as 'cfg3'")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true",
                     help="skip the bit-exact (stable) backend re-run")
@@ -541,6 +589,31 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line = measure(args, world, rank, local)
+    if line is not None and args.workload == "cfg2" and world == 1 \
+            and not args.no_cfg3:
+        # BASELINE configs[2] (IGB-Medium GAT), the largest single-GPU
+        # config, measured in the same run and reported inside the line
+        import copy
+        gc.collect()
+        torch.cuda.empty_cache()
+        a3 = copy.copy(args)
+        a3.workload, a3.no_alt = "igb-medium-gat", True
+        line["cfg3"] = measure(a3, world, rank, local)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure(args, world, rank, local):
+    """One workload on this rank; rank 0 returns its JSON-line dict."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_09402_b200 import _native as N
+    from paper_2605_09402_b200.runtime import Engine, PipelineConfig
+
     t_gen = time.perf_counter()
     if args.workload == "cfg2":
         graph, feats, weights = build_inputs()
@@ -788,12 +861,13 @@ def main():
             "clocks": clk,
             "setup_s": setup_s, "generate_s": gen_s,
         }
-        if not args.no_cpu_baseline and world == 1 and feats is not None:
-            line["cpu_baseline"] = cpu_baseline(graph, feats, weights)
-        print(json.dumps(line), flush=True)
+        if not args.no_cpu_baseline and world == 1:
+            if feats is not None:
+                line["cpu_baseline"] = cpu_baseline(graph, feats, weights)
+            elif is_gat:
+                line["cpu_baseline"] = gat_cpu_baseline(graph, x, weights)
     eng.close()
-    if world > 1:
-        dist.destroy_process_group()
+    return line if rank == 0 else None
 
 
 if __name__ == "__main__":

@@ -154,6 +154,7 @@ int atlas_graph_create(int32_t device, int64_t V, int64_t E,
                        const uint32_t* in_degrees_host, int64_t lo,
                        int64_t hi, void* stream, atlas_graph** out) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_graph_create");
     if (!out || V < 0 || E < 0 || lo < 0 || hi < lo || hi > V)
       fail(ATLAS_ECONFIG, "bad graph arguments");
     if (V >= (int64_t)0x7FFFFFFF || E >= (int64_t)0xFFFFFFFF)
@@ -181,6 +182,7 @@ int atlas_graph_update(atlas_graph* g, int64_t V, int64_t E,
                        const uint32_t* neighbors_host,
                        const uint32_t* in_degrees_host, void* stream) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_graph_update");
     if (!g || V < 0 || E < 0 || g->hi > V)
       fail(ATLAS_ECONFIG, "bad graph arguments");
     if (V >= (int64_t)0x7FFFFFFF || E >= (int64_t)0xFFFFFFFF)
@@ -207,6 +209,7 @@ int atlas_layer_create(const atlas_layer_desc* desc,
                        const uint32_t* in_degrees_host, void* stream,
                        atlas_layer** out) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_layer_create");
     if (!desc || !out) fail(ATLAS_ECONFIG, "null argument");
     const atlas_layer_desc& D = *desc;
     if (D.slot_count < 1) fail(ATLAS_ECONFIG, "hot_slots must be >= 1");
@@ -305,6 +308,7 @@ int atlas_chunk_submit(atlas_layer* L, int64_t start, int64_t end,
                        const int64_t* off, const int64_t* nbrs, int64_t m,
                        void* stream) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_chunk_submit");
     if (!L) fail(ATLAS_ECONFIG, "null layer");
     if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
     use_device(L->desc.device);
@@ -323,6 +327,7 @@ int atlas_chunk_graduated(atlas_layer* L, int64_t* ids, float* rows,
                           int64_t cap, int64_t* count, int64_t* batch_len,
                           int64_t batch_cap, int64_t* num_batches) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_chunk_graduated");
     if (!L) fail(ATLAS_ECONFIG, "null layer");
     use_device(L->desc.device);
     // the chunk's work was queued on the caller's stream (often a
@@ -363,6 +368,7 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
                              int64_t chunk_rows, const int32_t* input_flag,
                              void* stream) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_layer_run_resident");
     if (!L || !g) fail(ATLAS_ECONFIG, "null argument");
     const atlas_layer_desc& D = L->desc;
     if (g->V != D.num_vertices || g->lo != D.dst_lo || g->hi != D.dst_hi)
@@ -396,6 +402,7 @@ int atlas_layer_run_gat(atlas_layer* L, const atlas_graph* g, const void* z,
                         int64_t ldy, const float* attn_l,
                         int64_t chunk_rows, void* stream) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_layer_run_gat");
     if (!L || !g || !z || !bias || !y) fail(ATLAS_ECONFIG, "null argument");
     if (!L->gat) fail(ATLAS_ECONFIG, "layer was not created as GAT");
     const atlas_layer_desc& D = L->desc;
@@ -425,6 +432,7 @@ int atlas_layer_run_fused(atlas_layer* L, const atlas_graph* g,
                           int32_t* out_flag, void* y_host, int64_t ldy_host,
                           int32_t host_slices, void* stream) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_layer_run_fused");
     if (!L || !g || !z || !bias || !y) fail(ATLAS_ECONFIG, "null argument");
     if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
     const atlas_layer_desc& D = L->desc;
@@ -486,6 +494,7 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
                              int64_t tile_rows, int64_t chunk_rows,
                              void* stream) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_layer_run_streamed");
     if (!L || !g || !x_host) fail(ATLAS_ECONFIG, "null argument");
     const atlas_layer_desc& D = L->desc;
     if (g->V != D.num_vertices || g->lo != D.dst_lo || g->hi != D.dst_hi)
@@ -583,6 +592,7 @@ int atlas_layer_run_pieces(atlas_layer* L, const atlas_graph* g,
                            void* const* ready, int64_t chunk_rows,
                            void* stream) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_layer_run_pieces");
     if (!L || !g || !x || !bounds || npieces < 1)
       fail(ATLAS_ECONFIG, "null argument");
     const atlas_layer_desc& D = L->desc;
@@ -641,6 +651,7 @@ int atlas_reorder(int32_t device, int64_t V, int64_t E, const int64_t* off,
                   int64_t* old_to_new, int64_t* new_off, uint32_t* new_nbrs,
                   uint32_t* new_indeg, double* scores, void* stream) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_reorder");
     if (V < 0 || E < 0 || !off || !old_to_new || !new_off)
       fail(ATLAS_ECONFIG, "bad reorder arguments");
     if (V >= (int64_t)0x7FFFFFFF || E >= (int64_t)0x7FFFFFFF)
@@ -674,6 +685,7 @@ int atlas_transform(int32_t backend, const float* x, int64_t rows, int64_t k,
                     int32_t relu, void* y, int32_t y_dtype, int64_t ldy,
                     int32_t* flag, void* stream) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_transform");
     if (rows < 0 || k < 1 || n < 1 || ldx < k || ldy < n)
       fail(ATLAS_ECONFIG, "bad transform shape");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -697,6 +709,7 @@ int atlas_transform_typed(int32_t backend, const void* x, int32_t x_dtype,
                           int32_t relu, void* y, int32_t y_dtype, int64_t ldy,
                           int32_t* flag, void* stream) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_transform_typed");
     if (x_dtype == ATLAS_F32) {
       const int rc = atlas_transform(backend, static_cast<const float*>(x),
                                      rows, k, ldx, w, b, n, relu, y, y_dtype,
@@ -718,6 +731,7 @@ int atlas_transform_typed(int32_t backend, const void* x, int32_t x_dtype,
 
 int atlas_layer_finish(atlas_layer* L, atlas_layer_metrics* m) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_layer_finish");
     if (!L || !m) fail(ATLAS_ECONFIG, "null argument");
     use_device(L->desc.device);
     cudaStream_t s = nullptr;
@@ -822,6 +836,7 @@ int atlas_layer_chunk_stats(atlas_layer* L, int64_t* reloads, int64_t* touched,
 int atlas_layer_log(atlas_layer* L, int32_t which, int64_t* out, int64_t cap,
                     int64_t* count) {
   return guarded([&] {
+    ATLAS_NVTX("atlas_layer_log");
     if (!L) fail(ATLAS_ECONFIG, "null layer");
     if (!L->desc.record_log) fail(ATLAS_ECONFIG, "layer was not logging");
     use_device(L->desc.device);

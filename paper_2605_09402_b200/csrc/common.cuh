@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -41,6 +42,17 @@ struct Error {
   } while (0)
 
 #define ATLAS_LAUNCH_CHECK() ATLAS_CUDA(cudaGetLastError())
+
+// NVTX ranges around the C-ABI entry points (header-only nvtx3: a no-op
+// unless a profiler injects itself), so nsys/ncu timelines show the
+// layer stages by name.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define ATLAS_NVTX(name) ::atlas::NvtxRange atlas_nvtx_range_(name)
 
 constexpr int kWarp = 32;
 // SM count of the current device (148 on B200), queried once per device;

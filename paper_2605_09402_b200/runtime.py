@@ -487,10 +487,12 @@ class Engine:
                                 _torch_dtype(self.config.embed_dtype), "cuda")
             # every layer is queued before any metric is read back, so the
             # host never stalls the device between layers
+            torch.cuda.nvtx.range_push(f"atlas layer {l}")
             y, collect, _ = self.layer(
                 l, h, input_flag=flag, defer_metrics=True,
                 host_out=host_out if l == nl - 1 else None,
                 out=None if nxt is None else ex.own(nxt), pieces=pieces)
+            torch.cuda.nvtx.range_pop()
             pending.append(collect)
             if keep_layers:
                 outs.append(y)
@@ -502,7 +504,9 @@ class Engine:
                 if nxt is not None:
                     # the owners' pieces in ascending row order; the next
                     # layer folds each one in as soon as it lands
+                    torch.cuda.nvtx.range_push(f"atlas exchange {l + 1}")
                     h, pieces = nxt, ex.start(nxt)
+                    torch.cuda.nvtx.range_pop()
                 elif self.world > 1 and not self.transform_first(l + 1):
                     h = self.gather(y)  # a subclass's own gather
                 else:
