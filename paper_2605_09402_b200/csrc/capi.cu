@@ -270,6 +270,7 @@ int atlas_layer_reset(atlas_layer* L, void* stream) {
     L->chunk_reloads.clear();
     L->chunk_touched.clear();
     L->fast_path = false;
+    L->sweep_path = false;
     L->chunks_seen = 0;
     L->stream_step = 0;
     L->timing_ms[0] = L->timing_ms[1] = 0.f;
@@ -296,6 +297,7 @@ int atlas_layer_bind_graph(atlas_layer* L, const atlas_graph* g,
     L->chunk_reloads.clear();
     L->chunk_touched.clear();
     L->fast_path = false;
+    L->sweep_path = false;
     L->chunks_seen = 0;
     L->stream_step = 0;
     L->timing_ms[0] = L->timing_ms[1] = 0.f;
@@ -755,6 +757,18 @@ int atlas_layer_finish(atlas_layer* L, atlas_layer_metrics* m) {
       m->hot_peak = L->fp_hot_peak;
       return;
     }
+    if (L->sweep_path) {
+      m->messages = L->sw_messages;
+      m->evictions = L->sw_evictions;
+      m->reloads = L->sw_reloads;
+      m->admissions = L->sw_admissions;
+      m->graduations = L->nloc;
+      m->hot_peak = L->sw_hot_peak;
+      m->cold_bytes_written = L->sw_evictions * w;
+      m->cold_bytes_read = L->sw_reloads * w;
+      m->unique_reloads = L->sw_unique;
+      return;
+    }
     EngineScalars sc = read_scalars(L, s);
     m->messages = sc.messages;
     m->evictions = sc.evictions;
@@ -795,7 +809,7 @@ int atlas_layer_state(atlas_layer* L, uint32_t* pending, uint8_t* state,
     ATLAS_CUDA(cudaDeviceSynchronize());
     const int64_t n = L->nloc;
     if (n == 0) return;
-    if (L->fast_path && (pending || state)) {
+    if ((L->fast_path || L->sweep_path) && (pending || state)) {
       // the eviction-free replay never materialises per-vertex state:
       // every vertex ran to COMPLETED with zero pending
       if (pending) std::memset(pending, 0, n * sizeof(uint32_t));

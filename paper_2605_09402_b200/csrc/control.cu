@@ -19,6 +19,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 
 #include "internal.cuh"
@@ -453,6 +456,13 @@ static bool fast_verdict(atlas_layer* L, const atlas_graph* g, int64_t R,
 // single-CTA engine over them (synchronous)
 static void exact_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
                          cudaStream_t s) {
+  const char* prof = getenv("ATLAS_SWEEP_PROFILE");
+  const bool timed = prof && prof[0] == '1';
+  auto now = [&]() {
+    if (timed) cudaStreamSynchronize(s);
+    return std::chrono::steady_clock::now();
+  };
+  const auto t0 = now();
   const int64_t V = g->V;
   const int model = L->desc.model;
   Plan p{R, V, ceil_div(V, R)};
@@ -463,6 +473,7 @@ static void exact_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   const unsigned blocks = (unsigned)std::min<int64_t>(
       num_sms() * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
   L->fast_path = false;
+  L->sweep_path = false;
   const int64_t npos = g->E + (model == ATLAS_GCN ? 0 : V) + 1;
   DevBuf<uint64_t> at_pos, runs;
   DevBuf<int64_t> nsel;
@@ -519,6 +530,17 @@ static void exact_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   ATLAS_CUDA(cudaMemcpyAsync(d_bounds.ptr, bounds.data(),
                              2 * nchunks * sizeof(int64_t),
                              cudaMemcpyHostToDevice, s));
+  if (timed) {
+    const auto t1 = now();
+    fprintf(stderr, "[replay] runs materialised in %.3f ms (%lld runs)\n",
+            std::chrono::duration<double, std::milli>(t1 - t0).count(),
+            (long long)total_runs);
+  }
+  // MINPEND / LRU without logs: the sweep over sub-batches (sweep.cu);
+  // RND, logs and inconsistent inputs: the per-element machine
+  if (L->desc.policy != ATLAS_RND && !L->desc.record_log && sweep_enabled() &&
+      sweep_replay(L, g, R, runs.ptr, d_off.ptr, run_off, s))
+    return;
   engine_run_chunks(L, runs.ptr, d_off.ptr, d_bounds.ptr, nchunks,
                     run_off.data(), s);
 }

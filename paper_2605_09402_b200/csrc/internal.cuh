@@ -117,6 +117,16 @@ struct EngineConfig {
   int32_t model, policy, record_log;
 };
 
+// Workspaces of the sweep replay (sweep.cu), grow-only across layers.
+struct SweepWs {
+  DevBuf<uint32_t> zr, tmp_u32, el_v, el_cnt, el_sub, el_newp, el_nsub, iota,
+      sv, se, ent_sub, ent_next, boff, head, fresh, grad, cold, cold_out,
+      victims, flags;
+  DevBuf<uint8_t> el_fresh, cub_tmp;
+  DevBuf<unsigned long long> cs, P, lastP, count;
+  DevBuf<int64_t> eoff, soff, chunk64, out;
+};
+
 }  // namespace atlas
 
 struct atlas_layer {
@@ -146,6 +156,11 @@ struct atlas_layer {
   std::vector<int64_t> chunk_reloads, chunk_touched;
   bool engine_initialized = false;
   bool fast_path = false;
+  // sweep replay (sweep.cu) results: exact integers without per-vertex state
+  atlas::SweepWs* sweep = nullptr;
+  bool sweep_path = false;
+  int64_t sw_messages = 0, sw_evictions = 0, sw_reloads = 0, sw_hot_peak = 0,
+          sw_unique = 0, sw_admissions = 0;
   bool gat = false;  // GAT layer: GCN control plane, fused GAT data plane
   bool spans_host_done = false;
   int64_t chunks_seen = 0;
@@ -205,6 +220,7 @@ struct atlas_layer {
   // whole-input streaming: one ready event per in-flight tile
   cudaEvent_t tile_ev[atlas::kTileEvents] = {};
   ~atlas_layer() {
+    delete sweep;
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ctl_stream) cudaStreamDestroy(ctl_stream);
     for (auto& e : tev)
@@ -294,6 +310,12 @@ void chunk_spans(atlas_layer* L, int64_t start, int64_t end,
                  int64_t m, cudaStream_t s);
 void finish_spans(atlas_layer* L, cudaStream_t s);
 void check_engine_error(atlas_layer* L, cudaStream_t s);
+
+// sweep.cu
+bool sweep_enabled();
+bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
+                  const uint64_t* runs, const int64_t* run_off_dev,
+                  const std::vector<int64_t>& run_off, cudaStream_t s);
 
 // reorder.cu
 void reorder_graph(int64_t V, int64_t E, const int64_t* off_h,

@@ -647,6 +647,266 @@ __global__ void __launch_bounds__(kThreadsH, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// f32 x with K <= 128 and N <= 128: the transposed product on a TMEM-resident
+// W. D^T (N x rows) = W (N x K, A operand from TMEM) . x^T (B operand: the
+// x tile is rows x K, K-major, exactly the N x K K-major B layout). W hi/lo
+// live in TMEM columns [0, 2Kp), so shared memory holds nothing but x
+// stages (6 x 32 KB in flight instead of 2 next to a resident W in smem),
+// and the epilogue needs no transpose: TMEM lane = output column, so each
+// tcgen05.ld register is one row and a warp's store covers 32 consecutive
+// columns of that row (one 128-B line for f32).
+//   warp 0      TMA producer (x tiles, 128 rows x 32 f32, SWIZZLE_128B)
+//   warp 1      TMEM allocator + MMA issuer
+//   warps 2-5   splitter: x -> tf32 hi (in place) + lo
+//   warps 6-13  W -> TMEM (hi/lo split, tcgen05.st) once, then epilogue:
+//               warp 6+q / 10+q own TMEM lane quarter (warp & 3) and
+//               alternate 64-row halves of the tile
+constexpr int BR = 128;  // rows per tile = MMA N
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a,
+                                            uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(
+          tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, "
+      "%7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+      "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]),
+      "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+struct TtParams {
+  int64_t M;
+  int K, Kp, N, stages, kblocks, relu;
+  int64_t ldy;
+  const float* w;     // N x K row-major
+  const float* bias;
+  void* y;
+  int32_t* flag;
+};
+
+template <typename OutT>
+__global__ void __launch_bounds__(kThreads, 1)
+    transform_t_kernel(const __grid_constant__ CUtensorMap map_x,
+                       TtParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr uint32_t x_bytes = BR * BK * 4;
+  constexpr uint32_t stage_bytes = 2 * x_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + p.stages * stage_bytes);
+  uint64_t* split = full + p.stages;
+  uint64_t* empty = split + p.stages;
+  uint64_t* tfull = empty + p.stages;  // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint64_t* wready = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wready + 1);
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (p.M + BR - 1) / BR;
+  const uint32_t d_col0 = 2u * (uint32_t)p.Kp;  // D buffers after W hi/lo
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; a++) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps * 32);
+    }
+    mbar_init(wready, 4 * 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = threadIdx.x; j < 128; j += kThreads)
+    sbias[j] = j < p.N ? p.bias[j] : 0.0f;
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::
+            "r"(smem_u32(tmem_slot)),
+        "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kb = 0; kb < p.kblocks; kb++) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], x_bytes);
+          tma_load_2d(base + s * stage_bytes, &map_x, &full[s], kb * BK,
+                      (int)(t * BR));
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // M = 128 (output columns, W rows zero-padded), N = 128 rows
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                           ((uint32_t)(BR >> 3) << 17) |
+                           ((uint32_t)(128 >> 4) << 24);
+    mbar_wait(wready, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t aph[2] = {0, 0};
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], aph[acc] ^ 1);
+      aph[acc] ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dt = tmem_base + d_col0 + (uint32_t)(acc * BR);
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        mbar_wait(&split[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          uint8_t* st = base + s * stage_bytes;
+          const uint32_t b_hi = smem_u32(st), b_lo = smem_u32(st + x_bytes);
+#pragma unroll
+          for (int k = 0; k < BK / 8; k++) {  // UMMA_K = 8 tf32
+            const uint32_t col = (uint32_t)(kb * BK + k * 8);
+            const uint32_t a_hi = tmem_base + col;
+            const uint32_t a_lo = tmem_base + (uint32_t)p.Kp + col;
+            const uint32_t off = k * 32;
+            const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
+            mma_tf32_ts(dt, a_lo, sw128_desc(b_hi + off), idesc, first);
+            mma_tf32_ts(dt, a_hi, sw128_desc(b_lo + off), idesc, 1u);
+            mma_tf32_ts(dt, a_hi, sw128_desc(b_hi + off), idesc, 1u);
+          }
+          mma_commit(&empty[s]);
+          if (kb == p.kblocks - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      acc ^= 1;
+    }
+  } else if (warp < 6) {
+    const int tid = threadIdx.x - 64;  // 0..127
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        mbar_wait(&full[s], ph);
+        uint8_t* st = base + s * stage_bytes;
+        float4* xs = reinterpret_cast<float4*>(st);
+        float4* xl = reinterpret_cast<float4*>(st + x_bytes);
+#pragma unroll
+        for (int i = 0; i < (BR * BK / 4) / 128; i++) {
+          const int e = tid + i * 128;
+          const float4 v = xs[e];
+          float4 h, l;
+          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          l.x = v.x - h.x;
+          l.y = v.y - h.y;
+          l.z = v.z - h.z;
+          l.w = v.w - h.w;
+          xs[e] = h;
+          xl[e] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&split[s]);
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else {
+    const int ew = warp - 6;
+    const int quarter = warp & 3;
+    const int n = quarter * 32 + lane;  // TMEM lane = output column
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    if (ew < 4) {  // W -> TMEM: row n, hi at [0, Kp), lo at [Kp, 2Kp)
+      for (int c0 = 0; c0 < p.Kp; c0 += 16) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          const int c = c0 + j;
+          const float v = (n < p.N && c < p.K) ? p.w[(int64_t)n * p.K + c] : 0.0f;
+          const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+          hi[j] = __float_as_uint(h);
+          lo[j] = __float_as_uint(v - h);
+        }
+        tmem_st16(tmem_base + lane_off + (uint32_t)c0, hi);
+        tmem_st16(tmem_base + lane_off + (uint32_t)(p.Kp + c0), lo);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(wready);
+    }
+    const int half = ew >> 2;  // rows [64*half, 64*half + 64) of each tile
+    const float bias = sbias[n];
+    OutT* y = static_cast<OutT*>(p.y);
+    int acc = 0;
+    uint32_t aph[2] = {0, 0};
+    int bad = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&tfull[acc], aph[acc]);
+      aph[acc] ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem_base + lane_off + d_col0 + (uint32_t)(acc * BR);
+      const int64_t row0 = t * BR;
+      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
+        if (n < p.N) {
+#pragma unroll
+          for (int j = 0; j < 16; j++) {
+            const int64_t row = row0 + c0 + j;
+            if (row < p.M) {
+              float o = __fadd_rn(v[j], bias);
+              if (p.relu) o = relu_np(o);
+              const OutT q = cvt_out<OutT>(o);
+              bad |= is_extreme(to_f32(q));
+              y[row * p.ldy + n] = q;
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && p.flag)
+      atomicOr(p.flag, 1);
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile(
+        "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(
+            tmem_base),
+        "r"(512));
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                               void*, const cuuint64_t*, const cuuint64_t*,
                               const cuuint32_t*, const cuuint32_t*,
@@ -791,6 +1051,52 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
   return ok;
 }
 
+// ATLAS_TRANSFORM_T=0 (A/B probes): keep W in shared memory instead
+bool transposed_enabled() {
+  const char* e = getenv("ATLAS_TRANSFORM_T");
+  return !(e && e[0] == '0');
+}
+
+bool launch_transform_t(const void* x, int64_t rows, int64_t k, int64_t ldx,
+                        const float* w, const float* b, int64_t n, int relu,
+                        void* y, int y_dtype, int64_t ldy, int32_t* flag,
+                        cudaStream_t s) {
+  CUtensorMap mx;
+  if (!make_map(&mx, x, ATLAS_F32, rows, k, ldx, BR)) return false;
+  const int kblocks = (int)((k + BK - 1) / BK);
+  const int stage_bytes = 2 * BR * BK * 4;
+  const int fixed = 1024 + 8 * 64 + 16 + 4 * 128 + 64;
+  int stages = (227 * 1024 - fixed) / stage_bytes;
+  if (stages > 8) stages = 8;
+  const int smem = fixed + stages * stage_bytes;
+  TtParams p{};
+  p.M = rows;
+  p.K = (int)k;
+  p.Kp = kblocks * BK;
+  p.N = (int)n;
+  p.stages = stages;
+  p.kblocks = kblocks;
+  p.relu = relu;
+  p.ldy = ldy;
+  p.w = w;
+  p.bias = b;
+  p.y = y;
+  p.flag = flag;
+  const int64_t ntiles = (rows + BR - 1) / BR;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, num_sms());
+  auto launch = [&](auto kern) {
+    ATLAS_CUDA(cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kThreads, smem, s>>>(mx, p);
+  };
+  if (y_dtype == ATLAS_F32) launch(transform_t_kernel<float>);
+  else if (y_dtype == ATLAS_F16) launch(transform_t_kernel<__half>);
+  else launch(transform_t_kernel<__nv_bfloat16>);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  return true;
+}
+
 bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
                          int64_t ldx, const float* w, const float* b,
                          int64_t n, int relu, void* y, int y_dtype,
@@ -804,6 +1110,9 @@ bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
   if (n < 1 || n > 256 || k < 1 || (ldx * xs) % 16 != 0 || k % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) != 0)
     return false;
+  if (x_dtype == ATLAS_F32 && n <= 128 && k <= 128 && transposed_enabled())
+    return launch_transform_t(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
+                              flag, s);
   const int BN = (int)((n + 15) / 16 * 16);
   const int kblocks = (int)((k + BK - 1) / BK);
   if ((reinterpret_cast<uintptr_t>(w) & 15) != 0) return false;

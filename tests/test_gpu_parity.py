@@ -247,7 +247,10 @@ def test_stable_transform_bit_exact_vs_reference_backend():
                                         (4099, 128, 47, False),
                                         (300, 256, 128, True),
                                         (129, 8, 2, True), (64, 2048, 19, False),
-                                        (5000, 128, 256, True)])
+                                        (5000, 128, 256, True),
+                                        (100000, 128, 128, False),
+                                        (2400, 100, 64, True),
+                                        (777, 36, 120, False)])
 def test_tcgen05_transform_3xtf32_accuracy(m, k, n, relu):
     """tcgen05 backend: |y - y_f64| <= 2e-6 * (|x| |w| row-col scale)."""
     from paper_2605_09402_b200.compute import Tcgen05Backend

@@ -1,7 +1,8 @@
 """Exact control-plane replay under eviction pressure (diagnostic):
 per-layer control-stream time and eviction counts of a resident pass with
 a hot budget below the live set (min-pending eviction fires on every
-chunk). Usage: replay_probe.py V DEG DIM HOT_FRAC [MODEL]"""
+chunk). ATLAS_SWEEP=0 selects the per-element machine instead of the sweep.
+Usage: replay_probe.py V DEG DIM HOT_FRAC [MODEL]"""
 
 import sys
 import time
@@ -35,7 +36,9 @@ def main():
         wall = time.perf_counter() - t
         print(f"iter {it}: wall {wall:.2f} s | " + " | ".join(
             f"L{m.layer} ctl {m.control_ms:.1f} ms agg {m.agg_ms:.1f} ms "
-            f"fast {m.fast_path} evictions {m.evictions} reloads {m.reloads}"
+            f"fast {m.fast_path} evictions {m.evictions} reloads {m.reloads} "
+            f"unique {m.unique_reloads} peak {m.hot_peak} "
+            f"reload% {m.mean_reload_pct:.6f}"
             for m in ms), flush=True)
     eng.close()
 
