@@ -173,6 +173,28 @@ ATLAS_API int atlas_layer_run_resident(atlas_layer* layer, const atlas_graph* gr
                              const void* x_dev, int32_t dtype, int64_t ldx,
                              int64_t chunk_rows, const int32_t* input_flag,
                              void* stream);
+/* same layer pass with the device records bounded: destinations
+ * [v0, v0 + block_rows) aggregate into a block_rows x agg_dim record buffer
+ * and are transformed (backend ATLAS_BACKEND_*, W n x agg_dim, bias n,
+ * activation relu) into rows v0.. of y before the next block reuses the
+ * buffer -- the reference's "graduated batches are transformed and leave
+ * the hot store" (oocgnn/compute.py:125-205, memstore.py:479-494), so the
+ * hot budget, not the graph, bounds record memory. Records and outputs are
+ * bit-identical to atlas_layer_run_resident + atlas_transform. out_flag
+ * (device int, may be NULL) receives the output's extremes flag. */
+ATLAS_API int atlas_layer_run_blocked(atlas_layer* layer,
+                                      const atlas_graph* graph,
+                                      const void* x_dev, int32_t dtype,
+                                      int64_t ldx, int64_t chunk_rows,
+                                      const int32_t* input_flag,
+                                      int32_t backend, const float* w,
+                                      const float* bias, int64_t n,
+                                      int32_t relu, void* y, int32_t y_dtype,
+                                      int64_t ldy, int32_t* out_flag,
+                                      int64_t block_rows, void* stream);
+/* bytes of device record storage the layer holds (its accumulator) */
+ATLAS_API int atlas_layer_record_bytes(const atlas_layer* layer,
+                                       int64_t* bytes);
 /* same layer pass, but the input stays in (pinned) HOST memory: it is
  * streamed to HBM in tiles of tile_rows rows, double-buffered on a side
  * copy stream, and every tile is aggregated as soon as it lands (SURVEY.md

@@ -87,6 +87,10 @@ def _declare(lib):
        c_i64, c_i64, c_i64, c_vp)
     fn("atlas_layer_run_pieces", ctypes.c_int, c_vp, c_vp, c_vp, c_i32,
        c_i64, c_vp, c_i32, c_vp, c_i64, c_vp)
+    fn("atlas_layer_run_blocked", ctypes.c_int, c_vp, c_vp, c_vp, c_i32,
+       c_i64, c_i64, c_vp, c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32,
+       c_i64, c_vp, c_i64, c_vp)
+    fn("atlas_layer_record_bytes", ctypes.c_int, c_vp, P_i64)
     fn("atlas_layer_accumulator", ctypes.c_int, c_vp, ctypes.POINTER(c_vp),
        P_i64)
     fn("atlas_transform", ctypes.c_int, c_i32, c_vp, c_i64, c_i64, c_i64,
@@ -132,7 +136,8 @@ EXPORTED = [
     "atlas_layer_timing", "atlas_reorder", "atlas_transform_typed",
     "atlas_layer_run_gat", "atlas_layer_run_fused", "atlas_layer_bind_graph",
     "atlas_spill_read", "atlas_spill_write", "atlas_gather_replay",
-    "atlas_spill_write_runs",
+    "atlas_spill_write_runs", "atlas_layer_run_blocked",
+    "atlas_layer_record_bytes",
 ]
 
 

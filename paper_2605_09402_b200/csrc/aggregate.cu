@@ -1092,9 +1092,14 @@ int pick_vec(int d, int64_t ldx) {
 
 template <typename T, int VEC>
 void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
-                    float eps1, int d, float* acc, int64_t ldacc,
-                    cudaStream_t s) {
-  const int64_t blocks = ceil_div(g->nloc, 8);
+                    float eps1, int d, float* acc, int64_t ldacc, int64_t v0,
+                    int64_t v1, cudaStream_t s) {
+  // destinations [v0, v1) of the rank: the CSC pointers, in-degrees and
+  // global ids are offset views, acc row 0 is destination v0
+  const int64_t* csc_ptr = g->csc_ptr.ptr + v0;
+  const uint32_t* indeg = g->indeg.ptr + v0;
+  const int64_t lo = g->lo + v0, nloc = v1 - v0;
+  const int64_t blocks = ceil_div(nloc, 8);
   if (blocks == 0) return;
   // whether the division guard is needed: the producing transform's flag,
   // or one pass over the input
@@ -1115,8 +1120,8 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
       ATLAS_CUDA(cudaFuncSetAttribute(
           kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       kern<<<num_sms() * 3, 256, smem, s>>>(
-          x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
-          g->nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
+          x, ldx, csc_ptr, g->csc_src.ptr, indeg, lo,
+          nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
     };
     if (d <= 16 * VEC) {
       const int sub_smem = 8 * kSubRing * 32 * 16;
@@ -1124,8 +1129,8 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
         ATLAS_CUDA(cudaFuncSetAttribute(
             kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sub_smem));
         kern<<<num_sms() * kSubBlocks, 256, sub_smem, s>>>(
-            x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
-            g->nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
+            x, ldx, csc_ptr, g->csc_src.ptr, indeg, lo,
+            nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
       };
       if (d <= 8 * VEC) {
         if (model == ATLAS_GCN) sub(agg_sub_ring<T, 8, ATLAS_GCN>);
@@ -1160,8 +1165,8 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
       ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &per_sm, kern, kBulkWarps * 32, smem));
       kern<<<num_sms() * std::max(1, per_sm), kBulkWarps * 32, smem, s>>>(
-          x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
-          g->nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
+          x, ldx, csc_ptr, g->csc_src.ptr, indeg, lo,
+          nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
     };
     auto by_model = [&](auto ch) {
       constexpr int CH = decltype(ch)::value;
@@ -1178,7 +1183,7 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
   }
   auto go = [&](auto kern) {
     kern<<<(unsigned)blocks, 256, 0, s>>>(
-        x, ldx, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo, g->nloc,
+        x, ldx, csc_ptr, g->csc_src.ptr, indeg, lo, nloc,
         d, acc, ldacc, eps1, flag);
   };
   if (model == ATLAS_GCN) go(agg_resident<T, VEC, ATLAS_GCN>);
@@ -1191,17 +1196,17 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
 template <typename T>
 void resident_typed(const atlas_graph* g, const void* x, int64_t ldx,
                     int model, float eps1, int d, float* acc, int64_t ldacc,
-                    cudaStream_t s) {
+                    int64_t v0, int64_t v1, cudaStream_t s) {
   const T* xt = static_cast<const T*>(x);
   int vec = pick_vec<T>(d, ldx);
   if (vec > 1 && ldacc % 4 != 0) vec = 1;
   if (sizeof(T) == 4) {
-    if (vec == 4) resident_model<T, 4>(g, xt, ldx, model, eps1, d, acc, ldacc, s);
-    else resident_model<T, 1>(g, xt, ldx, model, eps1, d, acc, ldacc, s);
+    if (vec == 4) resident_model<T, 4>(g, xt, ldx, model, eps1, d, acc, ldacc, v0, v1, s);
+    else resident_model<T, 1>(g, xt, ldx, model, eps1, d, acc, ldacc, v0, v1, s);
   } else {
-    if (vec == 8) resident_model<T, 8>(g, xt, ldx, model, eps1, d, acc, ldacc, s);
-    else if (vec == 2) resident_model<T, 2>(g, xt, ldx, model, eps1, d, acc, ldacc, s);
-    else resident_model<T, 1>(g, xt, ldx, model, eps1, d, acc, ldacc, s);
+    if (vec == 8) resident_model<T, 8>(g, xt, ldx, model, eps1, d, acc, ldacc, v0, v1, s);
+    else if (vec == 2) resident_model<T, 2>(g, xt, ldx, model, eps1, d, acc, ldacc, v0, v1, s);
+    else resident_model<T, 1>(g, xt, ldx, model, eps1, d, acc, ldacc, v0, v1, s);
   }
 }
 
@@ -1459,14 +1464,27 @@ void launch_agg_resident(const atlas_graph* g, const void* x, int dtype,
                          int64_t ldx, int model, float gin_epsilon, int d,
                          float* acc, int64_t ldacc, const int32_t* input_flag,
                          cudaStream_t s) {
-  const float e1 = self_scale_of(gin_epsilon);
   g->known_flag = input_flag;
+  launch_agg_resident_range(g, x, dtype, ldx, model, gin_epsilon, d, acc,
+                            ldacc, 0, g->nloc, s);
+}
+
+// destinations [v0, v1) only (blocked records, atlas_layer_run_blocked):
+// record row 0 of acc is destination v0; with g->known_flag unset the
+// input is scanned for extremes on every call
+void launch_agg_resident_range(const atlas_graph* g, const void* x, int dtype,
+                               int64_t ldx, int model, float gin_epsilon,
+                               int d, float* acc, int64_t ldacc, int64_t v0,
+                               int64_t v1, cudaStream_t s) {
+  if (v1 <= v0) return;
+  const float e1 = self_scale_of(gin_epsilon);
   if (dtype == ATLAS_F32)
-    resident_typed<float>(g, x, ldx, model, e1, d, acc, ldacc, s);
+    resident_typed<float>(g, x, ldx, model, e1, d, acc, ldacc, v0, v1, s);
   else if (dtype == ATLAS_F16)
-    resident_typed<__half>(g, x, ldx, model, e1, d, acc, ldacc, s);
+    resident_typed<__half>(g, x, ldx, model, e1, d, acc, ldacc, v0, v1, s);
   else
-    resident_typed<__nv_bfloat16>(g, x, ldx, model, e1, d, acc, ldacc, s);
+    resident_typed<__nv_bfloat16>(g, x, ldx, model, e1, d, acc, ldacc, v0,
+                                  v1, s);
 }
 
 void launch_agg_resident_epi(const atlas_graph* g, const float* z,

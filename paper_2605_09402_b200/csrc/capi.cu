@@ -133,8 +133,9 @@ static void ensure_tile_events(atlas_layer* L) {
 }
 
 // the layer's f32 aggregation records (nloc x agg_dim), allocated lazily
-static void ensure_records(atlas_layer* L) {
-  const size_t want = (size_t)std::max<int64_t>(L->nloc, 1) * L->desc.agg_dim;
+static void ensure_records(atlas_layer* L, int64_t rows = -1) {
+  if (rows < 0) rows = L->nloc;
+  const size_t want = (size_t)std::max<int64_t>(rows, 1) * L->desc.agg_dim;
   if (L->acc.count < want) L->acc.alloc(want);
 }
 
@@ -392,6 +393,65 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
     ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
     control_queue(L, g, chunk_rows, s);
     L->timing_pending = true;
+  });
+}
+
+int atlas_layer_run_blocked(atlas_layer* L, const atlas_graph* g,
+                            const void* x, int32_t dtype, int64_t ldx,
+                            int64_t chunk_rows, const int32_t* input_flag,
+                            int32_t backend, const float* w, const float* b,
+                            int64_t n, int32_t relu, void* y, int32_t y_dtype,
+                            int64_t ldy, int32_t* out_flag, int64_t block_rows,
+                            void* stream) {
+  return guarded([&] {
+    ATLAS_NVTX("atlas_layer_run_blocked");
+    if (!L || !g || !w || !b || !y) fail(ATLAS_ECONFIG, "null argument");
+    const atlas_layer_desc& D = L->desc;
+    if (g->V != D.num_vertices || g->lo != D.dst_lo || g->hi != D.dst_hi)
+      fail(ATLAS_ECONFIG, "graph and layer disagree on the vertex range");
+    if (chunk_rows < 1) fail(ATLAS_ECONFIG, "chunk_rows must be >= 1");
+    if (block_rows < 1) fail(ATLAS_ECONFIG, "block_rows must be >= 1");
+    if (L->chunks_seen) fail(ATLAS_ECONFIG, "layer already consumed input");
+    if (L->gat) fail(ATLAS_ECONFIG, "GAT layers run through atlas_layer_run_gat");
+    if (n < 1 || ldy < n) fail(ATLAS_ECONFIG, "bad output width");
+    if (backend != ATLAS_BACKEND_STABLE && backend != ATLAS_BACKEND_TCGEN05)
+      fail(ATLAS_ECONFIG, "unknown transform backend");
+    use_device(D.device);
+    const int64_t rows = std::min<int64_t>(block_rows, std::max<int64_t>(L->nloc, 1));
+    ensure_records(L, rows);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    settle(L);
+    control_begin(L, s);
+    if (out_flag) ATLAS_CUDA(cudaMemsetAsync(out_flag, 0, sizeof(int32_t), s));
+    // the input's extremes flag: the producer's, or one scan on the first
+    // block that every later block reuses
+    g->known_flag = input_flag;
+    const int64_t k = D.agg_dim;
+    const size_t yes = y_dtype == ATLAS_F32 ? 4 : 2;
+    for (int64_t v0 = 0; v0 < L->nloc; v0 += rows) {
+      const int64_t v1 = std::min(L->nloc, v0 + rows);
+      launch_agg_resident_range(g, x, dtype, ldx, D.model, D.gin_epsilon,
+                                (int)D.embed_dim, L->acc.ptr, k, v0, v1, s);
+      if (!g->known_flag) g->known_flag = g->scan_flag.ptr;
+      void* yb = static_cast<uint8_t*>(y) + (size_t)v0 * ldy * yes;
+      if (backend == ATLAS_BACKEND_STABLE)
+        launch_transform_stable(L->acc.ptr, v1 - v0, k, k, w, b, n, relu, yb,
+                                y_dtype, ldy, out_flag, s);
+      else if (!launch_transform_tc(L->acc.ptr, ATLAS_F32, v1 - v0, k, k, w,
+                                    b, n, relu, yb, y_dtype, ldy, out_flag,
+                                    s))
+        fail(ATLAS_ECONFIG, "tcgen05 backend does not support this shape");
+    }
+    ATLAS_CUDA(cudaEventRecord(L->tev[1], s));
+    control_queue(L, g, chunk_rows, s);
+    L->timing_pending = true;
+  });
+}
+
+int atlas_layer_record_bytes(const atlas_layer* L, int64_t* bytes) {
+  return guarded([&] {
+    if (!L || !bytes) fail(ATLAS_ECONFIG, "null argument");
+    *bytes = (int64_t)L->acc.bytes();
   });
 }
 

@@ -475,10 +475,12 @@ static void exact_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   L->fast_path = false;
   L->sweep_path = false;
   const int64_t npos = g->E + (model == ATLAS_GCN ? 0 : V) + 1;
-  DevBuf<uint64_t> at_pos, runs;
-  DevBuf<int64_t> nsel;
-  at_pos.alloc(npos);
-  nsel.alloc(1);
+  SweepWs& W = sweep_ws_of(g);  // grow-only, shared by the graph's layers
+  DevBuf<uint64_t>& at_pos = W.at_pos;
+  DevBuf<uint64_t>& runs = W.runs;
+  DevBuf<int64_t>& nsel = W.nsel;
+  at_pos.reserve(npos);
+  nsel.reserve(1);
   fill_u64<<<grid_of(npos), 256, 0, s>>>(at_pos.ptr, npos, kNoRun);
   count_launch();
   ATLAS_CUDA(cudaMemsetAsync(hist.ptr, 0, hist.bytes(), s));
@@ -498,13 +500,13 @@ static void exact_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
     run_off[c + 1] = run_off[c] + (int64_t)h[6 * nchunks + c];
   }
   total_runs = run_off[nchunks];
-  runs.alloc(std::max<int64_t>(total_runs, 1));
+  runs.reserve(std::max<int64_t>(total_runs, 1));
   size_t tmp_bytes = 0;
   NotNoRun pred;
   ATLAS_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, at_pos.ptr, runs.ptr,
                                    nsel.ptr, npos, pred, s));
-  DevBuf<uint8_t> tmp;
-  tmp.alloc(tmp_bytes);
+  DevBuf<uint8_t>& tmp = W.sel_tmp;
+  tmp.reserve(tmp_bytes);
   ATLAS_CUDA(cub::DeviceSelect::If(tmp.ptr, tmp_bytes, at_pos.ptr, runs.ptr,
                                    nsel.ptr, npos, pred, s));
   count_launch();
@@ -516,9 +518,10 @@ static void exact_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
     fail(ATLAS_EINVARIANT, "run materialisation mismatch " +
                                std::to_string(got) + " vs " +
                                std::to_string(total_runs));
-  DevBuf<int64_t> d_off, d_bounds;
-  d_off.alloc(nchunks + 1);
-  d_bounds.alloc(2 * nchunks);
+  DevBuf<int64_t>& d_off = W.d_off;
+  DevBuf<int64_t>& d_bounds = W.d_bounds;
+  d_off.reserve(nchunks + 1);
+  d_bounds.reserve(2 * nchunks);
   std::vector<int64_t> bounds(2 * nchunks);
   for (int64_t c = 0; c < nchunks; c++) {
     bounds[2 * c] = c * R;

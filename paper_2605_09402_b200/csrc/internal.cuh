@@ -6,6 +6,11 @@
 
 #include "common.cuh"
 
+namespace atlas {
+struct SweepWs;
+void free_sweep_ws(SweepWs* w);
+}  // namespace atlas
+
 struct atlas_graph {
   int device = 0;
   int64_t V = 0;        // whole-graph vertices
@@ -34,8 +39,12 @@ struct atlas_graph {
   mutable cudaEvent_t chk_ev = nullptr;
   mutable bool chk_pending = false;
   int64_t chk_expect = 0;
+  // exact-replay workspaces (control.cu / sweep.cu), sized by the graph and
+  // shared by its layers: replays run one at a time, host-synchronously
+  mutable atlas::SweepWs* sweep_ws = nullptr;
   ~atlas_graph() {
     if (chk_ev) cudaEventDestroy(chk_ev);
+    atlas::free_sweep_ws(sweep_ws);
   }
 };
 
@@ -125,7 +134,16 @@ struct SweepWs {
   DevBuf<uint8_t> el_fresh, cub_tmp;
   DevBuf<unsigned long long> cs, P, lastP, count;
   DevBuf<int64_t> eoff, soff, chunk64, out;
+  // run materialisation (control.cu exact_replay)
+  DevBuf<uint64_t> at_pos, runs;
+  DevBuf<int64_t> nsel, d_off, d_bounds;
+  DevBuf<uint8_t> sel_tmp;
 };
+
+inline SweepWs& sweep_ws_of(const atlas_graph* g) {
+  if (!g->sweep_ws) g->sweep_ws = new SweepWs();
+  return *g->sweep_ws;
+}
 
 }  // namespace atlas
 
@@ -157,7 +175,6 @@ struct atlas_layer {
   bool engine_initialized = false;
   bool fast_path = false;
   // sweep replay (sweep.cu) results: exact integers without per-vertex state
-  atlas::SweepWs* sweep = nullptr;
   bool sweep_path = false;
   int64_t sw_messages = 0, sw_evictions = 0, sw_reloads = 0, sw_hot_peak = 0,
           sw_unique = 0, sw_admissions = 0;
@@ -220,7 +237,6 @@ struct atlas_layer {
   // whole-input streaming: one ready event per in-flight tile
   cudaEvent_t tile_ev[atlas::kTileEvents] = {};
   ~atlas_layer() {
-    delete sweep;
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ctl_stream) cudaStreamDestroy(ctl_stream);
     for (auto& e : tev)
@@ -248,6 +264,10 @@ void launch_agg_resident(const atlas_graph* g, const void* x, int dtype,
                          int64_t ldx, int model, float gin_epsilon, int d,
                          float* acc, int64_t ldacc, const int32_t* input_flag,
                          cudaStream_t s);
+void launch_agg_resident_range(const atlas_graph* g, const void* x, int dtype,
+                               int64_t ldx, int model, float gin_epsilon,
+                               int d, float* acc, int64_t ldacc, int64_t v0,
+                               int64_t v1, cudaStream_t s);
 void launch_agg_resident_epi(const atlas_graph* g, const float* z,
                              int64_t ldz, int data_model, float gin_epsilon,
                              int d, const int32_t* input_flag, void* y,

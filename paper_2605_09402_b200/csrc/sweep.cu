@@ -45,8 +45,7 @@ namespace atlas {
 namespace {
 
 constexpr int kSwThreads = 1024;
-constexpr int kSwBlock = 4096;   // sub-batches staged in shared memory
-constexpr int kSwPer = 4;        // bucket entries per thread per window
+constexpr int kSwBlock = 2048;   // sub-batches staged in shared memory
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 unsigned grid_of(int64_t n, int block = 256) {
@@ -290,8 +289,21 @@ struct SweepArgs {
   int64_t* out;              // evictions, reloads, hot_peak, nvict, err, info
 };
 
+// Bucket entries reach the CTA through two shared-memory window buffers
+// filled by bulk async copies (cp.async.bulk, one thread, mbarrier
+// completion): the entry lists are static, so a buffer is a cache of the
+// range [start, start + len) and the walk keeps the next window of the
+// same list in flight while it scans the current one.
+constexpr int kSwWin = 8192;                  // entries per window buffer
+constexpr int kSwPerT = kSwWin / kSwThreads;  // 8 entries per thread
+
 struct SweepSm {
+  uint32_t sub[2][kSwWin];   // window buffers: ent_sub
+  uint32_t nxt[2][kSwWin];   //                 ent_next
   uint32_t fresh[kSwBlock], grad[kSwBlock], cold[kSwBlock];
+  uint64_t bar[2];
+  uint32_t buf_start[2], buf_len[2], buf_phase[2];
+  int32_t buf_busy[2];       // a copy is in flight (not yet waited on)
   int64_t hot, peak, evictions, reloads, need_old, k, nv;
   int32_t i, mode, err;
   int64_t err_info;
@@ -299,8 +311,48 @@ struct SweepSm {
   uint32_t first_na[2];
 };
 
+__device__ __forceinline__ uint32_t sw_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// thread 0: start filling buffer q with entries [start, start + len)
+__device__ void sw_fetch(SweepSm& sm, const SweepArgs& A, int q,
+                         uint32_t start, uint32_t len) {
+  const uint32_t bytes = ((len + 3u) & ~3u) * 4u;  // arrays padded by 4
+  const uint32_t bar = sw_smem(&sm.bar[q]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+      "r"(2u * bytes)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(sw_smem(sm.sub[q])),
+      "l"(A.ent_sub + start), "r"(bytes), "r"(bar)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(sw_smem(sm.nxt[q])),
+      "l"(A.ent_next + start), "r"(bytes), "r"(bar)
+      : "memory");
+  sm.buf_start[q] = start;
+  sm.buf_len[q] = len;
+  sm.buf_busy[q] = 1;
+}
+
+__device__ __forceinline__ void sw_wait(SweepSm& sm, int q) {
+  const uint32_t bar = sw_smem(&sm.bar[q]), ph = sm.buf_phase[q];
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "SW_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SW_WAIT_%=;\n}" ::"r"(bar),
+      "r"(ph)
+      : "memory");
+}
+
 __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
-  extern __shared__ __align__(16) unsigned char sw_raw[];
+  extern __shared__ __align__(128) unsigned char sw_raw[];
   SweepSm& sm = *reinterpret_cast<SweepSm*>(sw_raw);
   using Scan = cub::BlockScan<int, kSwThreads>;
   __shared__ typename Scan::TempStorage scan;
@@ -309,6 +361,14 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
     sm.hot = sm.peak = sm.evictions = sm.reloads = sm.nv = 0;
     sm.err = 0;
     sm.err_info = 0;
+    for (int q = 0; q < 2; q++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+          sw_smem(&sm.bar[q])));
+      sm.buf_start[q] = sm.buf_len[q] = 0;
+      sm.buf_phase[q] = 0;
+      sm.buf_busy[q] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   for (int64_t base = 0; base < A.S; base += kSwBlock) {
@@ -389,25 +449,64 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
           b++;
           continue;
         }
-        const uint32_t w0 = h & ~3u;
-        const uint32_t j0 = w0 + (uint32_t)tid * kSwPer;
-        uint4 sub4 = make_uint4(kNone, kNone, kNone, kNone);
-        uint4 nxt4 = make_uint4(0, 0, 0, 0);
-        if (j0 < e_end) {
-          sub4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_sub + j0));
-          nxt4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_next + j0));
+        // a buffer holding h, else fetch [h & ~3, +kSwWin) into the idle one
+        if (tid == 0) {
+          int q = -1;
+          for (int c = 0; c < 2; c++)
+            if (h >= sm.buf_start[c] && h < sm.buf_start[c] + sm.buf_len[c])
+              q = c;
+          if (q < 0) {
+            q = (sm.buf_busy[0] && !sm.buf_busy[1]) ? 1 : 0;
+            if (sm.buf_busy[q]) {  // drain a stale prefetch first
+              sw_wait(sm, q);
+              sm.buf_phase[q] ^= 1;
+              sm.buf_busy[q] = 0;
+            }
+            const uint32_t w0 = h & ~3u;
+            sw_fetch(sm, A, q, w0, min((uint32_t)kSwWin, e_end - w0));
+          }
+          // keep the list's next window in flight in the other buffer
+          const int o = q ^ 1;
+          const uint32_t nx = sm.buf_start[q] + sm.buf_len[q];
+          if (nx < e_end && !sm.buf_busy[o] &&
+              !(nx >= sm.buf_start[o] && nx < sm.buf_start[o] + sm.buf_len[o]))
+            sw_fetch(sm, A, o, nx, min((uint32_t)kSwWin, e_end - nx));
+          sm.first_na[(w + 1) & 1] = (uint32_t)q;  // scratch: buffer index
         }
-        const uint32_t subs[4] = {sub4.x, sub4.y, sub4.z, sub4.w};
-        const uint32_t nxts[4] = {nxt4.x, nxt4.y, nxt4.z, nxt4.w};
+        __syncthreads();
+        const int q = (int)sm.first_na[(w + 1) & 1];
+        if (sm.buf_busy[q]) sw_wait(sm, q);
+        const uint32_t bs = sm.buf_start[q];
+        const uint32_t be = bs + sm.buf_len[q];
+        __syncthreads();
+        if (tid == 0) {
+          if (sm.buf_busy[q]) {
+            sm.buf_phase[q] ^= 1;
+            sm.buf_busy[q] = 0;
+          }
+          sm.first_na[(w + 1) & 1] = kNone;
+        }
+        // scan [max(h, bs), be): thread t takes 8 consecutive entries
+        const uint32_t j0 = bs + (uint32_t)tid * kSwPerT;
+        uint32_t subs[kSwPerT], nxts[kSwPerT];
+        {
+          const uint4* ps = reinterpret_cast<const uint4*>(sm.sub[q]) + tid * 2;
+          const uint4* pn = reinterpret_cast<const uint4*>(sm.nxt[q]) + tid * 2;
+          const uint4 s0 = ps[0], s1 = ps[1], n0 = pn[0], n1 = pn[1];
+          subs[0] = s0.x; subs[1] = s0.y; subs[2] = s0.z; subs[3] = s0.w;
+          subs[4] = s1.x; subs[5] = s1.y; subs[6] = s1.z; subs[7] = s1.w;
+          nxts[0] = n0.x; nxts[1] = n0.y; nxts[2] = n0.z; nxts[3] = n0.w;
+          nxts[4] = n1.x; nxts[5] = n1.y; nxts[6] = n1.z; nxts[7] = n1.w;
+        }
         int valid = 0, nvalid = 0;
         uint32_t first_na = kNone;
 #pragma unroll
-        for (int q = 0; q < kSwPer; q++) {
-          const uint32_t j = j0 + q;
-          if (j < h || j >= e_end) continue;
-          if (subs[q] < s) {
-            if (nxts[q] >= s) {
-              valid |= 1 << q;
+        for (int e = 0; e < kSwPerT; e++) {
+          const uint32_t j = j0 + e;
+          if (j < h || j >= be) continue;
+          if (subs[e] < s) {
+            if (nxts[e] >= s) {
+              valid |= 1 << e;
               nvalid++;
             }
           } else if (first_na == kNone) {
@@ -416,17 +515,15 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
         }
         int off, total;
         Scan(scan).ExclusiveSum(nvalid, off, total);
-        // slot w&1 was reset before its previous use was read by everyone
-        if (tid == 0) sm.first_na[(w + 1) & 1] = kNone;
         if (first_na != kNone) atomicMin(&sm.first_na[w & 1], first_na);
 #pragma unroll
-        for (int q = 0; q < kSwPer; q++) {
-          if (!(valid >> q & 1)) continue;
+        for (int e = 0; e < kSwPerT; e++) {
+          if (!(valid >> e & 1)) continue;
           const int64_t r = off++;
           if (r >= rem) break;
-          const uint32_t j = j0 + q;
+          const uint32_t j = j0 + e;
           A.victims[nv + r] = j;
-          const uint32_t nx = nxts[q];
+          const uint32_t nx = nxts[e];
           if ((int64_t)nx < win_hi) atomicAdd(&sm.cold[nx - base], 1u);
           else atomicAdd(A.cold + nx, 1u);
           if (r == rem - 1) sm.last_taken = j;
@@ -442,14 +539,12 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
           nv += total;
           rem -= total;
           const uint32_t fna = sm.first_na[w & 1];
-          const uint32_t wend =
-              min(e_end, w0 + (uint32_t)(kSwThreads * kSwPer));
           if (fna != kNone) {
             h_new = fna;  // the rest of the list is not delivered yet
             b++;
           } else {
-            h_new = wend;
-            if (wend >= e_end) b++;
+            h_new = be;
+            if (be >= e_end) b++;
           }
         }
         if (tid == 0) A.head[bcur] = h_new;
@@ -473,6 +568,11 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
     __syncthreads();
     if (sm.err) break;
   }
+  // no copy may outlive the CTA
+  if (tid == 0)
+    for (int q = 0; q < 2; q++)
+      if (sm.buf_busy[q]) sw_wait(sm, q);
+  __syncthreads();
   if (tid == 0) {
     A.out[0] = sm.evictions;
     A.out[1] = sm.reloads;
@@ -529,6 +629,8 @@ struct PhaseTimer {
 };
 
 // ATLAS_SWEEP=0 (tests, A/B probes): replay on the per-element machine
+void free_sweep_ws(SweepWs* w) { delete w; }
+
 bool sweep_enabled() {
   const char* e = getenv("ATLAS_SWEEP");
   return !(e && e[0] == '0');
@@ -545,8 +647,7 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   const int64_t V = g->V, lo = g->lo, hi = g->hi, nloc = L->nloc;
   const int64_t nchunks = ceil_div(V, R);
   const int64_t sb = L->sub_batch;
-  if (!L->sweep) L->sweep = new SweepWs();
-  SweepWs& W = *L->sweep;
+  SweepWs& W = sweep_ws_of(g);
   PhaseTimer T(s);
 
   // ---- per-chunk pass sizes and the element / sub-batch layout ----------

@@ -223,6 +223,30 @@ class DeviceLayer:
             x.stride(0), int(chunk_rows), N.ptr(input_flag),
             N.stream_handle(stream)))
 
+    def run_blocked(self, graph: DeviceGraph, x, chunk_rows: int, weight,
+                    bias, y, *, relu: bool, backend: int, block_rows: int,
+                    input_flag=None, out_flag=None, stream=None):
+        """Resident layer with bounded device records
+        (atlas_layer_run_blocked): destinations aggregate and transform in
+        blocks of ``block_rows`` records, the reference's graduated batches
+        leaving the hot store (oocgnn/compute.py:125-205). Writes y."""
+        if x.shape[1] != self.embed_dim or x.shape[0] != self.num_vertices:
+            raise ConfigError(f"input {tuple(x.shape)} does not match layer "
+                              f"({self.num_vertices}, {self.embed_dim})")
+        N.check(N.load_library().atlas_layer_run_blocked(
+            self.handle, graph.handle, x.data_ptr(), torch_dtype_code(x),
+            x.stride(0), int(chunk_rows), N.ptr(input_flag), int(backend),
+            weight.data_ptr(), bias.data_ptr(), weight.shape[0], int(relu),
+            y.data_ptr(), torch_dtype_code(y), y.stride(0), N.ptr(out_flag),
+            int(block_rows), N.stream_handle(stream)))
+
+    def record_bytes(self) -> int:
+        """Device bytes of f32 aggregation records the layer holds."""
+        n = ctypes.c_int64()
+        N.check(N.load_library().atlas_layer_record_bytes(
+            self.handle, ctypes.byref(n)))
+        return n.value
+
     def run_gat(self, graph: DeviceGraph, z, layout, bias, y, *,
                 mean_heads: bool, relu: bool, chunk_rows: int,
                 negative_slope: float = 0.2, attn_l=None, stream=None):

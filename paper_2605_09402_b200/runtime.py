@@ -84,6 +84,12 @@ class PipelineConfig:
     # multi-GPU exchange: each owner range is broadcast in up to this many
     # pieces, and the next layer folds every piece in as it lands
     exchange_pieces: int = 4
+    # bound the device records by the hot budget: destinations aggregate
+    # and transform in blocks of the layer's slot count, so the f32 records
+    # of at most that many vertices are ever resident (the reference's
+    # graduated batches leaving the hot store); same bits as the unbounded
+    # pass. Device backends and resident inputs only.
+    bound_records: bool = False
 
     def validate(self) -> None:
         if self.partitions < 1:
@@ -274,6 +280,12 @@ class Engine:
         if self.transform_first(l):
             return self._layer_transform_first(l, x, layer, rows, y, last,
                                                t0, defer_metrics, host_out)
+        code = device_code(self.backend)
+        if cfg.bound_records and x.is_cuda and pieces is None and \
+                code is not None:
+            return self._layer_blocked(l, x, layer, rows, y, last, t0,
+                                       defer_metrics, host_out, input_flag,
+                                       code)
         if not x.is_cuda and self.world > 1 and x.shape[0] == nloc \
                 and nloc != self.num_vertices:
             # a rank holding only its own rows (its partition of the layer
@@ -288,7 +300,6 @@ class Engine:
             layer.run_streamed(self.graph, x, rows,
                                tile_bytes=self.config.stream_tile_bytes)
         acc_ptr, ld = layer.accumulator_ptr()
-        code = device_code(self.backend)
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
@@ -314,6 +325,33 @@ class Engine:
             m = metrics_from_device(layer, l)
             m.agg_ms, m.control_ms = layer.timing()
             m.transform_ms = ev0.elapsed_time(ev1)
+            m.gpu_seconds = time.perf_counter() - t0
+            return m
+
+        if defer_metrics:
+            return y, collect, layer
+        return y, collect(), layer
+
+    def _layer_blocked(self, l, x, layer, rows, y, last, t0, defer_metrics,
+                       host_out, input_flag, code):
+        """Aggregate + transform in blocks of the slot budget: device
+        records never exceed slot_count x agg_dim f32."""
+        import torch
+
+        if l not in self.out_flags:
+            self.out_flags[l] = torch.zeros(1, dtype=torch.int32,
+                                            device="cuda")
+        layer.run_blocked(self.graph, x, rows, self.W[l], self.b[l], y,
+                          relu=not last, backend=code,
+                          block_rows=layer.slot_count, input_flag=input_flag,
+                          out_flag=self.out_flags[l])
+        if host_out is not None:
+            host_out.copy_(y, non_blocking=True)
+
+        def collect():
+            m = metrics_from_device(layer, l)
+            m.agg_ms, m.control_ms = layer.timing()
+            m.transform_ms = 0.0  # inside agg_ms, block by block
             m.gpu_seconds = time.perf_counter() - t0
             return m
 

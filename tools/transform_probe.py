@@ -1,0 +1,50 @@
+"""Transform kernel probe: device time of the tcgen05 transform on
+cfg2-sized shapes for each kernel variant (ATLAS_TRANSFORM_T=0: W in
+shared memory; 1: W in TMEM, transposed product) and output dtype.
+Usage: transform_probe.py [rows]"""
+
+import os
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+from paper_2605_09402_b200.engine import transform_typed  # noqa: E402
+
+PEAK = 6544.0
+
+
+def main():
+    rows = int(sys.argv[1]) if len(sys.argv) > 1 else 2_400_000
+    for k, n in [(100, 128), (128, 128), (128, 48), (128, 64), (64, 128)]:
+        x = torch.randn(rows, k, device="cuda")
+        w = torch.randn(n, k, device="cuda") / k ** 0.5
+        b = torch.randn(n, device="cuda")
+        for odt in (torch.float32, torch.float16):
+            y = torch.empty(rows, n, dtype=odt, device="cuda")
+            res = []
+            for t in ("0", "1"):
+                os.environ["ATLAS_TRANSFORM_T"] = t
+                for _ in range(3):
+                    transform_typed(x, w, b, True, y, 1)
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                ev[0].record()
+                for _ in range(10):
+                    transform_typed(x, w, b, True, y, 1)
+                ev[1].record()
+                torch.cuda.synchronize()
+                ms = ev[0].elapsed_time(ev[1]) / 10
+                byts = rows * (k * 4 + n * y.element_size())
+                res.append(f"T={t} {ms:.3f} ms {byts / ms / 1e6:.0f} GB/s "
+                           f"({byts / ms / 1e6 / PEAK:.2f})")
+                if t == "0":
+                    y0 = y.float().clone()
+            err = (y.float() - y0).abs().max().item()
+            print(f"k={k} n={n} out={odt}: " + " | ".join(res) +
+                  f" | max|T1-T0| {err:.2e}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
