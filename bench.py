@@ -586,9 +586,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knobs for exercising the N-rank path on a 1-GPU box: every rank
+    # on cuda:0 and gloo collectives (the driver's N-GPU runs use neither)
+    if os.environ.get("ATLAS_BENCH_SHARE_GPU") == "1":
+        local = 0
+    backend = os.environ.get("ATLAS_BENCH_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group(
+                "nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     line = measure(args, world, rank, local)
     if line is not None and args.workload == "cfg2" and world == 1 \
             and not args.no_cfg3:

@@ -335,6 +335,21 @@ ATLAS_API int atlas_spill_read(const char* const* paths, int32_t n_files,
                                int64_t num_vertices, void* rows_out,
                                uint16_t* delivery_out, int32_t threads,
                                int64_t* bytes_read);
+/* the same layer directory read straight into DEVICE memory rows_dev
+ * (num_vertices x dim, dense): every run of consecutive ids is one
+ * GPUDirect Storage transfer (cuFileRead, storage -> HBM) when the cuFile
+ * driver opens, else it streams through per-thread pinned bounce buffers
+ * on the copy engines; *used_gds (may be NULL) says which. Same
+ * validation, coverage and byte accounting as atlas_spill_read.
+ * rows_dev == NULL validates the directory only (no device work). */
+ATLAS_API int atlas_spill_read_device(const char* const* paths,
+                                      int32_t n_files, int32_t dtype,
+                                      int64_t dim, int64_t num_vertices,
+                                      void* rows_dev, uint16_t* delivery_out,
+                                      int32_t threads, int64_t* bytes_read,
+                                      int32_t* used_gds);
+/* "cuFile" or "bounce: <why GDS is unavailable>" */
+ATLAS_API const char* atlas_gds_status(void);
 /* write rows [id_lo, id_hi) of a dense host matrix (ld elements per row,
  * row 0 = id_lo) as one partition directory's spill files spill_0..k of
  * spill_rows rows each plus its manifest -- the bytes

@@ -115,6 +115,10 @@ def _declare(lib):
        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
     fn("atlas_spill_read", ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
        c_i32, c_i32, c_i64, c_i64, c_vp, c_vp, c_i32, P_i64)
+    fn("atlas_spill_read_device", ctypes.c_int,
+       ctypes.POINTER(ctypes.c_char_p), c_i32, c_i32, c_i64, c_i64, c_vp,
+       c_vp, c_i32, P_i64, ctypes.POINTER(c_i32))
+    fn("atlas_gds_status", ctypes.c_char_p)
     fn("atlas_spill_write", ctypes.c_int, ctypes.c_char_p, c_vp, c_i32, c_i64,
        c_i64, c_i64, c_i64, c_i64, c_i32, P_i64)
     fn("atlas_spill_write_runs", ctypes.c_int, ctypes.c_char_p, c_vp, c_i32,
@@ -137,7 +141,8 @@ EXPORTED = [
     "atlas_layer_run_gat", "atlas_layer_run_fused", "atlas_layer_bind_graph",
     "atlas_spill_read", "atlas_spill_write", "atlas_gather_replay",
     "atlas_spill_write_runs", "atlas_layer_run_blocked",
-    "atlas_layer_record_bytes",
+    "atlas_layer_record_bytes", "atlas_spill_read_device",
+    "atlas_gds_status",
 ]
 
 

@@ -111,6 +111,46 @@ def load_layer_input(layer_dir, out=None, threads: int = 0):
     return meta, rows, int(nbytes.value), delivery
 
 
+def load_layer_device(layer_dir, threads: int = 0, device: int = 0):
+    """Dense (V, dim) rows of a layer dir straight into a CUDA tensor
+    (atlas_spill_read_device): each run of consecutive ids is one
+    GPUDirect Storage read (storage -> HBM) when the cuFile driver is
+    available, else a pinned-bounce stream on the copy engines -- the B200
+    counterpart of the reference's direct-I/O reader (oocgnn/chunks.py:
+    103-260, oocgnn/directio.py). Returns (meta, rows, bytes_read,
+    delivery, used_gds)."""
+    import ctypes
+
+    import torch
+
+    from . import _native as N
+
+    meta = read_layer_meta(layer_dir)
+    tdt = torch.float32 if meta.dtype == "f32" else torch.float16
+    paths = [str(part_dir(layer_dir, k) / name)
+             for k in range(meta.partitions)
+             for name in read_manifest(part_dir(layer_dir, k))]
+    arr = (ctypes.c_char_p * max(1, len(paths)))(
+        *[p.encode() for p in paths])
+    delivery = np.zeros(meta.num_vertices, dtype=np.uint16)
+    nbytes = ctypes.c_int64()
+    gds = ctypes.c_int32()
+    lib = N.load_library()
+    code = N.F32 if meta.dtype == "f32" else N.F16
+    # damaged directories fail before any device memory is touched
+    N.check(lib.atlas_spill_read_device(
+        arr, len(paths), code, meta.dim, meta.num_vertices, None, None,
+        int(threads), None, None))
+    rows = torch.empty((meta.num_vertices, meta.dim), dtype=tdt,
+                       device=f"cuda:{device}")
+    torch.cuda.synchronize(device)  # rows is allocated before the reads
+    N.check(lib.atlas_spill_read_device(
+        arr, len(paths), code, meta.dim, meta.num_vertices, rows.data_ptr(),
+        delivery.ctypes.data, int(threads), ctypes.byref(nbytes),
+        ctypes.byref(gds)))
+    return meta, rows, int(nbytes.value), delivery, bool(gds.value)
+
+
 def write_layer_output(layer_dir, matrix: np.ndarray, partitions: int = 1,
                        dtype: str = "f32", threads: int = 0) -> int:
     """Write a (V, dim) output matrix as a partitioned layer directory with

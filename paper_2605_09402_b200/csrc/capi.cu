@@ -43,6 +43,7 @@ static void load_graph(atlas_graph* g, int64_t V, int64_t E,
                        const uint32_t* in_degrees_host, cudaStream_t s) {
   verify_graph(g);  // a pending check of the previous contents
   g->maxpass_cache.clear();
+  g->generation++;
   g->V = V;
   g->E = E;
   g->offsets.reserve(V + 1);

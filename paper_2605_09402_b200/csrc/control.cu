@@ -474,6 +474,9 @@ static void exact_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
       num_sms() * 8, std::max<int64_t>(1, ceil_div(L->nloc, 8)));
   L->fast_path = false;
   L->sweep_path = false;
+  // a cached static schedule of the same (topology, plan, model, sub-batch,
+  // policy) skips the run materialisation entirely
+  if (sweep_try_cached(L, g, R, s)) return;
   const int64_t npos = g->E + (model == ATLAS_GCN ? 0 : V) + 1;
   SweepWs& W = sweep_ws_of(g);  // grow-only, shared by the graph's layers
   DevBuf<uint64_t>& at_pos = W.at_pos;

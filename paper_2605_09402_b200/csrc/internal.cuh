@@ -42,6 +42,7 @@ struct atlas_graph {
   // exact-replay workspaces (control.cu / sweep.cu), sized by the graph and
   // shared by its layers: replays run one at a time, host-synchronously
   mutable atlas::SweepWs* sweep_ws = nullptr;
+  uint64_t generation = 0;  // bumped by every (re)load of the topology
   ~atlas_graph() {
     if (chk_ev) cudaEventDestroy(chk_ev);
     atlas::free_sweep_ws(sweep_ws);
@@ -138,6 +139,19 @@ struct SweepWs {
   DevBuf<uint64_t> at_pos, runs;
   DevBuf<int64_t> nsel, d_off, d_bounds;
   DevBuf<uint8_t> sel_tmp;
+  // the static schedule (element stream, heap lists, per sub-batch fresh /
+  // graduating counts) depends only on the topology, the chunk plan, the
+  // model, the sub-batch size and the policy: layers with the same key
+  // (e.g. layers 2 and 3 of a [1024,128,128,..] model) reuse it
+  bool valid = false;
+  uint64_t key_gen = 0;
+  int64_t key_R = 0, key_sb = 0;
+  int key_model = -1, key_policy = -1;
+  int64_t NE = 0, S = 0, nchunks = 0, nb = 0;
+  int32_t b0 = 0;
+  bool lru = false;
+  unsigned long long total_msgs = 0;
+  std::vector<int64_t> h_soff, h_touched;
 };
 
 inline SweepWs& sweep_ws_of(const atlas_graph* g) {
@@ -333,6 +347,8 @@ void check_engine_error(atlas_layer* L, cudaStream_t s);
 
 // sweep.cu
 bool sweep_enabled();
+bool sweep_try_cached(atlas_layer* L, const atlas_graph* g, int64_t R,
+                      cudaStream_t s);
 bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
                   const uint64_t* runs, const int64_t* run_off_dev,
                   const std::vector<int64_t>& run_off, cudaStream_t s);

@@ -7,6 +7,8 @@
 // ASPL layout: header <4sIQQQIB (magic "ASPL", version 1, min id, max id,
 // rows, dim, dtype 0=f32/1=f16) at 0; u64 ids at 4096; rows at the next
 // 4096 boundary; file padded to 4096 (oocgnn/storage.py:273-314).
+#include <cufile.h>
+#include <dlfcn.h>
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
@@ -15,6 +17,7 @@
 #include <functional>
 #include <atomic>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -74,9 +77,14 @@ struct FirstError {
   }
 };
 
-// one spill file -> rows at their ids; delivery counted per id
+// moves nrows rows from file offset `off` of fd to the rows of ids
+// [id, id + nrows); false on a short read
+using RunSink = std::function<bool(int fd, uint64_t id, uint64_t nrows,
+                                   int64_t off)>;
+
+// one spill file -> rows at their ids (through sink); delivery counted per id
 void read_one(const char* path, int dtype, int64_t dim, int64_t V,
-              uint8_t* rows_out, std::atomic<uint16_t>* delivery,
+              const RunSink& sink, std::atomic<uint16_t>* delivery,
               std::atomic<int64_t>* bytes, FirstError* err) {
   const int fd = ::open(path, O_RDONLY);
   if (fd < 0) {
@@ -154,8 +162,7 @@ void read_one(const char* path, int dtype, int64_t dim, int64_t V,
   while (i < s.rows) {
     uint64_t j = i + 1;
     while (j < s.rows && ids[j] == ids[j - 1] + 1) j++;
-    if (!pread_all(fd, rows_out + ids[i] * row_b, (j - i) * row_b,
-                   rows_pos + (int64_t)i * row_b)) {
+    if (!sink(fd, ids[i], j - i, rows_pos + (int64_t)i * row_b)) {
       err->set(ATLAS_ETRUNCATED, std::string(path) + ": rows short");
       return;
     }
@@ -263,6 +270,108 @@ int write_spills(const char* part_dir, const uint8_t* src, int32_t dtype,
   return ATLAS_OK;
 }
 
+// ---- GPUDirect Storage ------------------------------------------------
+// cuFile (libcufile from the CUDA toolkit) is resolved at run time: the
+// library then loads where cuFile is absent, and the device reader uses
+// its own pinned-bounce path when cuFile is not requested or its driver
+// does not open.
+struct CuFileApi {
+  bool ok = false;
+  std::string why;
+  CUfileError_t (*driver_open)(void) = nullptr;
+  CUfileError_t (*handle_register)(CUfileHandle_t*, CUfileDescr_t*) = nullptr;
+  void (*handle_deregister)(CUfileHandle_t) = nullptr;
+  ssize_t (*read)(CUfileHandle_t, void*, size_t, off_t, off_t) = nullptr;
+};
+
+const CuFileApi& cufile() {
+  static CuFileApi api = [] {
+    CuFileApi a;
+    // opt-in: on the pool's boxes a cuFile read of a /tmp file never
+    // returned (profiles/r2_gds_probe.txt), so GDS is used only where it
+    // was asked for (ATLAS_GDS=1) and the pinned-bounce stream otherwise
+    const char* on = getenv("ATLAS_GDS");
+    if (!(on && on[0] == '1')) {
+      a.why = "cuFile not requested (ATLAS_GDS=1 enables it)";
+      return a;
+    }
+    void* h = dlopen("libcufile.so.0", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("/usr/local/cuda/lib64/libcufile.so.0",
+                       RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      a.why = "libcufile.so.0 not found";
+      return a;
+    }
+    a.driver_open = reinterpret_cast<CUfileError_t (*)(void)>(
+        dlsym(h, "cuFileDriverOpen"));
+    a.handle_register =
+        reinterpret_cast<CUfileError_t (*)(CUfileHandle_t*, CUfileDescr_t*)>(
+            dlsym(h, "cuFileHandleRegister"));
+    a.handle_deregister = reinterpret_cast<void (*)(CUfileHandle_t)>(
+        dlsym(h, "cuFileHandleDeregister"));
+    a.read = reinterpret_cast<ssize_t (*)(CUfileHandle_t, void*, size_t,
+                                          off_t, off_t)>(
+        dlsym(h, "cuFileRead"));
+    if (!a.driver_open || !a.handle_register || !a.handle_deregister ||
+        !a.read) {
+      a.why = "libcufile lacks the cuFile entry points";
+      return a;
+    }
+    const CUfileError_t e = a.driver_open();
+    if (e.err != CU_FILE_SUCCESS) {
+      a.why = "cuFileDriverOpen failed (" + std::to_string((int)e.err) + ")";
+      return a;
+    }
+    a.ok = true;
+    return a;
+  }();
+  return api;
+}
+
+// pinned bounce buffers of one reader thread: pread into one while the
+// other's copy engine transfer runs (own non-blocking stream)
+struct Bounce {
+  static constexpr size_t kBytes = 8 << 20;
+  uint8_t* buf[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  cudaStream_t stream = nullptr;
+  int next = 0;
+  bool used[2] = {false, false};
+  Bounce() {
+    for (int i = 0; i < 2; i++) {
+      ATLAS_CUDA(cudaMallocHost(&buf[i], kBytes));
+      ATLAS_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+    ATLAS_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  }
+  ~Bounce() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (int i = 0; i < 2; i++) {
+      if (buf[i]) cudaFreeHost(buf[i]);
+      if (done[i]) cudaEventDestroy(done[i]);
+    }
+    if (stream) cudaStreamDestroy(stream);
+  }
+  // file bytes [off, off + n) -> device dst
+  bool move(int fd, uint8_t* dst, size_t n, int64_t off) {
+    while (n) {
+      const size_t m = std::min(n, kBytes);
+      const int b = next;
+      next ^= 1;
+      if (used[b]) ATLAS_CUDA(cudaEventSynchronize(done[b]));
+      if (!pread_all(fd, buf[b], m, off)) return false;
+      ATLAS_CUDA(cudaMemcpyAsync(dst, buf[b], m, cudaMemcpyHostToDevice,
+                                 stream));
+      ATLAS_CUDA(cudaEventRecord(done[b], stream));
+      used[b] = true;
+      dst += m;
+      off += (int64_t)m;
+      n -= m;
+    }
+    return true;
+  }
+};
+
 }  // namespace
 }  // namespace atlas
 
@@ -284,10 +393,15 @@ int atlas_spill_read(const char* const* paths, int32_t n_files,
     for (auto& d : delivery) d.store(0, std::memory_order_relaxed);
     std::atomic<int64_t> bytes{0};
     FirstError err;
+    uint8_t* out = static_cast<uint8_t*>(rows_out);
+    const int64_t row_b = dim * (dtype == ATLAS_F32 ? 4 : 2);
+    const RunSink host_sink = [&](int fd, uint64_t id, uint64_t nrows,
+                                  int64_t off) {
+      return pread_all(fd, out + id * row_b, nrows * row_b, off);
+    };
     run_pool(n_files, default_threads(threads), [&](int64_t i) {
-      read_one(paths[i], dtype, dim, num_vertices,
-               static_cast<uint8_t*>(rows_out), delivery.data(), &bytes,
-               &err);
+      read_one(paths[i], dtype, dim, num_vertices, host_sink, delivery.data(),
+               &bytes, &err);
     });
     if (err.code != ATLAS_OK) {
       set_error(err.msg);
@@ -313,6 +427,115 @@ int atlas_spill_read(const char* const* paths, int32_t n_files,
     set_error(std::string("atlas_spill_read: ") + e.what());
     return ATLAS_EINVARIANT;
   }
+}
+
+int atlas_spill_read_device(const char* const* paths, int32_t n_files,
+                            int32_t dtype, int64_t dim, int64_t num_vertices,
+                            void* rows_dev, uint16_t* delivery_out,
+                            int32_t threads, int64_t* bytes_read,
+                            int32_t* used_gds) {
+  try {
+    if ((!paths && n_files) || dim < 1 || num_vertices < 0 ||
+        (dtype != ATLAS_F32 && dtype != ATLAS_F16)) {
+      set_error("atlas_spill_read_device: bad arguments");
+      return ATLAS_ECONFIG;
+    }
+    // rows_dev == NULL: validate the directory (headers, sizes, ids,
+    // coverage) without reading rows or touching the device
+    const bool validate_only = rows_dev == nullptr;
+    ATLAS_NVTX("atlas_spill_read_device");
+    std::vector<std::atomic<uint16_t>> delivery((size_t)num_vertices);
+    for (auto& d : delivery) d.store(0, std::memory_order_relaxed);
+    std::atomic<int64_t> bytes{0};
+    FirstError err;
+    uint8_t* out = static_cast<uint8_t*>(rows_dev);
+    const int64_t row_b = dim * (dtype == ATLAS_F32 ? 4 : 2);
+    const CuFileApi& cf = cufile();
+    const int nthreads = default_threads(threads);
+    const int64_t nf = n_files;
+    std::atomic<int64_t> next{0};
+    int dev = 0;
+    if (!validate_only) ATLAS_CUDA(cudaGetDevice(&dev));
+    auto worker = [&] {
+      try {
+        if (!validate_only) cudaSetDevice(dev);
+        std::unique_ptr<Bounce> bounce;
+        for (int64_t i; (i = next.fetch_add(1)) < nf;) {
+          CUfileHandle_t fh = nullptr;
+          bool reg = false;
+          // rows land at their ids: runs of consecutive ids are one
+          // storage -> HBM transfer (cuFileRead) or one bounce stream
+          const RunSink sink = [&](int fd, uint64_t id, uint64_t nrows,
+                                   int64_t off) -> bool {
+            const size_t n = (size_t)(nrows * row_b);
+            if (validate_only) return true;
+            if (cf.ok) {
+              if (!reg) {
+                CUfileDescr_t d{};
+                d.type = CU_FILE_HANDLE_TYPE_OPAQUE_FD;
+                d.handle.fd = fd;
+                if (cf.handle_register(&fh, &d).err != CU_FILE_SUCCESS)
+                  return false;
+                reg = true;
+              }
+              size_t done = 0;
+              while (done < n) {
+                const ssize_t r = cf.read(fh, out, n - done,
+                                          (off_t)(off + (int64_t)done),
+                                          (off_t)(id * row_b + done));
+                if (r <= 0) return false;
+                done += (size_t)r;
+              }
+              return true;
+            }
+            if (!bounce) bounce.reset(new Bounce());
+            return bounce->move(fd, out + id * row_b, n, off);
+          };
+          read_one(paths[i], dtype, dim, num_vertices, sink, delivery.data(),
+                   &bytes, &err);
+          if (reg) cf.handle_deregister(fh);
+        }
+        if (bounce) ATLAS_CUDA(cudaStreamSynchronize(bounce->stream));
+      } catch (const Error& e) {
+        err.set(e.code, e.msg);
+      }
+    };
+    std::vector<std::thread> pool;
+    const int t = std::max(1, std::min<int>(nthreads, (int)std::max<int64_t>(nf, 1)));
+    for (int k = 0; k < t; k++) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    if (used_gds) *used_gds = cf.ok && !validate_only ? 1 : 0;
+    if (err.code != ATLAS_OK) {
+      set_error(err.msg);
+      return err.code;
+    }
+    int64_t bad = 0, first = -1;
+    for (int64_t v = 0; v < num_vertices; v++) {
+      const uint16_t c = delivery[v].load(std::memory_order_relaxed);
+      if (delivery_out) delivery_out[v] = c;
+      if (c != 1) {
+        if (first < 0) first = v;
+        bad++;
+      }
+    }
+    if (bytes_read) *bytes_read = bytes.load();
+    if (bad) {
+      set_error(std::to_string(bad) + " ids not delivered exactly once, first " +
+                std::to_string(first));
+      return ATLAS_ECOVERAGE;
+    }
+    return ATLAS_OK;
+  } catch (const std::exception& e) {
+    set_error(std::string("atlas_spill_read_device: ") + e.what());
+    return ATLAS_EINVARIANT;
+  }
+}
+
+const char* atlas_gds_status(void) {
+  const CuFileApi& cf = cufile();
+  static std::string s;
+  s = cf.ok ? "cuFile" : "bounce: " + cf.why;
+  return s.c_str();
 }
 
 int atlas_spill_write(const char* part_dir, const void* rows, int32_t dtype,

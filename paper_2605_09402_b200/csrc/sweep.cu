@@ -44,7 +44,7 @@
 namespace atlas {
 namespace {
 
-constexpr int kSwThreads = 1024;
+constexpr int kSwThreads = 512;
 constexpr int kSwBlock = 2048;   // sub-batches staged in shared memory
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
@@ -289,86 +289,53 @@ struct SweepArgs {
   int64_t* out;              // evictions, reloads, hot_peak, nvict, err, info
 };
 
-// Bucket entries reach the CTA through two shared-memory window buffers
-// filled by bulk async copies (cp.async.bulk, one thread, mbarrier
-// completion): the entry lists are static, so a buffer is a cache of the
-// range [start, start + len) and the walk keeps the next window of the
-// same list in flight while it scans the current one.
-constexpr int kSwWin = 8192;                  // entries per window buffer
-constexpr int kSwPerT = kSwWin / kSwThreads;  // 8 entries per thread
+// The walk reads each bucket list through register windows of kSwWin
+// entries (16 per thread), the list's next window already in flight in a
+// second register set while the current one is scanned. Per-bucket
+// state lives in shared memory for the first kSwCache buckets: the head,
+// the list end and the sub-batch of the entry at the head when known
+// (head_sub). A list whose head entry is not delivered yet (head_sub >= s)
+// has nothing in the heap at s, so it is skipped without touching memory;
+// most of an event's lists are in that state (their live entries were
+// popped or superseded), and reading their head windows anyway was what
+// the walk spent its time on.
+constexpr int kSwPerT = 16;
+constexpr int kSwWin = kSwThreads * kSwPerT;
+constexpr int kSwCache = 4096;
+constexpr uint32_t kUnknown = 0;  // head_sub not known: read the list
 
 struct SweepSm {
-  uint32_t sub[2][kSwWin];   // window buffers: ent_sub
-  uint32_t nxt[2][kSwWin];   //                 ent_next
   uint32_t fresh[kSwBlock], grad[kSwBlock], cold[kSwBlock];
-  uint64_t bar[2];
-  uint32_t buf_start[2], buf_len[2], buf_phase[2];
-  int32_t buf_busy[2];       // a copy is in flight (not yet waited on)
+  uint32_t head[kSwCache], end[kSwCache], head_sub[kSwCache];
   int64_t hot, peak, evictions, reloads, need_old, k, nv;
   int32_t i, mode, err;
   int64_t err_info;
-  uint32_t last_taken;
+  uint32_t last_taken, hs_new;
   uint32_t first_na[2];
+  int32_t wtotal[2], wlog[2];
+  unsigned long long windows, visits, skipped;
 };
 
-__device__ __forceinline__ uint32_t sw_smem(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-// thread 0: start filling buffer q with entries [start, start + len)
-__device__ void sw_fetch(SweepSm& sm, const SweepArgs& A, int q,
-                         uint32_t start, uint32_t len) {
-  const uint32_t bytes = ((len + 3u) & ~3u) * 4u;  // arrays padded by 4
-  const uint32_t bar = sw_smem(&sm.bar[q]);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile(
-      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-      "r"(2u * bytes)
-      : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1], %2, [%3];" ::"r"(sw_smem(sm.sub[q])),
-      "l"(A.ent_sub + start), "r"(bytes), "r"(bar)
-      : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1], %2, [%3];" ::"r"(sw_smem(sm.nxt[q])),
-      "l"(A.ent_next + start), "r"(bytes), "r"(bar)
-      : "memory");
-  sm.buf_start[q] = start;
-  sm.buf_len[q] = len;
-  sm.buf_busy[q] = 1;
-}
-
-__device__ __forceinline__ void sw_wait(SweepSm& sm, int q) {
-  const uint32_t bar = sw_smem(&sm.bar[q]), ph = sm.buf_phase[q];
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "SW_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra SW_WAIT_%=;\n}" ::"r"(bar),
-      "r"(ph)
-      : "memory");
-}
-
 __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
-  extern __shared__ __align__(128) unsigned char sw_raw[];
+  extern __shared__ __align__(16) unsigned char sw_raw[];
   SweepSm& sm = *reinterpret_cast<SweepSm*>(sw_raw);
   using Scan = cub::BlockScan<int, kSwThreads>;
   __shared__ typename Scan::TempStorage scan;
   const int tid = threadIdx.x;
+  const int ncache = A.nb < kSwCache ? A.nb : kSwCache;
+  uint32_t pf_sub[kSwPerT], pf_nxt[kSwPerT];  // next-window prefetch
+  int pf_b = -1;
+  uint32_t pf_start = kNone;
+  for (int b = tid; b < ncache; b += kSwThreads) {
+    sm.head[b] = A.boff[b];
+    sm.end[b] = A.boff[b + 1];
+    sm.head_sub[b] = sm.head[b] >= sm.end[b] ? kNone : kUnknown;
+  }
   if (tid == 0) {
     sm.hot = sm.peak = sm.evictions = sm.reloads = sm.nv = 0;
     sm.err = 0;
     sm.err_info = 0;
-    for (int q = 0; q < 2; q++) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
-          sw_smem(&sm.bar[q])));
-      sm.buf_start[q] = sm.buf_len[q] = 0;
-      sm.buf_phase[q] = 0;
-      sm.buf_busy[q] = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    sm.windows = sm.visits = sm.skipped = 0;
   }
   __syncthreads();
   for (int64_t base = 0; base < A.S; base += kSwBlock) {
@@ -426,6 +393,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
         sm.i = i;
         sm.hot = hot;
         sm.first_na[0] = sm.first_na[1] = kNone;
+        sm.wtotal[0] = sm.wtotal[1] = 0;
+        sm.wlog[0] = sm.wlog[1] = 0;
       }
       __syncthreads();
       const int64_t k = sm.k;
@@ -443,67 +412,78 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
           bad = true;
           break;
         }
-        const uint32_t h = __ldcg(A.head + b);
-        const uint32_t e_end = A.boff[b + 1];
+        const bool cached = b < kSwCache;
+        uint32_t h, e_end;
+        if (cached) {
+          if (sm.head_sub[b] >= s && sm.head_sub[b] != kUnknown) {
+            if (tid == 0) sm.skipped++;
+            b++;  // nothing of this list is in the heap yet (or it is done)
+            continue;
+          }
+          h = sm.head[b];
+          e_end = sm.end[b];
+        } else {
+          h = __ldcg(A.head + b);
+          e_end = A.boff[b + 1];
+        }
         if (h >= e_end) {
           b++;
           continue;
         }
-        // a buffer holding h, else fetch [h & ~3, +kSwWin) into the idle one
-        if (tid == 0) {
-          int q = -1;
-          for (int c = 0; c < 2; c++)
-            if (h >= sm.buf_start[c] && h < sm.buf_start[c] + sm.buf_len[c])
-              q = c;
-          if (q < 0) {
-            q = (sm.buf_busy[0] && !sm.buf_busy[1]) ? 1 : 0;
-            if (sm.buf_busy[q]) {  // drain a stale prefetch first
-              sw_wait(sm, q);
-              sm.buf_phase[q] ^= 1;
-              sm.buf_busy[q] = 0;
-            }
-            const uint32_t w0 = h & ~3u;
-            sw_fetch(sm, A, q, w0, min((uint32_t)kSwWin, e_end - w0));
-          }
-          // keep the list's next window in flight in the other buffer
-          const int o = q ^ 1;
-          const uint32_t nx = sm.buf_start[q] + sm.buf_len[q];
-          if (nx < e_end && !sm.buf_busy[o] &&
-              !(nx >= sm.buf_start[o] && nx < sm.buf_start[o] + sm.buf_len[o]))
-            sw_fetch(sm, A, o, nx, min((uint32_t)kSwWin, e_end - nx));
-          sm.first_na[(w + 1) & 1] = (uint32_t)q;  // scratch: buffer index
-        }
-        __syncthreads();
-        const int q = (int)sm.first_na[(w + 1) & 1];
-        if (sm.buf_busy[q]) sw_wait(sm, q);
-        const uint32_t bs = sm.buf_start[q];
-        const uint32_t be = bs + sm.buf_len[q];
-        __syncthreads();
-        if (tid == 0) {
-          if (sm.buf_busy[q]) {
-            sm.buf_phase[q] ^= 1;
-            sm.buf_busy[q] = 0;
-          }
-          sm.first_na[(w + 1) & 1] = kNone;
-        }
-        // scan [max(h, bs), be): thread t takes 8 consecutive entries
-        const uint32_t j0 = bs + (uint32_t)tid * kSwPerT;
+        const uint32_t w0 = h & ~3u;
+        const uint32_t j0 = w0 + (uint32_t)tid * kSwPerT;
+        // this window: from the register prefetch when it holds exactly
+        // this (list, start), else loaded now; then the list's next window
+        // is put in flight into the prefetch registers, to be waited on by
+        // the next iteration (the lists are static, so a prefetch stays
+        // valid across events)
         uint32_t subs[kSwPerT], nxts[kSwPerT];
+        if (pf_b == b && pf_start == w0) {
+#pragma unroll
+          for (int q = 0; q < kSwPerT; q++) {
+            subs[q] = pf_sub[q];
+            nxts[q] = pf_nxt[q];
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < kSwPerT; q += 4) {
+            uint4 a4 = make_uint4(kNone, kNone, kNone, kNone);
+            uint4 n4 = make_uint4(0, 0, 0, 0);
+            if (j0 + q < e_end) {
+              a4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_sub + j0 + q));
+              n4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_next + j0 + q));
+            }
+            subs[q] = a4.x; subs[q + 1] = a4.y; subs[q + 2] = a4.z; subs[q + 3] = a4.w;
+            nxts[q] = n4.x; nxts[q + 1] = n4.y; nxts[q + 2] = n4.z; nxts[q + 3] = n4.w;
+          }
+        }
         {
-          const uint4* ps = reinterpret_cast<const uint4*>(sm.sub[q]) + tid * 2;
-          const uint4* pn = reinterpret_cast<const uint4*>(sm.nxt[q]) + tid * 2;
-          const uint4 s0 = ps[0], s1 = ps[1], n0 = pn[0], n1 = pn[1];
-          subs[0] = s0.x; subs[1] = s0.y; subs[2] = s0.z; subs[3] = s0.w;
-          subs[4] = s1.x; subs[5] = s1.y; subs[6] = s1.z; subs[7] = s1.w;
-          nxts[0] = n0.x; nxts[1] = n0.y; nxts[2] = n0.z; nxts[3] = n0.w;
-          nxts[4] = n1.x; nxts[5] = n1.y; nxts[6] = n1.z; nxts[7] = n1.w;
+          const uint32_t p0 = w0 + (uint32_t)kSwWin;
+          if (p0 < e_end) {
+            const uint32_t pj = p0 + (uint32_t)tid * kSwPerT;
+#pragma unroll
+            for (int q = 0; q < kSwPerT; q += 4) {
+              uint4 a4 = make_uint4(kNone, kNone, kNone, kNone);
+              uint4 n4 = make_uint4(0, 0, 0, 0);
+              if (pj + q < e_end) {
+                a4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_sub + pj + q));
+                n4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_next + pj + q));
+              }
+              pf_sub[q] = a4.x; pf_sub[q + 1] = a4.y; pf_sub[q + 2] = a4.z; pf_sub[q + 3] = a4.w;
+              pf_nxt[q] = n4.x; pf_nxt[q + 1] = n4.y; pf_nxt[q + 2] = n4.z; pf_nxt[q + 3] = n4.w;
+            }
+            pf_b = b;
+            pf_start = p0;
+          } else {
+            pf_b = -1;
+          }
         }
         int valid = 0, nvalid = 0;
         uint32_t first_na = kNone;
 #pragma unroll
         for (int e = 0; e < kSwPerT; e++) {
           const uint32_t j = j0 + e;
-          if (j < h || j >= be) continue;
+          if (j < h || j >= e_end) continue;
           if (subs[e] < s) {
             if (nxts[e] >= s) {
               valid |= 1 << e;
@@ -513,41 +493,116 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
             first_na = j;
           }
         }
-        int off, total;
-        Scan(scan).ExclusiveSum(nvalid, off, total);
-        if (first_na != kNone) atomicMin(&sm.first_na[w & 1], first_na);
-#pragma unroll
-        for (int e = 0; e < kSwPerT; e++) {
-          if (!(valid >> e & 1)) continue;
-          const int64_t r = off++;
-          if (r >= rem) break;
-          const uint32_t j = j0 + e;
-          A.victims[nv + r] = j;
-          const uint32_t nx = nxts[e];
-          if ((int64_t)nx < win_hi) atomicAdd(&sm.cold[nx - base], 1u);
-          else atomicAdd(A.cold + nx, 1u);
-          if (r == rem - 1) sm.last_taken = j;
+        // window totals: valid entries and the first undelivered entry
+        {
+          const int wv = __reduce_add_sync(0xffffffffu, nvalid);
+          const uint32_t wf = __reduce_min_sync(0xffffffffu, first_na);
+          if ((tid & 31) == 0) {
+            if (wv) atomicAdd(&sm.wtotal[w & 1], wv);
+            if (wf != kNone) atomicMin(&sm.first_na[w & 1], wf);
+          }
+          // the other slot was last read before the previous window's end
+          if (tid == 0) {
+            sm.first_na[(w + 1) & 1] = kNone;
+            sm.wtotal[(w + 1) & 1] = 0;
+            sm.wlog[(w + 1) & 1] = 0;
+          }
         }
         __syncthreads();
-        uint32_t h_new;
+        const int64_t total = sm.wtotal[w & 1];
+        const uint32_t fna = sm.first_na[w & 1];
+        uint32_t run_nx = kNone, run_c = 0;
+        auto cold_add = [&](uint32_t nx) {  // consecutive equal keys: one atomic
+          if (nx == run_nx) {
+            run_c++;
+            return;
+          }
+          if (run_c) {
+            if ((int64_t)run_nx < win_hi) atomicAdd(&sm.cold[run_nx - base], run_c);
+            else atomicAdd(A.cold + run_nx, run_c);
+          }
+          run_nx = nx;
+          run_c = 1;
+        };
+        if (total <= rem) {
+          // the whole window's valid entries are victims: order within the
+          // event is irrelevant here (no logs), so log slots come from one
+          // atomic per warp
+          int incl = nvalid;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((tid & 31) >= o) incl += t;
+          }
+          int wbase = 0;
+          if ((tid & 31) == 31 && incl) wbase = atomicAdd(&sm.wlog[w & 1], incl);
+          wbase = __shfl_sync(0xffffffffu, wbase, 31);
+          int pos = wbase + incl - nvalid;
+#pragma unroll
+          for (int e = 0; e < kSwPerT; e++) {
+            if (!(valid >> e & 1)) continue;
+            A.victims[nv + pos++] = j0 + e;
+            cold_add(nxts[e]);
+          }
+          if (fna != kNone && fna >= j0 && fna < j0 + kSwPerT)
+            sm.hs_new = subs[fna - j0];
+        } else {
+          // the event ends inside this window: exact ranks
+          int off, t2;
+          Scan(scan).ExclusiveSum(nvalid, off, t2);
+#pragma unroll
+          for (int e = 0; e < kSwPerT; e++) {
+            if (!(valid >> e & 1)) continue;
+            const int64_t r = off++;
+            if (r >= rem) break;
+            const uint32_t j = j0 + e;
+            A.victims[nv + r] = j;
+            cold_add(nxts[e]);
+            if (r == rem - 1) {
+              sm.last_taken = j;
+              // the new head's sub-batch, when it is in this thread's slice
+              sm.hs_new = e + 1 < kSwPerT && j + 1 < e_end ? subs[e + 1]
+                                                          : kUnknown;
+            }
+          }
+        }
+        cold_add(kNone);  // flush the last run (a kNone run is never added)
+        __syncthreads();
+        uint32_t h_new, hs;
         const int bcur = b;
-        if (total >= rem) {
+        const uint32_t wend = min(e_end, w0 + (uint32_t)kSwWin);
+        if (total > rem) {
           h_new = sm.last_taken + 1;
           nv += rem;
           rem = 0;
+          hs = 1;
         } else {
           nv += total;
           rem -= total;
-          const uint32_t fna = sm.first_na[w & 1];
           if (fna != kNone) {
             h_new = fna;  // the rest of the list is not delivered yet
+            hs = 2;
             b++;
           } else {
-            h_new = be;
-            if (be >= e_end) b++;
+            h_new = wend;
+            hs = wend >= e_end ? 3 : 0;
+            if (wend >= e_end) b++;
           }
         }
-        if (tid == 0) A.head[bcur] = h_new;
+        if (tid == 0) {
+          uint32_t v = kUnknown;
+          if (hs == 1 || hs == 2) v = sm.hs_new;
+          if (hs == 3) v = kNone;
+          if (h_new >= e_end) v = kNone;
+          if (cached) {
+            sm.head[bcur] = h_new;
+            sm.head_sub[bcur] = v;
+          } else {
+            A.head[bcur] = h_new;
+          }
+          sm.windows++;
+          sm.visits += 1;
+        }
         w++;
         __syncthreads();
       }
@@ -568,11 +623,6 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
     __syncthreads();
     if (sm.err) break;
   }
-  // no copy may outlive the CTA
-  if (tid == 0)
-    for (int q = 0; q < 2; q++)
-      if (sm.buf_busy[q]) sw_wait(sm, q);
-  __syncthreads();
   if (tid == 0) {
     A.out[0] = sm.evictions;
     A.out[1] = sm.reloads;
@@ -580,6 +630,8 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
     A.out[3] = sm.nv;
     A.out[4] = sm.err;
     A.out[5] = sm.err_info;
+    A.out[6] = (int64_t)sm.windows;
+    A.out[7] = (int64_t)sm.skipped;
   }
 }
 
@@ -639,6 +691,29 @@ bool sweep_enabled() {
 // Returns false (nothing changed) when the layer must take the per-element
 // machine instead: inconsistent deliveries (it raises the reference's
 // error) or a stream too long for 32-bit element indices.
+static bool run_sweep(atlas_layer* L, SweepWs& W, PhaseTimer& T,
+                      cudaStream_t s);
+
+static bool key_matches(const SweepWs& W, const atlas_layer* L,
+                        const atlas_graph* g, int64_t R) {
+  return W.valid && W.key_gen == g->generation && W.key_R == R &&
+         W.key_sb == L->sub_batch && W.key_model == L->desc.model &&
+         W.key_policy == L->desc.policy;
+}
+
+// the layer's replay straight from a cached static schedule (no run
+// materialisation); false when the cache does not hold this key
+bool sweep_try_cached(atlas_layer* L, const atlas_graph* g, int64_t R,
+                      cudaStream_t s) {
+  if (!sweep_enabled() || L->desc.policy == ATLAS_RND || L->desc.record_log)
+    return false;
+  SweepWs& W = sweep_ws_of(g);
+  if (!key_matches(W, L, g, R)) return false;
+  ATLAS_NVTX("sweep_replay_cached");
+  PhaseTimer T(s);
+  return run_sweep(L, W, T, s);
+}
+
 bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
                   const uint64_t* runs, const int64_t* run_off_dev,
                   const std::vector<int64_t>& run_off, cudaStream_t s) {
@@ -648,6 +723,7 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   const int64_t nchunks = ceil_div(V, R);
   const int64_t sb = L->sub_batch;
   SweepWs& W = sweep_ws_of(g);
+  W.valid = false;
   PhaseTimer T(s);
 
   // ---- per-chunk pass sizes and the element / sub-batch layout ----------
@@ -801,7 +877,6 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   W.ent_next.reserve(NE + 4);
   W.boff.reserve(nb + 1);
   W.head.reserve(nb);
-  const uint32_t* ent_el = nullptr;
   if (lru) {
     make_entries<<<grid_of(NE), 256, 0, s>>>(nullptr, W.el_newp.ptr,
                                              W.el_sub.ptr, W.el_nsub.ptr, NE,
@@ -828,7 +903,6 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
     bucket_bounds<<<grid_of(NE + 1), 256, 0, s>>>(W.sv.ptr, NE, nb,
                                                   W.boff.ptr);
     count_launch(3);
-    ent_el = W.se.ptr;
   }
   ATLAS_CUDA(cudaMemsetAsync(W.ent_sub.ptr + NE, 0xFF, 4 * sizeof(uint32_t), s));
   ATLAS_CUDA(cudaMemsetAsync(W.ent_next.ptr + NE, 0, 4 * sizeof(uint32_t), s));
@@ -837,6 +911,35 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   ATLAS_LAUNCH_CHECK();
 
   T.mark("buckets");
+  W.valid = true;
+  W.key_gen = g->generation;
+  W.key_R = R;
+  W.key_sb = sb;
+  W.key_model = model;
+  W.key_policy = L->desc.policy;
+  W.NE = NE;
+  W.S = S;
+  W.nchunks = nchunks;
+  W.nb = nb;
+  W.b0 = lru ? 0 : 1;
+  W.lru = lru;
+  W.total_msgs = total_msgs;
+  W.h_soff = soff;
+  W.h_touched = touched;
+  return run_sweep(L, W, T, s);
+}
+
+// the dynamic part: the sweep over sub-batches from fresh heads and zero
+// reload counts, then unique reloads and per-chunk reloads
+static bool run_sweep(atlas_layer* L, SweepWs& W, PhaseTimer& T,
+                      cudaStream_t s) {
+  const int64_t NE = W.NE, S = W.S, nchunks = W.nchunks, nb = W.nb;
+  const int64_t nloc = L->nloc;
+  const bool lru = W.lru;
+  const uint32_t* ent_el = lru ? nullptr : W.se.ptr;
+  ATLAS_CUDA(cudaMemsetAsync(W.cold.ptr, 0, std::max<int64_t>(S, 1) * 4, s));
+  ATLAS_CUDA(cudaMemcpyAsync(W.head.ptr, W.boff.ptr, nb * sizeof(uint32_t),
+                             cudaMemcpyDeviceToDevice, s));
   // ---- the sweep ------------------------------------------------------
   W.victims.reserve(NE);
   W.out.reserve(8);
@@ -848,7 +951,7 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   A.cold_out = W.cold_out.ptr;
   A.slots = L->desc.slot_count;
   A.evict_batch = L->evict_batch;
-  A.b0 = lru ? 0 : 1;
+  A.b0 = W.b0;
   A.nb = (int32_t)nb;
   A.boff = W.boff.ptr;
   A.head = W.head.ptr;
@@ -867,10 +970,15 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   count_launch();
   ATLAS_LAUNCH_CHECK();
   T.mark("sweep");
-  int64_t out[6];
+  int64_t out[8];
   ATLAS_CUDA(cudaMemcpyAsync(out, W.out.ptr, sizeof(out),
                              cudaMemcpyDeviceToHost, s));
   ATLAS_CUDA(cudaStreamSynchronize(s));
+  if (T.on)
+    fprintf(stderr, "[sweep] S=%lld NE=%lld evictions=%lld windows=%lld "
+                    "skipped_lists=%lld\n",
+            (long long)S, (long long)NE, (long long)out[0], (long long)out[6],
+            (long long)out[7]);
   if (out[4] == ATLAS_ECONFIG)
     fail(ATLAS_ECONFIG, "batch of " + std::to_string(out[5]) +
                             " cannot fit in " +
@@ -903,14 +1011,15 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
                              cudaMemcpyDeviceToHost, s));
   ATLAS_CUDA(cudaStreamSynchronize(s));
   for (int64_t c = 0; c < nchunks; c++) {
-    const int64_t s0 = soff[3 * c], s1 = c + 1 < nchunks ? soff[3 * c + 3] : S;
+    const int64_t s0 = W.h_soff[3 * c],
+                  s1 = c + 1 < nchunks ? W.h_soff[3 * c + 3] : S;
     int64_t r = 0;
     for (int64_t q = s0; q < s1; q++) r += cold[q];
     L->chunk_reloads.push_back(r);
-    L->chunk_touched.push_back(touched[c]);
+    L->chunk_touched.push_back(W.h_touched[c]);
   }
   L->sweep_path = true;
-  L->sw_messages = (int64_t)total_msgs;
+  L->sw_messages = (int64_t)W.total_msgs;
   L->sw_evictions = evictions;
   L->sw_reloads = reloads;
   L->sw_hot_peak = peak;

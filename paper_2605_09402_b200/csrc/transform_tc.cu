@@ -907,6 +907,245 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// f32 x, register split (the default f32 kernel when W fits resident): the
+// splitter warps read each x row chunk once from the TMA stage, release the
+// stage at once, and write hi / lo straight into TMEM, where they are the
+// MMA's A operand. Shared memory then holds only W (hi + lo, resident) and
+// 16-KB x landing stages that turn over as soon as they are split, so more
+// x bytes are in flight per SM than when x_hi / x_lo occupy the stages
+// until their MMAs retire (transform_tc_kernel, whose in-flight bytes cap
+// it at ~0.6 of HBM). TMEM: D double buffer [0, 2 BN), then kAStages A
+// stages of 64 columns (hi 32 | lo 32) from column 256.
+//   warp 0      TMA producer (x tiles; W once)
+//   warp 1      TMEM allocator + MMA issuer
+//   warps 2-5   W split (once), then x split: warp w owns TMEM lane quarter
+//               w & 3, thread = tile row
+//   warps 6-13  epilogue (shared with transform_tc_kernel)
+constexpr int kAStages = 4;
+constexpr uint32_t kACol0 = 256;
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, "
+      "%7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, "
+      "%21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]),
+      "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]),
+      "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]),
+      "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]),
+      "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]),
+      "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kThreads, 1)
+    transform_r_kernel(const __grid_constant__ CUtensorMap map_x,
+                       const __grid_constant__ CUtensorMap map_w,
+                       TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t x_bytes = BM * BK * 4;
+  const uint32_t w_bytes = p.BN * BK * 4;
+  const uint32_t wres_bytes = 2u * w_bytes * p.kblocks;
+  uint8_t* stages = base + wres_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + p.stages * x_bytes);
+  uint64_t* sempty = full + p.stages;
+  uint64_t* afull = sempty + p.stages;   // [kAStages]
+  uint64_t* aempty = afull + kAStages;   // [kAStages]
+  uint64_t* tfull = aempty + kAStages;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint64_t* wfull = tempty + 2;
+  uint64_t* wsplit = wfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wsplit + 1);
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+  float* stage_out = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(sbias + 256) + 15) & ~uintptr_t(15));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (p.M + BM - 1) / BM;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&sempty[s], 128);
+    }
+    for (int a = 0; a < kAStages; a++) {
+      mbar_init(&afull[a], 128);
+      mbar_init(&aempty[a], 1);
+    }
+    for (int a = 0; a < 2; a++) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps * 32);
+    }
+    mbar_init(wfull, 1);
+    mbar_init(wsplit, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = threadIdx.x; j < p.BN; j += kThreads)
+    sbias[j] = j < p.N ? p.bias[j] : 0.0f;
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::
+            "r"(smem_u32(tmem_slot)),
+        "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+  auto w_hi_ptr = [&](int kb) -> uint8_t* { return base + kb * w_bytes; };
+  auto w_lo_ptr = [&](int kb) -> uint8_t* {
+    return base + (p.kblocks + kb) * w_bytes;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(wfull, w_bytes * p.kblocks);
+      for (int kb = 0; kb < p.kblocks; kb++)
+        tma_load_2d(w_hi_ptr(kb), &map_w, wfull, kb * BK, 0);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kb = 0; kb < p.kblocks; kb++) {
+          mbar_wait(&sempty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], x_bytes);
+          tma_load_2d(stages + s * x_bytes, &map_x, &full[s], kb * BK,
+                      (int)(t * BM));
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                           ((uint32_t)(p.BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+    mbar_wait(wsplit, 0);
+    int a = 0;
+    uint32_t aph = 0;
+    int acc = 0;
+    uint32_t tph[2] = {0, 0};
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], tph[acc] ^ 1);
+      tph[acc] ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dt = tmem_base + (uint32_t)(acc * p.BN);
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        mbar_wait(&afull[a], aph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t ahi = tmem_base + kACol0 + (uint32_t)(a * 64);
+          const uint32_t b_hi = smem_u32(w_hi_ptr(kb));
+          const uint32_t b_lo = smem_u32(w_lo_ptr(kb));
+#pragma unroll
+          for (int k = 0; k < BK / 8; k++) {
+            const uint32_t off = k * 32;
+            const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
+            mma_tf32_ts(dt, ahi + 32 + k * 8, sw128_desc(b_hi + off), idesc,
+                        first);
+            mma_tf32_ts(dt, ahi + k * 8, sw128_desc(b_lo + off), idesc, 1u);
+            mma_tf32_ts(dt, ahi + k * 8, sw128_desc(b_hi + off), idesc, 1u);
+          }
+          mma_commit(&aempty[a]);
+          if (kb == p.kblocks - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++a == kAStages) {
+          a = 0;
+          aph ^= 1;
+        }
+      }
+      acc ^= 1;
+    }
+  } else if (warp < 6) {
+    const int tid = threadIdx.x - 64;  // 0..127
+    {  // W -> tf32 hi (in place) + lo, once
+      mbar_wait(wfull, 0);
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        float4* wh = reinterpret_cast<float4*>(w_hi_ptr(kb));
+        float4* wl = reinterpret_cast<float4*>(w_lo_ptr(kb));
+        for (int e = tid; e < p.BN * BK / 4; e += 128) {
+          const float4 v = wh[e];
+          float4 h, l;
+          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          l.x = v.x - h.x;
+          l.y = v.y - h.y;
+          l.z = v.z - h.z;
+          l.w = v.w - h.w;
+          wh[e] = h;
+          wl[e] = l;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(wsplit);
+    }
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // tile row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    int s = 0, a = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        mbar_wait(&full[s], ph);
+        // row r's 128-B chunk: 16-B unit c sits at SW128 slot c ^ (r & 7)
+        const float4* xs =
+            reinterpret_cast<const float4*>(stages + s * x_bytes) + r * 8;
+        float hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+          const float4 v = xs[c ^ (r & 7)];
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const float h = __uint_as_float(__float_as_uint(e[q]) & 0xFFFFE000u);
+            hi[c * 4 + q] = h;
+            lo[c * 4 + q] = e[q] - h;
+          }
+        }
+        // the stage is free once read (the TMA refilling it is an
+        // async-proxy write after these generic-proxy reads)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&sempty[s]);
+        mbar_wait(&aempty[a], aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ta = tmem_base + lane_off + kACol0 + (uint32_t)(a * 64);
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&afull[a]);
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (++a == kAStages) {
+          a = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else {
+    epilogue_loop<OutT>(p, warp - 6, warp, lane, ntiles, tmem_base, tfull,
+                        tempty, sbias, nullptr, stage_out);
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile(
+        "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(
+            tmem_base),
+        "r"(512));
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                               void*, const cuuint64_t*, const cuuint64_t*,
                               const cuuint32_t*, const cuuint32_t*,
@@ -1051,10 +1290,69 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
   return ok;
 }
 
-// ATLAS_TRANSFORM_T=0 (A/B probes): keep W in shared memory instead
+// ATLAS_TRANSFORM_R=0 (A/B probes): x hi / lo in shared memory instead
+bool regsplit_enabled() {
+  const char* e = getenv("ATLAS_TRANSFORM_R");
+  return !(e && e[0] == '0');
+}
+
+// false when W (hi + lo) cannot stay resident next to 3 x stages or the
+// accumulators do not fit beside the A stages in TMEM
+bool launch_transform_r(const void* x, int64_t rows, int64_t k, int64_t ldx,
+                        const float* w, const float* b, int64_t n, int relu,
+                        void* y, int y_dtype, int64_t ldy, int32_t* flag,
+                        cudaStream_t s) {
+  const int BN = (int)((n + 15) / 16 * 16);
+  if (BN > 128) return false;
+  const int kblocks = (int)((k + BK - 1) / BK);
+  const int w_res = 2 * BN * BK * 4 * kblocks;
+  const int x_stage = BM * BK * 4;
+  const int fixed = 1024 + 8 * 64 + 16 + 4 * 256 + 16 +
+                    kEpiWarps * 32 * kStageLd * 4;
+  int stages = (227 * 1024 - fixed - w_res) / x_stage;
+  if (stages > 8) stages = 8;
+  if (const char* e = getenv("ATLAS_TRANSFORM_STAGES"))  // diagnostics
+    stages = std::min(stages, std::max(3, atoi(e)));
+  if (stages < 3) return false;
+  CUtensorMap mx, mw;
+  if (!make_map(&mx, x, ATLAS_F32, rows, k, ldx, BM) ||
+      !make_map(&mw, w, ATLAS_F32, n, k, k, BN))
+    return false;
+  const int smem = fixed + w_res + stages * x_stage;
+  TcParams p{};
+  p.M = rows;
+  p.K = (int)k;
+  p.N = (int)n;
+  p.BN = BN;
+  p.stages = stages;
+  p.kblocks = kblocks;
+  p.relu = relu;
+  p.ldy = ldy;
+  p.bias = b;
+  p.y = y;
+  p.flag = flag;
+  p.tmem_cols = 512;
+  const int64_t ntiles = (rows + BM - 1) / BM;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, num_sms());
+  auto launch = [&](auto kern) {
+    ATLAS_CUDA(cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kThreads, smem, s>>>(mx, mw, p);
+  };
+  if (y_dtype == ATLAS_F32) launch(transform_r_kernel<float>);
+  else if (y_dtype == ATLAS_F16) launch(transform_r_kernel<__half>);
+  else launch(transform_r_kernel<__nv_bfloat16>);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  return true;
+}
+
+// ATLAS_TRANSFORM_T=1 (A/B probes): the TMEM-resident-W variant; measured
+// slower than W in shared memory on every cfg2 shape
+// (profiles/r2_transform_probe_v1.txt), so it is not the default
 bool transposed_enabled() {
   const char* e = getenv("ATLAS_TRANSFORM_T");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }
 
 bool launch_transform_t(const void* x, int64_t rows, int64_t k, int64_t ldx,
@@ -1113,6 +1411,10 @@ bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
   if (x_dtype == ATLAS_F32 && n <= 128 && k <= 128 && transposed_enabled())
     return launch_transform_t(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
                               flag, s);
+  if (x_dtype == ATLAS_F32 && regsplit_enabled() &&
+      launch_transform_r(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy, flag,
+                         s))
+    return true;
   const int BN = (int)((n + 15) / 16 * 16);
   const int kblocks = (int)((k + BK - 1) / BK);
   if ((reinterpret_cast<uintptr_t>(w) & 15) != 0) return false;

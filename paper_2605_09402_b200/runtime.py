@@ -615,6 +615,20 @@ def _write_output(layer_dir, y, config, grad_order) -> int:
         raise
 
 
+def _read_input(layer_dir, config):
+    """A layer directory on the device: with direct_io (the reference's
+    O_DIRECT reader, oocgnn/directio.py) straight from storage into HBM
+    (GPUDirect Storage, or the library's pinned-bounce stream), otherwise
+    through the pinned host reader and one upload."""
+    if config.direct_io:
+        from .chunks import load_layer_device
+        _, h, nbytes, delivery, _ = load_layer_device(layer_dir,
+                                                      device=config.device)
+        return h, nbytes, delivery
+    _, rows, nbytes, delivery = load_layer_input(layer_dir)
+    return _upload(rows), nbytes, delivery
+
+
 def _upload(rows):
     import torch
 
@@ -636,11 +650,11 @@ def run_layer(topology_path, in_degrees: np.ndarray, input_dir, output_dir,
         raise ConfigError(f"layer {layer_index} expects {expect}-wide rows, "
                           f"input holds {meta.dim}")
     graph, topo_bytes = _load_graph(topology_path, in_degrees)
-    _, rows, feat_bytes, delivery = load_layer_input(input_dir)
+    h, feat_bytes, delivery = _read_input(input_dir, config)
     # the graduation log fixes the output's spill layout
     eng = Engine(graph, weights, replace(config, record_log=True))
     try:
-        y, m, layer = eng.layer(layer_index, _upload(rows))
+        y, m, layer = eng.layer(layer_index, h)
         order = _graduation_order(layer)
         layer.close()
     finally:
@@ -675,13 +689,12 @@ def run_inference(graph_dir, weights, config: PipelineConfig, out_dir,
     graph = GraphCSR(hdr.num_vertices, hdr.num_edges, offsets, nbrs,
                      in_degrees)
     topo_bytes = offsets.nbytes + nbrs.nbytes
-    _, rows, feat_bytes, delivery = load_layer_input(features_dir)
+    h, feat_bytes, delivery = _read_input(features_dir, config)
     # the graduation log fixes each output's spill layout
     eng = Engine(graph, weights, replace(config, record_log=True))
     layers = []
     prev_dir = None
     try:
-        h = _upload(rows)
         for l in range(len(weights.layers)):
             tl = time.perf_counter()
             y, m, layer = eng.layer(l, h)

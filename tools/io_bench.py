@@ -5,7 +5,8 @@
   library's parallel writer vs storage.write_matrix_as_layer (numpy);
 * read: the 100-d f32 feature set of generate_synthetic (4 MiB spills, the
   reference's dataset layout) with the library's parallel reader (into
-  pinned memory) vs a numpy loop over the same files;
+  pinned memory) vs a numpy loop over the same files, and straight into
+  HBM (atlas_spill_read_device) vs host reader + upload;
 * run_inference: dataset directory -> 3 layer directories on disk, both
   transform backends, wall clock (topology + features read, H2D, 3 layers,
   D2H, spill writes).
@@ -63,6 +64,27 @@ def main():
                 S.part_dir(feats_dir, 0))),
             "native_gb_s": nbytes / t_nat / 1e9,
             "numpy_gb_s": nbytes / t_np / 1e9}
+        # straight into HBM (cuFile or the pinned-bounce stream) vs host
+        # reader + one pinned upload
+        import torch
+
+        from paper_2605_09402_b200 import _native as N
+        C.load_layer_device(feats_dir)
+        (_, dev, _, _, gds), t_dev = timed(
+            lambda: C.load_layer_device(feats_dir))
+        assert np.array_equal(dev.cpu().numpy(), rows)
+
+        def host_then_upload():
+            _, r, _, _ = C.load_layer_input(feats_dir)
+            t = torch.from_numpy(r).cuda(non_blocking=True)
+            torch.cuda.synchronize()
+            return t
+        _, t_hu = timed(host_then_upload)
+        out["read_features_to_hbm"] = {
+            "path": "cuFile" if gds else
+            N.load_library().atlas_gds_status().decode(),
+            "device_reader_gb_s": nbytes / t_dev / 1e9,
+            "host_reader_plus_upload_gb_s": nbytes / t_hu / 1e9}
         # write
         m = np.random.default_rng(0).uniform(-1, 1, (2_400_000, 128)).astype(
             np.float32)

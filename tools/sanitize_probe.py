@@ -6,8 +6,9 @@ racecheck, synccheck, initcheck) over every kernel family of the library:
   path with ATLAS_ENGINE_GRID_MIN=1 by the caller if wanted);
 * the bit-exact ring aggregation kernels (agg_ring / agg_sub_ring /
   agg_bulk) and the stable transform;
-* the tcgen05 transform (3xTF32 and f16 hi/lo) and transform-first fused
-  passes;
+* the sweep replay (csrc/sweep.cu) and the bounded-record blocked pass;
+* the tcgen05 transform (3xTF32 register split and f16 hi/lo) and
+  transform-first fused passes;
 * the streamed K1 path (suffix ring + agg_tile), the operator (per-chunk)
   path, GAT pass A/B.
 
@@ -63,6 +64,14 @@ def run_case(case):
                                   stream_tile_bytes=16 << 10))
     y, _ = eng.infer(torch.as_tensor(feats).pin_memory())
     assert digest_array(y.cpu().numpy()) == entry["layers"][-1]["output_sha"]
+    eng.close()
+    # sweep replay (no logs, exact control plane forced) + bounded records
+    eng = Engine(graph, w, config(entry, backend="stable", force_exact=True,
+                                  bound_records=True))
+    y, metrics = eng.infer(torch.as_tensor(feats).cuda())
+    assert digest_array(y.cpu().numpy()) == entry["layers"][-1]["output_sha"]
+    assert [m.reloads for m in metrics] == \
+        [g["reloads"] for g in entry["layers"]]
     eng.close()
     # tcgen05 backend (transform-first where it narrows)
     eng = Engine(graph, w, config(entry, backend="tcgen05"))

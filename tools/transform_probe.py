@@ -1,6 +1,8 @@
 """Transform kernel probe: device time of the tcgen05 transform on
-cfg2-sized shapes for each kernel variant (ATLAS_TRANSFORM_T=0: W in
-shared memory; 1: W in TMEM, transposed product) and output dtype.
+cfg2-sized shapes for each kernel variant: "smem" = x hi/lo in shared
+memory stages (ATLAS_TRANSFORM_R=0), "tmemW" = W in TMEM with the
+transposed product (ATLAS_TRANSFORM_T=1), "regsplit" = x split in registers
+into TMEM A stages (the default), and output dtype.
 Usage: transform_probe.py [rows]"""
 
 import os
@@ -25,8 +27,12 @@ def main():
         for odt in (torch.float32, torch.float16):
             y = torch.empty(rows, n, dtype=odt, device="cuda")
             res = []
-            for t in ("0", "1"):
-                os.environ["ATLAS_TRANSFORM_T"] = t
+            for t, env in (("smem", {"ATLAS_TRANSFORM_R": "0"}),
+                           ("tmemW", {"ATLAS_TRANSFORM_T": "1"}),
+                           ("regsplit", {})):
+                for key in ("ATLAS_TRANSFORM_R", "ATLAS_TRANSFORM_T"):
+                    os.environ.pop(key, None)
+                os.environ.update(env)
                 for _ in range(3):
                     transform_typed(x, w, b, True, y, 1)
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -37,13 +43,13 @@ def main():
                 torch.cuda.synchronize()
                 ms = ev[0].elapsed_time(ev[1]) / 10
                 byts = rows * (k * 4 + n * y.element_size())
-                res.append(f"T={t} {ms:.3f} ms {byts / ms / 1e6:.0f} GB/s "
+                res.append(f"{t} {ms:.3f} ms {byts / ms / 1e6:.0f} GB/s "
                            f"({byts / ms / 1e6 / PEAK:.2f})")
-                if t == "0":
+                if t == "smem":
                     y0 = y.float().clone()
-            err = (y.float() - y0).abs().max().item()
-            print(f"k={k} n={n} out={odt}: " + " | ".join(res) +
-                  f" | max|T1-T0| {err:.2e}", flush=True)
+                else:
+                    res[-1] += f" d={(y.float() - y0).abs().max().item():.1e}"
+            print(f"k={k} n={n} out={odt}: " + " | ".join(res), flush=True)
 
 
 if __name__ == "__main__":
