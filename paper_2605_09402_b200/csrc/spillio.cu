@@ -372,6 +372,42 @@ struct Bounce {
   }
 };
 
+// pinned bounce buffers are kept between calls (a cudaMallocHost per
+// call and thread cost more than the reads of a small layer directory)
+struct BounceLease {
+  int dev;
+  Bounce* b = nullptr;
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::vector<std::pair<int, Bounce*>>& pool() {
+    static std::vector<std::pair<int, Bounce*>> p;  // process lifetime
+    return p;
+  }
+  explicit BounceLease(int d) : dev(d) {}
+  Bounce* get() {
+    if (b) return b;
+    {
+      std::lock_guard<std::mutex> lock(mu());
+      auto& p = pool();
+      for (size_t i = 0; i < p.size(); i++)
+        if (p[i].first == dev) {
+          b = p[i].second;
+          p.erase(p.begin() + i);
+          break;
+        }
+    }
+    if (!b) b = new Bounce();
+    return b;
+  }
+  ~BounceLease() {
+    if (!b) return;
+    std::lock_guard<std::mutex> lock(mu());
+    pool().emplace_back(dev, b);
+  }
+};
+
 }  // namespace
 }  // namespace atlas
 
@@ -459,7 +495,7 @@ int atlas_spill_read_device(const char* const* paths, int32_t n_files,
     auto worker = [&] {
       try {
         if (!validate_only) cudaSetDevice(dev);
-        std::unique_ptr<Bounce> bounce;
+        BounceLease bounce(dev);
         for (int64_t i; (i = next.fetch_add(1)) < nf;) {
           CUfileHandle_t fh = nullptr;
           bool reg = false;
@@ -488,14 +524,13 @@ int atlas_spill_read_device(const char* const* paths, int32_t n_files,
               }
               return true;
             }
-            if (!bounce) bounce.reset(new Bounce());
-            return bounce->move(fd, out + id * row_b, n, off);
+            return bounce.get()->move(fd, out + id * row_b, n, off);
           };
           read_one(paths[i], dtype, dim, num_vertices, sink, delivery.data(),
                    &bytes, &err);
           if (reg) cf.handle_deregister(fh);
         }
-        if (bounce) ATLAS_CUDA(cudaStreamSynchronize(bounce->stream));
+        if (bounce.b) ATLAS_CUDA(cudaStreamSynchronize(bounce.b->stream));
       } catch (const Error& e) {
         err.set(e.code, e.msg);
       }

@@ -44,7 +44,7 @@
 namespace atlas {
 namespace {
 
-constexpr int kSwThreads = 512;
+constexpr int kSwThreads = 1024;
 constexpr int kSwBlock = 2048;   // sub-batches staged in shared memory
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
@@ -287,11 +287,16 @@ struct SweepArgs {
   const uint32_t* ent_next;  // [n + 4]
   uint32_t* victims;         // popped entries, in pop order
   int64_t* out;              // evictions, reloads, hot_peak, nvict, err, info
+  int32_t diag_no_far;       // diagnostics only: skip far reload atomics
 };
 
 // The walk reads each bucket list through register windows of kSwWin
-// entries (16 per thread), the list's next window already in flight in a
-// second register set while the current one is scanned. Per-bucket
+// entries (8 per thread, four 16-B loads in flight per thread). Measured
+// and dropped: 512 threads x 16 entries with the next window prefetched in
+// registers (1.5x slower), an L2 bulk prefetch of the next windows and
+// shared-memory window buffers filled by bulk copies (no gain / slower):
+// the walk is bound by per-entry work and the victims' reload-count
+// atomics, not by the window loads. Per-bucket
 // state lives in shared memory for the first kSwCache buckets: the head,
 // the list end and the sub-batch of the entry at the head when known
 // (head_sub). A list whose head entry is not delivered yet (head_sub >= s)
@@ -299,7 +304,7 @@ struct SweepArgs {
 // most of an event's lists are in that state (their live entries were
 // popped or superseded), and reading their head windows anyway was what
 // the walk spent its time on.
-constexpr int kSwPerT = 16;
+constexpr int kSwPerT = 8;
 constexpr int kSwWin = kSwThreads * kSwPerT;
 constexpr int kSwCache = 4096;
 constexpr uint32_t kUnknown = 0;  // head_sub not known: read the list
@@ -323,9 +328,6 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
   __shared__ typename Scan::TempStorage scan;
   const int tid = threadIdx.x;
   const int ncache = A.nb < kSwCache ? A.nb : kSwCache;
-  uint32_t pf_sub[kSwPerT], pf_nxt[kSwPerT];  // next-window prefetch
-  int pf_b = -1;
-  uint32_t pf_start = kNone;
   for (int b = tid; b < ncache; b += kSwThreads) {
     sm.head[b] = A.boff[b];
     sm.end[b] = A.boff[b + 1];
@@ -432,51 +434,17 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
         }
         const uint32_t w0 = h & ~3u;
         const uint32_t j0 = w0 + (uint32_t)tid * kSwPerT;
-        // this window: from the register prefetch when it holds exactly
-        // this (list, start), else loaded now; then the list's next window
-        // is put in flight into the prefetch registers, to be waited on by
-        // the next iteration (the lists are static, so a prefetch stays
-        // valid across events)
         uint32_t subs[kSwPerT], nxts[kSwPerT];
-        if (pf_b == b && pf_start == w0) {
 #pragma unroll
-          for (int q = 0; q < kSwPerT; q++) {
-            subs[q] = pf_sub[q];
-            nxts[q] = pf_nxt[q];
+        for (int q = 0; q < kSwPerT; q += 4) {
+          uint4 a4 = make_uint4(kNone, kNone, kNone, kNone);
+          uint4 n4 = make_uint4(0, 0, 0, 0);
+          if (j0 + q < e_end) {
+            a4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_sub + j0 + q));
+            n4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_next + j0 + q));
           }
-        } else {
-#pragma unroll
-          for (int q = 0; q < kSwPerT; q += 4) {
-            uint4 a4 = make_uint4(kNone, kNone, kNone, kNone);
-            uint4 n4 = make_uint4(0, 0, 0, 0);
-            if (j0 + q < e_end) {
-              a4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_sub + j0 + q));
-              n4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_next + j0 + q));
-            }
-            subs[q] = a4.x; subs[q + 1] = a4.y; subs[q + 2] = a4.z; subs[q + 3] = a4.w;
-            nxts[q] = n4.x; nxts[q + 1] = n4.y; nxts[q + 2] = n4.z; nxts[q + 3] = n4.w;
-          }
-        }
-        {
-          const uint32_t p0 = w0 + (uint32_t)kSwWin;
-          if (p0 < e_end) {
-            const uint32_t pj = p0 + (uint32_t)tid * kSwPerT;
-#pragma unroll
-            for (int q = 0; q < kSwPerT; q += 4) {
-              uint4 a4 = make_uint4(kNone, kNone, kNone, kNone);
-              uint4 n4 = make_uint4(0, 0, 0, 0);
-              if (pj + q < e_end) {
-                a4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_sub + pj + q));
-                n4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_next + pj + q));
-              }
-              pf_sub[q] = a4.x; pf_sub[q + 1] = a4.y; pf_sub[q + 2] = a4.z; pf_sub[q + 3] = a4.w;
-              pf_nxt[q] = n4.x; pf_nxt[q + 1] = n4.y; pf_nxt[q + 2] = n4.z; pf_nxt[q + 3] = n4.w;
-            }
-            pf_b = b;
-            pf_start = p0;
-          } else {
-            pf_b = -1;
-          }
+          subs[q] = a4.x; subs[q + 1] = a4.y; subs[q + 2] = a4.z; subs[q + 3] = a4.w;
+          nxts[q] = n4.x; nxts[q + 1] = n4.y; nxts[q + 2] = n4.z; nxts[q + 3] = n4.w;
         }
         int valid = 0, nvalid = 0;
         uint32_t first_na = kNone;
@@ -519,7 +487,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
           }
           if (run_c) {
             if ((int64_t)run_nx < win_hi) atomicAdd(&sm.cold[run_nx - base], run_c);
-            else atomicAdd(A.cold + run_nx, run_c);
+            else if (!A.diag_no_far) atomicAdd(A.cold + run_nx, run_c);
           }
           run_nx = nx;
           run_c = 1;
@@ -537,12 +505,19 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
           int wbase = 0;
           if ((tid & 31) == 31 && incl) wbase = atomicAdd(&sm.wlog[w & 1], incl);
           wbase = __shfl_sync(0xffffffffu, wbase, 31);
-          int pos = wbase + incl - nvalid;
+          // slot e of every lane in one round: consecutive lanes write
+          // consecutive log slots (coalesced)
+          const unsigned lt = (1u << (tid & 31)) - 1u;
+          int run = 0;
 #pragma unroll
           for (int e = 0; e < kSwPerT; e++) {
-            if (!(valid >> e & 1)) continue;
-            A.victims[nv + pos++] = j0 + e;
-            cold_add(nxts[e]);
+            const bool v = valid >> e & 1;
+            const unsigned m = __ballot_sync(0xffffffffu, v);
+            if (v) {
+              A.victims[nv + wbase + run + __popc(m & lt)] = j0 + e;
+              cold_add(nxts[e]);
+            }
+            run += __popc(m);
           }
           if (fna != kNone && fna >= j0 && fna < j0 + kSwPerT)
             sm.hs_new = subs[fna - j0];
@@ -959,6 +934,10 @@ static bool run_sweep(atlas_layer* L, SweepWs& W, PhaseTimer& T,
   A.ent_next = W.ent_next.ptr;
   A.victims = W.victims.ptr;
   A.out = W.out.ptr;
+  {
+    const char* e = getenv("ATLAS_SWEEP_DIAG_NO_FAR");  // wrong results!
+    A.diag_no_far = e && e[0] == '1';
+  }
   const int smem = (int)sizeof(SweepSm);
   static bool attr = false;
   if (!attr) {

@@ -172,7 +172,7 @@ template <typename OutT>
 __device__ __forceinline__ void epilogue_loop(
     const TcParams& p, int ew, int warp, int lane, int64_t ntiles,
     uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
-    const float* sbias, const float* sscale, float* stage_out) {
+    const float* sbias, const float* sscale, float* stage_out, int sub = 1) {
   const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
   const int cpar = ew >> 2;      // which 16-col blocks this warp takes
   float* stage = stage_out + ew * 32 * kStageLd;
@@ -183,13 +183,15 @@ __device__ __forceinline__ void epilogue_loop(
   const bool vec_ok = (p.ldy % 4) == 0 &&
                       (reinterpret_cast<uintptr_t>(p.y) % (4 * sizeof(OutT))) == 0;
   int bad = 0;
+  // a tile is `sub` 128-row halves (sub accumulators of BN columns each)
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     mbar_wait(&tfull[acc], aph[acc]);
     aph[acc] ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int64_t row0 = t * BM + quarter * 32;
+    for (int u = 0; u < sub; u++) {
+    const int64_t row0 = (t * sub + u) * BM + quarter * 32;
     const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
-                           (uint32_t)(acc * p.BN);
+                           (uint32_t)((acc * sub + u) * p.BN);
     for (int c0 = cpar * 16; c0 < p.BN; c0 += 32) {
       float v[16];
       tmem_ld16(taddr + c0, v);
@@ -232,6 +234,7 @@ __device__ __forceinline__ void epilogue_loop(
       }
       __syncwarp();
     }
+    }  // halves
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     mbar_arrive(&tempty[acc]);
     acc ^= 1;
@@ -522,7 +525,10 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc,
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-template <typename OutT>
+// SUB = 2: 256-row tiles, two M=128 MMAs per k-step sharing one W stage,
+// so each W byte fetched from L2 serves twice the rows (BN <= 128: two
+// double-buffered accumulator pairs fill the 512 TMEM columns)
+template <typename OutT, int SUB>
 __global__ void __launch_bounds__(kThreadsH, 1)
     transform_h_kernel(const __grid_constant__ CUtensorMap map_x,
                        const __grid_constant__ CUtensorMap map_whi,
@@ -530,9 +536,9 @@ __global__ void __launch_bounds__(kThreadsH, 1)
                        TcParams p, const float* __restrict__ wscale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const uint32_t x_bytes = BM * BKH * 2;
+  const uint32_t x_bytes = BM * BKH * 2;  // one 128-row half
   const uint32_t w_bytes = p.BN * BKH * 2;
-  const uint32_t stage_bytes = x_bytes + 2 * w_bytes;
+  const uint32_t stage_bytes = SUB * x_bytes + 2 * w_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(base + p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;  // [2]
@@ -543,7 +549,7 @@ __global__ void __launch_bounds__(kThreadsH, 1)
   float* stage_out = reinterpret_cast<float*>(
       (reinterpret_cast<uintptr_t>(sscale + 256) + 15) & ~uintptr_t(15));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t ntiles = (p.M + BM - 1) / BM;
+  const int64_t ntiles = (p.M + BM * SUB - 1) / (BM * SUB);
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; s++) {
       mbar_init(&full[s], 1);
@@ -581,9 +587,12 @@ __global__ void __launch_bounds__(kThreadsH, 1)
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = base + s * stage_bytes;
           mbar_expect_tx(&full[s], stage_bytes);
-          tma_load_2d(st, &map_x, &full[s], kb * BKH, (int)(t * BM));
-          tma_load_2d(st + x_bytes, &map_whi, &full[s], kb * BKH, 0);
-          tma_load_2d(st + x_bytes + w_bytes, &map_wlo, &full[s], kb * BKH, 0);
+          for (int u = 0; u < SUB; u++)
+            tma_load_2d(st + u * x_bytes, &map_x, &full[s], kb * BKH,
+                        (int)((t * SUB + u) * BM));
+          tma_load_2d(st + SUB * x_bytes, &map_whi, &full[s], kb * BKH, 0);
+          tma_load_2d(st + SUB * x_bytes + w_bytes, &map_wlo, &full[s],
+                      kb * BKH, 0);
           if (++s == p.stages) {
             s = 0;
             ph ^= 1;
@@ -605,22 +614,27 @@ __global__ void __launch_bounds__(kThreadsH, 1)
       mbar_wait(&tempty[acc], aph[acc] ^ 1);
       aph[acc] ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t dt = tmem_base + (uint32_t)(acc * p.BN);
+      const uint32_t dt = tmem_base + (uint32_t)(acc * SUB * p.BN);
       for (int kb = 0; kb < p.kblocks; kb++) {
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
           uint8_t* st = base + s * stage_bytes;
-          const uint32_t a = smem_u32(st);
-          const uint32_t bh = smem_u32(st + x_bytes);
-          const uint32_t bl = smem_u32(st + x_bytes + w_bytes);
+          const uint32_t bh = smem_u32(st + SUB * x_bytes);
+          const uint32_t bl = smem_u32(st + SUB * x_bytes + w_bytes);
 #pragma unroll
           for (int k = 0; k < BKH / 16; k++) {  // UMMA_K = 16 f16 = 32 B
             const uint32_t off = k * 32;
             const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
-            mma_f16(dt, sw128_desc(a + off), sw128_desc(bl + off), idesc,
-                    first);
-            mma_f16(dt, sw128_desc(a + off), sw128_desc(bh + off), idesc, 1u);
+#pragma unroll
+            for (int u = 0; u < SUB; u++) {
+              const uint32_t a = smem_u32(st + u * x_bytes);
+              const uint32_t d = dt + (uint32_t)(u * p.BN);
+              mma_f16(d, sw128_desc(a + off), sw128_desc(bl + off), idesc,
+                      first);
+              mma_f16(d, sw128_desc(a + off), sw128_desc(bh + off), idesc,
+                      1u);
+            }
           }
           mma_commit(&empty[s]);
           if (kb == p.kblocks - 1) mma_commit(&tfull[acc]);
@@ -635,7 +649,7 @@ __global__ void __launch_bounds__(kThreadsH, 1)
     }
   } else {
     epilogue_loop<OutT>(p, warp - 2, warp, lane, ntiles, tmem_base, tfull,
-                        tempty, sbias, sscale, stage_out);
+                        tempty, sbias, sscale, stage_out, SUB);
   }
   __syncthreads();
   if (warp == 1) {
@@ -1236,7 +1250,10 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
     return false;
   const int BN = (int)((n + 15) / 16 * 16);
   const int kblocks = (int)((k + BKH - 1) / BKH);
-  const int stage_bytes = BM * BKH * 2 + 2 * BN * BKH * 2;
+  // 256-row tiles (two halves per W stage) unless ATLAS_TRANSFORM_H_SUB=1
+  const char* sub_env = getenv("ATLAS_TRANSFORM_H_SUB");
+  const int sub = (BN <= 128 && !(sub_env && sub_env[0] == '1')) ? 2 : 1;
+  const int stage_bytes = sub * BM * BKH * 2 + 2 * BN * BKH * 2;
   const int fixed = 1024 + 8 * 16 + 16 + 2 * 4 * 256 + 16 +
                     kEpiWarps * 32 * kStageLd * 4;
   int stages = (227 * 1024 - fixed) / stage_bytes;
@@ -1272,18 +1289,23 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
     p.y = y;
     p.flag = flag;
     uint32_t cols = 32;
-    while (cols < (uint32_t)(2 * BN)) cols <<= 1;
+    while (cols < (uint32_t)(2 * sub * BN)) cols <<= 1;
     p.tmem_cols = cols;
-    const int64_t ntiles = (rows + BM - 1) / BM;
+    const int64_t ntiles = (rows + BM * sub - 1) / (BM * sub);
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, num_sms());
     auto launch = [&](auto kern) {
       ATLAS_CUDA(cudaFuncSetAttribute(
           kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       kern<<<grid, kThreadsH, smem, s>>>(mx, mhi, mlo, p, wsc);
     };
-    if (y_dtype == ATLAS_F32) launch(transform_h_kernel<float>);
-    else if (y_dtype == ATLAS_F16) launch(transform_h_kernel<__half>);
-    else launch(transform_h_kernel<__nv_bfloat16>);
+    auto by_out = [&](auto sub_tag) {
+      constexpr int S = decltype(sub_tag)::value;
+      if (y_dtype == ATLAS_F32) launch(transform_h_kernel<float, S>);
+      else if (y_dtype == ATLAS_F16) launch(transform_h_kernel<__half, S>);
+      else launch(transform_h_kernel<__nv_bfloat16, S>);
+    };
+    if (sub == 2) by_out(std::integral_constant<int, 2>());
+    else by_out(std::integral_constant<int, 1>());
     count_launch();
     ATLAS_LAUNCH_CHECK();
   }

@@ -492,3 +492,26 @@ def test_degenerate_graphs_match_oracle(backend, kind, shape):
             assert getattr(metrics[l], f) == getattr(m, f), (l, f)
         h = want
     eng.close()
+
+
+@pytest.mark.parametrize("m,k,n,relu", [(300000, 1024, 128, True),
+                                        (5000, 1024, 19, False),
+                                        (70000, 128, 128, True),
+                                        (1000, 64, 200, False)])
+def test_tcgen05_f16_input_transform_accuracy(m, k, n, relu):
+    """f16 inputs on kind::f16 (256-row tiles when N <= 128, 128-row tiles
+    above): |y - y_f64| <= 4e-6 * (|x| |w| + 1e-3), the 3xTF32 bar."""
+    from paper_2605_09402_b200.engine import transform_typed
+    g = torch.Generator(device="cuda").manual_seed(m + k + n)
+    x = (torch.rand((m, k), device="cuda", generator=g) * 2 - 1).half()
+    w = (torch.rand((n, k), device="cuda", generator=g) * 2 - 1) / k ** 0.5
+    b = (torch.rand(n, device="cuda", generator=g) - 0.5) * 0.2
+    y = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    transform_typed(x, w, b, relu, y, N.BACKEND_TCGEN05)
+    ref = x.double() @ w.double().T + b.double()
+    if relu:
+        ref = ref.clamp_min(0.0)
+    scale = x.double().abs() @ w.double().abs().T
+    err = (y.double() - ref).abs()
+    assert bool((err <= 4e-6 * (scale + 1e-3)).all()), \
+        float((err / (scale + 1e-3)).max())

@@ -52,5 +52,36 @@ def main():
             print(f"k={k} n={n} out={odt}: " + " | ".join(res), flush=True)
 
 
+def f16_inputs(rows):
+    """transform_h (f16 x, kind::f16): 128-row vs 256-row tiles."""
+    for k, n in [(1024, 128), (1024, 19), (1024, 136)]:
+        x = torch.randn(rows, k, device="cuda").half()
+        w = torch.randn(n, k, device="cuda") / k ** 0.5
+        b = torch.randn(n, device="cuda")
+        y = torch.empty(rows, n, device="cuda")
+        res = []
+        for sub in ("1", "2"):
+            os.environ["ATLAS_TRANSFORM_H_SUB"] = sub
+            for _ in range(3):
+                transform_typed(x, w, b, True, y, 1)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
+            for _ in range(10):
+                transform_typed(x, w, b, True, y, 1)
+            ev[1].record()
+            torch.cuda.synchronize()
+            ms = ev[0].elapsed_time(ev[1]) / 10
+            byts = rows * (k * 2 + n * 4)
+            res.append(f"sub={sub} {ms:.3f} ms {byts / ms / 1e6:.0f} GB/s "
+                       f"({byts / ms / 1e6 / PEAK:.2f})")
+            if sub == "1":
+                y1 = y.clone()
+            else:
+                res[-1] += f" d={(y - y1).abs().max().item():.1e}"
+        os.environ.pop("ATLAS_TRANSFORM_H_SUB", None)
+        print(f"f16 x k={k} n={n}: " + " | ".join(res), flush=True)
+
+
 if __name__ == "__main__":
     main()
+    f16_inputs(int(sys.argv[2]) if len(sys.argv) > 2 else 3_000_000)
