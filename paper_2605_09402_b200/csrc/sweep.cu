@@ -291,12 +291,13 @@ struct SweepArgs {
 };
 
 // The walk reads each bucket list through register windows of kSwWin
-// entries (8 per thread, four 16-B loads in flight per thread). Measured
-// and dropped: 512 threads x 16 entries with the next window prefetched in
-// registers (1.5x slower), an L2 bulk prefetch of the next windows and
-// shared-memory window buffers filled by bulk copies (no gain / slower):
-// the walk is bound by per-entry work and the victims' reload-count
-// atomics, not by the window loads. Per-bucket
+// entries (8 per thread, four 16-B loads in flight per thread); victims go
+// to the log in coalesced rounds (lane-consecutive slots). Measured and
+// dropped (profiles/r2_sweep_variants.txt): 512 threads x 16 entries with
+// the next window prefetched in registers (1.5x slower), an L2 bulk
+// prefetch of the next windows and shared-memory window buffers filled by
+// bulk copies (no gain / slower), warp match-aggregated reload atomics
+// (1.7x slower). Per-bucket
 // state lives in shared memory for the first kSwCache buckets: the head,
 // the list end and the sub-batch of the entry at the head when known
 // (head_sub). A list whose head entry is not delivered yet (head_sub >= s)
@@ -486,12 +487,16 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
             return;
           }
           if (run_c) {
-            if ((int64_t)run_nx < win_hi) atomicAdd(&sm.cold[run_nx - base], run_c);
-            else if (!A.diag_no_far) atomicAdd(A.cold + run_nx, run_c);
+            if ((int64_t)run_nx < win_hi) {
+              if (A.diag_no_far < 2) atomicAdd(&sm.cold[run_nx - base], run_c);
+            } else if (!A.diag_no_far) {
+              atomicAdd(A.cold + run_nx, run_c);
+            }
           }
           run_nx = nx;
           run_c = 1;
         };
+
         if (total <= rem) {
           // the whole window's valid entries are victims: order within the
           // event is irrelevant here (no logs), so log slots come from one
@@ -936,7 +941,7 @@ static bool run_sweep(atlas_layer* L, SweepWs& W, PhaseTimer& T,
   A.out = W.out.ptr;
   {
     const char* e = getenv("ATLAS_SWEEP_DIAG_NO_FAR");  // wrong results!
-    A.diag_no_far = e && e[0] == '1';
+    A.diag_no_far = e ? atoi(e) : 0;  // 1: no far atomics, 2: none
   }
   const int smem = (int)sizeof(SweepSm);
   static bool attr = false;
