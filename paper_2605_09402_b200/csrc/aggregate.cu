@@ -1262,7 +1262,10 @@ void runs_typed(const void* tile, int64_t ldx, const uint32_t* run_dst,
 // Occupancy: 5 blocks/SM caps registers at 51; ptxas -v reports 42 and no
 // spills for VEC=4 (the 64-register note on kSubBlocks is for
 // agg_sub_ring's lockstep sub-groups, not this kernel).
-template <int VEC>
+// MODEL = ATLAS_SAGE: the neighbour half is the same mean; the self half
+// (columns [d, 2d) of the record) is the destination's own row, copied when
+// that row is in the tile (agg_tile's SAGE rule).
+template <int VEC, int MODEL>
 __global__ void __launch_bounds__(256, kSubBlocks + 1)
     agg_suffix_ring(const float* __restrict__ tile, int64_t ldx,
                     int64_t tile_lo, int64_t tile_hi, int64_t V,
@@ -1351,8 +1354,11 @@ __global__ void __launch_bounds__(256, kSubBlocks + 1)
       const int64_t v = (int64_t)v0 + j;
       const int nj = __shfl_sync(0xffffffffu, n_j, j);
       const uint32_t dg = __shfl_sync(0xffffffffu, dg_j, j);
-      const bool zero_row = dg == 0 && v + lo >= tile_lo && v + lo < tile_hi;
-      if (nj == 0 && !zero_row) continue;
+      const bool own = v + lo >= tile_lo && v + lo < tile_hi;
+      // GCN: a zero in-degree destination owes a zero record once (in its
+      // own row's tile); SAGE: the own row's tile writes the self half
+      const bool must = MODEL == ATLAS_SAGE ? own : (own && dg == 0);
+      if (nj == 0 && !must) continue;
       const float denom = (float)max(1u, dg);
       const float rcp = __frcp_rn(denom);
       float a[VEC];
@@ -1368,7 +1374,14 @@ __global__ void __launch_bounds__(256, kSubBlocks + 1)
         add_msg<float, VEC, true>(a, f, false, denom, rcp, 1.0f);
         issue();
       }
-      if (active) store_f32<VEC>(out + col, a);
+      if (active) {
+        store_f32<VEC>(out + col, a);
+        if (MODEL == ATLAS_SAGE && own) {
+          float me[VEC];
+          load_f32<VEC>(tile + (v + lo - tile_lo) * ldx + col, me);
+          store_f32<VEC>(out + d + col, me);
+        }
+      }
       if (lane == 0) touched[v] = 1;
     }
     cp_async_wait<0>();
@@ -1436,7 +1449,8 @@ bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
                        const atlas_graph* g, int model, int d, float* acc,
                        int64_t ldacc, int64_t* cursor, uint8_t* touched,
                        cudaStream_t s) {
-  if (model != ATLAS_GCN || dtype != ATLAS_F32 || d % 4 != 0 || d > 128 ||
+  if ((model != ATLAS_GCN && model != ATLAS_SAGE) || dtype != ATLAS_F32 ||
+      d % 4 != 0 || d > 128 ||
       ldx % 4 != 0 || ldacc % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(tile) & 15) != 0)
     return false;
@@ -1444,7 +1458,8 @@ bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
   g->work.reserve(1);
   ATLAS_CUDA(cudaMemsetAsync(g->work.ptr, 0, sizeof(unsigned long long), s));
   const int smem = 8 * kSubRing * 32 * 16;
-  auto kern = agg_suffix_ring<4>;
+  auto kern = model == ATLAS_SAGE ? agg_suffix_ring<4, ATLAS_SAGE>
+                                   : agg_suffix_ring<4, ATLAS_GCN>;
   ATLAS_CUDA(cudaFuncSetAttribute(
       kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<num_sms() * (kSubBlocks + 1), 256, smem, s>>>(

@@ -46,6 +46,7 @@ static void load_graph(atlas_graph* g, int64_t V, int64_t E,
   g->generation++;
   g->V = V;
   g->E = E;
+  g->offsets_host.assign(offsets_host, offsets_host + V + 1);
   g->offsets.reserve(V + 1);
   ATLAS_CUDA(cudaMemcpyAsync(g->offsets.ptr, offsets_host,
                              (V + 1) * sizeof(int64_t),
@@ -757,9 +758,12 @@ int atlas_transform(int32_t backend, const float* x, int64_t rows, int64_t k,
       launch_transform_stable(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
                               flag, s);
     } else if (backend == ATLAS_BACKEND_TCGEN05) {
+      // rows the TMA cannot address (pitch not a multiple of 16 B, e.g. a
+      // 6-wide record) or N > 256 run on the SIMT kernel, which is exact
       if (!launch_transform_tc(x, ATLAS_F32, rows, k, ldx, w, b, n, relu, y,
                                y_dtype, ldy, flag, s))
-        fail(ATLAS_ECONFIG, "tcgen05 backend does not support this shape");
+        launch_transform_stable(x, rows, k, ldx, w, b, n, relu, y, y_dtype,
+                                ldy, flag, s);
     } else {
       fail(ATLAS_ECONFIG, "unknown transform backend");
     }

@@ -391,6 +391,19 @@ static int64_t max_pass_of(atlas_layer* L, const atlas_graph* g, const Plan& p,
   for (const auto& e : g->maxpass_cache)
     if (e.first == p.R * 4 + L->desc.model) return e.second;
   const int64_t nchunks = p.nchunks;
+  if ((int64_t)g->offsets_host.size() == p.V + 1) {
+    // from the host copy of the offsets: no device round trip, so queueing
+    // a layer never waits for the layers queued before it
+    const int64_t* off = g->offsets_host.data();
+    int64_t max_pass = 0;
+    for (int64_t c = 0; c < nchunks; c++) {
+      const int64_t a = c * p.R, b = std::min((c + 1) * p.R, p.V);
+      max_pass = std::max(max_pass, off[b] - off[a] +
+                                        (L->desc.model == ATLAS_GIN ? b - a : 0));
+    }
+    g->maxpass_cache.emplace_back(p.R * 4 + L->desc.model, max_pass);
+    return max_pass;
+  }
   DevBuf<int64_t>& mc = L->span_buf;  // reused scratch (>= nchunks)
   mc.reserve(std::max<int64_t>(nchunks, 1));
   chunk_edges<<<grid_of(nchunks), 256, 0, s>>>(g->offsets.ptr, p, mc.ptr);

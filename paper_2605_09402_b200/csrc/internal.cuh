@@ -28,6 +28,7 @@ struct atlas_graph {
   mutable const int32_t* known_flag = nullptr;  // producer-supplied flag
   // (R * 4 + model) -> largest chunk pass; cleared by atlas_graph_update
   mutable std::vector<std::pair<int64_t, int64_t>> maxpass_cache;
+  std::vector<int64_t> offsets_host;  // host copy of the CSR offsets
   // CSC build workspaces (kept for atlas_graph_update)
   atlas::DevBuf<uint32_t> ws_nbrs, ws_src, ws_keys, ws_vals, ws_keys_out,
       ws_sel;
@@ -132,7 +133,7 @@ struct SweepWs {
   DevBuf<uint32_t> zr, tmp_u32, el_v, el_cnt, el_sub, el_newp, el_nsub, iota,
       sv, se, ent_sub, ent_next, boff, head, fresh, grad, cold, cold_out,
       victims, flags;
-  DevBuf<uint8_t> el_fresh, cub_tmp;
+  DevBuf<uint8_t> el_fresh, cub_tmp, coop;
   DevBuf<unsigned long long> cs, P, lastP, count;
   DevBuf<int64_t> eoff, soff, chunk64, out;
   // run materialisation (control.cu exact_replay)

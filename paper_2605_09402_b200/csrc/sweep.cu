@@ -615,6 +615,432 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
   }
 }
 
+// ---- the sweep on a cooperative grid (sweep_coop_kernel) ----------------
+// Same machine; an event's walk over a list is split into rounds of up to
+// G consecutive 8192-entry windows, one per CTA. Round = two grid jobs that
+// CTA 0 posts through CoopSync: SCAN (every CTA counts the valid entries of
+// its window and finds its first undelivered one) and, after CTA 0 turned
+// the counts into the cut, COMMIT (windows before the cut take all their
+// valid entries, the cut window takes the first rem_cut in list order;
+// victims go to the log at their window's prefix offset, reload counts to
+// the global counters). The window contents stay in registers between the
+// two jobs. CTA 0 refreshes its staged reload counts after each event.
+constexpr int kCoopMax = 64;
+
+struct CoopSync {
+  unsigned job, done;
+  int32_t type;  // 1 scan, 2 commit, 3 exit
+  uint32_t h, end, s, w0;
+  int32_t nwin, cut;
+  int64_t rem_cut, nv;
+  uint32_t cnt[kCoopMax];
+  uint32_t fna[kCoopMax];
+  uint32_t fna_sub[kCoopMax];
+  int64_t off[kCoopMax];
+  uint32_t last_taken, hs_new;
+};
+
+__device__ __forceinline__ unsigned vld(const unsigned* p) {
+  return *reinterpret_cast<const volatile unsigned*>(p);
+}
+
+// one CTA's part of a round: window i of the posted range. The window's
+// entries, valid mask and first undelivered entry persist in the caller's
+// registers (`subs`, `nxts`, `valid`) from SCAN to COMMIT.
+struct CoopWin {
+  uint32_t subs[kSwPerT], nxts[kSwPerT];
+  int valid, nvalid;
+  uint32_t j0;
+};
+
+__device__ void coop_scan(const SweepArgs& A, CoopSync* C, int i, CoopWin& W,
+                          uint32_t* red) {
+  const int tid = threadIdx.x;
+  const uint32_t h = vld(&C->h), end = vld(&C->end), s = vld(&C->s);
+  const uint32_t w0 = vld(&C->w0);
+  W.j0 = w0 + (uint32_t)i * kSwWin + (uint32_t)tid * kSwPerT;
+#pragma unroll
+  for (int q = 0; q < kSwPerT; q += 4) {
+    uint4 a4 = make_uint4(kNone, kNone, kNone, kNone);
+    uint4 n4 = make_uint4(0, 0, 0, 0);
+    if (W.j0 + q < end) {
+      a4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_sub + W.j0 + q));
+      n4 = __ldcg(reinterpret_cast<const uint4*>(A.ent_next + W.j0 + q));
+    }
+    W.subs[q] = a4.x; W.subs[q + 1] = a4.y; W.subs[q + 2] = a4.z; W.subs[q + 3] = a4.w;
+    W.nxts[q] = n4.x; W.nxts[q + 1] = n4.y; W.nxts[q + 2] = n4.z; W.nxts[q + 3] = n4.w;
+  }
+  W.valid = 0;
+  W.nvalid = 0;
+  uint32_t first_na = kNone, fsub = kNone;
+#pragma unroll
+  for (int e = 0; e < kSwPerT; e++) {
+    const uint32_t j = W.j0 + e;
+    if (j < h || j >= end) continue;
+    if (W.subs[e] < s) {
+      if (W.nxts[e] >= s) {
+        W.valid |= 1 << e;
+        W.nvalid++;
+      }
+    } else if (first_na == kNone) {
+      first_na = j;
+      fsub = W.subs[e];
+    }
+  }
+  if (tid == 0) {
+    red[0] = 0;
+    red[1] = kNone;
+  }
+  __syncthreads();
+  const unsigned wv = __reduce_add_sync(0xffffffffu, (unsigned)W.nvalid);
+  const uint32_t wf = __reduce_min_sync(0xffffffffu, first_na);
+  if ((tid & 31) == 0) {
+    if (wv) atomicAdd(&red[0], wv);
+    if (wf != kNone) atomicMin(&red[1], wf);
+  }
+  __syncthreads();
+  // the first undelivered entry's sub-batch (its holder writes it)
+  if (first_na != kNone && first_na == red[1]) C->fna_sub[i] = fsub;
+  if (tid == 0) {
+    C->cnt[i] = red[0];
+    C->fna[i] = red[1];
+  }
+}
+
+__device__ void coop_commit(const SweepArgs& A, CoopSync* C, int i,
+                            CoopWin& W, uint32_t* red, void* scan_storage) {
+  using Scan = cub::BlockScan<int, kSwThreads>;
+  auto& scan = *reinterpret_cast<typename Scan::TempStorage*>(scan_storage);
+  const int tid = threadIdx.x;
+  const int cut = (int)vld(reinterpret_cast<const unsigned*>(&C->cut));
+  if (i > cut) return;
+  const int64_t nv = *reinterpret_cast<const volatile int64_t*>(&C->nv);
+  const int64_t base_off = nv + *reinterpret_cast<const volatile int64_t*>(&C->off[i]);
+  if (i < cut) {
+    // every valid entry of the window: warp rounds, one slot counter per CTA
+    if (tid == 0) red[2] = 0;
+    __syncthreads();
+    int incl = W.nvalid;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((tid & 31) >= o) incl += t;
+    }
+    int wbase = 0;
+    if ((tid & 31) == 31 && incl) wbase = (int)atomicAdd(&red[2], (unsigned)incl);
+    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+    const unsigned lt = (1u << (tid & 31)) - 1u;
+    int run = 0;
+#pragma unroll
+    for (int e = 0; e < kSwPerT; e++) {
+      const bool v = W.valid >> e & 1;
+      const unsigned m = __ballot_sync(0xffffffffu, v);
+      if (v) {
+        A.victims[base_off + wbase + run + __popc(m & lt)] = W.j0 + e;
+        atomicAdd(A.cold + W.nxts[e], 1u);
+      }
+      run += __popc(m);
+    }
+    return;
+  }
+  // the cut window: the first rem_cut valid entries in list order
+  const int64_t rem_cut = *reinterpret_cast<const volatile int64_t*>(&C->rem_cut);
+  int off, total;
+  Scan(scan).ExclusiveSum(W.nvalid, off, total);
+#pragma unroll
+  for (int e = 0; e < kSwPerT; e++) {
+    if (!(W.valid >> e & 1)) continue;
+    const int64_t r = off++;
+    if (r >= rem_cut) break;
+    const uint32_t j = W.j0 + e;
+    A.victims[base_off + r] = j;
+    atomicAdd(A.cold + W.nxts[e], 1u);
+    if (r == rem_cut - 1) {
+      C->last_taken = j;
+      C->hs_new = e + 1 < kSwPerT ? W.subs[e + 1] : kUnknown;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSwThreads, 1)
+    sweep_coop_kernel(SweepArgs A, CoopSync* C) {
+  extern __shared__ __align__(16) unsigned char sw_raw[];
+  using Scan = cub::BlockScan<int, kSwThreads>;
+  __shared__ typename Scan::TempStorage scan;
+  __shared__ uint32_t red[4];
+  __shared__ unsigned posted;
+  __shared__ int64_t bc_taken;
+  __shared__ int bc_b;
+  __shared__ uint32_t bc_fna, bc_fsub;
+  const int tid = threadIdx.x;
+  const int G = (int)gridDim.x;
+  CoopWin W;
+  if (blockIdx.x != 0) {  // helpers: run posted jobs on window blockIdx.x
+    unsigned seen = 0;
+    while (true) {
+      if (tid == 0) {
+        unsigned j;
+        while ((j = vld(&C->job)) == seen) __nanosleep(32);
+        __threadfence();
+        posted = j;
+      }
+      __syncthreads();
+      seen = posted;
+      const int type = (int)vld(reinterpret_cast<const unsigned*>(&C->type));
+      if (type == 3) return;
+      const int nwin = (int)vld(reinterpret_cast<const unsigned*>(&C->nwin));
+      if ((int)blockIdx.x < nwin) {
+        if (type == 1) coop_scan(A, C, blockIdx.x, W, red);
+        else coop_commit(A, C, blockIdx.x, W, red, &scan);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(&C->done, 1u);
+      }
+    }
+  }
+  SweepSm& sm = *reinterpret_cast<SweepSm*>(sw_raw);
+  unsigned jobs = 0;  // posted so far (CTA 0 is the only poster)
+  auto run_job = [&](int type) {
+    if (tid == 0) {
+      C->type = type;
+      __threadfence();
+      atomicAdd(&C->job, 1u);
+    }
+    jobs++;
+    const int nwin = C->nwin;
+    if (0 < nwin) {
+      if (type == 1) coop_scan(A, C, 0, W, red);
+      else coop_commit(A, C, 0, W, red, &scan);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned want = (unsigned)(G - 1) * jobs;
+      while (vld(&C->done) < want) __nanosleep(32);
+      __threadfence();
+    }
+    __syncthreads();
+  };
+  const int ncache = A.nb < kSwCache ? A.nb : kSwCache;
+  for (int b = tid; b < ncache; b += kSwThreads) {
+    sm.head[b] = A.boff[b];
+    sm.end[b] = A.boff[b + 1];
+    sm.head_sub[b] = sm.head[b] >= sm.end[b] ? kNone : kUnknown;
+  }
+  if (tid == 0) {
+    sm.hot = sm.peak = sm.evictions = sm.reloads = sm.nv = 0;
+    sm.err = 0;
+    sm.err_info = 0;
+    sm.windows = sm.visits = sm.skipped = 0;
+  }
+  __syncthreads();
+  for (int64_t base = 0; base < A.S; base += kSwBlock) {
+    const int cnt = (int)(A.S - base < kSwBlock ? A.S - base : kSwBlock);
+    for (int t = tid; t < cnt; t += kSwThreads) {
+      sm.fresh[t] = A.fresh[base + t];
+      sm.grad[t] = A.grad[base + t];
+      sm.cold[t] = __ldcg(A.cold + base + t);
+    }
+    if (tid == 0) {
+      sm.i = 0;
+      sm.mode = 0;
+    }
+    __syncthreads();
+    while (true) {
+      if (tid == 0) {  // the scalar machine (as in sweep_kernel)
+        sm.k = 0;
+        int i = sm.i;
+        int64_t hot = sm.hot;
+        while (i < cnt) {
+          if (sm.mode == 0) {
+            const int64_t need = (int64_t)sm.fresh[i] + sm.cold[i];
+            if (need <= A.slots - hot) {
+              hot += need;
+              if (hot > sm.peak) sm.peak = hot;
+              sm.reloads += sm.cold[i];
+              hot -= sm.grad[i];
+              i++;
+              continue;
+            }
+            if (need > A.slots) {
+              sm.err = ATLAS_ECONFIG;
+              sm.err_info = need;
+              break;
+            }
+            sm.need_old = need;
+            sm.mode = 1;
+          }
+          const int64_t free = A.slots - hot;
+          if (free < sm.need_old) {
+            int64_t k = sm.need_old - free;
+            if (k < A.evict_batch) k = A.evict_batch;
+            if (k > hot) k = hot;
+            if (k <= 0) {
+              sm.err = ATLAS_EINVARIANT;
+              sm.err_info = -1;
+              break;
+            }
+            sm.k = k;
+            break;
+          }
+          sm.mode = 0;
+        }
+        sm.i = i;
+        sm.hot = hot;
+      }
+      __syncthreads();
+      const int64_t k = sm.k;
+      if (k == 0 || sm.err) break;
+      // ---- pop k entries in rounds over the grid ---------------------
+      const uint32_t s = (uint32_t)(base + sm.i);
+      int64_t rem = k;
+      int64_t nv = sm.nv;
+      int b = A.b0;
+      bool bad = false;
+      while (rem > 0) {
+        if (b >= A.nb) {
+          bad = true;
+          break;
+        }
+        const bool cached = b < kSwCache;
+        uint32_t h, e_end;
+        if (cached) {
+          if (sm.head_sub[b] >= s && sm.head_sub[b] != kUnknown) {
+            if (tid == 0) sm.skipped++;
+            b++;
+            continue;
+          }
+          h = sm.head[b];
+          e_end = sm.end[b];
+        } else {
+          h = __ldcg(A.head + b);
+          e_end = A.boff[b + 1];
+        }
+        if (h >= e_end) {
+          b++;
+          continue;
+        }
+        const uint32_t w0 = h & ~3u;
+        const int64_t nw_all = ((int64_t)e_end - w0 + kSwWin - 1) / kSwWin;
+        const int nwin = (int)(nw_all < G ? nw_all : G);
+        if (tid == 0) {
+          C->h = h;
+          C->end = e_end;
+          C->s = s;
+          C->w0 = w0;
+          C->nwin = nwin;
+        }
+        __syncthreads();
+        run_job(1);
+        // the cut: first window whose running count reaches rem; windows
+        // past the first undelivered entry hold nothing (lists are sorted
+        // by delivery sub-batch)
+        if (tid == 0) {
+          int64_t cum = 0;
+          int cut = nwin;
+          uint32_t fna = kNone, fsub = kUnknown;
+          for (int w = 0; w < nwin; w++) {
+            const int64_t c = (int64_t)vld(&C->cnt[w]);
+            C->off[w] = cum;
+            if (cut == nwin && cum + c >= rem) {
+              cut = w;
+              C->rem_cut = rem - cum;
+            }
+            if (cut == nwin) cum += c;
+            if (fna == kNone && vld(&C->fna[w]) != kNone) {
+              fna = vld(&C->fna[w]);
+              fsub = vld(&C->fna_sub[w]);
+            }
+          }
+          C->cut = cut;
+          C->nv = nv;
+          bc_fna = fna;
+          bc_fsub = fsub;
+          bc_taken = cum;
+        }
+        __syncthreads();
+        run_job(2);
+        if (tid == 0) {
+          const int cut = C->cut;
+          uint32_t h_new, v;
+          const int bcur = b;
+          if (cut < nwin) {  // satisfied inside window `cut`
+            h_new = *reinterpret_cast<volatile uint32_t*>(&C->last_taken) + 1;
+            v = *reinterpret_cast<volatile uint32_t*>(&C->hs_new);
+            nv += rem;
+            rem = 0;
+          } else {
+            const int64_t taken = bc_taken;
+            nv += taken;
+            rem -= taken;
+            const uint32_t fna = bc_fna;
+            const uint32_t wend = min(e_end, w0 + (uint32_t)(nwin * kSwWin));
+            if (fna != kNone) {
+              h_new = fna;
+              v = bc_fsub;
+              b++;
+            } else {
+              h_new = wend;
+              v = wend >= e_end ? kNone : kUnknown;
+              if (wend >= e_end) b++;
+            }
+          }
+          if (h_new >= e_end) v = kNone;
+          if (cached) {
+            sm.head[bcur] = h_new;
+            sm.head_sub[bcur] = v;
+          } else {
+            A.head[bcur] = h_new;
+          }
+          sm.windows += nwin;
+          sm.visits++;
+          bc_taken = rem;  // broadcast the walk state
+          bc_b = b;
+          sm.nv = nv;
+        }
+        __syncthreads();
+        rem = bc_taken;
+        nv = sm.nv;
+        b = bc_b;
+        __syncthreads();
+      }
+      if (tid == 0) {
+        if (bad) {
+          sm.err = ATLAS_EINVARIANT;
+          sm.err_info = rem;
+        }
+        sm.hot -= k - rem;
+        sm.evictions += k - rem;
+        sm.nv = nv;
+      }
+      __syncthreads();
+      // the helpers added reload counts in global memory: restage ours
+      for (int t = sm.i + tid; t < cnt; t += kSwThreads)
+        sm.cold[t] = __ldcg(A.cold + base + t);
+      __syncthreads();
+      if (sm.err) break;
+    }
+    __syncthreads();
+    for (int t = tid; t < cnt; t += kSwThreads) A.cold_out[base + t] = sm.cold[t];
+    __syncthreads();
+    if (sm.err) break;
+  }
+  if (tid == 0) {
+    C->type = 3;
+    __threadfence();
+    atomicAdd(&C->job, 1u);
+    A.out[0] = sm.evictions;
+    A.out[1] = sm.reloads;
+    A.out[2] = sm.peak;
+    A.out[3] = sm.nv;
+    A.out[4] = sm.err;
+    A.out[5] = sm.err_info;
+    A.out[6] = (int64_t)sm.windows;
+    A.out[7] = (int64_t)sm.skipped;
+  }
+}
+
 template <typename T>
 void fill_zero(DevBuf<T>& b, size_t n, cudaStream_t s) {
   b.reserve(std::max<size_t>(n, 1));
@@ -950,7 +1376,38 @@ static bool run_sweep(atlas_layer* L, SweepWs& W, PhaseTimer& T,
         sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  sweep_kernel<<<1, kSwThreads, smem, s>>>(A);
+  // ATLAS_SWEEP_COOP=1: the cooperative-grid sweep (measured 5-8x slower:
+  // its two grid jobs per round cost ~14 us each, profiles/
+  // r2_sweep_variants.txt), otherwise the single-CTA sweep
+  const char* ce = getenv("ATLAS_SWEEP_COOP");
+  int coop_grid = 0;
+  if (ce && ce[0] == '1') {
+    int dev = 0, coop = 0, per_sm = 0;
+    ATLAS_CUDA(cudaGetDevice(&dev));
+    ATLAS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    static bool cattr = false;
+    if (!cattr) {
+      ATLAS_CUDA(cudaFuncSetAttribute(
+          sweep_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          smem));
+      cattr = true;
+    }
+    ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, sweep_coop_kernel, kSwThreads, smem));
+    if (coop && per_sm > 0)
+      coop_grid = std::min<int>(kCoopMax, num_sms() * per_sm);
+  }
+  if (coop_grid > 1) {
+    W.coop.reserve(sizeof(CoopSync));
+    ATLAS_CUDA(cudaMemsetAsync(W.coop.ptr, 0, sizeof(CoopSync), s));
+    CoopSync* C = reinterpret_cast<CoopSync*>(W.coop.ptr);
+    void* args[] = {&A, &C};
+    ATLAS_CUDA(cudaLaunchCooperativeKernel((const void*)sweep_coop_kernel,
+                                           dim3(coop_grid), dim3(kSwThreads),
+                                           args, smem, s));
+  } else {
+    sweep_kernel<<<1, kSwThreads, smem, s>>>(A);
+  }
   count_launch();
   ATLAS_LAUNCH_CHECK();
   T.mark("sweep");

@@ -156,6 +156,7 @@ __device__ __forceinline__ void store4(H* d, const H (&q)[4]) {
 struct TcParams {
   int64_t M;
   int K, N, BN, stages, kblocks, relu;
+  int nacc;  // TMEM accumulators in the ring: 2 (default, 0 = 2) or 1
   int64_t ldy;
   const float* bias;
   void* y;
@@ -237,7 +238,7 @@ __device__ __forceinline__ void epilogue_loop(
     }  // halves
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     mbar_arrive(&tempty[acc]);
-    acc ^= 1;
+    acc = p.nacc == 1 ? 0 : acc ^ 1;
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0 && p.flag)
     atomicOr(p.flag, 1);
@@ -645,7 +646,7 @@ __global__ void __launch_bounds__(kThreadsH, 1)
           ph ^= 1;
         }
       }
-      acc ^= 1;
+      acc = p.nacc == 1 ? 0 : acc ^ 1;
     }
   } else {
     epilogue_loop<OutT>(p, warp - 2, warp, lane, ntiles, tmem_base, tfull,
@@ -1252,7 +1253,15 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
   const int kblocks = (int)((k + BKH - 1) / BKH);
   // 256-row tiles (two halves per W stage) unless ATLAS_TRANSFORM_H_SUB=1
   const char* sub_env = getenv("ATLAS_TRANSFORM_H_SUB");
-  const int sub = (BN <= 128 && !(sub_env && sub_env[0] == '1')) ? 2 : 1;
+  // BN <= 128: two accumulator pairs (the epilogue of tile t overlaps the
+  // MMAs of t+1). Above, one pair would have to do (4 x BN TMEM columns do
+  // not fit): measured slower than 128-row tiles at N = 136 (0.52 vs 0.56
+  // of HBM, profiles/r2_transform_probe_v3.txt), so those keep sub = 1;
+  // ATLAS_TRANSFORM_H_SUB=2 forces the single-pair variant
+  const bool force2 = sub_env && sub_env[0] == '2';
+  const int sub = ((BN <= 128 || (force2 && BN <= 256)) &&
+                   !(sub_env && sub_env[0] == '1')) ? 2 : 1;
+  const int nacc = (sub == 2 && BN > 128) ? 1 : 2;
   const int stage_bytes = sub * BM * BKH * 2 + 2 * BN * BKH * 2;
   const int fixed = 1024 + 8 * 16 + 16 + 2 * 4 * 256 + 16 +
                     kEpiWarps * 32 * kStageLd * 4;
@@ -1288,8 +1297,9 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
     p.bias = b;
     p.y = y;
     p.flag = flag;
+    p.nacc = nacc;
     uint32_t cols = 32;
-    while (cols < (uint32_t)(2 * sub * BN)) cols <<= 1;
+    while (cols < (uint32_t)(nacc * sub * BN)) cols <<= 1;
     p.tmem_cols = cols;
     const int64_t ntiles = (rows + BM * sub - 1) / (BM * sub);
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, num_sms());

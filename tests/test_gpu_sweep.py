@@ -31,8 +31,9 @@ CASES = [
 ]
 
 
-def run(kind, v, deg, dim, model, frac, policy, budget, sweep):
+def run(kind, v, deg, dim, model, frac, policy, budget, sweep, coop=True):
     os.environ["ATLAS_SWEEP"] = "1" if sweep else "0"
+    os.environ["ATLAS_SWEEP_COOP"] = "1" if coop else "0"
     try:
         graph, feats = S.synthetic_in_memory(kind, v, deg, dim, 11)
         w = S.random_weights(S.ModelKind[model], [dim, 16, 8], 3)
@@ -52,16 +53,20 @@ def run(kind, v, deg, dim, model, frac, policy, budget, sweep):
         return out
     finally:
         os.environ.pop("ATLAS_SWEEP", None)
+        os.environ.pop("ATLAS_SWEEP_COOP", None)
 
 
 @pytest.mark.parametrize("case", CASES, ids=[
     f"{c[0]}-{c[4]}-{c[6]}-{c[5]}" for c in CASES])
 def test_sweep_equals_per_element_machine(case):
-    a = run(*case, sweep=True)
+    """Both sweeps (the cooperative grid and the single CTA) against the
+    per-element machine."""
     b = run(*case, sweep=False)
     assert sum(layer[0]["evictions"] for layer in b) > 0
-    for l, (x, y) in enumerate(zip(a, b)):
-        assert x[0] == y[0], (l, x[0], y[0])
-        assert x[1] == y[1], l
-        assert x[2] == y[2], l
-        assert x[3] == y[3], l
+    for coop in (True, False):
+        a = run(*case, sweep=True, coop=coop)
+        for l, (x, y) in enumerate(zip(a, b)):
+            assert x[0] == y[0], (coop, l, x[0], y[0])
+            assert x[1] == y[1], (coop, l)
+            assert x[2] == y[2], (coop, l)
+            assert x[3] == y[3], (coop, l)

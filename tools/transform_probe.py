@@ -60,7 +60,7 @@ def f16_inputs(rows):
         b = torch.randn(n, device="cuda")
         y = torch.empty(rows, n, device="cuda")
         res = []
-        for sub in ("1", "2"):
+        for sub in ("1", "2") if n <= 128 else ("1", "2"):
             os.environ["ATLAS_TRANSFORM_H_SUB"] = sub
             for _ in range(3):
                 transform_typed(x, w, b, True, y, 1)
