@@ -170,7 +170,13 @@ struct RowFeeder {
     ne = (int)(end - e0);
     pe = ibase = 0;
     isrc = lane < ne ? src0[lane] : 0u;
-    while (pe < ne && n_issued - n_used <= SLOTS - G) issue_group(base, ld);
+    if (pe < ne && n_issued - n_used <= SLOTS - G) {
+      __syncwarp();  // slots freed by release_n without a refill: order
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      do {
+        issue_group(base, ld);
+      } while (pe < ne && n_issued - n_used <= SLOTS - G);
+    }
   }
   // wait for the next row in edge order; returns its shared address
   __device__ __forceinline__ uint32_t wait() {
@@ -197,6 +203,10 @@ struct RowFeeder {
     n_used += n;
     if (pe < ne && n_issued - n_used <= SLOTS - G) {
       __syncwarp();  // every lane is done with the slots being refilled
+      // ...and those generic-proxy reads are ordered before the
+      // async-proxy bulk copies that overwrite the slots (compute-sanitizer
+      // racecheck flags the WAR without it, profiles/r2_sanitize_*.txt)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       do {
         issue_group(base, ld);
       } while (pe < ne && n_issued - n_used <= SLOTS - G);

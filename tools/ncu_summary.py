@@ -3,7 +3,7 @@ profiles/r1_ncu_final.json (key metrics per launch) and
 profiles/agg_traffic_<workload>.json (DRAM bytes per launch of each
 aggregation kernel kind, read by bench.py as roofline.traffic), and the
 launch-list CSV into profiles/r1_launches_final.txt.
-Usage: ncu_summary.py GPURUN_OUT_DIR"""
+Usage: ncu_summary.py GPURUN_OUT_DIR [ROUND_TAG]"""
 
 import csv
 import json
@@ -61,6 +61,7 @@ def kind_of(name):
 
 def main():
     src = Path(sys.argv[1] if len(sys.argv) > 1 else ROOT / "gpurun_out")
+    tag_round = sys.argv[2] if len(sys.argv) > 2 else "r1"
     final = {"note": "ncu --set full --clock-control none, one bench step "
                      "per workload (tools/gpu_profile.sh), per launch; "
                      "tensor-pipe utilisation of the tcgen05 transforms: "
@@ -80,12 +81,12 @@ def main():
                 traffic[k].append(r["dram_bytes_total"])
         if traffic:
             out = {k: sum(v) / len(v) for k, v in traffic.items()}
-            out["source"] = ("profiles/r1_ncu_final.json: dram__bytes_read."
+            out["source"] = (f"profiles/{tag_round}_ncu_final.json: dram__bytes_read."
                              "sum + dram__bytes_write.sum per launch of that "
                              "kernel kind, ncu --set full")
             (ROOT / "profiles" / f"agg_traffic_{workload}.json").write_text(
                 json.dumps(out, indent=1))
-    (ROOT / "profiles" / "r1_ncu_final.json").write_text(
+    (ROOT / "profiles" / f"{tag_round}_ncu_final.json").write_text(
         json.dumps(final, indent=1))
     lp = src / "launches_cfg2.csv"
     if lp.exists():
@@ -112,7 +113,7 @@ def main():
         for name, (n, ms) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
             lines.append(f"{n:4d}  {ms:9.3f} ms  {100 * ms / allms:4.1f}% "
                          f"{name}")
-        (ROOT / "profiles" / "r1_launches_final.txt").write_text(
+        (ROOT / "profiles" / f"{tag_round}_launches_final.txt").write_text(
             "\n".join(lines) + "\n")
 
 
