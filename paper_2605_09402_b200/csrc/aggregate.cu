@@ -1264,10 +1264,14 @@ void runs_typed(const void* tile, int64_t ldx, const uint32_t* run_dst,
 // agg_sub_ring's lockstep sub-groups, not this kernel).
 // MODEL = ATLAS_SAGE: the neighbour half is the same mean; the self half
 // (columns [d, 2d) of the record) is the destination's own row, copied when
-// that row is in the tile (agg_tile's SAGE rule).
-template <int VEC, int MODEL>
+// that row is in the tile (agg_tile's SAGE rule). MODEL = ATLAS_GIN: a sum
+// (no division) with the self term (1 + eps) * x_v folded at its place in
+// ascending source order -- before the first remaining source >= v -- in
+// the tile holding row v. T: the stored input type (f32 or 2-byte rows,
+// widened exactly); each lane moves 16 B of the row per edge.
+template <typename T, int VEC, int MODEL>
 __global__ void __launch_bounds__(256, kSubBlocks + 1)
-    agg_suffix_ring(const float* __restrict__ tile, int64_t ldx,
+    agg_suffix_ring(const T* __restrict__ tile, int64_t ldx,
                     int64_t tile_lo, int64_t tile_hi, int64_t V,
                     const int64_t* __restrict__ csc_ptr,
                     const uint32_t* __restrict__ csc_src,
@@ -1275,8 +1279,10 @@ __global__ void __launch_bounds__(256, kSubBlocks + 1)
                     int64_t nloc, int d, float* __restrict__ acc,
                     int64_t ldacc, int64_t* __restrict__ cursor,
                     uint8_t* __restrict__ touched,
-                    unsigned long long* __restrict__ work) {
-  using F = Frag<float, VEC>;
+                    unsigned long long* __restrict__ work,
+                    float self_scale) {
+  using F = Frag<T, VEC>;
+  constexpr bool kMean = MODEL != ATLAS_GIN;
   extern __shared__ uint4 ring_smem[];
   const int lane = threadIdx.x & 31;
   const int col = lane * VEC;
@@ -1286,7 +1292,7 @@ __global__ void __launch_bounds__(256, kSubBlocks + 1)
       (uint32_t)__cvta_generic_to_shared(ring_smem +
                                          (threadIdx.x >> 5) * (kSubRing * 32)) +
       (uint32_t)lane * 16u;
-  const float* __restrict__ xc = tile + colc;
+  const T* __restrict__ xc = tile + colc;
   while (true) {
     unsigned long long v0 = 0;
     if (lane == 0) v0 = atomicAdd(work, (unsigned long long)kGrab);
@@ -1294,10 +1300,11 @@ __global__ void __launch_bounds__(256, kSubBlocks + 1)
     if ((int64_t)v0 >= nloc) break;
     const int64_t v1 = min((int64_t)v0 + kGrab, nloc);
     // lane j: destination v0 + j, its suffix [b_j, b_j + n_j), its place
-    // off_j in the grab's concatenated edge list
+    // off_j in the grab's concatenated edge list; GIN: sp_j = edges of the
+    // suffix before the self term (sources < v)
     const int64_t vj = (int64_t)v0 + lane;
     int64_t b_j = 0;
-    int n_j = 0;
+    int n_j = 0, sp_j = 0;
     uint32_t dg_j = 0, tch_j = 0;  // in-degree, touched flag of v0 + j
     if (vj < v1) {
       b_j = cursor[vj];
@@ -1312,6 +1319,16 @@ __global__ void __launch_bounds__(256, kSubBlocks + 1)
         cursor[vj] = e;  // the next tile resumes here
       }
       n_j = (int)(e - b_j);
+      if (MODEL == ATLAS_GIN) {
+        const int64_t vg = vj + lo;
+        int64_t a = b_j, z = e;
+        while (a < z) {
+          const int64_t m = (a + z) >> 1;
+          if ((int64_t)csc_src[m] < vg) a = m + 1;
+          else z = m;
+        }
+        sp_j = (int)(a - b_j);
+      }
       dg_j = indeg[vj];
       tch_j = touched[vj];
     }
@@ -1356,30 +1373,45 @@ __global__ void __launch_bounds__(256, kSubBlocks + 1)
       const uint32_t dg = __shfl_sync(0xffffffffu, dg_j, j);
       const bool own = v + lo >= tile_lo && v + lo < tile_hi;
       // GCN: a zero in-degree destination owes a zero record once (in its
-      // own row's tile); SAGE: the own row's tile writes the self half
-      const bool must = MODEL == ATLAS_SAGE ? own : (own && dg == 0);
+      // own row's tile); SAGE / GIN: the own row's tile writes the self
+      // half / folds the self term
+      const bool must = MODEL == ATLAS_GCN ? (own && dg == 0) : own;
       if (nj == 0 && !must) continue;
-      const float denom = (float)max(1u, dg);
-      const float rcp = __frcp_rn(denom);
+      const float denom = kMean ? (float)max(1u, dg) : 1.0f;
+      const float rcp = kMean ? __frcp_rn(denom) : 1.0f;
       float a[VEC];
 #pragma unroll
       for (int e = 0; e < VEC; e++) a[e] = 0.0f;
       const bool resume = __shfl_sync(0xffffffffu, tch_j, j) != 0;
       float* out = acc + v * ldacc;
       if (resume && active) load_f32<VEC>(out + col, a);
+      const int sp = MODEL == ATLAS_GIN && own
+                         ? __shfl_sync(0xffffffffu, sp_j, j) : -1;
+      auto fold_self = [&]() {
+        if (active) {
+          F me;
+          me.load(tile + (v + lo - tile_lo) * ldx + col);
+          add_msg<T, VEC, false>(a, me, true, 1.0f, 1.0f, self_scale);
+        }
+      };
       for (int c = 0; c < nj; c++, ce++) {
+        if (c == sp) fold_self();
         cp_async_wait<kSubRing - 1>();
         F f;
         f.raw = lds16(ring_lane + ((uint32_t)(ce & (kSubRing - 1)) << 9));
-        add_msg<float, VEC, true>(a, f, false, denom, rcp, 1.0f);
+        add_msg<T, VEC, kMean>(a, f, false, denom, rcp, 1.0f);
         issue();
       }
+      if (sp == nj) fold_self();  // every remaining source is below v
       if (active) {
         store_f32<VEC>(out + col, a);
         if (MODEL == ATLAS_SAGE && own) {
-          float me[VEC];
-          load_f32<VEC>(tile + (v + lo - tile_lo) * ldx + col, me);
-          store_f32<VEC>(out + d + col, me);
+          F me;
+          me.load(tile + (v + lo - tile_lo) * ldx + col);
+          float h[VEC];
+#pragma unroll
+          for (int e = 0; e < VEC; e++) h[e] = me.get(e);
+          store_f32<VEC>(out + d + col, h);
         }
       }
       if (lane == 0) touched[v] = 1;
@@ -1446,27 +1478,40 @@ void launch_agg_tile(const void* tile, int dtype, int64_t ldx, int64_t tile_lo,
 
 bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
                        int64_t tile_lo, int64_t tile_hi,
-                       const atlas_graph* g, int model, int d, float* acc,
-                       int64_t ldacc, int64_t* cursor, uint8_t* touched,
-                       cudaStream_t s) {
-  if ((model != ATLAS_GCN && model != ATLAS_SAGE) || dtype != ATLAS_F32 ||
-      d % 4 != 0 || d > 128 ||
-      ldx % 4 != 0 || ldacc % 4 != 0 ||
-      (reinterpret_cast<uintptr_t>(tile) & 15) != 0)
+                       const atlas_graph* g, int model, float gin_epsilon,
+                       int d, float* acc, int64_t ldacc, int64_t* cursor,
+                       uint8_t* touched, cudaStream_t s) {
+  // 16 B per lane per edge: f32 rows up to 128 columns, 2-byte rows up to
+  // 256, whole 16-B chunks, 16-B aligned rows
+  const int es = dtype == ATLAS_F32 ? 4 : 2;
+  const int vec = 16 / es;
+  if (d % vec != 0 || d > 32 * vec || (ldx * es) % 16 != 0 ||
+      ldacc % 4 != 0 || (reinterpret_cast<uintptr_t>(tile) & 15) != 0)
     return false;
   if (g->nloc == 0) return true;
   g->work.reserve(1);
   ATLAS_CUDA(cudaMemsetAsync(g->work.ptr, 0, sizeof(unsigned long long), s));
   const int smem = 8 * kSubRing * 32 * 16;
-  auto kern = model == ATLAS_SAGE ? agg_suffix_ring<4, ATLAS_SAGE>
-                                   : agg_suffix_ring<4, ATLAS_GCN>;
-  ATLAS_CUDA(cudaFuncSetAttribute(
-      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<num_sms() * (kSubBlocks + 1), 256, smem, s>>>(
-      static_cast<const float*>(tile), ldx, tile_lo, tile_hi, g->V,
-      g->csc_ptr.ptr,
-      g->csc_src.ptr, g->indeg.ptr, g->lo, g->nloc, d, acc, ldacc, cursor,
-      touched, g->work.ptr);
+  const float e1 = 1.0f + gin_epsilon;  // np.float32(1) + np.float32(eps)
+  auto go = [&](auto kern, auto tag) {
+    using T = decltype(tag);
+    ATLAS_CUDA(cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<num_sms() * (kSubBlocks + 1), 256, smem, s>>>(
+        static_cast<const T*>(tile), ldx, tile_lo, tile_hi, g->V,
+        g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo, g->nloc, d, acc,
+        ldacc, cursor, touched, g->work.ptr, e1);
+  };
+  auto by_model = [&](auto tag) {
+    using T = decltype(tag);
+    constexpr int V = 16 / sizeof(T);
+    if (model == ATLAS_GCN) go(agg_suffix_ring<T, V, ATLAS_GCN>, tag);
+    else if (model == ATLAS_SAGE) go(agg_suffix_ring<T, V, ATLAS_SAGE>, tag);
+    else go(agg_suffix_ring<T, V, ATLAS_GIN>, tag);
+  };
+  if (dtype == ATLAS_F32) by_model(float());
+  else if (dtype == ATLAS_F16) by_model(__half());
+  else by_model(__nv_bfloat16());
   count_launch();
   ATLAS_LAUNCH_CHECK();
   return true;

@@ -627,10 +627,10 @@ int atlas_layer_run_streamed(atlas_layer* L, const atlas_graph* g,
       ATLAS_CUDA(cudaStreamWaitEvent(
           s, whole ? L->tile_ev[t % kTileEvents] : L->ev_ready[b], 0));
       const bool suffix =
-          whole && L->nloc > 0 &&
+          L->nloc > 0 &&
           launch_agg_suffix(tile_ptr(t), dtype, ldx, r0, r1, g, D.model,
-                            (int)D.embed_dim, L->acc.ptr, D.agg_dim,
-                            L->cursor.ptr, L->touched.ptr, s);
+                            D.gin_epsilon, (int)D.embed_dim, L->acc.ptr,
+                            D.agg_dim, L->cursor.ptr, L->touched.ptr, s);
       if (L->nloc > 0 && !suffix)
         launch_agg_tile(tile_ptr(t), dtype, ldx, r0, r1, g, D.model,
                         D.gin_epsilon, (int)D.embed_dim, L->acc.ptr,
@@ -697,8 +697,9 @@ int atlas_layer_run_pieces(atlas_layer* L, const atlas_graph* g,
       if (r1 == r0 || L->nloc == 0) continue;
       const uint8_t* tile = base + (size_t)r0 * row_b;
       const bool suffix = launch_agg_suffix(
-          tile, dtype, ldx, r0, r1, g, D.model, (int)D.embed_dim, L->acc.ptr,
-          D.agg_dim, L->cursor.ptr, L->touched.ptr, s);
+          tile, dtype, ldx, r0, r1, g, D.model, D.gin_epsilon,
+          (int)D.embed_dim, L->acc.ptr, D.agg_dim, L->cursor.ptr,
+          L->touched.ptr, s);
       if (!suffix)
         launch_agg_tile(tile, dtype, ldx, r0, r1, g, D.model, D.gin_epsilon,
                         (int)D.embed_dim, L->acc.ptr, D.agg_dim,

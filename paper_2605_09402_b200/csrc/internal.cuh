@@ -130,11 +130,11 @@ struct EngineConfig {
 
 // Workspaces of the sweep replay (sweep.cu), grow-only across layers.
 struct SweepWs {
-  DevBuf<uint32_t> zr, tmp_u32, el_v, el_cnt, el_sub, el_newp, el_nsub, iota,
+  DevBuf<uint32_t> zr, tmp_u32, el_v, el_cnt, el_sub,
       sv, se, ent_sub, ent_next, boff, head, fresh, grad, cold, cold_out,
       victims, flags;
-  DevBuf<uint8_t> el_fresh, cub_tmp, coop;
-  DevBuf<unsigned long long> cs, P, lastP, count;
+  DevBuf<uint8_t> cub_tmp, coop;
+  DevBuf<unsigned long long> cs, P, lastP, count, pk, svk, sk64;
   DevBuf<int64_t> eoff, soff, chunk64, out;
   // run materialisation (control.cu exact_replay)
   DevBuf<uint64_t> at_pos, runs;
@@ -300,9 +300,9 @@ void launch_agg_runs(const void* tile, int dtype, int64_t ldx,
 // cp.async ring (GCN, f32 rows <= 512 B); false if the shape does not fit
 bool launch_agg_suffix(const void* tile, int dtype, int64_t ldx,
                        int64_t tile_lo, int64_t tile_hi,
-                       const atlas_graph* g, int model, int d, float* acc,
-                       int64_t ldacc, int64_t* cursor, uint8_t* touched,
-                       cudaStream_t s);
+                       const atlas_graph* g, int model, float gin_epsilon,
+                       int d, float* acc, int64_t ldacc, int64_t* cursor,
+                       uint8_t* touched, cudaStream_t s);
 void launch_agg_tile(const void* tile, int dtype, int64_t ldx, int64_t tile_lo,
                      int64_t tile_hi, const atlas_graph* g, int model,
                      float gin_epsilon, int d, float* acc, int64_t ldacc,

@@ -139,19 +139,7 @@ __global__ void chunk_zero_counts(const uint32_t* __restrict__ zr,
   }
 }
 
-__global__ void iota_u32(uint32_t* p, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = (uint32_t)i;
-}
 
-__global__ void gather_cnt(const uint32_t* __restrict__ se,
-                           const uint32_t* __restrict__ el_cnt, int64_t n,
-                           unsigned long long* __restrict__ out) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    out[j] = el_cnt[se[j]];
-}
 
 // per vertex: the prefix at its last element (elements grouped by vertex)
 __global__ void vertex_last(const uint32_t* __restrict__ sv,
@@ -162,36 +150,67 @@ __global__ void vertex_last(const uint32_t* __restrict__ sv,
     if (j == n - 1 || sv[j + 1] != sv[j]) lastP[sv[j]] = P[j];
 }
 
-// pending after each delivery, successor's sub-batch, first-delivery flag;
-// a vertex whose deliveries do not add up to its pending count is flagged
-// (the per-element machine then reproduces the reference's error)
-__global__ void chain_links(const uint32_t* __restrict__ sv,
-                            const uint32_t* __restrict__ se,
-                            const unsigned long long* __restrict__ P,
-                            const unsigned long long* __restrict__ lastP,
-                            const uint32_t* __restrict__ el_cnt,
-                            const uint32_t* __restrict__ el_sub,
-                            const uint32_t* __restrict__ indeg, int self_term,
-                            int64_t n, uint32_t* __restrict__ el_newp,
-                            uint32_t* __restrict__ el_nsub,
-                            uint8_t* __restrict__ el_fresh,
-                            int* __restrict__ mismatch,
-                            unsigned* __restrict__ maxp) {
+
+
+
+
+// values of the vertex sort: element index (high word) | count (low)
+__global__ void pack_idx_cnt(const uint32_t* __restrict__ el_cnt, int64_t n,
+                             unsigned long long* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ((unsigned long long)i << 32) | el_cnt[i];
+}
+
+__global__ void low_words(const unsigned long long* __restrict__ in, int64_t n,
+                          unsigned long long* __restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = in[j] & 0xFFFFFFFFull;
+}
+
+// In vertex order (each vertex's deliveries in stream order): pending after
+// each delivery, its successor's sub-batch, fresh / graduating counts per
+// sub-batch, and the heap entry of the delivery keyed (pending << 32 |
+// element) -- MINPEND's bucket FIFOs once sorted -- or (element) for LRU,
+// with value (sub << 32 | successor's sub; 0 when it graduates: never in
+// the heap). Only two random reads per delivery (its and its successor's
+// sub-batch); everything else streams.
+__global__ void chain_entries(const uint32_t* __restrict__ sv,
+                              const unsigned long long* __restrict__ sval,
+                              const unsigned long long* __restrict__ P,
+                              const unsigned long long* __restrict__ lastP,
+                              const uint32_t* __restrict__ el_sub,
+                              const uint32_t* __restrict__ indeg,
+                              int self_term, int lru, int64_t n,
+                              unsigned long long* __restrict__ key_out,
+                              unsigned long long* __restrict__ val_out,
+                              uint32_t* __restrict__ fresh,
+                              uint32_t* __restrict__ grad,
+                              int* __restrict__ mismatch,
+                              unsigned* __restrict__ maxp) {
   unsigned my_max = 0;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = sv[j], i = se[j];
+    const uint32_t v = sv[j];
+    const unsigned long long x = sval[j];
+    const uint32_t i = (uint32_t)(x >> 32), cnt = (uint32_t)x;
     const bool first = j == 0 || sv[j - 1] != v;
     const bool last = j == n - 1 || sv[j + 1] != v;
     const unsigned long long left = lastP[v] - P[j];
     if (first) {
       const unsigned long long p0 = (unsigned long long)indeg[v] + self_term;
-      if (left + el_cnt[i] != p0) atomicExch(mismatch, 1);
+      if (left + cnt != p0) atomicExch(mismatch, 1);
     }
     const uint32_t np = left > 0xFFFFFFF0ull ? 0xFFFFFFF0u : (uint32_t)left;
-    el_newp[i] = np;
-    el_nsub[i] = last ? 0u : el_sub[se[j + 1]];
-    el_fresh[i] = first ? 1 : 0;
+    const uint32_t sub = el_sub[i];
+    const uint32_t nsub =
+        (last || np == 0) ? 0u : el_sub[(uint32_t)(sval[j + 1] >> 32)];
+    if (first) atomicAdd(fresh + sub, 1u);
+    if (np == 0) atomicAdd(grad + sub, 1u);
+    key_out[j] = lru ? (unsigned long long)i
+                     : (((unsigned long long)np << 32) | i);
+    val_out[j] = ((unsigned long long)sub << 32) | nsub;
     my_max = max(my_max, np);
   }
   for (int o = 16; o > 0; o >>= 1)
@@ -199,53 +218,28 @@ __global__ void chain_links(const uint32_t* __restrict__ sv,
   if ((threadIdx.x & 31) == 0 && my_max) atomicMax(maxp, my_max);
 }
 
-// per sub-batch fresh and graduating counts (elements in stream order, so
-// a warp's elements mostly share one sub-batch)
-__global__ void sub_stats(const uint32_t* __restrict__ el_sub,
-                          const uint8_t* __restrict__ el_fresh,
-                          const uint32_t* __restrict__ el_newp, int64_t n,
-                          uint32_t* __restrict__ fresh,
-                          uint32_t* __restrict__ grad) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += stride) {
-    const int64_t i = i0 + threadIdx.x;
-    const bool in = i < n;
-    const uint32_t s = in ? el_sub[i] : kNone;
-    const unsigned f = in ? el_fresh[i] : 0u;
-    const unsigned g = (in && el_newp[i] == 0) ? 1u : 0u;
-    const unsigned peers = __match_any_sync(0xffffffffu, s);
-    const unsigned fsum = __reduce_add_sync(peers, f);
-    const unsigned gsum = __reduce_add_sync(peers, g);
-    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1 && in) {
-      if (fsum) atomicAdd(fresh + s, fsum);
-      if (gsum) atomicAdd(grad + s, gsum);
-    }
-  }
-}
-
-// bucket list entries (sorted by key, stream order within a key)
-__global__ void make_entries(const uint32_t* __restrict__ be,
-                             const uint32_t* __restrict__ bk,
-                             const uint32_t* __restrict__ el_sub,
-                             const uint32_t* __restrict__ el_nsub, int64_t n,
-                             uint32_t* __restrict__ ent_sub,
-                             uint32_t* __restrict__ ent_next) {
+__global__ void entries_from_sorted(const unsigned long long* __restrict__ skey,
+                                    const unsigned long long* __restrict__ sval,
+                                    int64_t n, uint32_t* __restrict__ ent_sub,
+                                    uint32_t* __restrict__ ent_next,
+                                    uint32_t* __restrict__ ent_el) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t i = be ? be[k] : (uint32_t)k;
-    const uint32_t key = bk[be ? k : i];
-    ent_sub[k] = el_sub[i];
-    ent_next[k] = key > 0 ? el_nsub[i] : 0u;  // pending 0: never in the heap
+    const unsigned long long v = sval[k];
+    ent_sub[k] = (uint32_t)(v >> 32);
+    ent_next[k] = (uint32_t)v;
+    ent_el[k] = (uint32_t)skey[k];
   }
 }
 
-// boff[b] = first entry with key >= b, for b in [0, nb]
-__global__ void bucket_bounds(const uint32_t* __restrict__ bk, int64_t n,
-                              int64_t nb, uint32_t* __restrict__ boff) {
+// boff[b] = first entry with key >= b (key = high word), b in [0, nb]
+__global__ void bucket_bounds64(const unsigned long long* __restrict__ skey,
+                                int64_t n, int64_t nb,
+                                uint32_t* __restrict__ boff) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= n;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t prev = k == 0 ? -1 : (int64_t)bk[k - 1];
-    const int64_t cur = k == n ? nb : min((int64_t)bk[k], nb);
+    const int64_t prev = k == 0 ? -1 : (int64_t)(skey[k - 1] >> 32);
+    const int64_t cur = k == n ? nb : min((int64_t)(skey[k] >> 32), nb);
     for (int64_t b = prev + 1; b <= cur; b++) boff[b] = (uint32_t)k;
   }
 }
@@ -1208,28 +1202,30 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   }
   ATLAS_LAUNCH_CHECK();
   T.mark("fill");
-  // group by vertex (stable: each vertex's deliveries in stream order)
-  W.iota.reserve(NE);
+  // group by vertex (stable: each vertex's deliveries in stream order);
+  // the values carry (element, count) so the chain below streams
   W.sv.reserve(NE);
   W.se.reserve(NE);
-  iota_u32<<<grid_of(NE), 256, 0, s>>>(W.iota.ptr, NE);
+  W.pk.reserve(NE);
+  W.svk.reserve(NE);
+  pack_idx_cnt<<<grid_of(NE), 256, 0, s>>>(W.el_cnt.ptr, NE, W.pk.ptr);
   count_launch();
   {
     size_t tb = 0;
     const int vb = bits_for((uint64_t)std::max<int64_t>(nloc - 1, 1));
     ATLAS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, W.el_v.ptr,
-                                               W.sv.ptr, W.iota.ptr, W.se.ptr,
+                                               W.sv.ptr, W.pk.ptr, W.svk.ptr,
                                                NE, 0, vb, s));
     W.cub_tmp.reserve(tb);
     ATLAS_CUDA(cub::DeviceRadixSort::SortPairs(W.cub_tmp.ptr, tb, W.el_v.ptr,
-                                               W.sv.ptr, W.iota.ptr, W.se.ptr,
+                                               W.sv.ptr, W.pk.ptr, W.svk.ptr,
                                                NE, 0, vb, s));
     count_launch();
   }
   T.mark("sort_v");
   W.cs.reserve(NE);
   W.P.reserve(NE);
-  gather_cnt<<<grid_of(NE), 256, 0, s>>>(W.se.ptr, W.el_cnt.ptr, NE, W.cs.ptr);
+  low_words<<<grid_of(NE), 256, 0, s>>>(W.svk.ptr, NE, W.cs.ptr);
   count_launch();
   {
     size_t tb = 0;
@@ -1243,14 +1239,18 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   T.mark("scan");
   W.lastP.reserve(std::max<int64_t>(nloc, 1));
   vertex_last<<<grid_of(NE), 256, 0, s>>>(W.sv.ptr, W.P.ptr, NE, W.lastP.ptr);
-  W.el_newp.reserve(NE);
-  W.el_nsub.reserve(NE);
-  W.el_fresh.reserve(NE);
   fill_zero(W.flags, 4, s);  // mismatch, max pending
-  chain_links<<<grid_of(NE), 256, 0, s>>>(
-      W.sv.ptr, W.se.ptr, W.P.ptr, W.lastP.ptr, W.el_cnt.ptr, W.el_sub.ptr,
-      L->indeg.ptr, model == ATLAS_GCN ? 0 : 1, NE, W.el_newp.ptr,
-      W.el_nsub.ptr, W.el_fresh.ptr, reinterpret_cast<int*>(W.flags.ptr),
+  fill_zero(W.fresh, S, s);
+  fill_zero(W.grad, S, s);
+  fill_zero(W.cold, S, s);
+  W.cold_out.reserve(std::max<int64_t>(S, 1));
+  const bool lru = L->desc.policy == ATLAS_LRU;
+  // keys into pk (free after the vertex sort), values into cs (free after
+  // the scan)
+  chain_entries<<<grid_of(NE), 256, 0, s>>>(
+      W.sv.ptr, W.svk.ptr, W.P.ptr, W.lastP.ptr, W.el_sub.ptr, L->indeg.ptr,
+      model == ATLAS_GCN ? 0 : 1, lru ? 1 : 0, NE, W.pk.ptr, W.cs.ptr,
+      W.fresh.ptr, W.grad.ptr, reinterpret_cast<int*>(W.flags.ptr),
       W.flags.ptr + 1);
   count_launch(2);
   ATLAS_LAUNCH_CHECK();
@@ -1264,56 +1264,43 @@ bool sweep_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
   ATLAS_CUDA(cudaStreamSynchronize(s));
   if (hflags[0]) return false;  // deliveries != pending: exact errors
   const uint32_t maxp = hflags[1];
-
-  // ---- per sub-batch statics ------------------------------------------
-  fill_zero(W.fresh, S, s);
-  fill_zero(W.grad, S, s);
-  fill_zero(W.cold, S, s);
-  W.cold_out.reserve(std::max<int64_t>(S, 1));
-  sub_stats<<<grid_of(NE), 256, 0, s>>>(W.el_sub.ptr, W.el_fresh.ptr,
-                                        W.el_newp.ptr, NE, W.fresh.ptr,
-                                        W.grad.ptr);
-  count_launch();
-
   T.mark("sub_stats");
-  // ---- heap lists: MINPEND = one per pending value; LRU = the stream --
-  const bool lru = L->desc.policy == ATLAS_LRU;
+
+  // ---- heap lists: MINPEND = one FIFO per pending value, i.e. the entries
+  // sorted by (pending, element); LRU = the stream (sorted by element) ----
   const int64_t nb = lru ? 1 : (int64_t)maxp + 1;
   W.ent_sub.reserve(NE + 4);
   W.ent_next.reserve(NE + 4);
   W.boff.reserve(nb + 1);
   W.head.reserve(nb);
+  W.sk64.reserve(NE);
+  {
+    size_t tb = 0;
+    const int kb = lru ? 32 : 32 + bits_for(maxp);
+    ATLAS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, W.pk.ptr,
+                                               W.sk64.ptr, W.cs.ptr,
+                                               W.svk.ptr, NE, 0, kb, s));
+    W.cub_tmp.reserve(tb);
+    ATLAS_CUDA(cub::DeviceRadixSort::SortPairs(W.cub_tmp.ptr, tb, W.pk.ptr,
+                                               W.sk64.ptr, W.cs.ptr,
+                                               W.svk.ptr, NE, 0, kb, s));
+    count_launch();
+  }
+  entries_from_sorted<<<grid_of(NE), 256, 0, s>>>(W.sk64.ptr, W.svk.ptr, NE,
+                                                  W.ent_sub.ptr,
+                                                  W.ent_next.ptr, W.se.ptr);
+  count_launch();
   if (lru) {
-    make_entries<<<grid_of(NE), 256, 0, s>>>(nullptr, W.el_newp.ptr,
-                                             W.el_sub.ptr, W.el_nsub.ptr, NE,
-                                             W.ent_sub.ptr, W.ent_next.ptr);
     const uint32_t hb[2] = {0u, (uint32_t)NE};
     ATLAS_CUDA(cudaMemcpyAsync(W.boff.ptr, hb, sizeof(hb),
                                cudaMemcpyHostToDevice, s));
-    count_launch();
   } else {
-    // stable by key: stream order within each pending value (the FIFO)
-    size_t tb = 0;
-    const int kb = bits_for(maxp);
-    ATLAS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, W.el_newp.ptr,
-                                               W.sv.ptr, W.iota.ptr, W.se.ptr,
-                                               NE, 0, kb, s));
-    W.cub_tmp.reserve(tb);
-    ATLAS_CUDA(cub::DeviceRadixSort::SortPairs(W.cub_tmp.ptr, tb,
-                                               W.el_newp.ptr, W.sv.ptr,
-                                               W.iota.ptr, W.se.ptr, NE, 0,
-                                               kb, s));
-    make_entries<<<grid_of(NE), 256, 0, s>>>(W.se.ptr, W.sv.ptr, W.el_sub.ptr,
-                                             W.el_nsub.ptr, NE, W.ent_sub.ptr,
-                                             W.ent_next.ptr);
-    bucket_bounds<<<grid_of(NE + 1), 256, 0, s>>>(W.sv.ptr, NE, nb,
-                                                  W.boff.ptr);
-    count_launch(3);
+    bucket_bounds64<<<grid_of(NE + 1), 256, 0, s>>>(W.sk64.ptr, NE, nb,
+                                                    W.boff.ptr);
+    count_launch();
   }
   ATLAS_CUDA(cudaMemsetAsync(W.ent_sub.ptr + NE, 0xFF, 4 * sizeof(uint32_t), s));
   ATLAS_CUDA(cudaMemsetAsync(W.ent_next.ptr + NE, 0, 4 * sizeof(uint32_t), s));
-  ATLAS_CUDA(cudaMemcpyAsync(W.head.ptr, W.boff.ptr, nb * sizeof(uint32_t),
-                             cudaMemcpyDeviceToDevice, s));
   ATLAS_LAUNCH_CHECK();
 
   T.mark("buckets");
@@ -1341,8 +1328,7 @@ static bool run_sweep(atlas_layer* L, SweepWs& W, PhaseTimer& T,
                       cudaStream_t s) {
   const int64_t NE = W.NE, S = W.S, nchunks = W.nchunks, nb = W.nb;
   const int64_t nloc = L->nloc;
-  const bool lru = W.lru;
-  const uint32_t* ent_el = lru ? nullptr : W.se.ptr;
+  const uint32_t* ent_el = W.se.ptr;  // element of each heap entry
   ATLAS_CUDA(cudaMemsetAsync(W.cold.ptr, 0, std::max<int64_t>(S, 1) * 4, s));
   ATLAS_CUDA(cudaMemcpyAsync(W.head.ptr, W.boff.ptr, nb * sizeof(uint32_t),
                              cudaMemcpyDeviceToDevice, s));
