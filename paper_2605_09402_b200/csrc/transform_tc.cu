@@ -1161,6 +1161,212 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// f32 x, register split, W too large to stay resident (K x BN x 8 B > ~190
+// KB, e.g. SAGE's K = 256 aggregate at BN = 128): W is pre-split once into
+// tf32 hi / lo arrays in global memory and streamed through its own ring
+// of (hi, lo) k-block stages next to the x landing ring; x is split into
+// TMEM A stages exactly as in transform_r_kernel. Ring stages are released
+// by the splitter (x) and by the MMA's commit (W).
+__global__ void split_w_tf32(const float* __restrict__ w, int64_t n,
+                             float* __restrict__ hi, float* __restrict__ lo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = w[i];
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kThreads, 1)
+    transform_rs_kernel(const __grid_constant__ CUtensorMap map_x,
+                        const __grid_constant__ CUtensorMap map_whi,
+                        const __grid_constant__ CUtensorMap map_wlo,
+                        TcParams p, int wst) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t x_bytes = BM * BK * 4;
+  const uint32_t w_bytes = p.BN * BK * 4;
+  uint8_t* xring = base;
+  uint8_t* wring = base + p.stages * x_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(wring + wst * 2 * w_bytes);
+  uint64_t* sempty = full + p.stages;
+  uint64_t* wfull = sempty + p.stages;   // [wst]
+  uint64_t* wempty = wfull + wst;        // [wst]
+  uint64_t* afull = wempty + wst;        // [kAStages]
+  uint64_t* aempty = afull + kAStages;   // [kAStages]
+  uint64_t* tfull = aempty + kAStages;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+  float* stage_out = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(sbias + 256) + 15) & ~uintptr_t(15));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (p.M + BM - 1) / BM;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&sempty[s], 128);
+    }
+    for (int s = 0; s < wst; s++) {
+      mbar_init(&wfull[s], 1);
+      mbar_init(&wempty[s], 1);
+    }
+    for (int a = 0; a < kAStages; a++) {
+      mbar_init(&afull[a], 128);
+      mbar_init(&aempty[a], 1);
+    }
+    for (int a = 0; a < 2; a++) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = threadIdx.x; j < p.BN; j += kThreads)
+    sbias[j] = j < p.N ? p.bias[j] : 0.0f;
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::
+            "r"(smem_u32(tmem_slot)),
+        "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int xs = 0, ws = 0;
+      uint32_t xph = 0, wph = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kb = 0; kb < p.kblocks; kb++) {
+          mbar_wait(&sempty[xs], xph ^ 1);
+          mbar_expect_tx(&full[xs], x_bytes);
+          tma_load_2d(xring + xs * x_bytes, &map_x, &full[xs], kb * BK,
+                      (int)(t * BM));
+          mbar_wait(&wempty[ws], wph ^ 1);
+          mbar_expect_tx(&wfull[ws], 2 * w_bytes);
+          uint8_t* wst_ptr = wring + ws * 2 * w_bytes;
+          tma_load_2d(wst_ptr, &map_whi, &wfull[ws], kb * BK, 0);
+          tma_load_2d(wst_ptr + w_bytes, &map_wlo, &wfull[ws], kb * BK, 0);
+          if (++xs == p.stages) {
+            xs = 0;
+            xph ^= 1;
+          }
+          if (++ws == wst) {
+            ws = 0;
+            wph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                           ((uint32_t)(p.BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+    int a = 0, ws = 0;
+    uint32_t aph = 0, wph = 0;
+    int acc = 0;
+    uint32_t tph[2] = {0, 0};
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], tph[acc] ^ 1);
+      tph[acc] ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dt = tmem_base + (uint32_t)(acc * p.BN);
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        mbar_wait(&afull[a], aph);
+        mbar_wait(&wfull[ws], wph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t ahi = tmem_base + kACol0 + (uint32_t)(a * 64);
+          const uint32_t b_hi = smem_u32(wring + ws * 2 * w_bytes);
+          const uint32_t b_lo = b_hi + w_bytes;
+#pragma unroll
+          for (int k = 0; k < BK / 8; k++) {
+            const uint32_t off = k * 32;
+            const uint32_t first = (kb == 0 && k == 0) ? 0u : 1u;
+            mma_tf32_ts(dt, ahi + 32 + k * 8, sw128_desc(b_hi + off), idesc,
+                        first);
+            mma_tf32_ts(dt, ahi + k * 8, sw128_desc(b_lo + off), idesc, 1u);
+            mma_tf32_ts(dt, ahi + k * 8, sw128_desc(b_hi + off), idesc, 1u);
+          }
+          mma_commit(&aempty[a]);
+          mma_commit(&wempty[ws]);
+          if (kb == p.kblocks - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++a == kAStages) {
+          a = 0;
+          aph ^= 1;
+        }
+        if (++ws == wst) {
+          ws = 0;
+          wph ^= 1;
+        }
+      }
+      acc ^= 1;
+    }
+  } else if (warp < 6) {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // tile row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    int s = 0, a = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        mbar_wait(&full[s], ph);
+        const float4* xs =
+            reinterpret_cast<const float4*>(xring + s * x_bytes) + r * 8;
+        float hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+          const float4 v = xs[c ^ (r & 7)];
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const float h = __uint_as_float(__float_as_uint(e[q]) & 0xFFFFE000u);
+            hi[c * 4 + q] = h;
+            lo[c * 4 + q] = e[q] - h;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&sempty[s]);
+        mbar_wait(&aempty[a], aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ta = tmem_base + lane_off + kACol0 + (uint32_t)(a * 64);
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&afull[a]);
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (++a == kAStages) {
+          a = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else {
+    epilogue_loop<OutT>(p, warp - 6, warp, lane, ntiles, tmem_base, tfull,
+                        tempty, sbias, nullptr, stage_out);
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile(
+        "tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(
+            tmem_base),
+        "r"(512));
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                               void*, const cuuint64_t*, const cuuint64_t*,
                               const cuuint32_t*, const cuuint32_t*,
@@ -1379,6 +1585,66 @@ bool launch_transform_r(const void* x, int64_t rows, int64_t k, int64_t ldx,
   return true;
 }
 
+// register split with W streamed (pre-split in global memory): false when
+// BN > 128 or the rings do not fit
+bool launch_transform_rs(const void* x, int64_t rows, int64_t k, int64_t ldx,
+                         const float* w, const float* b, int64_t n, int relu,
+                         void* y, int y_dtype, int64_t ldy, int32_t* flag,
+                         cudaStream_t s) {
+  const int BN = (int)((n + 15) / 16 * 16);
+  if (BN > 128) return false;
+  const int kblocks = (int)((k + BK - 1) / BK);
+  const int x_stage = BM * BK * 4;
+  const int w_stage = 2 * BN * BK * 4;
+  const int fixed = 1024 + 8 * 64 + 16 + 4 * 256 + 16 +
+                    kEpiWarps * 32 * kStageLd * 4;
+  const int xst = 4;
+  int wst = (227 * 1024 - fixed - xst * x_stage) / w_stage;
+  if (wst > 4) wst = 4;
+  if (wst < 2) return false;
+  // pre-split W into the (device, stream)'s grow-only scratch
+  SplitScratch& ws = split_scratch(s);
+  ws.buf.reserve((size_t)(2 * n * k * sizeof(float) + 64));
+  float* whi = reinterpret_cast<float*>(ws.buf.ptr);
+  float* wlo = whi + n * k;
+  split_w_tf32<<<(unsigned)std::min<int64_t>(ceil_div(n * k, 256), 4096), 256,
+                 0, s>>>(w, n * k, whi, wlo);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  CUtensorMap mx, mhi, mlo;
+  if (!make_map(&mx, x, ATLAS_F32, rows, k, ldx, BM) ||
+      !make_map(&mhi, whi, ATLAS_F32, n, k, k, BN) ||
+      !make_map(&mlo, wlo, ATLAS_F32, n, k, k, BN))
+    return false;
+  const int smem = fixed + xst * x_stage + wst * w_stage + 8 * 2 * wst;
+  TcParams p{};
+  p.M = rows;
+  p.K = (int)k;
+  p.N = (int)n;
+  p.BN = BN;
+  p.stages = xst;
+  p.kblocks = kblocks;
+  p.relu = relu;
+  p.ldy = ldy;
+  p.bias = b;
+  p.y = y;
+  p.flag = flag;
+  p.tmem_cols = 512;
+  const int64_t ntiles = (rows + BM - 1) / BM;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, num_sms());
+  auto launch = [&](auto kern) {
+    ATLAS_CUDA(cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kThreads, smem, s>>>(mx, mhi, mlo, p, wst);
+  };
+  if (y_dtype == ATLAS_F32) launch(transform_rs_kernel<float>);
+  else if (y_dtype == ATLAS_F16) launch(transform_rs_kernel<__half>);
+  else launch(transform_rs_kernel<__nv_bfloat16>);
+  count_launch();
+  ATLAS_LAUNCH_CHECK();
+  return true;
+}
+
 // ATLAS_TRANSFORM_T=1 (A/B probes): the TMEM-resident-W variant; measured
 // slower than W in shared memory on every cfg2 shape
 // (profiles/r2_transform_probe_v1.txt), so it is not the default
@@ -1444,8 +1710,10 @@ bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
     return launch_transform_t(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
                               flag, s);
   if (x_dtype == ATLAS_F32 && regsplit_enabled() &&
-      launch_transform_r(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy, flag,
-                         s))
+      (launch_transform_r(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
+                          flag, s) ||
+       launch_transform_rs(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
+                           flag, s)))
     return true;
   const int BN = (int)((n + 15) / 16 * 16);
   const int kblocks = (int)((k + BK - 1) / BK);

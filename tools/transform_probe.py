@@ -20,7 +20,8 @@ PEAK = 6544.0
 
 def main():
     rows = int(sys.argv[1]) if len(sys.argv) > 1 else 2_400_000
-    for k, n in [(100, 128), (128, 128), (128, 48), (128, 64), (64, 128)]:
+    for k, n in [(100, 128), (128, 128), (128, 48), (128, 64), (64, 128),
+                 (256, 128)]:
         x = torch.randn(rows, k, device="cuda")
         w = torch.randn(n, k, device="cuda") / k ** 0.5
         b = torch.randn(n, device="cuda")
