@@ -21,6 +21,8 @@
 //  * runs: one caller-supplied chunk tile; destination runs come from the
 //    per-chunk stable sort (chunk.cu); a record is read back only if an
 //    earlier chunk already touched it.
+#include <cstdlib>
+#include <string>
 #include "bulk.cuh"
 
 namespace atlas {
@@ -768,6 +770,182 @@ __global__ void __launch_bounds__(256, kTfBlocks<LPD>)
       flush();
     }
     cp_async_wait<0>();
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0 && epi.flag)
+    atomicOr(epi.flag, 1);
+}
+
+// transform-first layer, multi-chunk lanes: the agg_tf_ring walk with each
+// lane owning CPL 16-byte chunks of the z row (chunk sl + j*LPD), so a
+// 48-wide row (12 chunks, cfg2's 47-wide last layer) runs 4-lane groups
+// with every lane busy instead of 16-lane groups with 4 idle, and one
+// iteration serves 8 edges per warp instead of 2 (the per-edge issue,
+// shuffle and loop cost is what bound agg_tf_ring: ncu 83 % issue-active
+// at 0.69 of HBM). Ring slot s, chunk j of a lane sits at plane s*CPL + j
+// (512 B per plane, lane-contiguous: conflict-free).
+template <int LPD, int CPL, int DEPTH, int MODEL, typename OutT, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB)
+    agg_tf_multi(const float* __restrict__ z, int64_t ldz,
+                 const int64_t* __restrict__ csc_ptr,
+                 const uint32_t* __restrict__ csc_src,
+                 const uint32_t* __restrict__ indeg, int64_t lo, int64_t nloc,
+                 int d, float self_scale, EpiArgs epi,
+                 unsigned long long* __restrict__ work) {
+  constexpr int DPW = 32 / LPD;
+  constexpr int kWarpDst = kGrab * DPW;  // destinations per warp grab
+  constexpr int kIdR = LPD >= 16 ? 1 : 16 / LPD;
+  extern __shared__ uint4 ring_smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, sub = lane / LPD, sl = lane % LPD;
+  // per-warp grab metadata after the rings: CSC offsets relative to the
+  // grab's first edge, and the mean's reciprocal per destination, loaded
+  // once per grab (coalesced) so a finished destination never waits on a
+  // dependent global load
+  uint32_t* mptr = reinterpret_cast<uint32_t*>(ring_smem + 8 * DEPTH * CPL * 32) +
+                   warp * (2 * kWarpDst + 4);
+  float* mrcp = reinterpret_cast<float*>(mptr + kWarpDst + 4);
+  int colc[CPL];
+  bool on[CPL];
+#pragma unroll
+  for (int j = 0; j < CPL; j++) {
+    const int c = (sl + j * LPD) * 4;
+    on[j] = c < d;
+    colc[j] = on[j] ? c : d - 4;
+  }
+  const uint32_t ring_lane =
+      (uint32_t)__cvta_generic_to_shared(ring_smem + warp * (DEPTH * CPL * 32)) +
+      (uint32_t)lane * 16u;
+  int bad = 0;
+  while (true) {
+    unsigned long long w0 = 0;
+    if (lane == 0) w0 = atomicAdd(work, (unsigned long long)kWarpDst);
+    w0 = __shfl_sync(0xffffffffu, w0, 0) + (unsigned long long)epi.vbeg;
+    if ((int64_t)w0 >= nloc) break;
+    const int nw = (int)min((int64_t)kWarpDst, nloc - (int64_t)w0);
+    const int64_t ew = csc_ptr[w0];
+    for (int i = lane; i <= nw; i += 32)
+      mptr[i] = (uint32_t)(csc_ptr[w0 + i] - ew);
+    if (MODEL != ATLAS_GIN)
+      for (int i = lane; i < nw; i += 32)
+        mrcp[i] = 1.0f / (float)max(1u, indeg[w0 + i]);
+    __syncwarp();
+    // this sub-group's destinations [lv, lv_end) of the grab
+    int lv = min(sub * kGrab, nw);
+    const int lv_end = min(lv + kGrab, nw);
+    const uint32_t e_rel = mptr[lv];
+    const int ne = (int)(mptr[lv_end] - e_rel);
+    const uint32_t* __restrict__ src0 = csc_src + ew + e_rel;
+    int ce = 0, pe = 0;
+    int dend = lv < lv_end ? (int)(mptr[lv + 1] - e_rel) : ne;
+    // source ids in register batches of kIdR x LPD edges (lane sl holds
+    // edge base + sl + r * LPD), the next batch loaded one batch ahead so
+    // the id load is never on the cp.async issue path
+    uint32_t cur[kIdR], nxt[kIdR];
+    int pbase = 0;
+#pragma unroll
+    for (int r = 0; r < kIdR; r++) {
+      const int i0 = sl + r * LPD, i1 = i0 + kIdR * LPD;
+      cur[r] = i0 < ne ? src0[i0] : 0u;
+      nxt[r] = i1 < ne ? src0[i1] : 0u;
+    }
+    float a[CPL][4];
+#pragma unroll
+    for (int j = 0; j < CPL; j++) a[j][0] = a[j][1] = a[j][2] = a[j][3] = 0.0f;
+    auto issue = [&]() {
+      const bool more = pe < ne;
+      if (more && pe - pbase == kIdR * LPD) {
+        pbase = pe;
+#pragma unroll
+        for (int r = 0; r < kIdR; r++) {
+          cur[r] = nxt[r];
+          const int i1 = pbase + kIdR * LPD + sl + r * LPD;
+          nxt[r] = i1 < ne ? src0[i1] : 0u;
+        }
+      }
+      const int q = pe - pbase;
+      uint32_t pick = cur[0];
+#pragma unroll
+      for (int r = 1; r < kIdR; r++)
+        if (q / LPD == r) pick = cur[r];
+      const uint32_t u = LPD == 1 ? pick
+                                  : __shfl_sync(0xffffffffu, pick,
+                                                q & (LPD - 1), LPD);
+      if (more) {
+        const float* row = z + (int64_t)u * ldz;
+        const uint32_t slot =
+            ring_lane + ((uint32_t)(pe & (DEPTH - 1)) * CPL << 9);
+#pragma unroll
+        for (int j = 0; j < CPL; j++)
+          if (on[j]) cp_async16_s(slot + ((uint32_t)j << 9), row + colc[j]);
+        pe++;
+      }
+      cp_async_commit();  // one group per lane per iteration, maybe empty
+    };
+    auto flush = [&]() {
+      while (lv < lv_end && ce == dend) {
+        const int64_t v = (int64_t)w0 + lv;
+        const float r = MODEL == ATLAS_GIN ? 1.0f : mrcp[lv];
+        OutT* yrow = static_cast<OutT*>(epi.y) + v * epi.ldy;
+#pragma unroll
+        for (int j = 0; j < CPL; j++) {
+          if (!on[j]) continue;
+          const int col = colc[j];
+          float o4[4] = {a[j][0], a[j][1], a[j][2], a[j][3]};
+          if (MODEL == ATLAS_GIN) {
+            const float4 me = __ldg(
+                reinterpret_cast<const float4*>(z + (v + lo) * ldz + col));
+            o4[0] += self_scale * me.x;
+            o4[1] += self_scale * me.y;
+            o4[2] += self_scale * me.z;
+            o4[3] += self_scale * me.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; e++) o4[e] *= r;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const int c = col + e;
+            if (c < epi.n) {
+              float o = o4[e];
+              if (epi.self_rows) o += epi.self_rows[v * epi.ld_self + c];
+              o += __ldg(epi.bias + c);
+              if (epi.relu) o = (o >= 0.0f || o != o) ? o : 0.0f;
+              const OutT q = cvt_from_f32<OutT>(o);
+              bad |= is_extreme(to_f32(q));
+              yrow[c] = q;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CPL; j++)
+          a[j][0] = a[j][1] = a[j][2] = a[j][3] = 0.0f;
+        lv++;
+        dend = lv < lv_end ? (int)(mptr[lv + 1] - e_rel) : ne;
+      }
+    };
+#pragma unroll 1
+    for (int k = 0; k < DEPTH; k++) issue();
+    flush();
+    while (__any_sync(0xffffffffu, ce < ne)) {
+      cp_async_wait<DEPTH - 1>();  // the row issued DEPTH iterations ago
+      if (ce < ne) {
+        const uint32_t slot =
+            ring_lane + ((uint32_t)(ce & (DEPTH - 1)) * CPL << 9);
+#pragma unroll
+        for (int j = 0; j < CPL; j++) {
+          const uint4 r = lds16(slot + ((uint32_t)j << 9));
+          a[j][0] += __uint_as_float(r.x);
+          a[j][1] += __uint_as_float(r.y);
+          a[j][2] += __uint_as_float(r.z);
+          a[j][3] += __uint_as_float(r.w);
+        }
+        ce++;
+      }
+      issue();
+      flush();
+    }
+    cp_async_wait<0>();
+    __syncwarp();  // metadata reads done before the next grab rewrites it
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0 && epi.flag)
     atomicOr(epi.flag, 1);
@@ -1588,8 +1766,74 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
       else
         narrow(lpd_tag, std::integral_constant<int, ATLAS_GCN>());
     };
-    if (d <= 32) by_model(std::integral_constant<int, 8>());
-    else by_model(std::integral_constant<int, 16>());
+    static const bool old_ring = [] {
+      const char* e = std::getenv("ATLAS_TF_RING");
+      return e && std::string(e) == "old";
+    }();
+    static const int depth = [] {
+      const char* e = std::getenv("ATLAS_TF_DEPTH");
+      return e ? std::atoi(e) : 0;
+    }();
+    const int nch = d / 4;
+    if (old_ring) {
+      if (d <= 32) by_model(std::integral_constant<int, 8>());
+      else by_model(std::integral_constant<int, 16>());
+    } else {
+      // lanes per row x chunks per lane covering nch with the least waste
+      auto multi = [&](auto lpd_tag, auto cpl_tag, auto depth_tag,
+                       auto minb_tag) {
+        constexpr int LPD = decltype(lpd_tag)::value;
+        constexpr int CPL = decltype(cpl_tag)::value;
+        constexpr int DEPTH = decltype(depth_tag)::value;
+        constexpr int MINB = decltype(minb_tag)::value;
+        const int smem = 8 * DEPTH * CPL * 32 * 16 +
+                         8 * (2 * kGrab * (32 / LPD) + 4) * 4;
+        auto go = [&](auto kern) {
+          ATLAS_CUDA(cudaFuncSetAttribute(
+              kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          int per_sm = 0;
+          ATLAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+              &per_sm, kern, 256, smem));
+          kern<<<num_sms() * std::max(1, per_sm), 256, smem, s>>>(
+              z, ldz, g->csc_ptr.ptr, g->csc_src.ptr, g->indeg.ptr, g->lo,
+              v_end, d, e1, epi, g->work.ptr);
+        };
+        auto by_out = [&](auto model_tag) {
+          constexpr int M = decltype(model_tag)::value;
+          if (y_dtype == ATLAS_F32)
+            go(agg_tf_multi<LPD, CPL, DEPTH, M, float, MINB>);
+          else if (y_dtype == ATLAS_F16)
+            go(agg_tf_multi<LPD, CPL, DEPTH, M, __half, MINB>);
+          else
+            go(agg_tf_multi<LPD, CPL, DEPTH, M, __nv_bfloat16, MINB>);
+        };
+        if (data_model == ATLAS_GIN)
+          by_out(std::integral_constant<int, ATLAS_GIN>());
+        else
+          by_out(std::integral_constant<int, ATLAS_GCN>());
+      };
+      using I = std::integral_constant<int, 1>;
+      using I2 = std::integral_constant<int, 2>;
+      using I3 = std::integral_constant<int, 3>;
+      using I4 = std::integral_constant<int, 4>;
+      using I5 = std::integral_constant<int, 5>;
+      using I8 = std::integral_constant<int, 8>;
+      using I16 = std::integral_constant<int, 16>;
+      if (nch <= 4) {
+        if (depth == 11) multi(I8(), I(), I8(), I5());
+        else multi(I4(), I(), I8(), I4());
+      } else if (nch <= 8) {
+        if (depth == 12) multi(I2(), I3(), I4(), I3());
+        else if (depth == 13) multi(I8(), I(), I4(), I5());
+        else multi(I8(), I(), I8(), I5());
+      } else if (nch <= 12) {
+        if (depth == 6) multi(I8(), I2(), I4(), I5());
+        else if (depth == 7) multi(I8(), I2(), I2(), I4());
+        else if (depth == 9) multi(I16(), I(), I4(), I5());
+        else if (depth == 4) multi(I4(), I3(), I4(), I3());
+        else multi(I8(), I2(), I4(), I4());
+      } else multi(I8(), I2(), I4(), I4());
+    }
     count_launch();
     ATLAS_LAUNCH_CHECK();
     return;

@@ -133,7 +133,7 @@ struct SweepWs {
   DevBuf<uint32_t> zr, tmp_u32, el_v, el_cnt, el_sub,
       sv, se, ent_sub, ent_next, boff, head, fresh, grad, cold, cold_out,
       victims, flags;
-  DevBuf<uint8_t> cub_tmp, coop;
+  DevBuf<uint8_t> cub_tmp, coop, flags8;
   DevBuf<unsigned long long> cs, P, lastP, count, pk, svk, sk64;
   DevBuf<int64_t> eoff, soff, chunk64, out;
   // run materialisation (control.cu exact_replay)

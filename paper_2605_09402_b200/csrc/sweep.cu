@@ -255,6 +255,33 @@ __global__ void mark_unique(const uint32_t* __restrict__ victims, int64_t nv,
   }
 }
 
+// unique reloads from the single-CTA sweep's pop marks: every popped entry
+// has a successor delivery, where its vertex reloads
+__global__ void mark_unique_popped(const uint8_t* __restrict__ popped,
+                                   int64_t n, const uint32_t* __restrict__ ent_el,
+                                   const uint32_t* __restrict__ el_v,
+                                   uint8_t* __restrict__ flag) {
+  const int64_t n4 = n >> 2;
+  const uint32_t* p4 = reinterpret_cast<const uint32_t*>(popped);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4 + 1;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m;
+    if (q < n4) {
+      m = p4[q];
+    } else {  // tail
+      m = 0;
+      for (int64_t e = q * 4; e < n; e++)
+        m |= (uint32_t)popped[e] << (8 * (e - q * 4));
+    }
+    while (m) {
+      const int b = __ffs(m) - 1;
+      const int64_t e = q * 4 + (b >> 3);
+      flag[el_v[ent_el ? ent_el[e] : e]] = 1;
+      m &= ~(0xFFu << (b & ~7));
+    }
+  }
+}
+
 __global__ void count_flags(const uint8_t* __restrict__ f, int64_t n,
                             unsigned long long* __restrict__ out) {
   unsigned long long c = 0;
@@ -279,7 +306,8 @@ struct SweepArgs {
   uint32_t* head;            // [nb]
   const uint32_t* ent_sub;   // [n + 4]
   const uint32_t* ent_next;  // [n + 4]
-  uint32_t* victims;         // popped entries, in pop order
+  uint32_t* victims;         // popped entries, in pop order (coop kernel)
+  uint8_t* popped;           // [n] 1 = entry popped (single-CTA kernel)
   int64_t* out;              // evictions, reloads, hot_peak, nvict, err, info
   int32_t diag_no_far;       // diagnostics only: skip far reload atomics
 };
@@ -495,28 +523,15 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
           // the whole window's valid entries are victims: order within the
           // event is irrelevant here (no logs), so log slots come from one
           // atomic per warp
-          int incl = nvalid;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if ((tid & 31) >= o) incl += t;
-          }
-          int wbase = 0;
-          if ((tid & 31) == 31 && incl) wbase = atomicAdd(&sm.wlog[w & 1], incl);
-          wbase = __shfl_sync(0xffffffffu, wbase, 31);
-          // slot e of every lane in one round: consecutive lanes write
-          // consecutive log slots (coalesced)
-          const unsigned lt = (1u << (tid & 31)) - 1u;
-          int run = 0;
+          // pop marks: one byte per entry, stored by the thread owning
+          // it (no log offsets to agree on); entries before the head are
+          // never rewritten, so earlier marks in the window survive
 #pragma unroll
           for (int e = 0; e < kSwPerT; e++) {
-            const bool v = valid >> e & 1;
-            const unsigned m = __ballot_sync(0xffffffffu, v);
-            if (v) {
-              A.victims[nv + wbase + run + __popc(m & lt)] = j0 + e;
+            if (valid >> e & 1) {
+              A.popped[j0 + e] = 1;
               cold_add(nxts[e]);
             }
-            run += __popc(m);
           }
           if (fna != kNone && fna >= j0 && fna < j0 + kSwPerT)
             sm.hs_new = subs[fna - j0];
@@ -530,7 +545,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(SweepArgs A) {
             const int64_t r = off++;
             if (r >= rem) break;
             const uint32_t j = j0 + e;
-            A.victims[nv + r] = j;
+            A.popped[j] = 1;
             cold_add(nxts[e]);
             if (r == rem - 1) {
               sm.last_taken = j;
@@ -1350,6 +1365,9 @@ static bool run_sweep(atlas_layer* L, SweepWs& W, PhaseTimer& T,
   A.ent_sub = W.ent_sub.ptr;
   A.ent_next = W.ent_next.ptr;
   A.victims = W.victims.ptr;
+  W.flags8.reserve(NE + 4);
+  ATLAS_CUDA(cudaMemsetAsync(W.flags8.ptr, 0, NE + 4, s));
+  A.popped = W.flags8.ptr;
   A.out = W.out.ptr;
   {
     const char* e = getenv("ATLAS_SWEEP_DIAG_NO_FAR");  // wrong results!
@@ -1420,10 +1438,14 @@ static bool run_sweep(atlas_layer* L, SweepWs& W, PhaseTimer& T,
   ATLAS_CUDA(cudaMemsetAsync(L->unique_reloaded.ptr, 0,
                              std::max<int64_t>(nloc, 1), s));
   fill_zero(W.count, 1, s);
-  if (nvict > 0) {
+  if (nvict > 0 && coop_grid > 1) {
     mark_unique<<<grid_of(nvict), 256, 0, s>>>(W.victims.ptr, nvict, ent_el,
                                                W.el_v.ptr,
                                                L->unique_reloaded.ptr);
+    count_launch();
+  } else if (nvict > 0) {
+    mark_unique_popped<<<grid_of(NE / 4 + 1), 256, 0, s>>>(
+        W.flags8.ptr, NE, ent_el, W.el_v.ptr, L->unique_reloaded.ptr);
     count_launch();
   }
   count_flags<<<grid_of(nloc), 256, 0, s>>>(L->unique_reloaded.ptr, nloc,

@@ -517,3 +517,30 @@ def test_tcgen05_f16_input_transform_accuracy(m, k, n, relu):
     err = (y.double() - ref).abs()
     assert bool((err <= 4e-6 * (scale + 1e-3)).all()), \
         float((err / (scale + 1e-3)).max())
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("out", [3, 13, 19, 24, 30, 47, 52, 60])
+def test_transform_first_narrow_widths(kind, out):
+    """Every lanes-per-row x chunks-per-lane shape of the narrow
+    transform-first aggregation (agg_tf_multi: 1..16 chunks of z per row,
+    cfg2's 47-wide last layer = 12 chunks on 4 lanes x 3) against the
+    float64 oracle, same stated tolerance as the pipeline test."""
+    from oracle import gather as OG
+    from paper_2605_09402_b200.storage import (ModelKind, random_weights,
+                                               synthetic_in_memory)
+    graph, feats = synthetic_in_memory("pa", 5000, 11, 64, 3 + out)
+    w = random_weights(ModelKind(kind), [64, out], 5, gin_epsilon=0.25)
+    want = OG.per_layer(graph.num_vertices, graph.offsets, graph.neighbors,
+                        graph.in_degrees, feats.astype(np.float64), kind,
+                        [(lw.weight, lw.bias) for lw in w.layers],
+                        gin_epsilon=w.gin_epsilon)
+    eng = Engine(graph, w, PipelineConfig(chunk_budget=1 << 20,
+                                          hot_slots=5000, backend="tcgen05",
+                                          transform_first=True))
+    assert eng.transform_first(0)
+    _, _ = eng.infer(torch.as_tensor(feats).cuda(), keep_layers=True)
+    got = eng.last_layers[0].double().cpu().numpy()
+    eng.close()
+    err = float(np.abs(got - want[0]).max())
+    assert err <= 1e-5 * float(np.abs(want[0]).max()), err
