@@ -1819,14 +1819,12 @@ void launch_agg_resident_epi(const atlas_graph* g, const float* z,
       using I5 = std::integral_constant<int, 5>;
       using I8 = std::integral_constant<int, 8>;
       using I16 = std::integral_constant<int, 16>;
-      if (nch <= 4) {
-        if (depth == 11) multi(I8(), I(), I8(), I5());
-        else multi(I4(), I(), I8(), I4());
-      } else if (nch <= 8) {
-        if (depth == 12) multi(I2(), I3(), I4(), I3());
-        else if (depth == 13) multi(I8(), I(), I4(), I5());
-        else multi(I8(), I(), I8(), I5());
-      } else if (nch <= 12) {
+      // measured (profiles/r2_tf_multi_shapes.txt): 8-lane groups with a
+      // 4-deep ring at 4-5 blocks/SM beat both wider groups (fewer edges
+      // per iteration) and narrower ones (more flushes per iteration)
+      if (nch <= 4) multi(I4(), I(), I4(), I5());
+      else if (nch <= 8) multi(I8(), I(), I4(), I5());
+      else if (nch <= 12) {
         if (depth == 6) multi(I8(), I2(), I4(), I5());
         else if (depth == 7) multi(I8(), I2(), I2(), I4());
         else if (depth == 9) multi(I16(), I(), I4(), I5());

@@ -78,6 +78,37 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map,
       : "memory");
 }
 
+// L2 prefetch of a tensor tile (no shared memory, no barrier): the
+// producers run these a few k-blocks ahead of their shared-memory loads so
+// the loads hit L2 instead of waiting a full DRAM latency; the x bytes in
+// flight are then no longer bounded by the stages that fit next to W
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0,
+                                                int c1) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// the (tile, k-block) cursor of a producer's L2 prefetches
+struct L2Ahead {
+  int64_t t;
+  int kb;
+  __device__ __forceinline__ void run(const CUtensorMap* m, int64_t ntiles,
+                                      int kblocks, int bk, int rows, int sub,
+                                      int n) {
+    for (int i = 0; i < n && t < ntiles; i++) {
+      for (int u = 0; u < sub; u++)
+        tma_prefetch_2d(m, kb * bk, (int)((t * sub + u) * rows));
+      if (++kb == kblocks) {
+        kb = 0;
+        t += gridDim.x;
+      }
+    }
+  }
+};
+
 // K-major, SWIZZLE_128B UMMA shared-memory descriptor (sm100 version 1):
 // start >> 4, LBO = 1 (unused when swizzled), SBO = 1024 B (8 rows x 128 B)
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -162,7 +193,18 @@ struct TcParams {
   void* y;
   uint32_t tmem_cols;
   int32_t* flag;
+  int l2ahead;  // x k-blocks prefetched into L2 ahead of the loads
 };
+
+// ATLAS_TF_L2AHEAD: x k-blocks the producers prefetch into L2 ahead of
+// their shared-memory loads (0 = off)
+static int l2ahead_knob() {
+  static const int v = [] {
+    const char* e = std::getenv("ATLAS_TF_L2AHEAD");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
 
 // Epilogue warps (8): thread = accumulator row (TMEM lane) for
 // tcgen05.ld; each 32 x 16 block is transposed through a per-warp smem tile
@@ -326,8 +368,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       int s = 0;
       uint32_t ph = 0;
+      L2Ahead pf{(int64_t)blockIdx.x, 0};
+      pf.run(&map_x, ntiles, p.kblocks, BK, BM, 1, p.l2ahead);
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kb = 0; kb < p.kblocks; kb++) {
+          pf.run(&map_x, ntiles, p.kblocks, BK, BM, 1, p.l2ahead > 0 ? 1 : 0);
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = stages + s * stage_bytes;
           mbar_expect_tx(&full[s], BM * BK * (uint32_t)sizeof(TIn) +
@@ -583,8 +628,11 @@ __global__ void __launch_bounds__(kThreadsH, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      L2Ahead pf{(int64_t)blockIdx.x, 0};
+      pf.run(&map_x, ntiles, p.kblocks, BKH, BM, SUB, p.l2ahead);
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kb = 0; kb < p.kblocks; kb++) {
+          pf.run(&map_x, ntiles, p.kblocks, BKH, BM, SUB, p.l2ahead > 0 ? 1 : 0);
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = base + s * stage_bytes;
           mbar_expect_tx(&full[s], stage_bytes);
@@ -708,6 +756,7 @@ struct TtParams {
   const float* bias;
   void* y;
   int32_t* flag;
+  int l2ahead;
 };
 
 template <typename OutT>
@@ -762,8 +811,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      L2Ahead pf{(int64_t)blockIdx.x, 0};
+      pf.run(&map_x, ntiles, p.kblocks, BK, BR, 1, p.l2ahead);
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kb = 0; kb < p.kblocks; kb++) {
+          pf.run(&map_x, ntiles, p.kblocks, BK, BR, 1, p.l2ahead > 0 ? 1 : 0);
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], x_bytes);
           tma_load_2d(base + s * stage_bytes, &map_x, &full[s], kb * BK,
@@ -1023,8 +1075,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(w_hi_ptr(kb), &map_w, wfull, kb * BK, 0);
       int s = 0;
       uint32_t ph = 0;
+      L2Ahead pf{(int64_t)blockIdx.x, 0};
+      pf.run(&map_x, ntiles, p.kblocks, BK, BM, 1, p.l2ahead);
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kb = 0; kb < p.kblocks; kb++) {
+          pf.run(&map_x, ntiles, p.kblocks, BK, BM, 1, p.l2ahead > 0 ? 1 : 0);
           mbar_wait(&sempty[s], ph ^ 1);
           mbar_expect_tx(&full[s], x_bytes);
           tma_load_2d(stages + s * x_bytes, &map_x, &full[s], kb * BK,
@@ -1242,8 +1297,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int xs = 0, ws = 0;
       uint32_t xph = 0, wph = 0;
+      L2Ahead pf{(int64_t)blockIdx.x, 0};
+      pf.run(&map_x, ntiles, p.kblocks, BK, BM, 1, p.l2ahead);
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kb = 0; kb < p.kblocks; kb++) {
+          pf.run(&map_x, ntiles, p.kblocks, BK, BM, 1, p.l2ahead > 0 ? 1 : 0);
           mbar_wait(&sempty[xs], xph ^ 1);
           mbar_expect_tx(&full[xs], x_bytes);
           tma_load_2d(xring + xs * x_bytes, &map_x, &full[xs], kb * BK,
@@ -1492,6 +1550,7 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
   if (ok) {
     const int smem = fixed + stages * stage_bytes;
     TcParams p{};
+    p.l2ahead = l2ahead_knob();
     p.M = rows;
     p.K = (int)k;
     p.N = (int)n;
@@ -1558,6 +1617,7 @@ bool launch_transform_r(const void* x, int64_t rows, int64_t k, int64_t ldx,
     return false;
   const int smem = fixed + w_res + stages * x_stage;
   TcParams p{};
+    p.l2ahead = l2ahead_knob();
   p.M = rows;
   p.K = (int)k;
   p.N = (int)n;
@@ -1618,6 +1678,7 @@ bool launch_transform_rs(const void* x, int64_t rows, int64_t k, int64_t ldx,
     return false;
   const int smem = fixed + xst * x_stage + wst * w_stage + 8 * 2 * wst;
   TcParams p{};
+    p.l2ahead = l2ahead_knob();
   p.M = rows;
   p.K = (int)k;
   p.N = (int)n;
@@ -1666,6 +1727,7 @@ bool launch_transform_t(const void* x, int64_t rows, int64_t k, int64_t ldx,
   if (stages > 8) stages = 8;
   const int smem = fixed + stages * stage_bytes;
   TtParams p{};
+  p.l2ahead = l2ahead_knob();
   p.M = rows;
   p.K = (int)k;
   p.Kp = kblocks * BK;
@@ -1736,6 +1798,7 @@ bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
                    8 * (3 * stages + 6) + 16 + 4 * 256 + 16 +
                    kEpiWarps * 32 * kStageLd * 4;
   TcParams p{};
+    p.l2ahead = l2ahead_knob();
   p.M = rows;
   p.K = (int)k;
   p.N = (int)n;
