@@ -268,6 +268,25 @@ ATLAS_API int atlas_transform_typed(int32_t backend, const void* x_dev,
                                     int64_t ldy, int32_t* extremes_flag,
                                     void* stream);
 
+/* GAT pass A with the attention score er fused into the epilogue:
+ * y[:, 0:n] = x . W^T + b as atlas_transform_typed (tcgen05 backend,
+ * register-split f32/bf16 or f16 kernels only, n <= 128), and
+ * y[r, er_col + h] = sum_{c in head h} y[r, c] * er_w[c] for h < heads,
+ * head h = columns [h*head_stride, (h+1)*head_stride), head_stride a
+ * multiple of 16, heads <= 8. er_w (n, device) holds a_r[h] at head h's
+ * columns (zero padding). It replaces the a_r^T W_h rows of W_ext, which
+ * took n past 128 (128 + el + er = 136 for 4 x 32 heads) and so off the
+ * fast kernels; pass B (gat_ring) recomputes el per edge and never reads
+ * it. Returns ATLAS_ECONFIG when the shape needs another kernel. */
+ATLAS_API int atlas_transform_er(int32_t backend, const void* x_dev,
+                                 int32_t x_dtype, int64_t rows, int64_t k,
+                                 int64_t ldx, const float* w_dev,
+                                 const float* b_dev, int64_t n, void* y_dev,
+                                 int32_t y_dtype, int64_t ldy,
+                                 const float* er_w_dev, int32_t er_col,
+                                 int32_t heads, int32_t head_stride,
+                                 void* stream);
+
 /* GAT layer pass B over a resident z_ext (device, V rows of ldz elements:
  * [z: head h at columns h*head_stride .. +head_dim | el (heads) at el_col |
  *  er (heads) at er_col]; head_stride = head_dim rounded up to 16 bytes):

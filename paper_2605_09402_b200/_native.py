@@ -98,6 +98,9 @@ def _declare(lib):
     fn("atlas_transform_typed", ctypes.c_int, c_i32, c_vp, c_i32, c_i64,
        c_i64, c_i64, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_i64, c_vp,
        c_vp)
+    fn("atlas_transform_er", ctypes.c_int, c_i32, c_vp, c_i32, c_i64,
+       c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_i64, c_vp, c_i32,
+       c_i32, c_i32, c_vp)
     fn("atlas_layer_run_gat", ctypes.c_int, c_vp, c_vp, c_vp, c_i32, c_i64,
        c_i32, c_i32, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, ctypes.c_float,
        c_vp, c_i32, c_i64, c_vp, c_i64, c_vp)
@@ -142,7 +145,7 @@ EXPORTED = [
     "atlas_spill_read", "atlas_spill_write", "atlas_gather_replay",
     "atlas_spill_write_runs", "atlas_layer_run_blocked",
     "atlas_layer_record_bytes", "atlas_spill_read_device",
-    "atlas_gds_status",
+    "atlas_gds_status", "atlas_transform_er",
 ]
 
 

@@ -797,6 +797,31 @@ int atlas_transform_typed(int32_t backend, const void* x, int32_t x_dtype,
   });
 }
 
+int atlas_transform_er(int32_t backend, const void* x, int32_t x_dtype,
+                       int64_t rows, int64_t k, int64_t ldx, const float* w,
+                       const float* b, int64_t n, void* y, int32_t y_dtype,
+                       int64_t ldy, const float* er_w, int32_t er_col,
+                       int32_t heads, int32_t head_stride, void* stream) {
+  return guarded([&] {
+    ATLAS_NVTX("atlas_transform_er");
+    if (rows < 0 || k < 1 || n < 1 || n > 128 || ldx < k || !er_w ||
+        heads < 1 || heads > 8 || head_stride < 16 || head_stride % 16 != 0 ||
+        (int64_t)heads * head_stride != (n + 15) / 16 * 16 || er_col < n ||
+        ldy < er_col + heads)
+      fail(ATLAS_ECONFIG, "bad transform_er shape");
+    if (backend != ATLAS_BACKEND_TCGEN05)
+      fail(ATLAS_ECONFIG, "transform_er needs the tcgen05 backend");
+    struct Clear {
+      ~Clear() { set_transform_er(nullptr, 0, 0, 0); }
+    } clear;
+    set_transform_er(er_w, er_col, heads, head_stride);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!launch_transform_tc(x, x_dtype, rows, k, ldx, w, b, n, 0, y, y_dtype,
+                             ldy, nullptr, s))
+      fail(ATLAS_ECONFIG, "no register-split kernel takes this shape");
+  });
+}
+
 int atlas_layer_finish(atlas_layer* L, atlas_layer_metrics* m) {
   return guarded([&] {
     ATLAS_NVTX("atlas_layer_finish");

@@ -330,6 +330,9 @@ bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
                          int64_t ldx, const float* w, const float* b,
                          int64_t n, int relu, void* y, int y_dtype,
                          int64_t ldy, int32_t* flag, cudaStream_t s);
+// pending er request for the next launch_transform_tc on this host thread
+// (atlas_transform_er); w = nullptr clears it
+void set_transform_er(const float* w, int col, int heads, int hs);
 
 // control.cu
 void engine_init(atlas_layer* L, cudaStream_t s);

@@ -194,7 +194,28 @@ struct TcParams {
   uint32_t tmem_cols;
   int32_t* flag;
   int l2ahead;  // x k-blocks prefetched into L2 ahead of the loads
+  // GAT pass A: er[h] = sum over head h's columns of z * er_w (written at
+  // column er_col + h of each output row; null = off)
+  const float* er_w;
+  int er_col, er_heads, er_hs;
 };
+
+// the er request of the current atlas_transform_er call (host thread)
+struct ErSpec {
+  const float* w = nullptr;
+  int col = 0, heads = 0, hs = 0;
+};
+static thread_local ErSpec g_er;
+constexpr int kErMaxHeads = 8;
+// pair exchange of er partials: 2 parities x 4 lane quarters x heads x 32
+constexpr int kErBytes = 2 * 4 * kErMaxHeads * 32 * 4;
+static void apply_er(TcParams& p) {
+  p.er_w = g_er.w;
+  p.er_col = g_er.col;
+  p.er_heads = g_er.heads;
+  p.er_hs = g_er.hs;
+}
+static int er_smem() { return g_er.w ? kErBytes : 0; }
 
 // ATLAS_TF_L2AHEAD: x k-blocks the producers prefetch into L2 ahead of
 // their shared-memory loads (0 = off)
@@ -226,6 +247,13 @@ __device__ __forceinline__ void epilogue_loop(
   const bool vec_ok = (p.ldy % 4) == 0 &&
                       (reinterpret_cast<uintptr_t>(p.y) % (4 * sizeof(OutT))) == 0;
   int bad = 0;
+  // er: each thread (= row) folds its 16-column blocks into per-head
+  // partials; the two warps sharing a lane quarter hold alternate blocks,
+  // so the odd-block warp hands its partials over through shared memory
+  // (named barrier per quarter) and the even-block warp stores er
+  const bool er_on = p.er_w != nullptr;
+  float* erx = stage_out + kEpiWarps * 32 * kStageLd;
+  int xpar = 0;
   // a tile is `sub` 128-row halves (sub accumulators of BN columns each)
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     mbar_wait(&tfull[acc], aph[acc]);
@@ -235,9 +263,24 @@ __device__ __forceinline__ void epilogue_loop(
     const int64_t row0 = (t * sub + u) * BM + quarter * 32;
     const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) +
                            (uint32_t)((acc * sub + u) * p.BN);
+    float erp[kErMaxHeads];
+#pragma unroll
+    for (int hh = 0; hh < kErMaxHeads; hh++) erp[hh] = 0.0f;
     for (int c0 = cpar * 16; c0 < p.BN; c0 += 32) {
       float v[16];
       tmem_ld16(taddr + c0, v);
+      if (er_on) {
+        const int hd = c0 / p.er_hs;
+        float sacc = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          const float zj = sscale ? v[j] * sscale[c0 + j] : v[j];
+          sacc = fmaf(zj, __ldg(p.er_w + c0 + j), sacc);
+        }
+#pragma unroll
+        for (int hh = 0; hh < kErMaxHeads; hh++)
+          if (hh == hd) erp[hh] += sacc;
+      }
 #pragma unroll
       for (int j = 0; j < 16; j += 4)
         *reinterpret_cast<float4*>(&stage[lane * kStageLd + j]) =
@@ -276,6 +319,20 @@ __device__ __forceinline__ void epilogue_loop(
         }
       }
       __syncwarp();
+    }
+    if (er_on) {
+      float* xb = erx + ((xpar & 1) * 4 + quarter) * kErMaxHeads * 32;
+      if (cpar == 1)
+        for (int hh = 0; hh < p.er_heads; hh++) xb[hh * 32 + lane] = erp[hh];
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+      const int64_t row = row0 + lane;
+      if (cpar == 0 && row < p.M) {
+        OutT* dst = y + row * p.ldy + p.er_col;
+#pragma unroll
+        for (int hh = 0; hh < kErMaxHeads; hh++)
+          if (hh < p.er_heads) dst[hh] = cvt_out<OutT>(erp[hh] + xb[hh * 32 + lane]);
+      }
+      xpar++;
     }
     }  // halves
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1529,7 +1586,7 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
   const int stage_bytes = sub * BM * BKH * 2 + 2 * BN * BKH * 2;
   const int fixed = 1024 + 8 * 16 + 16 + 2 * 4 * 256 + 16 +
                     kEpiWarps * 32 * kStageLd * 4;
-  int stages = (227 * 1024 - fixed) / stage_bytes;
+  int stages = (227 * 1024 - fixed - er_smem()) / stage_bytes;
   if (stages > 6) stages = 6;
   if (stages < 2) return false;
   // pre-split W into the (device, stream)'s grow-only scratch: work on one
@@ -1548,8 +1605,9 @@ bool launch_transform_h(const void* x, int64_t rows, int64_t k, int64_t ldx,
             make_map_h(&mhi, whi, n, k, k, BN) &&
             make_map_h(&mlo, wlo, n, k, k, BN);
   if (ok) {
-    const int smem = fixed + stages * stage_bytes;
+    const int smem = fixed + stages * stage_bytes + er_smem();
     TcParams p{};
+    apply_er(p);
     p.l2ahead = l2ahead_knob();
     p.M = rows;
     p.K = (int)k;
@@ -1615,8 +1673,12 @@ bool launch_transform_r(const void* x, int64_t rows, int64_t k, int64_t ldx,
   if (!make_map(&mx, x, ATLAS_F32, rows, k, ldx, BM) ||
       !make_map(&mw, w, ATLAS_F32, n, k, k, BN))
     return false;
-  const int smem = fixed + w_res + stages * x_stage;
+  if (g_er.w && stages * x_stage + er_smem() > 227 * 1024 - fixed - w_res)
+    stages--;
+  if (stages < 3) return false;
+  const int smem = fixed + w_res + stages * x_stage + er_smem();
   TcParams p{};
+  apply_er(p);
     p.l2ahead = l2ahead_knob();
   p.M = rows;
   p.K = (int)k;
@@ -1659,7 +1721,7 @@ bool launch_transform_rs(const void* x, int64_t rows, int64_t k, int64_t ldx,
   const int fixed = 1024 + 8 * 64 + 16 + 4 * 256 + 16 +
                     kEpiWarps * 32 * kStageLd * 4;
   const int xst = 4;
-  int wst = (227 * 1024 - fixed - xst * x_stage) / w_stage;
+  int wst = (227 * 1024 - fixed - er_smem() - xst * x_stage) / w_stage;
   if (wst > 4) wst = 4;
   if (wst < 2) return false;
   // pre-split W into the (device, stream)'s grow-only scratch
@@ -1676,8 +1738,10 @@ bool launch_transform_rs(const void* x, int64_t rows, int64_t k, int64_t ldx,
       !make_map(&mhi, whi, ATLAS_F32, n, k, k, BN) ||
       !make_map(&mlo, wlo, ATLAS_F32, n, k, k, BN))
     return false;
-  const int smem = fixed + xst * x_stage + wst * w_stage + 8 * 2 * wst;
+  const int smem =
+      fixed + xst * x_stage + wst * w_stage + 8 * 2 * wst + er_smem();
   TcParams p{};
+  apply_er(p);
     p.l2ahead = l2ahead_knob();
   p.M = rows;
   p.K = (int)k;
@@ -1768,7 +1832,9 @@ bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
   if (n < 1 || n > 256 || k < 1 || (ldx * xs) % 16 != 0 || k % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) != 0)
     return false;
-  if (x_dtype == ATLAS_F32 && n <= 128 && k <= 128 && transposed_enabled())
+  if (g_er.w && x_dtype == ATLAS_F16) return false;  // er: h kernel only
+  if (x_dtype == ATLAS_F32 && n <= 128 && k <= 128 && transposed_enabled() &&
+      !g_er.w)
     return launch_transform_t(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
                               flag, s);
   if (x_dtype == ATLAS_F32 && regsplit_enabled() &&
@@ -1777,6 +1843,7 @@ bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
        launch_transform_rs(x, rows, k, ldx, w, b, n, relu, y, y_dtype, ldy,
                            flag, s)))
     return true;
+  if (g_er.w) return false;  // er: register-split kernels only
   const int BN = (int)((n + 15) / 16 * 16);
   const int kblocks = (int)((k + BK - 1) / BK);
   if ((reinterpret_cast<uintptr_t>(w) & 15) != 0) return false;
@@ -1837,6 +1904,13 @@ bool launch_transform_tc(const void* x, int x_dtype, int64_t rows, int64_t k,
   count_launch();
   ATLAS_LAUNCH_CHECK();
   return true;
+}
+
+void set_transform_er(const float* w, int col, int heads, int hs) {
+  g_er.w = w;
+  g_er.col = col;
+  g_er.heads = heads;
+  g_er.hs = hs;
 }
 
 }  // namespace atlas

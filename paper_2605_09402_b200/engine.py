@@ -429,6 +429,17 @@ def transform_typed(x, w, b, relu: bool, y, backend_code: int, rows=None,
         N.stream_handle(stream)))
 
 
+def transform_er(x, w, b, y, n: int, er_w, er_col: int, heads: int,
+                 head_stride: int, stream=None):
+    """GAT pass A with er fused (atlas_transform_er): y[:, :n] = x . W^T + b
+    and y[:, er_col + h] = z_h . a_r[h] (tcgen05 register-split kernels)."""
+    N.check(N.load_library().atlas_transform_er(
+        1, x.data_ptr(), torch_dtype_code(x), x.shape[0], x.shape[1],
+        x.stride(0), w.data_ptr(), b.data_ptr(), n, y.data_ptr(),
+        torch_dtype_code(y), y.stride(0), er_w.data_ptr(), er_col, heads,
+        head_stride, N.stream_handle(stream)))
+
+
 def percentile99(count: int, q_lo: int, q_hi: int) -> float:
     """np.percentile(spans, 99) from its two order statistics
     (numpy 'linear' method: virtual index (n-1)*0.99, _lerp)."""

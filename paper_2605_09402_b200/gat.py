@@ -29,6 +29,7 @@ heads, head_dim) and f32 W (H*F x in), a_l (H x F), a_r (H x F), b (H*F).
 
 from __future__ import annotations
 
+import os
 import struct
 import time
 from dataclasses import dataclass
@@ -285,6 +286,11 @@ class GATEngine:
         item = torch.empty(0, dtype=self.zt).element_size()
         self.layouts, self.w_ext, self.zero_b, self.bias = [], [], [], []
         self.attn_l = []  # a_l at the strided z columns (line_rows layouts)
+        # pass A with er fused into the GEMM epilogue (atlas_transform_er):
+        # W is just the z rows, so 4 x 32 heads stay at n = 128 and on the
+        # register-split / f16 kernels (W_ext's 136 rows did not)
+        self.w_z, self.attn_r = [], []
+        fuse_er = os.environ.get("ATLAS_GAT_ER", "1") != "0"
         for lw in weights.layers:
             lay = ZLayout(lw.heads, lw.head_dim, item)
             self.layouts.append(lay)
@@ -297,6 +303,15 @@ class GATEngine:
                 al[:, :lw.head_dim] = lw.attn_l
                 al = torch.as_tensor(al.reshape(-1)).cuda()
             self.attn_l.append(al)
+            ar = wz = None
+            if (fuse_er and al is not None and lw.heads <= 8
+                    and lay.head_stride % 16 == 0 and lay.el_col <= 128):
+                ar = np.zeros((lw.heads, lay.head_stride), dtype=np.float32)
+                ar[:, :lw.head_dim] = lw.attn_r
+                ar = torch.as_tensor(ar.reshape(-1)).cuda()
+                wz = self.w_ext[-1][:lay.el_col].contiguous()
+            self.attn_r.append(ar)
+            self.w_z.append(wz)
         self._layers = {}
         self.last_layers = []
         self.exchange = None
@@ -361,7 +376,7 @@ class GATEngine:
         (y (nloc, out), metrics or a collector, device layer)."""
         import torch
 
-        from .engine import transform_typed
+        from .engine import transform_er, transform_typed
 
         w = self.weights
         lw, lay = w.layers[l], self.layouts[l]
@@ -384,7 +399,14 @@ class GATEngine:
         else:
             z_local = torch.empty((h_local.shape[0], lay.ldz), dtype=self.zt,
                                   device="cuda")
-        if h_local.shape[0]:
+        if h_local.shape[0] and self.w_z[l] is not None and \
+                h_local.dtype in (torch.float32, torch.float16):
+            # z columns and er; el stays unwritten (gat_ring recomputes it
+            # per edge from the z row it loads)
+            transform_er(h_local, self.w_z[l], self.zero_b[l], z_local,
+                         lay.el_col, self.attn_r[l], lay.er_col, lw.heads,
+                         lay.head_stride)
+        elif h_local.shape[0]:
             transform_typed(h_local, self.w_ext[l], self.zero_b[l], False,
                             z_local[:, :lay.ncols], 1)
         ev[1].record()

@@ -34,7 +34,11 @@ def hub_graph(v=3000, seed=4):
 @pytest.mark.parametrize("feat_dtype", ["f32", "f16"])
 @pytest.mark.parametrize("heads,dims", [(4, [64, 128, 128, 19]),
                                         (2, [24, 16, 5]), (1, [16, 8, 8]),
-                                        (1, [16, 100, 12])])
+                                        (1, [16, 100, 12]),
+                                        # er fused into pass A's epilogue
+                                        # (16-column heads, 2 and 8 heads)
+                                        (2, [32, 32, 16]),
+                                        (8, [64, 128, 8])])
 def test_gat_matches_f64_oracle(zdtype, feat_dtype, heads, dims):
     g = hub_graph()
     w = G.random_gat_weights(dims, heads, seed=5)
@@ -81,3 +85,40 @@ def test_gat_single_vertex_and_empty_range():
         y, _ = eng.infer(torch.as_tensor(x).cuda())
         np.testing.assert_allclose(y.cpu().numpy(), want[-1], atol=1e-5)
         eng.close()
+
+
+@pytest.mark.parametrize("feat_dtype", ["f32", "f16"])
+def test_gat_fused_er_equals_extended_weight(feat_dtype):
+    """atlas_transform_er (z GEMM on the register-split / f16 kernels with
+    er from the epilogue) against pass A through W_ext (el and er as extra
+    GEMM rows): z and er equal to f32 rounding (the kernels may order the
+    split products differently)."""
+    from paper_2605_09402_b200.engine import transform_er, transform_typed
+    w = G.random_gat_weights([256, 128, 19], 4, seed=9)
+    lw = w.layers[0]
+    lay = G.ZLayout(lw.heads, lw.head_dim, 4)
+    assert lay.line_rows and lay.el_col == 128
+    ext = torch.as_tensor(G.extended_weight(lw, lay)).cuda()
+    x = torch.randn(70001, 256, device="cuda")
+    if feat_dtype == "f16":
+        x = x.half()
+    zb = torch.zeros(lay.ncols, device="cuda")
+    y_ext = torch.zeros(x.shape[0], lay.ldz, device="cuda")
+    transform_typed(x, ext, zb, False, y_ext[:, :lay.ncols], 1)
+    ar = np.zeros((lw.heads, lay.head_stride), np.float32)
+    ar[:, :lw.head_dim] = lw.attn_r
+    y_er = torch.zeros_like(y_ext)
+    transform_er(x, ext[:lay.el_col].contiguous(), zb, y_er, lay.el_col,
+                 torch.as_tensor(ar.reshape(-1)).cuda(), lay.er_col,
+                 lw.heads, lay.head_stride)
+    torch.cuda.synchronize()
+    a, b = y_ext.cpu().numpy(), y_er.cpu().numpy()
+    # different kernels (n = 136 vs 128) may order the split products
+    # differently: equal to f32 rounding
+    zs = float(np.abs(a[:, :128]).max())
+    assert float(np.abs(a[:, :128] - b[:, :128]).max()) <= 2e-6 * zs
+    er_a = a[:, lay.er_col:lay.er_col + lw.heads]
+    er_b = b[:, lay.er_col:lay.er_col + lw.heads]
+    scale = float(np.abs(er_a).max())
+    assert float(np.abs(er_a - er_b).max()) <= 2e-5 * scale
+
