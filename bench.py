@@ -818,7 +818,7 @@ def measure(args, world, rank, local):
 
         def kind_of(l):
             if eng.transform_first(l):
-                return "agg_tf_ring / agg_ring_epi (transform-first)"
+                return "agg_tf_multi / agg_ring_epi (transform-first)"
             row = weights.embedding_dim(l) * in_sizes[l]
             return ("agg_bulk" if row > 512 else
                     "agg_ring" if row > 256 else "agg_sub_ring")

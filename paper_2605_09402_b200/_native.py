@@ -13,7 +13,8 @@ import numpy as np
 
 from .errors import DeviceError, IncompleteLayerError, raise_for_status
 
-LIB_PATH = Path(__file__).resolve().parent / "libatlas_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / os.environ.get(
+    "ATLAS_LIB", "libatlas_b200.so")  # ATLAS_LIB: A/B builds (diagnostics)
 
 GCN, SAGE, GIN, GAT = 0, 1, 2, 3
 F32, F16, BF16 = 0, 1, 2

@@ -509,6 +509,9 @@ __global__ void __launch_bounds__(256, 3)
 constexpr int kSubRing = 8;
 constexpr int kSubBlocks = 4;  // agg_sub_ring blocks per SM (64 registers
                                 // each: no address rematerialisation)
+// per-warp grab metadata words of agg_sub_ring (offsets + denominators)
+template <int LPD>
+constexpr int kSubMeta = 2 * kGrab * (32 / LPD) + 4;
 
 template <typename T, int LPD, int MODEL, bool GUARD>
 __device__ __forceinline__ void sub_ring_body(
@@ -516,9 +519,15 @@ __device__ __forceinline__ void sub_ring_body(
     const uint32_t* __restrict__ csc_src, const uint32_t* __restrict__ indeg,
     int64_t lo, int64_t nloc, int d, float* __restrict__ acc, int64_t ldacc,
     float self_scale, unsigned long long* __restrict__ work,
-    uint4* __restrict__ ring) {
+    uint4* __restrict__ ring, uint32_t* __restrict__ mptr) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int DPW = 32 / LPD;
+  constexpr int kWarpDst = kGrab * DPW;
+  constexpr int kIdR = LPD >= 16 ? 1 : 16 / LPD;
+  // per-warp grab metadata (as in agg_tf_multi): CSC offsets relative to
+  // the grab's first edge and the mean's denominators, staged once per
+  // grab so arming a destination never waits on a dependent global load
+  float* mden = reinterpret_cast<float*>(mptr + kWarpDst + 4);
   constexpr bool kMean = MODEL != ATLAS_GIN;
   using F = Frag<T, VEC>;
   const int lane = threadIdx.x & 31, sub = lane / LPD, sl = lane % LPD;
@@ -535,24 +544,43 @@ __device__ __forceinline__ void sub_ring_body(
     if (lane == 0) w0 = atomicAdd(work, (unsigned long long)(kGrab * DPW));
     w0 = __shfl_sync(0xffffffffu, w0, 0);
     if ((int64_t)w0 >= nloc) break;
-    // this sub-group's destinations [v, v_end) and its edges [0, ne)
-    // relative to e_beg
-    int64_t v = min((int64_t)w0 + (int64_t)sub * kGrab, nloc);
-    const int64_t v_end = min(v + kGrab, nloc);
-    const int64_t e_beg = csc_ptr[v];
-    const int ne = (int)(csc_ptr[v_end] - e_beg);
-    const uint32_t* __restrict__ src0 = csc_src + e_beg;
+    const int nw = (int)min((int64_t)kWarpDst, nloc - (int64_t)w0);
+    const int64_t ew = csc_ptr[w0];
+    for (int i = lane; i <= nw; i += 32)
+      mptr[i] = (uint32_t)(csc_ptr[w0 + i] - ew);
+    if (kMean)
+      for (int i = lane; i < nw; i += 32)
+        mden[i] = (float)max(1u, indeg[w0 + i]);
+    __syncwarp();
+    // this sub-group's destinations [v, v_end) (grab-local lv) and its
+    // edges [0, ne) relative to its first edge
+    int lv = min(sub * kGrab, nw);
+    const int lv_end = min(lv + kGrab, nw);
+    int64_t v = (int64_t)w0 + lv;
+    const int64_t v_end = (int64_t)w0 + lv_end;
+    const uint32_t e_rel = mptr[lv];
+    const int ne = (int)(mptr[lv_end] - e_rel);
+    const uint32_t* __restrict__ src0 = csc_src + ew + e_rel;
     int ce = 0, pe = 0;
     int dend = 0;
     float denom = 1.0f, rcp = 1.0f;
     bool self_pending = false;
-    uint32_t isrc = sl < ne ? src0[sl] : 0u;
-    uint32_t csrc = isrc;  // GIN: consume-side source ids, LPD at a time
+    // source ids in register batches of kIdR x LPD edges, the next batch
+    // loaded one batch ahead (off the cp.async issue path)
+    uint32_t cur[kIdR], nxt[kIdR];
+    int pbase = 0;
+#pragma unroll
+    for (int r = 0; r < kIdR; r++) {
+      const int i0 = sl + r * LPD, i1 = i0 + kIdR * LPD;
+      cur[r] = i0 < ne ? src0[i0] : 0u;
+      nxt[r] = i1 < ne ? src0[i1] : 0u;
+    }
+    uint32_t csrc = cur[0];  // GIN: consume-side source ids, LPD at a time
     float a[VEC];
     auto start_dest = [&]() {  // arm destination v (v < v_end)
-      dend = (int)(csc_ptr[v + 1] - e_beg);
+      dend = (int)(mptr[lv + 1] - e_rel);
       if (kMean) {
-        denom = (float)max(1u, indeg[v]);
+        denom = mden[lv];
         rcp = __frcp_rn(denom);
       }
       self_pending = MODEL == ATLAS_GIN;
@@ -568,9 +596,21 @@ __device__ __forceinline__ void sub_ring_body(
     };
     auto issue = [&]() {
       const bool more = pe < ne;
-      if (more && (pe & (LPD - 1)) == 0 && pe != 0)
-        isrc = pe + sl < ne ? src0[pe + sl] : 0u;
-      const uint32_t u = __shfl_sync(0xffffffffu, isrc, pe & (LPD - 1), LPD);
+      if (more && pe - pbase == kIdR * LPD) {
+        pbase = pe;
+#pragma unroll
+        for (int r = 0; r < kIdR; r++) {
+          cur[r] = nxt[r];
+          const int i1 = pbase + kIdR * LPD + sl + r * LPD;
+          nxt[r] = i1 < ne ? src0[i1] : 0u;
+        }
+      }
+      const int q = pe - pbase;
+      uint32_t pick = cur[0];
+#pragma unroll
+      for (int r = 1; r < kIdR; r++)
+        if (q / LPD == r) pick = cur[r];
+      const uint32_t u = __shfl_sync(0xffffffffu, pick, q & (LPD - 1), LPD);
       if (more) {
         cp_async16_s(ring_lane + ((uint32_t)(pe & (kSubRing - 1)) << 9),
                      reinterpret_cast<const void*>(
@@ -596,6 +636,7 @@ __device__ __forceinline__ void sub_ring_body(
           }
         }
         v++;
+        lv++;
         if (v < v_end) start_dest();
       }
     };
@@ -628,6 +669,7 @@ __device__ __forceinline__ void sub_ring_body(
       flush();
     }
     cp_async_wait<0>();
+    __syncwarp();  // metadata reads done before the next grab rewrites it
   }
 }
 
@@ -642,14 +684,16 @@ __global__ void __launch_bounds__(256, kSubBlocks)
                  unsigned long long* __restrict__ work) {
   extern __shared__ uint4 ring_smem[];
   uint4* ring = ring_smem + (threadIdx.x >> 5) * (kSubRing * 32);
+  uint32_t* meta = reinterpret_cast<uint32_t*>(ring_smem + 8 * kSubRing * 32) +
+                   (threadIdx.x >> 5) * kSubMeta<LPD>;
   if (*guard_flag)
     sub_ring_body<T, LPD, MODEL, true>(x, ldx, csc_ptr, csc_src, indeg, lo,
                                        nloc, d, acc, ldacc, self_scale, work,
-                                       ring);
+                                       ring, meta);
   else
     sub_ring_body<T, LPD, MODEL, false>(x, ldx, csc_ptr, csc_src, indeg, lo,
                                         nloc, d, acc, ldacc, self_scale, work,
-                                        ring);
+                                        ring, meta);
 }
 
 // transform-first layer, narrow z rows (<= 64 f32), streaming version:
@@ -1302,7 +1346,7 @@ void resident_model(const atlas_graph* g, const T* x, int64_t ldx, int model,
           nloc, d, acc, ldacc, eps1, flag, g->work.ptr);
     };
     if (d <= 16 * VEC) {
-      const int sub_smem = 8 * kSubRing * 32 * 16;
+      const int sub_smem = 8 * kSubRing * 32 * 16 + 8 * kSubMeta<8> * 4;
       auto sub = [&](auto kern) {
         ATLAS_CUDA(cudaFuncSetAttribute(
             kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sub_smem));

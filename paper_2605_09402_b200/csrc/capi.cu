@@ -101,9 +101,30 @@ static void control_begin(atlas_layer* L, cudaStream_t s) {
 // queue the control plane and make s wait for it
 static void control_queue(atlas_layer* L, const atlas_graph* g,
                           int64_t chunk_rows, cudaStream_t s) {
+  if (!L->ctl_queued) {
+    resident_control(L, g, chunk_rows, L->ctl_stream);
+    ATLAS_CUDA(cudaEventRecord(L->tev[3], L->ctl_stream));
+  }
+  L->ctl_queued = false;
+  ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
+}
+
+// ATLAS_CTL_FIRST=1: queue the control plane BEFORE the data plane of a
+// resident pass, so its short kernels take SMs ahead of the persistent
+// aggregation grid instead of waiting for its CTAs to retire (the
+// per-layer tail of control_ms over agg_ms). Only when queueing cannot
+// block the host: the pass's chunk-statistics bound is cached and no exact
+// replay is forced.
+static void control_early(atlas_layer* L, const atlas_graph* g,
+                          int64_t chunk_rows) {
+  static const bool on = [] {
+    const char* e = std::getenv("ATLAS_CTL_FIRST");
+    return e && e[0] == '1';
+  }();
+  if (!on || !control_is_async(L, g, chunk_rows)) return;
   resident_control(L, g, chunk_rows, L->ctl_stream);
   ATLAS_CUDA(cudaEventRecord(L->tev[3], L->ctl_stream));
-  ATLAS_CUDA(cudaStreamWaitEvent(s, L->tev[3], 0));
+  L->ctl_queued = true;
 }
 
 // side copy stream and its events (created once per layer)
@@ -388,6 +409,7 @@ int atlas_layer_run_resident(atlas_layer* L, const atlas_graph* g,
     // control plane on its own stream beside the scatter-aggregate; s
     // waits for it at the end
     control_begin(L, s);
+    control_early(L, g, chunk_rows);
     if (L->nloc > 0)
       launch_agg_resident(g, x, dtype, ldx, D.model, D.gin_epsilon,
                           (int)D.embed_dim, L->acc.ptr, D.agg_dim,
@@ -514,6 +536,7 @@ int atlas_layer_run_fused(atlas_layer* L, const atlas_graph* g,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     settle(L);
     control_begin(L, s);
+    control_early(L, g, chunk_rows);
     if (out_flag) ATLAS_CUDA(cudaMemsetAsync(out_flag, 0, sizeof(int32_t), s));
     if (!y_host) {
       launch_agg_resident_epi(g, z, ldz, data_model, D.gin_epsilon, (int)d,

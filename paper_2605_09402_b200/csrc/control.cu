@@ -288,9 +288,120 @@ __global__ void span_pick(const unsigned long long* sum_count,
   }
 }
 
+// The two order statistics by MSB-first radix select instead of a sort:
+// per digit (<= 10 bits) one histogram pass over the spans whose higher
+// digits match each rank's prefix, then one block turns the histograms
+// into the next digit and the rank within it. The kernels hold 8 KB of
+// shared memory and a few registers, so they co-reside with the
+// persistent aggregation grid on the data stream (a device radix sort's
+// passes could not, and queued behind it as the layer's control tail).
+struct SpanSel {
+  long long pre[2];  // selected high digits of rank lo_i / hi_i
+  long long k[2];    // rank within the current prefix
+};
+constexpr int kSelMaxBits = 10;
+
+__global__ void span_sel_init(const unsigned long long* __restrict__ sc,
+                              SpanSel* __restrict__ st,
+                              unsigned* __restrict__ hist) {
+  const long long cnt = (long long)sc[1];
+  if (threadIdx.x == 0) {
+    long long lo_i = 0, hi_i = 0;
+    if (cnt > 0) {
+      const double vi = (double)(cnt - 1) * 0.99;
+      lo_i = (long long)floor(vi);
+      hi_i = lo_i + 1 < cnt ? lo_i + 1 : cnt - 1;
+    }
+    st->pre[0] = st->pre[1] = 0;
+    st->k[0] = lo_i;
+    st->k[1] = hi_i;
+  }
+  for (int i = threadIdx.x; i < 2 << kSelMaxBits; i += blockDim.x) hist[i] = 0;
+}
+
+__global__ void __launch_bounds__(256)
+    span_sel_hist(const int64_t* __restrict__ spans, int64_t n,
+                  int64_t sentinel, const SpanSel* __restrict__ st, int shift,
+                  int width, unsigned* __restrict__ hist) {
+  __shared__ unsigned h[2 << kSelMaxBits];
+  const int nb = 1 << width;
+  for (int i = threadIdx.x; i < 2 * nb; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const long long p0 = st->pre[0], p1 = st->pre[1];
+  const int hs = shift + width;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const long long key = spans[i];
+    if (key == sentinel) continue;
+    const long long top = hs >= 63 ? 0 : key >> hs;
+    const int bin = (int)((key >> shift) & (nb - 1));
+    if (top == p0) atomicAdd(&h[bin], 1u);
+    if (top == p1) atomicAdd(&h[nb + bin], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * nb; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// one block of 1024 threads: bin t of each rank's histogram
+__global__ void __launch_bounds__(1024)
+    span_sel_pick(SpanSel* __restrict__ st, unsigned* __restrict__ hist,
+                  int width) {
+  __shared__ unsigned long long part[32];
+  const int nb = 1 << width, t = threadIdx.x;
+  for (int r = 0; r < 2; r++) {
+    const unsigned c = t < nb ? hist[r * nb + t] : 0u;
+    // block exclusive scan of the bin counts
+    unsigned long long x = c;
+    const int lane = t & 31, w = t >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) part[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      unsigned long long q = part[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, q, o);
+        if (lane >= o) q += y;
+      }
+      part[lane] = q;  // inclusive over warps
+    }
+    __syncthreads();
+    const unsigned long long excl = x - c + (w ? part[w - 1] : 0ull);
+    const long long k = st->k[r];
+    if (c && (long long)excl <= k && k < (long long)(excl + c)) {
+      st->pre[r] = (st->pre[r] << width) | t;
+      st->k[r] = k - (long long)excl;
+    }
+    __syncthreads();
+  }
+  for (int i = t; i < 2 * nb; i += blockDim.x) hist[i] = 0;
+}
+
+__global__ void span_sel_out(const unsigned long long* __restrict__ sc,
+                             const SpanSel* __restrict__ st,
+                             int64_t* __restrict__ out) {
+  const int64_t cnt = (int64_t)sc[1];
+  out[0] = (int64_t)sc[0];
+  out[1] = cnt;
+  out[2] = cnt > 0 ? st->pre[0] : 0;
+  out[3] = cnt > 0 ? st->pre[1] : 0;
+}
+
 // Whole-layer passes: the spans' reductions are queued on the control
 // stream right behind the walk that produced first/last positions, so
 // finalize_layer only reads four pinned integers.
+// ATLAS_SPAN_SORT=1: order statistics through a device radix sort (A/B)
+static bool span_sort_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ATLAS_SPAN_SORT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 void queue_spans(atlas_layer* L, const atlas_graph* g, cudaStream_t s) {
   const int64_t n = L->nloc;
   L->span_pin.reserve(4);
@@ -317,17 +428,43 @@ void queue_spans(atlas_layer* L, const atlas_graph* g, cudaStream_t s) {
                                            n, spans.ptr, sc.ptr, sentinel);
     count_launch();
     ATLAS_LAUNCH_CHECK();
-    size_t tmp_bytes = 0;
-    ATLAS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, spans.ptr,
-                                              sorted.ptr, n, 0, bits, s));
-    DevBuf<uint8_t>& tmp = L->span_tmp;
-    tmp.reserve(tmp_bytes);
-    ATLAS_CUDA(cub::DeviceRadixSort::SortKeys(tmp.ptr, tmp_bytes, spans.ptr,
-                                              sorted.ptr, n, 0, bits, s));
-    count_launch();
-    span_pick<<<1, 1, 0, s>>>(sc.ptr, sorted.ptr, L->span_dev.ptr);
-    count_launch();
-    ATLAS_LAUNCH_CHECK();
+    if (span_sort_enabled()) {  // A/B: the device radix sort
+      size_t tmp_bytes = 0;
+      ATLAS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, spans.ptr,
+                                                sorted.ptr, n, 0, bits, s));
+      DevBuf<uint8_t>& tmp = L->span_tmp;
+      tmp.reserve(tmp_bytes);
+      ATLAS_CUDA(cub::DeviceRadixSort::SortKeys(tmp.ptr, tmp_bytes, spans.ptr,
+                                                sorted.ptr, n, 0, bits, s));
+      count_launch();
+      span_pick<<<1, 1, 0, s>>>(sc.ptr, sorted.ptr, L->span_dev.ptr);
+      count_launch();
+      ATLAS_LAUNCH_CHECK();
+    } else {
+      // valid spans < 2^(bits - 1): digits of <= kSelMaxBits from the top
+      const int vbits = bits - 1;
+      const int passes = (vbits + kSelMaxBits - 1) / kSelMaxBits;
+      const int width = (vbits + passes - 1) / passes;
+      // scratch: SpanSel (32 B) + 2 x 1024 histogram words
+      sorted.reserve(4 + (2 << kSelMaxBits) / 2);
+      SpanSel* st = reinterpret_cast<SpanSel*>(sorted.ptr);
+      unsigned* hist = reinterpret_cast<unsigned*>(sorted.ptr + 4);
+      span_sel_init<<<1, 256, 0, s>>>(sc.ptr, st, hist);
+      count_launch();
+      const unsigned hgrid = (unsigned)std::min<int64_t>(
+          ceil_div(n, 256), (int64_t)num_sms() * 2);
+      for (int hi_bit = vbits; hi_bit > 0; hi_bit -= width) {
+        const int lo_bit = std::max(0, hi_bit - width);
+        span_sel_hist<<<hgrid, 256, 0, s>>>(spans.ptr, n, sentinel, st,
+                                            lo_bit, hi_bit - lo_bit, hist);
+        span_sel_pick<<<1, 1024, 0, s>>>(st, hist, hi_bit - lo_bit);
+        count_launch();
+        count_launch();
+      }
+      span_sel_out<<<1, 1, 0, s>>>(sc.ptr, st, L->span_dev.ptr);
+      count_launch();
+      ATLAS_LAUNCH_CHECK();
+    }
   }
   ATLAS_CUDA(cudaMemcpyAsync(L->span_pin.ptr, L->span_dev.ptr,
                              4 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -571,6 +708,20 @@ static void exact_replay(atlas_layer* L, const atlas_graph* g, int64_t R,
 // settle_control(): the host never waits for the data plane here. A
 // negative verdict then runs the exact replay (which only touches control
 // state, never the records).
+// true when resident_control(L, g, R) only queues device work (the
+// eviction-free walk with a deferred verdict): it never waits on the host
+bool control_is_async(atlas_layer* L, const atlas_graph* g, int64_t R) {
+  if (L->desc.record_log || L->desc.force_exact) return false;
+  const int64_t V = g->V;
+  Plan p{R, V, ceil_div(V, R)};
+  bool cached = (int64_t)g->offsets_host.size() == V + 1;
+  for (const auto& e : g->maxpass_cache)
+    if (e.first == p.R * 4 + L->desc.model) cached = true;
+  if (!cached) return false;
+  const int64_t max_pass = std::min(max_pass_of(L, g, p, nullptr), L->nloc);
+  return L->sub_batch >= max_pass;
+}
+
 void resident_control(atlas_layer* L, const atlas_graph* g, int64_t R,
                       cudaStream_t s) {
   const int64_t V = g->V;

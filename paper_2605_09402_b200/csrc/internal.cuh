@@ -229,6 +229,7 @@ struct atlas_layer {
   cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool timing_pending = false;
   bool ctl_deferred = false;
+  bool ctl_queued = false;  // control plane queued ahead of the data plane
   const atlas_graph* ctl_graph = nullptr;
   int64_t ctl_R = 0;
   atlas::PinnedBuf<unsigned long long> pin_hist;
@@ -340,6 +341,7 @@ void engine_run_chunks(atlas_layer* L, const uint64_t* runs,
                        const int64_t* run_off, const int64_t* chunk_bounds,
                        int64_t nchunks, const int64_t* host_run_off,
                        cudaStream_t s);
+bool control_is_async(atlas_layer* L, const atlas_graph* g, int64_t R);
 void resident_control(atlas_layer* L, const atlas_graph* g,
                       int64_t chunk_rows, cudaStream_t s);
 void settle_control(atlas_layer* L);

@@ -22,7 +22,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum",
         "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg."
         "pct_of_peak_sustained_elapsed"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-KINDS = ["agg_sub_ring", "agg_ring_epi", "agg_tf_ring", "agg_ring",
+KINDS = ["agg_sub_ring", "agg_ring_epi", "agg_tf_multi", "agg_tf_ring", "agg_ring",
          "agg_bulk", "gat_ring", "gat_bulk"]
 WORKLOAD = {"cfg2": "cfg2", "igbgcn": "igb-medium-gcn",
             "igbgat": "igb-medium-gat", "papers": "papers100m-sage-rank0of8"}
