@@ -1317,6 +1317,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(sbias + 256) + 15) & ~uintptr_t(15));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (p.M + BM - 1) / BM;
+  // TMEM: the two accumulators take [0, 2 BN); A stages of 64 columns
+  // follow (4 when BN <= 128, 2 for 128 < BN <= 192)
+  const uint32_t acol0 = p.BN <= 128 ? kACol0 : (uint32_t)((2 * p.BN + 63) / 64 * 64);
+  const int na = min(kAStages, (int)((512 - acol0) / 64));
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; s++) {
       mbar_init(&full[s], 1);
@@ -1326,7 +1330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&wfull[s], 1);
       mbar_init(&wempty[s], 1);
     }
-    for (int a = 0; a < kAStages; a++) {
+    for (int a = 0; a < na; a++) {
       mbar_init(&afull[a], 128);
       mbar_init(&aempty[a], 1);
     }
@@ -1397,7 +1401,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&wfull[ws], wph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
-          const uint32_t ahi = tmem_base + kACol0 + (uint32_t)(a * 64);
+          const uint32_t ahi = tmem_base + acol0 + (uint32_t)(a * 64);
           const uint32_t b_hi = smem_u32(wring + ws * 2 * w_bytes);
           const uint32_t b_lo = b_hi + w_bytes;
 #pragma unroll
@@ -1414,7 +1418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (kb == p.kblocks - 1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
-        if (++a == kAStages) {
+        if (++a == na) {
           a = 0;
           aph ^= 1;
         }
@@ -1452,7 +1456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&sempty[s]);
         mbar_wait(&aempty[a], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t ta = tmem_base + lane_off + kACol0 + (uint32_t)(a * 64);
+        const uint32_t ta = tmem_base + lane_off + acol0 + (uint32_t)(a * 64);
         tmem_st32(ta, hi);
         tmem_st32(ta + 32, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1462,7 +1466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           s = 0;
           ph ^= 1;
         }
-        if (++a == kAStages) {
+        if (++a == na) {
           a = 0;
           aph ^= 1;
         }
@@ -1707,6 +1711,12 @@ bool launch_transform_r(const void* x, int64_t rows, int64_t k, int64_t ldx,
   return true;
 }
 
+// ATLAS_TRANSFORM_RS_WIDE=0 (A/B): N in (128, 192] back on transform_tc
+static bool wide_rs_enabled() {
+  const char* e = getenv("ATLAS_TRANSFORM_RS_WIDE");
+  return !(e && e[0] == '0');
+}
+
 // register split with W streamed (pre-split in global memory): false when
 // BN > 128 or the rings do not fit
 bool launch_transform_rs(const void* x, int64_t rows, int64_t k, int64_t ldx,
@@ -1714,7 +1724,9 @@ bool launch_transform_rs(const void* x, int64_t rows, int64_t k, int64_t ldx,
                          void* y, int y_dtype, int64_t ldy, int32_t* flag,
                          cudaStream_t s) {
   const int BN = (int)((n + 15) / 16 * 16);
-  if (BN > 128) return false;
+  // above 128 columns the accumulator pair leaves TMEM for 2 A stages
+  // (BN <= 192; e.g. the papers100M SAGE head, K = 256 -> 172)
+  if (BN > 192 || (BN > 128 && (k < 256 || !wide_rs_enabled()))) return false;
   const int kblocks = (int)((k + BK - 1) / BK);
   const int x_stage = BM * BK * 4;
   const int w_stage = 2 * BN * BK * 4;

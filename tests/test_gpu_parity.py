@@ -252,7 +252,11 @@ def test_stable_transform_bit_exact_vs_reference_backend():
                                         (2400, 100, 64, True),
                                         (777, 36, 120, False),
                                         (100000, 256, 128, True),
-                                        (50000, 512, 100, False)])
+                                        (50000, 512, 100, False),
+                                        # 128 < n <= 192: the streamed-W
+                                        # register split with 2 A stages
+                                        (30001, 256, 172, True),
+                                        (4096, 64, 192, False)])
 def test_tcgen05_transform_3xtf32_accuracy(m, k, n, relu):
     """tcgen05 backend: |y - y_f64| <= 2e-6 * (|x| |w| row-col scale)."""
     from paper_2605_09402_b200.compute import Tcgen05Backend
