@@ -336,11 +336,15 @@ class DeviceLayer:
 
         p, ld = self.accumulator_ptr()
         n = self.hi - self.lo
-        out = torch.empty((n, ld), dtype=torch.float32, device="cuda")
-        if n:
-            cudart = torch.cuda.cudart()
-            cudart.cudaMemcpy(out.data_ptr(), p, n * ld * 4, 4)
-        return out
+        if not n:
+            return torch.empty((0, ld), dtype=torch.float32, device="cuda")
+
+        class _Records:  # zero-copy view of the library's device buffer
+            __cuda_array_interface__ = {"shape": (n, ld), "typestr": "<f4",
+                                        "data": (p, False), "version": 3}
+
+        torch.cuda.current_stream().synchronize()
+        return torch.as_tensor(_Records(), device="cuda").clone()
 
     # -- results ------------------------------------------------------------
     def finish(self) -> RawMetrics:

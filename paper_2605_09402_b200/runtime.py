@@ -313,7 +313,7 @@ class Engine:
                                  flag=self.out_flags[l])
             else:  # host plug-in backend (reference MatmulBackend protocol)
                 from .compute import transform
-                agg = layer.accumulator().cpu().numpy()
+                agg = layer.accumulator()[:, :w.agg_dim(l)].cpu().numpy()
                 y.copy_(torch.as_tensor(transform(
                     agg, w.layers[l], apply_activation=not last,
                     backend=self.backend)))

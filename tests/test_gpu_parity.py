@@ -548,3 +548,48 @@ def test_transform_first_narrow_widths(kind, out):
     eng.close()
     err = float(np.abs(got - want[0]).max())
     assert err <= 1e-5 * float(np.abs(want[0]).max()), err
+
+
+def test_user_host_backend_plugin_matches_stable():
+    """A user MatmulBackend object without a device code (the reference's
+    plug-in protocol: name, max_batch_rows, apply(batch, weight, bias)) is
+    honoured on the host, exactly as oocgnn/compute.py:76-97 calls it; the
+    aggregation stays on the device. It is never a fallback: the built-in
+    backends always carry a device code. Written as the reference's own
+    f32 chain (out = b; out += x_k * w_k, k ascending), it reproduces the
+    stable backend's bits."""
+    from paper_2605_09402_b200 import _native as NN
+    from paper_2605_09402_b200.storage import (ModelKind, random_weights,
+                                               synthetic_in_memory)
+
+    class ChainBackend:
+        name = "user_chain"
+        max_batch_rows = 1000
+
+        def __init__(self):
+            self.calls = 0
+
+        def apply(self, batch, weight, bias):
+            self.calls += 1
+            out = np.broadcast_to(bias.astype(np.float32),
+                                  (len(batch), len(bias))).copy()
+            for k in range(batch.shape[1]):
+                out += batch[:, k:k + 1] * weight[:, k]
+            return out
+
+    graph, feats = synthetic_in_memory("pa", 3000, 7, 24, 17)
+    w = random_weights(ModelKind.SAGE, [24, 16, 8], 5)
+    user = ChainBackend()
+    lib = NN.load_library()
+    outs = {}
+    for name, be in (("stable", "stable"), ("user", user)):
+        eng = Engine(graph, w, PipelineConfig(chunk_budget=64 << 10,
+                                              hot_slots=3000, backend=be))
+        before = lib.atlas_kernel_launches()
+        y, _ = eng.infer(torch.as_tensor(feats).cuda())
+        torch.cuda.synchronize()
+        assert lib.atlas_kernel_launches() > before  # device aggregation
+        outs[name] = y.cpu().numpy()
+        eng.close()
+    assert user.calls >= 6  # 3000 rows in batches of 1000, two layers
+    np.testing.assert_array_equal(outs["user"], outs["stable"])
