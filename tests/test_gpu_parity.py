@@ -593,3 +593,42 @@ def test_user_host_backend_plugin_matches_stable():
         eng.close()
     assert user.calls >= 6  # 3000 rows in batches of 1000, two layers
     np.testing.assert_array_equal(outs["user"], outs["stable"])
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("embed", ["f16", "bf16"])
+@pytest.mark.parametrize("transform_first", [True, False])
+def test_two_byte_embeddings_within_tolerance(kind, embed, transform_first):
+    """Intermediate embeddings stored in f16 / bf16 (PipelineConfig.
+    embed_dtype, the slice workloads' default): 2-byte rows through the
+    aggregation kernels (widened exactly, f32 accumulation) and 2-byte
+    transform inputs (kind::f16 for f16, tf32 for bf16). Stated tolerance
+    per layer against the float64 oracle: 3e-3 * max|y| for f16, 2e-2 for
+    bf16 (one rounding of each stored embedding: 2^-11 / 2^-8 relative,
+    compounded over the layers); integer metrics equal the f32 run's."""
+    from oracle import gather as OG
+    from paper_2605_09402_b200.storage import (ModelKind, random_weights,
+                                               synthetic_in_memory)
+    graph, feats = synthetic_in_memory("pa", 8000, 9, 64, 29)
+    w = random_weights(ModelKind(kind), [64, 96, 128, 40], 5, gin_epsilon=0.25)
+    want = OG.per_layer(graph.num_vertices, graph.offsets, graph.neighbors,
+                        graph.in_degrees, feats.astype(np.float64), kind,
+                        [(lw.weight, lw.bias) for lw in w.layers],
+                        gin_epsilon=w.gin_epsilon)
+    tol = {"f16": 3e-3, "bf16": 2e-2}[embed]
+    runs = {}
+    for dt in (embed, "f32"):
+        eng = Engine(graph, w, PipelineConfig(
+            chunk_budget=256 << 10, hot_slots=8000, backend="tcgen05",
+            embed_dtype=dt, transform_first=transform_first))
+        _, metrics = eng.infer(torch.as_tensor(feats).cuda(),
+                               keep_layers=True)
+        runs[dt] = ([y.double().cpu().numpy() for y in eng.last_layers],
+                    metrics)
+        eng.close()
+    for l, (got, ref) in enumerate(zip(runs[embed][0], want)):
+        err = float(np.abs(got - ref).max())
+        assert err <= tol * float(np.abs(ref).max()), (l, err)
+    for a, b in zip(runs[embed][1], runs["f32"][1]):
+        for f in METRICS:
+            assert getattr(a, f) == getattr(b, f), f
