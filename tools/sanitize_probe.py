@@ -102,6 +102,29 @@ def run_gat():
         eng.close()
 
 
+def run_extra():
+    """Round-2b kernels: the wide streamed-W transform (128 < N <= 192),
+    2-byte intermediate embeddings (agg_tf_multi / 2-byte rings)."""
+    from paper_2605_09402_b200 import storage as S
+    from paper_2605_09402_b200.engine import transform_typed
+    x = torch.randn(3001, 256, device="cuda")
+    wt = torch.randn(172, 256, device="cuda") / 16
+    b = torch.randn(172, device="cuda")
+    y = torch.empty(3001, 172, device="cuda")
+    transform_typed(x, wt, b, True, y, 1)
+    ref = (x.double() @ wt.double().T + b.double()).clamp_min(0)
+    assert float((y.double() - ref).abs().max()) < 1e-4
+    graph, feats = S.synthetic_in_memory("pa", 4000, 7, 48, 3)
+    w = S.random_weights(S.ModelKind.GCN, [48, 64, 20], 5)
+    for dt in ("f16", "bf16"):
+        eng = Engine(graph, w, PipelineConfig(chunk_budget=64 << 10,
+                                              hot_slots=4000,
+                                              backend="tcgen05",
+                                              embed_dtype=dt))
+        eng.infer(torch.as_tensor(feats).cuda())
+        eng.close()
+
+
 def run_operator():
     from paper_2605_09402_b200.chunks import chunk_from_csr, chunk_rows
     from paper_2605_09402_b200.orchestrator import (finalize_layer,
@@ -135,6 +158,7 @@ if __name__ == "__main__":
     for c in (CASES[:3] if quick else CASES):
         run_case(c)
     run_gat()
+    run_extra()
     run_operator()
     torch.cuda.synchronize()
     print("sanitize probe ok", flush=True)
